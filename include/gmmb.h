@@ -1,0 +1,165 @@
+/*
+ * gmmb.h — C ABI of the B200-native Gaussian-mixture learner
+ * (libgmmb.so, package paper_2307_00071_b200).
+ *
+ * Drop-in boundary for the reference's fit path (gmmscape, C++ library,
+ * /root/reference/proj). The reference exposes no FFI; its public C++ API is
+ * include/gmmscape/sogmm.hpp + gmm.hpp. Each entry point below names the
+ * reference symbol it replaces. include/gmmb.hpp wraps this ABI back into the
+ * reference's C++ shape (exceptions, value types) and INTEGRATION.md shows
+ * the bindings.
+ *
+ * Conventions (all follow the reference):
+ *  - points: N x D column-major doubles, D in {3, 4}: pts[j*N + i] is
+ *    coordinate j of point i (Eigen MatX4, common.hpp:11). D = 4 is
+ *    xyz + intensity in [0, 1] (point_cloud.hpp:7-24); D = 3 is xyz.
+ *  - model: weights[M]; means[M*D] row-major; covs[M*D(D+1)/2] packed lower
+ *    triangle in row-major order (0,0),(1,0),(1,1),(2,0),... (packed10.hpp).
+ *  - log_gamma: N x M column-major (sogmm.hpp Responsibilities).
+ *  - return codes: 0 ok, 1 I/O / device failure, 2 invalid argument
+ *    (std::invalid_argument), 3 numerical error (NumericalError) — the
+ *    CLI's exit-code classes, gmmscape_cli.cpp:508-528. The message is in
+ *    gmmb_last_error() (thread-local).
+ *  - all calls are blocking; the library copies host buffers in and out and
+ *    keeps no pointer after return. A context owns one CUDA device/stream
+ *    and reusable device buffers; calls on one context must not overlap.
+ */
+#ifndef GMMB_H_
+#define GMMB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gmmb_ctx gmmb_ctx;
+
+/* EmParams (sogmm.hpp:36-41). ll_rel_tol = 0 runs exactly max_iters E steps
+ * (extension: the reference requires > 0, sogmm.cpp:468). */
+typedef struct {
+  int max_iters;      /* default 100 */
+  double ll_rel_tol;  /* default 1e-5 */
+  double cov_reg;     /* default 1e-6 */
+  uint64_t seed;      /* default 0 (kinit) */
+} gmmb_em_params;
+
+/* FitResult (sogmm.hpp:65-71) minus gbms_components, plus K bookkeeping and
+ * device-side stage timings (CUDA events, milliseconds). */
+typedef struct {
+  int em_iterations;           /* E steps executed */
+  double final_log_likelihood; /* natural log, D-dimensional density */
+  int removed_components;      /* degenerate components removed */
+  int k_out;                   /* components in the returned model */
+  int k_init;                  /* min(K, N) (sogmm.cpp:477) */
+  int converged;               /* 1 if the tolerance test ended the loop */
+  double ms_layout;            /* validate + Morton sort + recentring */
+  double ms_kinit;             /* keys + k-means++ + fix-up */
+  double ms_mstep0;            /* initial hard-assignment M step */
+  double ms_em;                /* EM loop */
+  double units;                /* sum over E steps of N * K_t */
+} gmmb_fit_stats;
+
+const char* gmmb_last_error(void);
+void gmmb_em_params_default(gmmb_em_params* p);
+
+/* Context on a CUDA device (one process may hold several). */
+int gmmb_ctx_create(int device, gmmb_ctx** out);
+/* Sharded context: this rank holds points [offset, offset+n) of a cloud
+ * split over `world` ranks; sufficient statistics and k-means++ candidates
+ * are combined with NCCL (libnccl.so.2, loaded at run time). nccl_id is the
+ * 128-byte ncclUniqueId from gmmb_nccl_unique_id on rank 0, broadcast by the
+ * caller (e.g. torch.distributed). */
+int gmmb_nccl_unique_id(void* out128);
+int gmmb_ctx_create_sharded(int device, int rank, int world,
+                            const void* nccl_id128, gmmb_ctx** out);
+void gmmb_ctx_destroy(gmmb_ctx* ctx);
+int gmmb_device_info(gmmb_ctx* ctx, int* sm_count, int* cc_major,
+                     int* cc_minor);
+
+/* ---- full fits ---------------------------------------------------------
+ * fit(cloud, bandwidth, em) (sogmm.hpp:74-75, sogmm.cpp:465-510) with the
+ * component count given instead of estimated by GBMS:
+ * k = min(K, N) -> kinit -> m_step -> EM loop (sogmm.cpp:477-509).
+ * Outputs are sized for min(K, N) components; stats->k_out says how many
+ * are valid. ll_trace[max_iters] (nullable) receives every E step's ll.
+ * labels[N] / centers[k] (nullable) receive the kinit assignment.
+ * offset: global index of this rank's first point (0 unless sharded). */
+int gmmb_fit_k(gmmb_ctx* ctx, const double* pts, int64_t n, int d, int K,
+               const gmmb_em_params* em, double* w_out, double* mu_out,
+               double* cov_out, double* ll_trace, gmmb_fit_stats* stats,
+               int32_t* labels, int64_t* centers);
+
+/* EM loop of fit (sogmm.cpp:484-509) from a caller-supplied initial model
+ * (the "fixed init" configuration). */
+int gmmb_fit_from(gmmb_ctx* ctx, const double* pts, int64_t n, int d, int m,
+                  const double* w0, const double* mu0, const double* cov0,
+                  const gmmb_em_params* em, double* w_out, double* mu_out,
+                  double* cov_out, double* ll_trace, gmmb_fit_stats* stats);
+
+/* Device-resident variants (points uploaded once, fits re-run on them):
+ * gmmb_upload validates and lays out the cloud (PointCloud4D::validate,
+ * point_cloud.hpp:15-24). */
+int gmmb_upload(gmmb_ctx* ctx, const double* pts, int64_t n, int d,
+                int64_t offset, int64_t n_global);
+int gmmb_fit_k_resident(gmmb_ctx* ctx, int K, const gmmb_em_params* em,
+                        double* w_out, double* mu_out, double* cov_out,
+                        double* ll_trace, gmmb_fit_stats* stats,
+                        int32_t* labels, int64_t* centers);
+int gmmb_fit_from_resident(gmmb_ctx* ctx, int m, const double* w0,
+                           const double* mu0, const double* cov0,
+                           const gmmb_em_params* em, double* w_out,
+                           double* mu_out, double* cov_out, double* ll_trace,
+                           gmmb_fit_stats* stats);
+
+/* ---- single steps (teacher forcing / API parity) -----------------------*/
+/* kinit (sogmm.hpp:52, sogmm.cpp:197-337): labels[N] = column of the 0 in
+ * each row of the one-hot log_gamma; centers[k] = k-means++ seed indices. */
+int gmmb_kinit(gmmb_ctx* ctx, const double* pts, int64_t n, int d, int k,
+               uint64_t seed, int32_t* labels, int64_t* centers);
+
+/* e_step (sogmm.hpp:55-57, sogmm.cpp:341-395) in FP64: ll and optionally
+ * the N x M log responsibilities (nullable). */
+int gmmb_e_step(gmmb_ctx* ctx, const double* pts, int64_t n, int d, int m,
+                const double* w, const double* mu, const double* cov,
+                double* ll_out, double* log_gamma_out);
+
+/* m_step (sogmm.hpp:62-63, sogmm.cpp:399-463) from an N x M log_gamma.
+ * Outputs sized for m; *m_out = kept components; *removed = m - *m_out. */
+int gmmb_m_step(gmmb_ctx* ctx, const double* pts, int64_t n, int d,
+                const double* log_gamma, int m, double cov_reg, double* w_out,
+                double* mu_out, double* cov_out, int* m_out, int* removed);
+
+/* One fused EM iteration of the production path (E step + sufficient
+ * statistics + M step) on a given model: ll of the E step and the model
+ * the next iteration would use. */
+int gmmb_em_step(gmmb_ctx* ctx, const double* pts, int64_t n, int d, int m,
+                 const double* w, const double* mu, const double* cov,
+                 double cov_reg, double* ll_out, double* w_out,
+                 double* mu_out, double* cov_out, int* m_out, int* removed);
+
+/* cholesky_cache (gmm.hpp:44-52, gmm.cpp:33-48) on the device, FP64:
+ * lower/precision as M x D x D row-major, log_det_terms[M]. */
+int gmmb_cholesky_cache(gmmb_ctx* ctx, int d, int m, const double* covs,
+                        double* lower, double* precision,
+                        double* log_det_terms);
+
+/* ---- synthetic inputs (synthetic.cpp / ingest.cpp restated, host) ------
+ * make_synthetic_frame + image_pair_to_cloud (synthetic.cpp:9-72,
+ * ingest.cpp:27-57): writes up to width*height points (col-major, D=4,
+ * capacity width*height rows, leading dimension = *n_out). */
+int gmmb_synthetic_frame_cloud(int width, int height, double depth_scale,
+                               double* pts_out, int64_t* n_out);
+/* make_structured_scene (synthetic.cpp:94-129): N x 4 col-major. */
+int gmmb_structured_scene(int64_t n, uint64_t seed, double noise_sigma,
+                          double* pts_out);
+/* make_blob_cloud (synthetic.cpp:74-92): centers[k*4] row-major. */
+int gmmb_blob_cloud(const double* centers, int k, double sigma,
+                    int64_t per_blob, uint64_t seed, double* pts_out);
+/* cfg3 frame jitter: xyz += sigma * normal_pair(seed, 13, 4i..) (D=4). */
+int gmmb_jitter_cloud(double* pts, int64_t n, double sigma, uint64_t seed);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GMMB_H_ */

@@ -1,0 +1,478 @@
+"""B200-native Gaussian-mixture learner (k-means++ init + full-covariance EM).
+
+Host-side mirror of the reference's fit API (gmmscape, /root/reference/proj/
+include/gmmscape/sogmm.hpp + gmm.hpp) over the C ABI in include/gmmb.h
+(libgmmb.so, built in-tree from paper_2307_00071_b200/csrc). Every compute
+call runs the CUDA library; there is no CPU fallback — importing this module
+without the built library raises.
+
+Reference -> this module:
+  EmParams            sogmm.hpp:36-41          EmParams
+  Gmm4                gmm.hpp:15-34            Gmm (D = 3 or 4)
+  FitResult           sogmm.hpp:65-71          FitResult
+  kinit               sogmm.hpp:52             kinit
+  e_step              sogmm.hpp:55-57          e_step
+  m_step              sogmm.hpp:62-63          m_step
+  fit(cloud, bw, em)  sogmm.hpp:74-75          fit_k(points, K, em)  (K given
+                                               instead of GBMS-estimated) and
+                                               fit_from(points, model, em)
+  cholesky_cache      gmm.hpp:52               cholesky_cache
+  NumericalError      common.hpp:27-30         NumericalError
+  std::invalid_argument                        ValueError
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+from typing import Optional
+
+import numpy as np
+
+__all__ = [
+    "EmParams", "Gmm", "FitResult", "CholeskyCache", "Context",
+    "NumericalError", "IoError", "fit_k", "fit_from", "kinit", "e_step",
+    "m_step", "em_step", "cholesky_cache", "synthetic_frame_cloud",
+    "structured_scene", "blob_cloud", "jitter_cloud", "lib_path", "load",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def lib_path() -> str:
+    return os.path.join(_HERE, "libgmmb.so")
+
+
+class NumericalError(RuntimeError):
+    """common.hpp:27-30 — non-SPD matrices, degenerate models, bad clouds."""
+
+
+class IoError(RuntimeError):
+    """common.hpp:23-25 — here: CUDA / NCCL / device failures (code 1)."""
+
+
+class _EmParams(ctypes.Structure):
+    _fields_ = [("max_iters", ctypes.c_int), ("ll_rel_tol", ctypes.c_double),
+                ("cov_reg", ctypes.c_double), ("seed", ctypes.c_uint64)]
+
+
+class _FitStats(ctypes.Structure):
+    _fields_ = [("em_iterations", ctypes.c_int),
+                ("final_log_likelihood", ctypes.c_double),
+                ("removed_components", ctypes.c_int), ("k_out", ctypes.c_int),
+                ("k_init", ctypes.c_int), ("converged", ctypes.c_int),
+                ("ms_layout", ctypes.c_double), ("ms_kinit", ctypes.c_double),
+                ("ms_mstep0", ctypes.c_double), ("ms_em", ctypes.c_double),
+                ("units", ctypes.c_double)]
+
+
+_lib = None
+
+_D = ctypes.POINTER(ctypes.c_double)
+_I32 = ctypes.POINTER(ctypes.c_int32)
+_I64 = ctypes.POINTER(ctypes.c_int64)
+_I = ctypes.POINTER(ctypes.c_int)
+_V = ctypes.c_void_p
+_SIGS = {
+    "gmmb_last_error": (ctypes.c_char_p, []),
+    "gmmb_em_params_default": (None, [ctypes.POINTER(_EmParams)]),
+    "gmmb_ctx_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_V)]),
+    "gmmb_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
+    "gmmb_ctx_create_sharded": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                               ctypes.c_char_p, ctypes.POINTER(_V)]),
+    "gmmb_ctx_destroy": (None, [_V]),
+    "gmmb_device_info": (ctypes.c_int, [_V, _I, _I, _I]),
+    "gmmb_fit_k": (ctypes.c_int, [_V, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                  ctypes.POINTER(_EmParams), _D, _D, _D, _D,
+                                  ctypes.POINTER(_FitStats), _I32, _I64]),
+    "gmmb_fit_from": (ctypes.c_int, [_V, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                     _D, _D, _D, ctypes.POINTER(_EmParams), _D, _D, _D, _D,
+                                     ctypes.POINTER(_FitStats)]),
+    "gmmb_upload": (ctypes.c_int, [_V, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_int64,
+                                   ctypes.c_int64]),
+    "gmmb_fit_k_resident": (ctypes.c_int, [_V, ctypes.c_int, ctypes.POINTER(_EmParams),
+                                           _D, _D, _D, _D, ctypes.POINTER(_FitStats),
+                                           _I32, _I64]),
+    "gmmb_fit_from_resident": (ctypes.c_int, [_V, ctypes.c_int, _D, _D, _D,
+                                              ctypes.POINTER(_EmParams), _D, _D, _D, _D,
+                                              ctypes.POINTER(_FitStats)]),
+    "gmmb_kinit": (ctypes.c_int, [_V, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                  ctypes.c_uint64, _I32, _I64]),
+    "gmmb_e_step": (ctypes.c_int, [_V, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                   _D, _D, _D, _D, _D]),
+    "gmmb_m_step": (ctypes.c_int, [_V, _D, ctypes.c_int64, ctypes.c_int, _D, ctypes.c_int,
+                                   ctypes.c_double, _D, _D, _D, _I, _I]),
+    "gmmb_em_step": (ctypes.c_int, [_V, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                    _D, _D, _D, ctypes.c_double, _D, _D, _D, _D, _I, _I]),
+    "gmmb_cholesky_cache": (ctypes.c_int, [_V, ctypes.c_int, ctypes.c_int, _D, _D, _D, _D]),
+    "gmmb_synthetic_frame_cloud": (ctypes.c_int, [ctypes.c_int, ctypes.c_int,
+                                                  ctypes.c_double, _D, _I64]),
+    "gmmb_structured_scene": (ctypes.c_int, [ctypes.c_int64, ctypes.c_uint64,
+                                             ctypes.c_double, _D]),
+    "gmmb_blob_cloud": (ctypes.c_int, [_D, ctypes.c_int, ctypes.c_double, ctypes.c_int64,
+                                       ctypes.c_uint64, _D]),
+    "gmmb_jitter_cloud": (ctypes.c_int, [_D, ctypes.c_int64, ctypes.c_double,
+                                         ctypes.c_uint64]),
+}
+
+
+def load() -> ctypes.CDLL:
+    """Loads libgmmb.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        p = lib_path()
+        if not os.path.exists(p):
+            raise ImportError(
+                f"{p} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                " (there is no CPU fallback)")
+        lib = ctypes.CDLL(p)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def _check(code: int) -> None:
+    if code == 0:
+        return
+    msg = load().gmmb_last_error().decode(errors="replace")
+    if code == 2:
+        raise ValueError(msg)
+    if code == 3:
+        raise NumericalError(msg)
+    raise IoError(msg)
+
+
+def _ptr(a: Optional[np.ndarray], t=_D):
+    if a is None:
+        return None
+    return a.ctypes.data_as(t)
+
+
+def _points(points) -> tuple[np.ndarray, int, int]:
+    """(N, D) array-like -> Fortran-ordered float64 (Eigen MatX4 layout)."""
+    p = np.asarray(points, dtype=np.float64)
+    if p.ndim != 2 or p.shape[1] not in (3, 4):
+        raise ValueError("points must be an (N, 3) or (N, 4) array")
+    return np.asfortranarray(p), p.shape[0], p.shape[1]
+
+
+@dataclasses.dataclass
+class EmParams:
+    """sogmm.hpp:36-41. ll_rel_tol = 0 runs exactly max_iters E steps."""
+    max_iters: int = 100
+    ll_rel_tol: float = 1e-5
+    cov_reg: float = 1e-6
+    seed: int = 0
+
+    def _c(self) -> _EmParams:
+        return _EmParams(self.max_iters, self.ll_rel_tol, self.cov_reg, self.seed)
+
+
+@dataclasses.dataclass
+class Gmm:
+    """Gmm4 (gmm.hpp:15-34) generalised to D in {3, 4}: packed covariances in
+    the packed10 order (0,0),(1,0),(1,1),(2,0),... (packed10.hpp:11-14)."""
+    weights: np.ndarray      # (M,)
+    means: np.ndarray        # (M, D)
+    covariances: np.ndarray  # (M, D(D+1)/2)
+
+    @property
+    def dim(self) -> int:
+        return int(self.means.shape[1])
+
+    def components(self) -> int:
+        return int(self.weights.shape[0])
+
+    def covariance(self, b: int) -> np.ndarray:
+        return unpack_symmetric(self.covariances[b], self.dim)
+
+    def memory_footprint(self) -> int:
+        """gmm.hpp:38-40: 4 bytes per float, 1 + D + D(D+1)/2 per component."""
+        d = self.dim
+        return 4 * self.components() * (1 + d + d * (d + 1) // 2)
+
+
+def packed_index(d: int):
+    rows, cols = [], []
+    for i in range(d):
+        for j in range(i + 1):
+            rows.append(i)
+            cols.append(j)
+    return np.array(rows), np.array(cols)
+
+
+def unpack_symmetric(p: np.ndarray, d: int) -> np.ndarray:
+    r, c = packed_index(d)
+    m = np.zeros((d, d))
+    m[r, c] = p
+    m[c, r] = p
+    return m
+
+
+def pack_symmetric(m: np.ndarray) -> np.ndarray:
+    r, c = packed_index(m.shape[0])
+    return m[r, c].copy()
+
+
+@dataclasses.dataclass
+class FitResult:
+    """sogmm.hpp:65-71 (gbms_components -> k_init) plus the ll trace."""
+    model: Gmm
+    em_iterations: int
+    final_log_likelihood: float
+    removed_components: int
+    k_init: int
+    converged: bool
+    ll_trace: np.ndarray
+    units: float                  # sum over E steps of N * K_t
+    ms_layout: float = 0.0
+    ms_kinit: float = 0.0
+    ms_mstep0: float = 0.0
+    ms_em: float = 0.0
+    labels: Optional[np.ndarray] = None
+    centers: Optional[np.ndarray] = None
+
+
+@dataclasses.dataclass
+class CholeskyCache:
+    """gmm.hpp:44-48."""
+    lower: np.ndarray       # (M, D, D)
+    precision: np.ndarray   # (M, D, D) = L^-1
+    log_det_terms: np.ndarray  # (M,) = sum ln diag P
+
+
+class Context:
+    """One CUDA device + stream + reusable device buffers (gmmb_ctx)."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1,
+                 nccl_id: Optional[bytes] = None):
+        lib = load()
+        h = ctypes.c_void_p()
+        if world > 1:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ValueError("sharded context needs the 128-byte NCCL id")
+            _check(lib.gmmb_ctx_create_sharded(device, rank, world, nccl_id, ctypes.byref(h)))
+        else:
+            _check(lib.gmmb_ctx_create(device, ctypes.byref(h)))
+        self._h = h
+        self.rank, self.world, self.device = rank, world, device
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(load().gmmb_nccl_unique_id(buf))
+        return buf.raw
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            load().gmmb_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def device_info(self) -> tuple[int, int, int]:
+        a, b, c = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _check(load().gmmb_device_info(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return a.value, b.value, c.value
+
+    @property
+    def handle(self):
+        return self._h
+
+    # -- device-resident fits (bench "value": inputs already in HBM) ------
+    def upload(self, points, offset: int = 0, n_global: int = 0) -> None:
+        p, n, d = _points(points)
+        self._n, self._d = n, d
+        _check(load().gmmb_upload(self._h, _ptr(p), n, d, offset, n_global))
+
+    def fit_k_resident(self, k: int, em: EmParams = EmParams(),
+                       want_labels: bool = False) -> FitResult:
+        n, d = self._n, self._d
+        kk = max(1, min(k, 1 << 30))
+        out = _alloc_model(min(kk, 4096), d)
+        ll = np.zeros(max(em.max_iters, 1))
+        st = _FitStats()
+        lab = np.zeros(n, np.int32) if want_labels else None
+        cen = np.zeros(min(kk, 4096), np.int64) if want_labels else None
+        _check(load().gmmb_fit_k_resident(self._h, k, ctypes.byref(em._c()), _ptr(out[0]),
+                                          _ptr(out[1]), _ptr(out[2]), _ptr(ll),
+                                          ctypes.byref(st), _ptr(lab, _I32), _ptr(cen, _I64)))
+        return _result(out, ll, st, lab, cen)
+
+
+def _alloc_model(m: int, d: int):
+    return (np.zeros(m), np.zeros((m, d)), np.zeros((m, d * (d + 1) // 2)))
+
+
+def _result(out, ll, st: _FitStats, lab=None, cen=None) -> FitResult:
+    k = st.k_out
+    model = Gmm(out[0][:k].copy(), out[1][:k].copy(), out[2][:k].copy())
+    if cen is not None:
+        cen = cen[:st.k_init].copy()
+    return FitResult(model, st.em_iterations, st.final_log_likelihood,
+                     st.removed_components, st.k_init, bool(st.converged),
+                     ll[:st.em_iterations].copy(), st.units, st.ms_layout,
+                     st.ms_kinit, st.ms_mstep0, st.ms_em, lab, cen)
+
+
+_default_ctx: Optional[Context] = None
+
+
+def _ctx(ctx: Optional[Context]) -> Context:
+    global _default_ctx
+    if ctx is not None:
+        return ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+def fit_k(points, k: int, em: EmParams = EmParams(), ctx: Optional[Context] = None,
+          want_labels: bool = False) -> FitResult:
+    """fit (sogmm.cpp:465-510) with K given: kinit -> m_step -> EM."""
+    c = _ctx(ctx)
+    p, n, d = _points(points)
+    kk = max(1, min(int(k), n if c.world == 1 else int(k)))
+    out = _alloc_model(kk, d)
+    ll = np.zeros(max(em.max_iters, 1))
+    st = _FitStats()
+    lab = np.zeros(n, np.int32) if want_labels else None
+    cen = np.zeros(kk, np.int64) if want_labels else None
+    _check(load().gmmb_fit_k(c.handle, _ptr(p), n, d, int(k), ctypes.byref(em._c()),
+                             _ptr(out[0]), _ptr(out[1]), _ptr(out[2]), _ptr(ll),
+                             ctypes.byref(st), _ptr(lab, _I32), _ptr(cen, _I64)))
+    return _result(out, ll, st, lab, cen)
+
+
+def _model_arrays(model: Gmm, d: int):
+    w = np.ascontiguousarray(model.weights, dtype=np.float64)
+    mu = np.ascontiguousarray(model.means, dtype=np.float64)
+    cov = np.ascontiguousarray(model.covariances, dtype=np.float64)
+    m = w.shape[0]
+    if mu.shape != (m, d) or cov.shape != (m, d * (d + 1) // 2):
+        raise ValueError("model field sizes disagree")
+    return w, mu, cov, m
+
+
+def fit_from(points, model: Gmm, em: EmParams = EmParams(),
+             ctx: Optional[Context] = None) -> FitResult:
+    """EM loop (sogmm.cpp:484-509) from a given initial model."""
+    c = _ctx(ctx)
+    p, n, d = _points(points)
+    w, mu, cov, m = _model_arrays(model, d)
+    out = _alloc_model(m, d)
+    ll = np.zeros(max(em.max_iters, 1))
+    st = _FitStats()
+    _check(load().gmmb_fit_from(c.handle, _ptr(p), n, d, m, _ptr(w), _ptr(mu), _ptr(cov),
+                                ctypes.byref(em._c()), _ptr(out[0]), _ptr(out[1]),
+                                _ptr(out[2]), _ptr(ll), ctypes.byref(st)))
+    return _result(out, ll, st)
+
+
+def kinit(points, k: int, seed: int = 0, ctx: Optional[Context] = None):
+    """sogmm.cpp:197-337. Returns (labels[N] int32, centers[k] int64); the
+    reference's Responsibilities is the one-hot of labels (0 / -inf)."""
+    c = _ctx(ctx)
+    p, n, d = _points(points)
+    lab = np.zeros(n, np.int32)
+    cen = np.zeros(max(int(k), 1), np.int64)
+    _check(load().gmmb_kinit(c.handle, _ptr(p), n, d, int(k), seed, _ptr(lab, _I32),
+                             _ptr(cen, _I64)))
+    return lab, cen
+
+
+def e_step(points, model: Gmm, want_log_gamma: bool = True,
+           ctx: Optional[Context] = None):
+    """sogmm.cpp:387-395: (log_gamma (N, M) or None, log-likelihood)."""
+    c = _ctx(ctx)
+    p, n, d = _points(points)
+    w, mu, cov, m = _model_arrays(model, d)
+    ll = ctypes.c_double()
+    lg = np.zeros((n, m), order="F") if want_log_gamma else None
+    _check(load().gmmb_e_step(c.handle, _ptr(p), n, d, m, _ptr(w), _ptr(mu), _ptr(cov),
+                              ctypes.byref(ll), _ptr(lg)))
+    return lg, ll.value
+
+
+def m_step(points, log_gamma, cov_reg: float = 1e-6, ctx: Optional[Context] = None):
+    """sogmm.cpp:459-463: returns (Gmm, removed)."""
+    c = _ctx(ctx)
+    p, n, d = _points(points)
+    lg = np.asfortranarray(np.asarray(log_gamma, dtype=np.float64))
+    if lg.ndim != 2 or lg.shape[0] != n:
+        raise ValueError("responsibility rows != point count")
+    m = lg.shape[1]
+    out = _alloc_model(m, d)
+    mo, rm = ctypes.c_int(), ctypes.c_int()
+    _check(load().gmmb_m_step(c.handle, _ptr(p), n, d, _ptr(lg), m, cov_reg, _ptr(out[0]),
+                              _ptr(out[1]), _ptr(out[2]), ctypes.byref(mo), ctypes.byref(rm)))
+    k = mo.value
+    return Gmm(out[0][:k].copy(), out[1][:k].copy(), out[2][:k].copy()), rm.value
+
+
+def em_step(points, model: Gmm, cov_reg: float = 1e-6, ctx: Optional[Context] = None):
+    """One production EM iteration (fused E + statistics + M) from `model`:
+    returns (ll of the E step, next model, removed)."""
+    c = _ctx(ctx)
+    p, n, d = _points(points)
+    w, mu, cov, m = _model_arrays(model, d)
+    out = _alloc_model(m, d)
+    ll = ctypes.c_double()
+    mo, rm = ctypes.c_int(), ctypes.c_int()
+    _check(load().gmmb_em_step(c.handle, _ptr(p), n, d, m, _ptr(w), _ptr(mu), _ptr(cov),
+                               cov_reg, ctypes.byref(ll), _ptr(out[0]), _ptr(out[1]),
+                               _ptr(out[2]), ctypes.byref(mo), ctypes.byref(rm)))
+    k = mo.value
+    return ll.value, Gmm(out[0][:k].copy(), out[1][:k].copy(), out[2][:k].copy()), rm.value
+
+
+def cholesky_cache(model: Gmm, ctx: Optional[Context] = None) -> CholeskyCache:
+    """gmm.cpp:33-48 on the device (FP64)."""
+    c = _ctx(ctx)
+    d = model.dim
+    cov = np.ascontiguousarray(model.covariances, dtype=np.float64)
+    m = cov.shape[0]
+    lo = np.zeros((m, d, d))
+    pr = np.zeros((m, d, d))
+    ld = np.zeros(m)
+    _check(load().gmmb_cholesky_cache(c.handle, d, m, _ptr(cov), _ptr(lo), _ptr(pr), _ptr(ld)))
+    return CholeskyCache(lo, pr, ld)
+
+
+# ---- synthetic inputs (host C++ in libgmmb.so; no GPU needed) -----------
+def synthetic_frame_cloud(width: int = 640, height: int = 480,
+                          depth_scale: float = 1000.0) -> np.ndarray:
+    """make_synthetic_frame + image_pair_to_cloud -> (N, 4)."""
+    buf = np.zeros(width * height * 4)
+    n = ctypes.c_int64()
+    _check(load().gmmb_synthetic_frame_cloud(width, height, depth_scale, _ptr(buf),
+                                             ctypes.byref(n)))
+    nn = n.value
+    return buf[:4 * nn].reshape(4, nn).T.copy()
+
+
+def structured_scene(n: int, seed: int = 0, noise_sigma: float = 0.005) -> np.ndarray:
+    buf = np.zeros(4 * n)
+    _check(load().gmmb_structured_scene(n, seed, noise_sigma, _ptr(buf)))
+    return buf.reshape(4, n).T.copy()
+
+
+def blob_cloud(centers, sigma: float, per_blob: int, seed: int = 0) -> np.ndarray:
+    c = np.ascontiguousarray(centers, dtype=np.float64)
+    k = c.shape[0]
+    buf = np.zeros(4 * k * per_blob)
+    _check(load().gmmb_blob_cloud(_ptr(c), k, sigma, per_blob, seed, _ptr(buf)))
+    return buf.reshape(4, k * per_blob).T.copy()
+
+
+def jitter_cloud(points: np.ndarray, sigma: float, seed: int) -> np.ndarray:
+    p = np.asfortranarray(np.array(points, dtype=np.float64))
+    _check(load().gmmb_jitter_cloud(_ptr(p), p.shape[0], sigma, seed))
+    return np.ascontiguousarray(p)

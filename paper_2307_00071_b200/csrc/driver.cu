@@ -1,0 +1,940 @@
+// driver.cu — host driver + extern "C" ABI (include/gmmb.h).
+//
+// One context = one CUDA device + stream + grow-only device buffers. The
+// fit path mirrors gmmscape::fit with K given (sogmm.cpp:477-509):
+//   upload (validate + layout) -> kinit (keys, k-means++, fix-up)
+//   -> initial M step from labels -> EM loop on the device.
+// The EM loop runs in chunks of iterations enqueued back to back; each
+// iteration is [fused E+stats] -> [ordered reduce] -> (NCCL allreduce when
+// sharded) -> [per-component finalize] -> [commit]. Convergence is decided on
+// the device (commit kernel); the host reads the 64-byte state once per
+// chunk to stop enqueuing.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "../../include/gmmb.h"
+#include "em_kernels.cuh"
+#include "kinit_kernels.cuh"
+#include "layout.cuh"
+
+using namespace gmmb;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Err {
+  int code;
+  std::string msg;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw Err{1, std::string(what) + ": " + cudaGetErrorString(e)};
+  }
+}
+
+// ---- NCCL, loaded lazily (only sharded contexts need it) -----------------
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t,
+                            ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t,
+                            ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+Nccl& nccl() {
+  static Nccl n;
+  if (!n.h) {
+    n.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!n.h) throw Err{1, std::string("cannot load libnccl.so.2: ") + dlerror()};
+    n.GetUniqueId = (decltype(n.GetUniqueId))dlsym(n.h, "ncclGetUniqueId");
+    n.CommInitRank = (decltype(n.CommInitRank))dlsym(n.h, "ncclCommInitRank");
+    n.CommDestroy = (decltype(n.CommDestroy))dlsym(n.h, "ncclCommDestroy");
+    n.AllReduce = (decltype(n.AllReduce))dlsym(n.h, "ncclAllReduce");
+    n.AllGather = (decltype(n.AllGather))dlsym(n.h, "ncclAllGather");
+    n.GetErrorString = (decltype(n.GetErrorString))dlsym(n.h, "ncclGetErrorString");
+    if (!n.GetUniqueId || !n.CommInitRank || !n.AllReduce || !n.AllGather) {
+      throw Err{1, "libnccl.so.2 lacks required symbols"};
+    }
+  }
+  return n;
+}
+
+void nck(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) {
+    throw Err{1, std::string(what) + ": " +
+                     (nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error")};
+  }
+}
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t count) {
+    if (count <= cap && p) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    const size_t c = std::max<size_t>(count, 1);
+    ck(cudaMalloc(&p, c * sizeof(T)), "cudaMalloc");
+    cap = c;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace
+
+struct gmmb_ctx {
+  int device = 0;
+  int sm_count = 148;
+  int cc_major = 0, cc_minor = 0;
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev[8] = {};
+  // sharding
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  // resident cloud
+  int64_t n = 0, offset = 0, n_global = 0;
+  int d = 0;
+  bool have_cloud = false;
+  DevBuf<double> x64;
+  DevBuf<float4> xt;
+  DevBuf<double> tc;
+  DevBuf<int32_t> perm;
+  DevBuf<double> bbox_part;
+  DevBuf<uint64_t> mkeys_in, mkeys_out;
+  DevBuf<int32_t> midx;
+  DevBuf<unsigned char> sort_tmp;
+  DevBuf<int> flags;
+  // kinit
+  DevBuf<uint64_t> keys;
+  DevBuf<double> kd2;
+  DevBuf<int32_t> labels;
+  DevBuf<unsigned char> chosen;
+  DevBuf<KppSlot> slots;
+  DevBuf<int> owned;
+  DevBuf<long long> centers;
+  DevBuf<KppRankSlot> rslots;  // [world] gathered + [1] own
+  DevBuf<int> ticket;
+  DevBuf<long long> ll64;      // sharded fix-up scratch
+  // model
+  DevBuf<double> mw[2], mmu[2], mcov[2];
+  DevBuf<CompConst> mcst[2];
+  DevBuf<double> rcount, rmean, rcov, rlogdet;
+  DevBuf<float> rpc;
+  DevBuf<int> rflags;
+  DevBuf<double> mpart, msums, mmeans, mcounts;
+  DevBuf<double> partials, ll_part, red, ll_trace;
+  DevBuf<double> dense;  // log_gamma staging for m_step / e_step
+  DevBuf<EmState> st;
+  EmState* st_host = nullptr;  // pinned
+  ModelBuf bufs[2];
+  RecBuf rec;
+};
+
+namespace {
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const Err& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+void set_device(gmmb_ctx* c) { ck(cudaSetDevice(c->device), "cudaSetDevice"); }
+
+void check_d(int d) {
+  if (d != 3 && d != 4) throw Err{2, "dimension must be 3 (xyz) or 4 (xyz+intensity)"};
+}
+
+void check_em(const gmmb_em_params* em) {
+  // sogmm.cpp:468-470 (ll_rel_tol = 0 allowed: fixed iteration count)
+  if (!em || em->max_iters < 1 || !(em->ll_rel_tol >= 0.0)) {
+    throw Err{2, "bad EM parameters"};
+  }
+  if (em->cov_reg < 0.0) throw Err{2, "cov_reg must be >= 0"};
+}
+
+// ---- device allocation ----------------------------------------------------
+void ensure_model(gmmb_ctx* c, int k) {
+  const size_t kc = std::max(k, 32);
+  for (int b = 0; b < 2; ++b) {
+    c->mw[b].ensure(kc);
+    c->mmu[b].ensure(kc * 4);
+    c->mcov[b].ensure(kc * 10);
+    c->mcst[b].ensure(kc);
+    c->bufs[b] = ModelBuf{c->mw[b].p, c->mmu[b].p, c->mcov[b].p, c->mcst[b].p};
+  }
+  c->rcount.ensure(kc);
+  c->rmean.ensure(kc * 4);
+  c->rcov.ensure(kc * 10);
+  c->rlogdet.ensure(kc);
+  c->rpc.ensure(kc * 16);
+  c->rflags.ensure(kc);
+  c->rec = RecBuf{c->rcount.p, c->rmean.p, c->rcov.p, c->rlogdet.p, c->rpc.p, c->rflags.p};
+  c->red.ensure(kc * 16 + 1);
+  c->st.ensure(1);
+}
+
+void reset_state(gmmb_ctx* c, int k, const gmmb_em_params* em, int removed0) {
+  EmState h{};
+  h.iter = 0;
+  h.done = 0;
+  h.k_cur = k;
+  h.cur = 0;
+  h.removed = removed0;
+  h.error = 0;
+  h.error_index = std::numeric_limits<int>::max();
+  h.error_kind = 0;
+  h.ll_prev = -INFINITY;
+  h.ll = -INFINITY;
+  h.converged = 0;
+  h.max_iters = em ? em->max_iters : 1;
+  h.tol = em ? em->ll_rel_tol : 0.0;
+  h.cov_reg = em ? em->cov_reg : 0.0;
+  h.npts = static_cast<double>(c->n_global);
+  h.units = 0.0;
+  ck(cudaMemcpyAsync(c->st.p, &h, sizeof(h), cudaMemcpyHostToDevice, c->s), "state H2D");
+}
+
+EmState read_state(gmmb_ctx* c) {
+  ck(cudaMemcpyAsync(c->st_host, c->st.p, sizeof(EmState), cudaMemcpyDeviceToHost, c->s),
+     "state D2H");
+  ck(cudaStreamSynchronize(c->s), "stream sync");
+  return *c->st_host;
+}
+
+void raise_state_error(const EmState& h) {
+  if (!h.error) return;
+  switch (h.error_kind) {
+    case 1:
+      throw Err{3, "m_step: component " + std::to_string(h.error_index) +
+                       " covariance not positive definite after regularization"};
+    case 2:
+      throw Err{3, "m_step: all components degenerate"};
+    case 3:
+      throw Err{3, "cholesky failed: block " + std::to_string(h.error_index) +
+                       " is not positive definite"};
+    default:
+      throw Err{3, "numerical error"};
+  }
+}
+
+void allreduce_sum(gmmb_ctx* c, double* p, int64_t count) {
+  if (c->world <= 1) return;
+  nck(nccl().AllReduce(p, p, static_cast<size_t>(count), ncclFloat64, ncclSum,
+                       c->comm, c->s),
+      "ncclAllReduce");
+}
+
+void moments_allreduce_cb(double* p, int64_t count, void* ctx) {
+  allreduce_sum(static_cast<gmmb_ctx*>(ctx), p, count);
+}
+
+// ---- upload + layout ------------------------------------------------------
+void upload(gmmb_ctx* c, const double* pts, int64_t n, int d, int64_t offset,
+            int64_t n_global) {
+  check_d(d);
+  if (n < 1) throw Err{3, "point cloud is empty"};
+  if (!pts) throw Err{2, "null point buffer"};
+  if (n > (int64_t{1} << 31) - 1) throw Err{2, "too many points for one device"};
+  set_device(c);
+  c->x64.ensure(static_cast<size_t>(n) * 4 + 4);
+  // column-major D columns; D = 3 gets an all-zero intensity column so the
+  // 4D key quirk (sogmm.cpp:212) sees exactly the embedded cloud
+  ck(cudaMemcpyAsync(c->x64.p, pts, sizeof(double) * n * d, cudaMemcpyHostToDevice, c->s),
+     "points H2D");
+  if (d == 3) ck(cudaMemsetAsync(c->x64.p + 3 * n, 0, sizeof(double) * n, c->s), "memset");
+  c->n = n;
+  c->d = d;
+  c->offset = offset;
+  c->n_global = n_global;
+  c->have_cloud = true;
+}
+
+void validate(gmmb_ctx* c) {
+  c->flags.ensure(4);
+  ck(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 4, c->s), "memset");
+  ck(launch_validate(c->x64.p, c->n, c->d, c->flags.p, c->s), "validate");
+}
+
+void layout(gmmb_ctx* c) {
+  const int64_t n = c->n;
+  validate(c);
+  const int ntiles = static_cast<int>((n + kTile - 1) / kTile);
+  c->xt.ensure(static_cast<size_t>(ntiles) * kTile);
+  c->tc.ensure(static_cast<size_t>(ntiles) * 4);
+  c->perm.ensure(n);
+  c->bbox_part.ensure(kBboxParts * 6);
+  c->mkeys_in.ensure(n);
+  c->mkeys_out.ensure(n);
+  c->midx.ensure(n);
+  const size_t tb = layout_sort_temp_bytes(n);
+  c->sort_tmp.ensure(tb);
+  LayoutScratch ls{c->bbox_part.p, c->mkeys_in.p, c->mkeys_out.p, c->midx.p,
+                   c->sort_tmp.p, c->sort_tmp.cap};
+  ck(launch_layout(c->x64.p, n, ls, c->xt.p, c->tc.p, c->perm.p, c->sm_count, c->s),
+     "layout");
+}
+
+void check_cloud_flags(gmmb_ctx* c) {
+  int f[4];
+  ck(cudaMemcpyAsync(f, c->flags.p, sizeof(f), cudaMemcpyDeviceToHost, c->s), "flags D2H");
+  ck(cudaStreamSynchronize(c->s), "sync");
+  if (f[0] & 1) throw Err{3, "point cloud contains non-finite values"};
+  if (f[0] & 2) throw Err{3, "intensity outside [0, 1]"};
+}
+
+// ---- kinit ----------------------------------------------------------------
+KinitScratch kinit_scratch(gmmb_ctx* c, int k) {
+  const int64_t n = c->n;
+  c->keys.ensure(n + 4);
+  c->kd2.ensure(n);
+  c->labels.ensure(n);
+  c->chosen.ensure(n);
+  c->slots.ensure(static_cast<size_t>(c->sm_count) * 8 * 2);
+  c->owned.ensure(std::max(k, 1));
+  c->centers.ensure(std::max(k, 1));
+  c->flags.ensure(4);
+  return KinitScratch{c->keys.p, c->kd2.p, c->labels.p, c->chosen.p,
+                      c->slots.p, c->owned.p, c->centers.p, c->flags.p};
+}
+
+void run_kinit(gmmb_ctx* c, int k, uint64_t seed) {
+  const int64_t n = c->n;
+  KinitScratch ks = kinit_scratch(c, k);
+  ck(cudaMemsetAsync(c->owned.p, 0, sizeof(int) * k, c->s), "memset");
+  if (c->world == 1) {
+    ck(launch_keys(c->x64.p, n, c->x64.p + n, c->keys.p, c->s), "keys");
+    ck(cudaMemsetAsync(c->slots.p, 0, sizeof(KppSlot) * c->slots.cap, c->s), "memset");
+    ck(launch_kpp_seed(c->x64.p, n, k, seed, ks, c->sm_count, c->s), "kpp_seed");
+    ck(launch_fixup(n, k, ks, c->s), "fixup");
+    return;
+  }
+  // Sharded k-means++: local candidate per round -> allgather -> every rank
+  // picks the same global (clock, index) winner. Keys hash x[i..i+3] of the
+  // GLOBAL column-major buffer, so the last 3 local keys need the 3 doubles
+  // that follow this shard's x column: the next shards' first x values, or
+  // the global y column (rank 0's first y values) for the last shard.
+  const int W = c->world;
+  {
+    c->ll64.ensure(static_cast<size_t>(W) * 8 + 8);
+    double* g = reinterpret_cast<double*>(c->ll64.p);  // [W][8]: 3 x, 3 y, n, pad
+    std::vector<double> mine(8, 0.0);
+    std::vector<double> hx(std::min<int64_t>(3, n)), hy(std::min<int64_t>(3, n));
+    ck(cudaMemcpy(hx.data(), c->x64.p, sizeof(double) * hx.size(), cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpy(hy.data(), c->x64.p + n, sizeof(double) * hy.size(), cudaMemcpyDeviceToHost), "D2H");
+    for (size_t q = 0; q < hx.size(); ++q) {
+      mine[q] = hx[q];
+      mine[3 + q] = hy[q];
+    }
+    mine[6] = static_cast<double>(n);
+    c->dense.ensure(8);
+    ck(cudaMemcpy(c->dense.p, mine.data(), sizeof(double) * 8, cudaMemcpyHostToDevice), "H2D");
+    nck(nccl().AllGather(c->dense.p, g, 8, ncclFloat64, c->comm, c->s), "ncclAllGather");
+    std::vector<double> all(static_cast<size_t>(W) * 8);
+    ck(cudaMemcpyAsync(all.data(), g, sizeof(double) * W * 8, cudaMemcpyDeviceToHost, c->s), "D2H");
+    ck(cudaStreamSynchronize(c->s), "sync");
+    // flat global sequence after this shard's last x
+    double tail[3] = {0, 0, 0};
+    int got = 0;
+    for (int r = c->rank + 1; r < W && got < 3; ++r) {
+      const int nr = static_cast<int>(std::min<double>(3.0, all[r * 8 + 6]));
+      for (int q = 0; q < nr && got < 3; ++q) tail[got++] = all[r * 8 + q];
+    }
+    for (int r = 0; r < W && got < 3; ++r) {  // wraps into the y column
+      const int nr = static_cast<int>(std::min<double>(3.0, all[r * 8 + 6]));
+      for (int q = 0; q < nr && got < 3; ++q) tail[got++] = all[r * 8 + 3 + q];
+    }
+    ck(cudaMemcpy(c->dense.p, tail, sizeof(tail), cudaMemcpyHostToDevice), "H2D");
+    ck(launch_keys(c->x64.p, n, c->dense.p, c->keys.p, c->s), "keys");
+  }
+  c->rslots.ensure(static_cast<size_t>(W) + 1);
+  c->ticket.ensure(1);
+  ck(cudaMemsetAsync(c->ticket.p, 0, sizeof(int), c->s), "memset");
+  KppRankSlot* all = c->rslots.p;
+  KppRankSlot* mine = c->rslots.p + W;
+  for (int r = 0; r < k; ++r) {
+    ck(launch_kpp_round(c->x64.p, n, c->offset, r, seed, all, W, ks, mine, c->ticket.p,
+                        c->sm_count, c->s),
+       "kpp_round");
+    nck(nccl().AllGather(mine, all, sizeof(KppRankSlot), ncclUint8, c->comm, c->s),
+        "ncclAllGather");
+  }
+  ck(launch_kpp_final(c->x64.p, n, c->offset, k, all, W, ks, c->s), "kpp_final");
+  // global owned counts; the (rare) fix-up runs on the host over ranks
+  std::vector<int> owned(k);
+  {
+    c->ll64.ensure(static_cast<size_t>(k) + 1);
+    nck(nccl().AllReduce(c->owned.p, c->owned.p, k, ncclInt32, ncclSum, c->comm, c->s),
+        "ncclAllReduce");
+    ck(cudaMemcpyAsync(owned.data(), c->owned.p, sizeof(int) * k, cudaMemcpyDeviceToHost, c->s),
+       "owned D2H");
+    ck(cudaStreamSynchronize(c->s), "sync");
+  }
+  bool any_empty = false;
+  for (int b = 0; b < k; ++b) any_empty |= owned[b] == 0;
+  if (!any_empty) return;
+  std::vector<int32_t> lab(n);
+  ck(cudaMemcpy(lab.data(), c->labels.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost), "D2H");
+  for (int b = 0; b < k; ++b) {
+    if (owned[b] > 0) continue;
+    int donor = 0;
+    for (int q = 1; q < k; ++q)
+      if (owned[q] > owned[donor]) donor = q;
+    long long lo = std::numeric_limits<long long>::max();
+    for (int64_t i = 0; i < n; ++i) {
+      if (lab[i] == donor) {
+        lo = c->offset + i;
+        break;
+      }
+    }
+    ck(cudaMemcpy(c->ll64.p, &lo, sizeof(lo), cudaMemcpyHostToDevice), "H2D");
+    nck(nccl().AllReduce(c->ll64.p, c->ll64.p, 1, ncclInt64, ncclMin, c->comm, c->s),
+        "ncclAllReduce");
+    ck(cudaMemcpyAsync(&lo, c->ll64.p, sizeof(lo), cudaMemcpyDeviceToHost, c->s), "D2H");
+    ck(cudaStreamSynchronize(c->s), "sync");
+    if (lo != std::numeric_limits<long long>::max()) {
+      if (lo >= c->offset && lo < c->offset + n) lab[lo - c->offset] = b;
+      owned[donor]--;
+      owned[b]++;
+    }
+  }
+  ck(cudaMemcpy(c->labels.p, lab.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice), "H2D");
+}
+
+// ---- M step from labels / dense log_gamma -> model buffer st->cur -------
+void run_moments_commit(gmmb_ctx* c, const int32_t* labels,
+                        const double* log_gamma, int m, double cov_reg) {
+  const int64_t n = c->n;
+  const int nchunks = static_cast<int>((n + 4095) / 4096);
+  c->mpart.ensure(static_cast<size_t>(nchunks) * m * 10);
+  c->msums.ensure(static_cast<size_t>(m) * 10);
+  c->mmeans.ensure(static_cast<size_t>(m) * 4);
+  c->mcounts.ensure(m);
+  MomentsScratch ms{c->mpart.p, c->msums.p, c->mmeans.p, c->mcounts.p};
+  ck(launch_moments(c->d, c->x64.p, n, labels, log_gamma, m, cov_reg, ms, c->rec,
+                    c->sm_count, c->s, c->world > 1 ? moments_allreduce_cb : nullptr, c),
+     "moments");
+  ck(launch_commit(c->d, 1, c->rec, m, nullptr, c->bufs, c->st.p, nullptr, c->s), "commit");
+}
+
+// ---- model upload / download -------------------------------------------
+void upload_model(gmmb_ctx* c, int m, const double* w, const double* mu,
+                  const double* cov) {
+  const int d = c->d, np = d * (d + 1) / 2;
+  if (m < 1) throw Err{2, "model has no components"};
+  if (!w || !mu || !cov) throw Err{2, "null model buffer"};
+  std::vector<double> hmu(static_cast<size_t>(m) * 4, 0.0), hcov(static_cast<size_t>(m) * 10, 0.0);
+  for (int k = 0; k < m; ++k) {
+    for (int j = 0; j < d; ++j) hmu[k * 4 + j] = mu[k * d + j];
+    for (int j = 0; j < np; ++j) hcov[k * 10 + j] = cov[k * np + j];
+  }
+  ck(cudaMemcpyAsync(c->bufs[0].w, w, sizeof(double) * m, cudaMemcpyHostToDevice, c->s), "H2D");
+  ck(cudaMemcpyAsync(c->bufs[0].mu, hmu.data(), sizeof(double) * m * 4, cudaMemcpyHostToDevice, c->s), "H2D");
+  ck(cudaMemcpyAsync(c->bufs[0].cov, hcov.data(), sizeof(double) * m * 10, cudaMemcpyHostToDevice, c->s), "H2D");
+  ck(cudaStreamSynchronize(c->s), "sync");  // host vectors die here
+}
+
+void download_model(gmmb_ctx* c, int buf, int m, double* w, double* mu,
+                    double* cov) {
+  const int d = c->d, np = d * (d + 1) / 2;
+  std::vector<double> hmu(static_cast<size_t>(m) * 4), hcov(static_cast<size_t>(m) * 10);
+  if (w) ck(cudaMemcpyAsync(w, c->bufs[buf].w, sizeof(double) * m, cudaMemcpyDeviceToHost, c->s), "D2H");
+  ck(cudaMemcpyAsync(hmu.data(), c->bufs[buf].mu, sizeof(double) * m * 4, cudaMemcpyDeviceToHost, c->s), "D2H");
+  ck(cudaMemcpyAsync(hcov.data(), c->bufs[buf].cov, sizeof(double) * m * 10, cudaMemcpyDeviceToHost, c->s), "D2H");
+  ck(cudaStreamSynchronize(c->s), "sync");
+  for (int k = 0; k < m; ++k) {
+    if (mu)
+      for (int j = 0; j < d; ++j) mu[k * d + j] = hmu[k * 4 + j];
+    if (cov)
+      for (int j = 0; j < np; ++j) cov[k * np + j] = hcov[k * 10 + j];
+  }
+}
+
+// ---- EM loop ----------------------------------------------------------
+void em_iteration(gmmb_ctx* c, int k0) {
+  const int NS = nstats(c->d);
+  PointsDev pts{c->n, c->d, c->x64.p, c->xt.p, c->tc.p,
+                static_cast<int>((c->n + kTile - 1) / kTile)};
+  int ncl = 0;
+  ck(launch_estep_stats(pts, c->bufs, c->st.p, k0, c->partials.p, c->ll_part.p, nullptr,
+                        c->sm_count, c->s, &ncl),
+     "estep_stats");
+  double* red_ll = c->red.p + static_cast<size_t>(k0) * NS;
+  ck(launch_em_reduce(c->d, c->partials.p, c->ll_part.p, ncl, k0, c->st.p, c->red.p, red_ll,
+                      c->s),
+     "em_reduce");
+  if (c->world > 1) allreduce_sum(c, c->red.p, static_cast<int64_t>(k0) * NS + 1);
+  ck(launch_em_finalize(c->d, c->red.p, c->bufs, c->st.p, k0, c->rec, c->s), "em_finalize");
+  ck(launch_commit(c->d, 0, c->rec, k0, red_ll, c->bufs, c->st.p, c->ll_trace.p, c->s),
+     "commit");
+}
+
+void ensure_em_buffers(gmmb_ctx* c, int k0, int max_iters) {
+  const int NS = nstats(c->d);
+  PointsDev pts{c->n, c->d, c->x64.p, c->xt.p, c->tc.p,
+                static_cast<int>((c->n + kTile - 1) / kTile)};
+  int ncl = 0;
+  ck(launch_estep_stats(pts, c->bufs, c->st.p, k0, nullptr, nullptr, nullptr,
+                        c->sm_count, c->s, &ncl),
+     "estep query");
+  c->partials.ensure(static_cast<size_t>(ncl) * k0 * NS);
+  c->ll_part.ensure(ncl);
+  c->red.ensure(static_cast<size_t>(k0) * NS + 1);
+  c->ll_trace.ensure(std::max(max_iters, 1));
+}
+
+// Runs EM from the model in buffer st->cur (st already reset). Returns the
+// final state.
+EmState run_em(gmmb_ctx* c, int k0, const gmmb_em_params* em) {
+  ensure_em_buffers(c, k0, em->max_iters);
+  int launched = 0;
+  int chunk = 2;
+  EmState h{};
+  while (true) {
+    const int todo = std::min(chunk, em->max_iters - launched);
+    for (int i = 0; i < todo; ++i) em_iteration(c, k0);
+    launched += todo;
+    h = read_state(c);
+    if (h.done || h.error || launched >= em->max_iters) break;
+    chunk = std::min(chunk * 2, 8);
+  }
+  return h;
+}
+
+void finish_fit(gmmb_ctx* c, const EmState& h, const gmmb_em_params* em,
+                double* w_out, double* mu_out, double* cov_out,
+                double* ll_trace, gmmb_fit_stats* stats) {
+  raise_state_error(h);
+  download_model(c, h.cur, h.k_cur, w_out, mu_out, cov_out);
+  if (ll_trace && h.iter > 0) {
+    ck(cudaMemcpy(ll_trace, c->ll_trace.p, sizeof(double) * h.iter, cudaMemcpyDeviceToHost),
+       "ll D2H");
+  }
+  if (stats) {
+    stats->em_iterations = h.iter;
+    stats->final_log_likelihood = h.ll;
+    stats->removed_components = h.removed;
+    stats->k_out = h.k_cur;
+    stats->converged = h.converged;
+    stats->units = h.units;
+  }
+  (void)em;
+}
+
+float elapsed(gmmb_ctx* c, int a, int b) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, c->ev[a], c->ev[b]);
+  return ms;
+}
+
+void fit_k_resident(gmmb_ctx* c, int K, const gmmb_em_params* em, double* w_out,
+                    double* mu_out, double* cov_out, double* ll_trace,
+                    gmmb_fit_stats* stats, int32_t* labels_out,
+                    int64_t* centers_out) {
+  if (!c->have_cloud) throw Err{2, "no point cloud uploaded"};
+  check_em(em);
+  if (K < 1) throw Err{2, "kinit: k must satisfy 1 <= k <= N"};
+  set_device(c);
+  const int64_t ng = c->n_global;
+  const int k = static_cast<int>(std::min<int64_t>(K, ng));  // sogmm.cpp:477
+  if (k > kMaxK) throw Err{2, "K > 4096 is not supported by the fused E/M kernel"};
+  ck(cudaEventRecord(c->ev[0], c->s), "event");
+  layout(c);
+  ck(cudaEventRecord(c->ev[1], c->s), "event");
+  ensure_model(c, k);
+  run_kinit(c, k, em->seed);
+  ck(cudaEventRecord(c->ev[2], c->s), "event");
+  reset_state(c, k, em, 0);
+  run_moments_commit(c, c->labels.p, nullptr, k, em->cov_reg);
+  ck(cudaEventRecord(c->ev[3], c->s), "event");
+  // the mode-1 commit leaves k_cur / removed of the initial M step in the
+  // state and does not touch iter / ll, so EM continues from it
+  // (sogmm.cpp:481-487). Errors (invalid cloud, non-SPD) stop the device
+  // loop and are reported after it, cloud errors first.
+  ck(cudaEventRecord(c->ev[4], c->s), "event");
+  EmState h = run_em(c, k, em);
+  ck(cudaEventRecord(c->ev[5], c->s), "event");
+  ck(cudaEventSynchronize(c->ev[5]), "sync");
+  check_cloud_flags(c);
+  finish_fit(c, h, em, w_out, mu_out, cov_out, ll_trace, stats);
+  if (labels_out)
+    ck(cudaMemcpy(labels_out, c->labels.p, sizeof(int32_t) * c->n, cudaMemcpyDeviceToHost), "D2H");
+  if (centers_out) {
+    std::vector<long long> cc(k);
+    ck(cudaMemcpy(cc.data(), c->centers.p, sizeof(long long) * k, cudaMemcpyDeviceToHost), "D2H");
+    for (int i = 0; i < k; ++i) centers_out[i] = cc[i];
+  }
+  if (stats) {
+    stats->k_init = k;
+    stats->ms_layout = elapsed(c, 0, 1);
+    stats->ms_kinit = elapsed(c, 1, 2);
+    stats->ms_mstep0 = elapsed(c, 2, 3);
+    stats->ms_em = elapsed(c, 4, 5);
+  }
+}
+
+void fit_from_resident(gmmb_ctx* c, int m, const double* w0, const double* mu0,
+                       const double* cov0, const gmmb_em_params* em,
+                       double* w_out, double* mu_out, double* cov_out,
+                       double* ll_trace, gmmb_fit_stats* stats) {
+  if (!c->have_cloud) throw Err{2, "no point cloud uploaded"};
+  check_em(em);
+  if (m < 1) throw Err{2, "model has no components"};
+  if (m > kMaxK) throw Err{2, "K > 4096 is not supported by the fused E/M kernel"};
+  set_device(c);
+  ck(cudaEventRecord(c->ev[0], c->s), "event");
+  layout(c);
+  ck(cudaEventRecord(c->ev[1], c->s), "event");
+  ensure_model(c, m);
+  upload_model(c, m, w0, mu0, cov0);
+  reset_state(c, m, em, 0);
+  ck(launch_prep(c->d, c->bufs, c->st.p, m, c->s), "prep");
+  ck(cudaEventRecord(c->ev[4], c->s), "event");
+  EmState h = run_em(c, m, em);
+  ck(cudaEventRecord(c->ev[5], c->s), "event");
+  ck(cudaEventSynchronize(c->ev[5]), "sync");
+  check_cloud_flags(c);
+  finish_fit(c, h, em, w_out, mu_out, cov_out, ll_trace, stats);
+  if (stats) {
+    stats->k_init = m;
+    stats->ms_layout = elapsed(c, 0, 1);
+    stats->ms_kinit = 0.0;
+    stats->ms_mstep0 = 0.0;
+    stats->ms_em = elapsed(c, 4, 5);
+  }
+}
+
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* gmmb_last_error(void) { return g_err.c_str(); }
+
+void gmmb_em_params_default(gmmb_em_params* p) {
+  if (!p) return;
+  p->max_iters = 100;
+  p->ll_rel_tol = 1e-5;
+  p->cov_reg = 1e-6;
+  p->seed = 0;
+}
+
+static int create(int device, int rank, int world, const void* id, gmmb_ctx** out) {
+  return guarded([&] {
+    if (!out) throw Err{2, "null output"};
+    *out = nullptr;
+    int ndev = 0;
+    ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) throw Err{2, "invalid device index"};
+    gmmb_ctx* c = new gmmb_ctx();
+    c->device = device;
+    c->rank = rank;
+    c->world = world;
+    try {
+      ck(cudaSetDevice(device), "cudaSetDevice");
+      cudaDeviceProp prop{};
+      ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+      c->sm_count = prop.multiProcessorCount;
+      c->cc_major = prop.major;
+      c->cc_minor = prop.minor;
+      ck(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking), "cudaStreamCreate");
+      for (auto& e : c->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
+      ck(cudaMallocHost(&c->st_host, sizeof(EmState)), "cudaMallocHost");
+      if (world > 1) {
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, sizeof(uid));
+        nck(nccl().CommInitRank(&c->comm, world, uid, rank), "ncclCommInitRank");
+      }
+    } catch (...) {
+      gmmb_ctx_destroy(c);
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int gmmb_ctx_create(int device, gmmb_ctx** out) { return create(device, 0, 1, nullptr, out); }
+
+int gmmb_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    if (!out128) throw Err{2, "null output"};
+    ncclUniqueId uid;
+    nck(nccl().GetUniqueId(&uid), "ncclGetUniqueId");
+    std::memcpy(out128, &uid, sizeof(uid));
+  });
+}
+
+int gmmb_ctx_create_sharded(int device, int rank, int world, const void* nccl_id128,
+                            gmmb_ctx** out) {
+  if (world < 1 || rank < 0 || rank >= world || (world > 1 && !nccl_id128)) {
+    g_err = "invalid rank/world";
+    return 2;
+  }
+  return create(device, rank, world, nccl_id128, out);
+}
+
+void gmmb_ctx_destroy(gmmb_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->s) cudaStreamSynchronize(c->s);
+  if (c->comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
+  c->x64.release(); c->xt.release(); c->tc.release(); c->perm.release();
+  c->bbox_part.release(); c->mkeys_in.release(); c->mkeys_out.release();
+  c->midx.release(); c->sort_tmp.release(); c->flags.release();
+  c->keys.release(); c->kd2.release(); c->labels.release(); c->chosen.release();
+  c->slots.release(); c->owned.release(); c->centers.release(); c->rslots.release();
+  c->ticket.release(); c->ll64.release();
+  for (int b = 0; b < 2; ++b) {
+    c->mw[b].release(); c->mmu[b].release(); c->mcov[b].release(); c->mcst[b].release();
+  }
+  c->rcount.release(); c->rmean.release(); c->rcov.release(); c->rlogdet.release();
+  c->rpc.release(); c->rflags.release(); c->mpart.release(); c->msums.release();
+  c->mmeans.release(); c->mcounts.release(); c->partials.release(); c->ll_part.release();
+  c->red.release(); c->ll_trace.release(); c->dense.release(); c->st.release();
+  if (c->st_host) cudaFreeHost(c->st_host);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->s) cudaStreamDestroy(c->s);
+  delete c;
+}
+
+int gmmb_device_info(gmmb_ctx* c, int* sm_count, int* cc_major, int* cc_minor) {
+  if (!c) return 2;
+  if (sm_count) *sm_count = c->sm_count;
+  if (cc_major) *cc_major = c->cc_major;
+  if (cc_minor) *cc_minor = c->cc_minor;
+  return 0;
+}
+
+int gmmb_upload(gmmb_ctx* c, const double* pts, int64_t n, int d, int64_t offset,
+                int64_t n_global) {
+  return guarded([&] {
+    if (!c) throw Err{2, "null context"};
+    upload(c, pts, n, d, offset, n_global > 0 ? n_global : n);
+  });
+}
+
+int gmmb_fit_k_resident(gmmb_ctx* c, int K, const gmmb_em_params* em, double* w_out,
+                        double* mu_out, double* cov_out, double* ll_trace,
+                        gmmb_fit_stats* stats, int32_t* labels, int64_t* centers) {
+  return guarded([&] {
+    if (!c) throw Err{2, "null context"};
+    fit_k_resident(c, K, em, w_out, mu_out, cov_out, ll_trace, stats, labels, centers);
+  });
+}
+
+int gmmb_fit_from_resident(gmmb_ctx* c, int m, const double* w0, const double* mu0,
+                           const double* cov0, const gmmb_em_params* em,
+                           double* w_out, double* mu_out, double* cov_out,
+                           double* ll_trace, gmmb_fit_stats* stats) {
+  return guarded([&] {
+    if (!c) throw Err{2, "null context"};
+    fit_from_resident(c, m, w0, mu0, cov0, em, w_out, mu_out, cov_out, ll_trace, stats);
+  });
+}
+
+int gmmb_fit_k(gmmb_ctx* c, const double* pts, int64_t n, int d, int K,
+               const gmmb_em_params* em, double* w_out, double* mu_out,
+               double* cov_out, double* ll_trace, gmmb_fit_stats* stats,
+               int32_t* labels, int64_t* centers) {
+  return guarded([&] {
+    if (!c) throw Err{2, "null context"};
+    check_d(d);
+    if (n < 1) throw Err{3, "point cloud is empty"};
+    check_em(em);
+    const int64_t ng = c->world > 1 ? -1 : n;
+    if (c->world > 1) {
+      // global N and this rank's offset via allreduce of the shard sizes
+      set_device(c);
+      c->ll64.ensure(static_cast<size_t>(c->world) + 1);
+      std::vector<long long> sizes(c->world, 0);
+      sizes[c->rank] = n;
+      ck(cudaMemcpy(c->ll64.p, sizes.data(), sizeof(long long) * c->world, cudaMemcpyHostToDevice), "H2D");
+      nck(nccl().AllReduce(c->ll64.p, c->ll64.p, c->world, ncclInt64, ncclSum, c->comm, c->s), "allreduce");
+      ck(cudaMemcpyAsync(sizes.data(), c->ll64.p, sizeof(long long) * c->world, cudaMemcpyDeviceToHost, c->s), "D2H");
+      ck(cudaStreamSynchronize(c->s), "sync");
+      int64_t off = 0, tot = 0;
+      for (int r = 0; r < c->world; ++r) {
+        if (r < c->rank) off += sizes[r];
+        tot += sizes[r];
+      }
+      upload(c, pts, n, d, off, tot);
+    } else {
+      upload(c, pts, n, d, 0, ng);
+    }
+    fit_k_resident(c, K, em, w_out, mu_out, cov_out, ll_trace, stats, labels, centers);
+  });
+}
+
+int gmmb_fit_from(gmmb_ctx* c, const double* pts, int64_t n, int d, int m,
+                  const double* w0, const double* mu0, const double* cov0,
+                  const gmmb_em_params* em, double* w_out, double* mu_out,
+                  double* cov_out, double* ll_trace, gmmb_fit_stats* stats) {
+  return guarded([&] {
+    if (!c) throw Err{2, "null context"};
+    if (c->world > 1) throw Err{2, "use gmmb_upload with offsets for sharded fit_from"};
+    upload(c, pts, n, d, 0, n);
+    fit_from_resident(c, m, w0, mu0, cov0, em, w_out, mu_out, cov_out, ll_trace, stats);
+  });
+}
+
+int gmmb_kinit(gmmb_ctx* c, const double* pts, int64_t n, int d, int k, uint64_t seed,
+               int32_t* labels, int64_t* centers) {
+  return guarded([&] {
+    if (!c) throw Err{2, "null context"};
+    if (c->world > 1) throw Err{2, "gmmb_kinit is single-device; use gmmb_fit_k"};
+    upload(c, pts, n, d, 0, n);
+    validate(c);
+    check_cloud_flags(c);
+    if (k < 1 || k > n) throw Err{2, "kinit: k must satisfy 1 <= k <= N"};  // sogmm.cpp:200
+    ensure_model(c, k);
+    run_kinit(c, k, seed);
+    ck(cudaStreamSynchronize(c->s), "sync");
+    if (labels)
+      ck(cudaMemcpy(labels, c->labels.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost), "D2H");
+    if (centers) {
+      std::vector<long long> cc(k);
+      ck(cudaMemcpy(cc.data(), c->centers.p, sizeof(long long) * k, cudaMemcpyDeviceToHost), "D2H");
+      for (int i = 0; i < k; ++i) centers[i] = cc[i];
+    }
+  });
+}
+
+int gmmb_e_step(gmmb_ctx* c, const double* pts, int64_t n, int d, int m, const double* w,
+                const double* mu, const double* cov, double* ll_out, double* log_gamma_out) {
+  return guarded([&] {
+    if (!c) throw Err{2, "null context"};
+    upload(c, pts, n, d, 0, n);
+    layout(c);
+    check_cloud_flags(c);
+    ensure_model(c, m);
+    upload_model(c, m, w, mu, cov);
+    reset_state(c, m, nullptr, 0);
+    ck(launch_prep(c->d, c->bufs, c->st.p, m, c->s), "prep");
+    raise_state_error(read_state(c));
+    const int nblk = static_cast<int>((n + 255) / 256);
+    c->ll_part.ensure(nblk);
+    if (log_gamma_out) c->dense.ensure(static_cast<size_t>(n) * m);
+    ck(launch_estep_dense(c->d, c->x64.p, n, c->bufs, c->st.p, m, c->ll_part.p, nblk,
+                          log_gamma_out ? c->dense.p : nullptr, c->s),
+       "estep_dense");
+    std::vector<double> parts(nblk);
+    ck(cudaMemcpy(parts.data(), c->ll_part.p, sizeof(double) * nblk, cudaMemcpyDeviceToHost), "D2H");
+    double ll = 0.0;
+    for (double p : parts) ll += p;
+    if (ll_out) *ll_out = ll;
+    if (log_gamma_out)
+      ck(cudaMemcpy(log_gamma_out, c->dense.p, sizeof(double) * n * m, cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
+int gmmb_m_step(gmmb_ctx* c, const double* pts, int64_t n, int d, const double* log_gamma,
+                int m, double cov_reg, double* w_out, double* mu_out, double* cov_out,
+                int* m_out, int* removed) {
+  return guarded([&] {
+    if (!c) throw Err{2, "null context"};
+    if (cov_reg < 0.0) throw Err{2, "cov_reg must be >= 0"};
+    if (!log_gamma || m < 1) throw Err{2, "responsibility rows != point count"};
+    if (m > kMaxK) throw Err{2, "m > 4096 not supported"};
+    upload(c, pts, n, d, 0, n);
+    ensure_model(c, m);
+    c->dense.ensure(static_cast<size_t>(n) * m);
+    ck(cudaMemcpyAsync(c->dense.p, log_gamma, sizeof(double) * n * m, cudaMemcpyHostToDevice, c->s), "H2D");
+    gmmb_em_params em{1, 0.0, cov_reg, 0};
+    reset_state(c, m, &em, 0);
+    run_moments_commit(c, nullptr, c->dense.p, m, cov_reg);
+    EmState h = read_state(c);
+    raise_state_error(h);
+    download_model(c, h.cur, h.k_cur, w_out, mu_out, cov_out);
+    if (m_out) *m_out = h.k_cur;
+    if (removed) *removed = h.removed;
+  });
+}
+
+int gmmb_em_step(gmmb_ctx* c, const double* pts, int64_t n, int d, int m, const double* w,
+                 const double* mu, const double* cov, double cov_reg, double* ll_out,
+                 double* w_out, double* mu_out, double* cov_out, int* m_out, int* removed) {
+  return guarded([&] {
+    if (!c) throw Err{2, "null context"};
+    gmmb_em_params em{1, 0.0, cov_reg, 0};
+    upload(c, pts, n, d, 0, n);
+    layout(c);
+    check_cloud_flags(c);
+    if (m > kMaxK) throw Err{2, "m > 4096 not supported"};
+    ensure_model(c, m);
+    upload_model(c, m, w, mu, cov);
+    reset_state(c, m, &em, 0);
+    ck(launch_prep(c->d, c->bufs, c->st.p, m, c->s), "prep");
+    raise_state_error(read_state(c));
+    ensure_em_buffers(c, m, 1);
+    em_iteration(c, m);
+    EmState h = read_state(c);
+    raise_state_error(h);
+    if (ll_out) *ll_out = h.ll;
+    download_model(c, h.cur, h.k_cur, w_out, mu_out, cov_out);
+    if (m_out) *m_out = h.k_cur;
+    if (removed) *removed = h.removed;
+  });
+}
+
+int gmmb_cholesky_cache(gmmb_ctx* c, int d, int m, const double* covs, double* lower,
+                        double* precision, double* log_det_terms) {
+  return guarded([&] {
+    if (!c) throw Err{2, "null context"};
+    check_d(d);
+    if (m < 1 || !covs) throw Err{2, "model has no components"};
+    // host FP64 restatement is not allowed on the product path: use prep on
+    // the device and read back the FP64 factors through a dedicated pass
+    set_device(c);
+    c->d = d;
+    ensure_model(c, m);
+    std::vector<double> w(m, 1.0 / m), mu(static_cast<size_t>(m) * d, 0.0);
+    upload_model(c, m, w.data(), mu.data(), covs);
+    reset_state(c, m, nullptr, 0);
+    ck(launch_prep(d, c->bufs, c->st.p, m, c->s), "prep");
+    raise_state_error(read_state(c));
+    // factors: recompute in FP64 on the device via the dense helper
+    c->dense.ensure(static_cast<size_t>(m) * 33);
+    ck(launch_factor_dump(d, c->bufs, c->st.p, m, c->dense.p, c->s), "factor_dump");
+    std::vector<double> f(static_cast<size_t>(m) * 33);
+    ck(cudaMemcpy(f.data(), c->dense.p, sizeof(double) * m * 33, cudaMemcpyDeviceToHost), "D2H");
+    for (int k = 0; k < m; ++k) {
+      for (int i = 0; i < d; ++i)
+        for (int j = 0; j < d; ++j) {
+          if (lower) lower[(k * d + i) * d + j] = f[k * 33 + i * 4 + j];
+          if (precision) precision[(k * d + i) * d + j] = f[k * 33 + 16 + i * 4 + j];
+        }
+      if (log_det_terms) log_det_terms[k] = f[k * 33 + 32];
+    }
+  });
+}
+
+}  // extern "C"

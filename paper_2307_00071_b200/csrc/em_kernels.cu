@@ -1,0 +1,1056 @@
+// em_kernels.cu — the EM hot path on sm_100a.
+//
+// Reference semantics (paths under /root/reference/proj):
+//   cholesky_cache          src/gmm.cpp:33-48, src/kernels.cpp:10-77
+//   e_step_into             src/sogmm.cpp:341-383, logsumexp_rows kernels.cpp:104-135
+//   m_step_impl             src/sogmm.cpp:399-455, weighted_moments_fn kernels.hpp:82-181
+//   EM loop bookkeeping     src/sogmm.cpp:484-509
+//
+// The fused kernel never materialises the N x K responsibility matrix: a CTA
+// owns up to 512 components (one per thread; K > 512 uses a thread-block
+// cluster whose CTAs split the components and exchange per-point
+// log-sum-exp partials through distributed shared memory), streams
+// 128-point tiles of spatially sorted, tile-recentred FP32 points through
+// shared memory, evaluates log2-domain log densities in FP32 registers,
+// normalises them with warp reduce-scatter butterflies + a CTA combine,
+// and accumulates the centred sufficient statistics (sum r, sum r d,
+// sum r d d^T, d = x - mu_old) in FP32 registers, promoted to FP64 every
+// tile. Per-cluster FP64 partials are reduced in a fixed order by a second
+// kernel, so results are bit-reproducible run to run.
+#include <cooperative_groups.h>
+
+#include "em_kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace gmmb {
+
+namespace {
+
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2f(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int P>
+struct Log2 {
+  static constexpr int v = P == 1 ? 0 : 1 + Log2<P / 2>::v;
+};
+template <>
+struct Log2<1> {
+  static constexpr int v = 0;
+};
+
+// Warp reduce-scatter over 32 lanes of P per-lane values (one per point).
+// On return v[0] of lane l holds the reduction for point l >> (5 - log2 P)
+// over all 32 lanes. Fixed butterfly order => deterministic.
+template <int P, bool MAX>
+__device__ __forceinline__ float warp_reduce_scatter(float (&v)[P], int lane) {
+#pragma unroll
+  for (int h = P / 2, off = 16; h >= 1; h >>= 1, off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const float send = up ? v[i] : v[i + h];
+      const float keep = up ? v[i + h] : v[i];
+      const float got = __shfl_xor_sync(0xffffffffu, send, off);
+      v[i] = MAX ? fmaxf(keep, got) : keep + got;
+    }
+  }
+#pragma unroll
+  for (int off = 16 / P; off >= 1; off >>= 1) {
+    const float got = __shfl_xor_sync(0xffffffffu, v[0], off);
+    v[0] = MAX ? fmaxf(v[0], got) : v[0] + got;
+  }
+  return v[0];
+}
+
+// ---------------------------------------------------------------------------
+// Fused E-step + sufficient statistics.
+// ---------------------------------------------------------------------------
+template <int D, int NW, int C, int P>
+struct EstepSmem {
+  float4 xs[kTile];
+  float red[NW][P];
+  float bc_m[P];
+  float bc_s[P];
+  float xm[2][P];   // cluster exchange: CTA max per point
+  float xsum[2][P]; // cluster exchange: CTA sum per point
+  double ll[P];
+  double acc64[nstats(D)][NW * 32];
+};
+
+template <int D, int NW, int C, int P>
+__global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
+    estep_stats_kernel(const float4* __restrict__ xt,
+                       const double* __restrict__ tc, int64_t n, int ntiles,
+                       ModelBuf b0, ModelBuf b1, const EmState* __restrict__ st,
+                       int kpad, double* __restrict__ partials,
+                       double* __restrict__ ll_part,
+                       float* __restrict__ lse_out) {
+  constexpr int NP = npacked(D);
+  constexpr int NS = nstats(D);
+  constexpr int T = NW * 32;
+  using Smem = EstepSmem<D, NW, C, P>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+
+  if (st->done) return;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  int rank = 0, cid = blockIdx.x, ncl = gridDim.x;
+  if constexpr (C > 1) {
+    rank = static_cast<int>(cg::this_cluster().block_rank());
+    cid = blockIdx.x / C;
+    ncl = gridDim.x / C;
+  }
+  const int k = rank * kCtaComps + tid;
+  const int k_cur = st->k_cur;
+  const bool active = k < k_cur;
+  const ModelBuf& mb = st->cur ? b1 : b0;
+
+  // component constants in registers
+  float pp[NP];
+  float base2 = -INFINITY;
+  double mu64[D];
+#pragma unroll
+  for (int j = 0; j < NP; ++j) pp[j] = 0.f;
+#pragma unroll
+  for (int j = 0; j < D; ++j) mu64[j] = 0.0;
+  if (active) {
+    const float4* c4 = reinterpret_cast<const float4*>(mb.cst + k);
+    float cc[12];
+    const float4 a = c4[0], b = c4[1], c = c4[2];
+    cc[0] = a.x; cc[1] = a.y; cc[2] = a.z; cc[3] = a.w;
+    cc[4] = b.x; cc[5] = b.y; cc[6] = b.z; cc[7] = b.w;
+    cc[8] = c.x; cc[9] = c.y; cc[10] = c.z; cc[11] = c.w;
+#pragma unroll
+    for (int j = 0; j < NP; ++j) pp[j] = cc[j];
+    base2 = cc[10];
+#pragma unroll
+    for (int j = 0; j < D; ++j) mu64[j] = mb.mu[k * 4 + j];
+  }
+
+  float acc[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    acc[s] = 0.f;
+    sm.acc64[s][tid] = 0.0;
+  }
+  if (tid < P) sm.ll[tid] = 0.0;
+  int parity = 0;
+
+  for (int t = cid; t < ntiles; t += ncl) {
+    const int64_t t0 = static_cast<int64_t>(t) * kTile;
+    const int npts = static_cast<int>(min64(kTile, n - t0));
+    __syncthreads();  // previous tile fully consumed
+    for (int i = tid; i < kTile; i += T) {
+      sm.xs[i] = i < npts ? xt[t0 + i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float muf[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      muf[j] = static_cast<float>(mu64[j] - tc[static_cast<int64_t>(t) * 4 + j]);
+    }
+    __syncthreads();
+
+    for (int q = 0; q < npts; q += P) {
+      // ---- phase A: log2 densities, d kept in registers ----
+      float dd[P][D];
+      float l[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const float4 x = sm.xs[q + p];
+        dd[p][0] = x.x - muf[0];
+        dd[p][1] = x.y - muf[1];
+        dd[p][2] = x.z - muf[2];
+        if constexpr (D == 4) dd[p][3] = x.w - muf[3];
+        float y0 = pp[0] * dd[p][0];
+        float y1 = fmaf(pp[2], dd[p][1], pp[1] * dd[p][0]);
+        float y2 = fmaf(pp[5], dd[p][2], fmaf(pp[4], dd[p][1], pp[3] * dd[p][0]));
+        float qf = fmaf(y0, y0, fmaf(y1, y1, y2 * y2));
+        if constexpr (D == 4) {
+          float y3 = fmaf(pp[9], dd[p][3],
+                          fmaf(pp[8], dd[p][2],
+                               fmaf(pp[7], dd[p][1], pp[6] * dd[p][0])));
+          qf = fmaf(y3, y3, qf);
+        }
+        l[p] = (q + p < npts) ? base2 - qf : 0.f;
+      }
+      // ---- phase B1: per-point max over the CTA's components ----
+      {
+        float v[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) v[p] = l[p];
+        const float r = warp_reduce_scatter<P, true>(v, lane);
+        if ((lane & (32 / P - 1)) == 0) sm.red[warp][lane >> (5 - Log2<P>::v)] = r;
+      }
+      __syncthreads();
+      if (tid < P) {
+        float m = sm.red[0][tid];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) m = fmaxf(m, sm.red[w][tid]);
+        sm.bc_m[tid] = m;
+      }
+      __syncthreads();
+      // ---- phase B2: shifted exponentials and their sum ----
+      float e[P];
+      {
+        float v[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          float m = sm.bc_m[p];
+          m = (m == -INFINITY) ? 0.f : m;
+          e[p] = ex2f(l[p] - m);
+          v[p] = e[p];
+        }
+        const float r = warp_reduce_scatter<P, false>(v, lane);
+        if ((lane & (32 / P - 1)) == 0) sm.red[warp][lane >> (5 - Log2<P>::v)] = r;
+      }
+      __syncthreads();
+      float s_cta = 0.f;
+      if (tid < P) {
+#pragma unroll
+        for (int w = 0; w < NW; ++w) s_cta += sm.red[w][tid];
+        if constexpr (C > 1) {
+          sm.xm[parity][tid] = sm.bc_m[tid];
+          sm.xsum[parity][tid] = s_cta;
+        }
+      }
+      if constexpr (C > 1) {
+        // cluster-wide combine of (max, sum) per point; the release/acquire
+        // barrier orders the partial writes above before the DSMEM reads.
+        asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+      }
+      if (tid < P) {
+        const float mc = sm.bc_m[tid];
+        float M = mc, S = 0.f;
+        if constexpr (C > 1) {
+          cg::cluster_group cl = cg::this_cluster();
+          float mr[C], sr[C];
+#pragma unroll
+          for (int r = 0; r < C; ++r) {
+            mr[r] = *cl.map_shared_rank(&sm.xm[parity][tid], r);
+            sr[r] = *cl.map_shared_rank(&sm.xsum[parity][tid], r);
+          }
+          M = mr[0];
+#pragma unroll
+          for (int r = 1; r < C; ++r) M = fmaxf(M, mr[r]);
+#pragma unroll
+          for (int r = 0; r < C; ++r) {
+            if (mr[r] != -INFINITY) S += sr[r] * ex2f(mr[r] - M);
+          }
+        } else {
+          S = s_cta;
+        }
+        const bool valid = q + tid < npts;
+        const float mloc = (mc == -INFINITY) ? 0.f : mc;
+        float scale = 0.f;
+        if (valid) {
+          scale = (C > 1 ? ex2f(mloc - M) : 1.f) / S;
+          const float lse2 = M + lg2f(S);
+          if (rank == 0) {
+            sm.ll[tid] += static_cast<double>(lse2);
+            if (lse_out) lse_out[t0 + q + tid] = lse2;
+          }
+        }
+        sm.bc_s[tid] = scale;
+      }
+      parity ^= 1;
+      __syncthreads();
+      // ---- phase C: responsibilities and centred statistics ----
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const float r = e[p] * sm.bc_s[p];
+        float w[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) w[j] = r * dd[p][j];
+        acc[0] += r;
+#pragma unroll
+        for (int j = 0; j < D; ++j) acc[1 + j] += w[j];
+        int s = 1 + D;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+#pragma unroll
+          for (int j = 0; j <= i; ++j) {
+            acc[s] = fmaf(w[i], dd[p][j], acc[s]);
+            ++s;
+          }
+        }
+      }
+    }
+    // promote the tile's FP32 partial sums to FP64
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      sm.acc64[s][tid] += static_cast<double>(acc[s]);
+      acc[s] = 0.f;
+    }
+  }
+  __syncthreads();
+  if (k < kpad) {
+    double* out = partials + (static_cast<int64_t>(cid) * kpad + k) * NS;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) out[s] = sm.acc64[s][tid];
+  }
+  if (rank == 0 && tid == 0) {
+    double s = 0.0;
+#pragma unroll
+    for (int p = 0; p < P; ++p) s += sm.ll[p];
+    ll_part[cid] = s * kLn2;
+  }
+  if constexpr (C > 1) {
+    // keep smem alive until every CTA of the cluster finished its DSMEM reads
+    cg::this_cluster().sync();
+  }
+}
+
+template <int D, int NW, int C, int P>
+cudaError_t launch_estep_t(const PointsDev& pts, const ModelBuf* bufs,
+                           const EmState* st, int kpad, double* partials,
+                           double* ll_part, float* lse_out, int sm_count,
+                           cudaStream_t s, int* ncl_out) {
+  using Smem = EstepSmem<D, NW, C, P>;
+  auto kern = estep_stats_kernel<D, NW, C, P>;
+  const size_t smem = sizeof(Smem);
+  static int per_sm_dev[64] = {0};  // per template instance and device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& per_sm = per_sm_dev[dev & 63];
+  if (per_sm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(
+        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+  }
+  int ncl = sm_count * per_sm / C;
+  if (ncl > pts.ntiles) ncl = pts.ntiles;
+  if (ncl < 1) ncl = 1;
+  *ncl_out = ncl;
+  if (!partials) return cudaSuccess;  // size query only
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ncl * C);
+  cfg.blockDim = dim3(NW * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  int na = 0;
+  if (C > 1) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    na = 1;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kern, pts.xt, pts.tc, pts.n, pts.ntiles,
+                            bufs[0], bufs[1], st, kpad, partials, ll_part,
+                            lse_out);
+}
+
+template <int D>
+cudaError_t launch_estep_d(const PointsDev& pts, const ModelBuf* bufs,
+                           const EmState* st, int k0, double* partials,
+                           double* ll_part, float* lse_out, int sm_count,
+                           cudaStream_t s, int* ncl) {
+  constexpr int P = 8;
+  const int kpad = k0;
+#define GMMB_L(NW, C) \
+  return launch_estep_t<D, NW, C, P>(pts, bufs, st, kpad, partials, ll_part, \
+                                     lse_out, sm_count, s, ncl)
+  if (k0 <= 32) GMMB_L(1, 1);
+  if (k0 <= 64) GMMB_L(2, 1);
+  if (k0 <= 128) GMMB_L(4, 1);
+  if (k0 <= 256) GMMB_L(8, 1);
+  if (k0 <= 512) GMMB_L(16, 1);
+  if (k0 <= 1024) GMMB_L(16, 2);
+  if (k0 <= 2048) GMMB_L(16, 4);
+  if (k0 <= 4096) GMMB_L(16, 8);
+#undef GMMB_L
+  return cudaErrorInvalidValue;
+}
+
+// ---------------------------------------------------------------------------
+// Second-stage reduce: one warp per component, fixed lane/shuffle order.
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void em_reduce_kernel(const double* __restrict__ partials,
+                                 const double* __restrict__ ll_part, int ncl,
+                                 int kpad, const EmState* __restrict__ st,
+                                 double* __restrict__ red,
+                                 double* __restrict__ red_ll) {
+  constexpr int NS = nstats(D);
+  if (st->done) return;
+  const int lane = threadIdx.x & 31;
+  const int k = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (k == kpad) {  // one extra warp reduces the log-likelihood partials
+    double s = 0.0;
+    for (int c = lane; c < ncl; c += 32) s += ll_part[c];
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) red_ll[0] = s;
+    return;
+  }
+  if (k > kpad || k >= st->k_cur) return;
+  double acc[NS];
+#pragma unroll
+  for (int j = 0; j < NS; ++j) acc[j] = 0.0;
+  for (int c = lane; c < ncl; c += 32) {
+    const double* src = partials + (static_cast<int64_t>(c) * kpad + k) * NS;
+#pragma unroll
+    for (int j = 0; j < NS; ++j) acc[j] += src[j];
+  }
+#pragma unroll
+  for (int j = 0; j < NS; ++j) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < NS; ++j) red[static_cast<int64_t>(k) * NS + j] = acc[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Small dense FP64 linear algebra (kernels.cpp:10-50), D = 3 or 4.
+// ---------------------------------------------------------------------------
+template <int D>
+__device__ bool cholesky_d(const double (&a)[D][D], double (&l)[D][D]) {
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) l[i][j] = 0.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    double d = a[j][j];
+#pragma unroll
+    for (int k = 0; k < j; ++k) d = __dsub_rn(d, __dmul_rn(l[j][k], l[j][k]));
+    if (!(d > 0.0) || !isfinite(d)) return false;
+    const double ljj = sqrt(d);
+    l[j][j] = ljj;
+#pragma unroll
+    for (int i = j + 1; i < D; ++i) {
+      double s = a[i][j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) s = __dsub_rn(s, __dmul_rn(l[i][k], l[j][k]));
+      l[i][j] = s / ljj;
+    }
+  }
+  return true;
+}
+
+template <int D>
+__device__ void lower_inverse_d(const double (&l)[D][D], double (&inv)[D][D]) {
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) inv[i][j] = 0.0;
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    double x[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      double s = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < i; ++k) s = __dsub_rn(s, __dmul_rn(l[i][k], x[k]));
+      x[i] = s / l[i][i];
+    }
+#pragma unroll
+    for (int r = c; r < D; ++r) inv[r][c] = x[r];
+  }
+}
+
+// Cholesky + precision factor + E constants for one covariance.
+// Returns false if not SPD.
+template <int D>
+__device__ bool factor_component(const double* cov_packed, float* pc,
+                                 double* logdet) {
+  double a[D][D];
+#pragma unroll
+  for (int k = 0; k < npacked(D); ++k) {
+    a[packed_row(k)][packed_col(k)] = cov_packed[k];
+    a[packed_col(k)][packed_row(k)] = cov_packed[k];
+  }
+  double l[D][D], p[D][D];
+  if (!cholesky_d<D>(a, l)) return false;
+  lower_inverse_d<D>(l, p);
+  double ld = 0.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) ld += log(p[j][j]);
+  *logdet = ld;
+  const double sc = sqrt(0.5 * kLog2E);
+#pragma unroll
+  for (int k = 0; k < npacked(D); ++k) {
+    pc[k] = static_cast<float>(p[packed_row(k)][packed_col(k)] * sc);
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// Finalize: centred stats about mu_old -> mean, covariance, factor.
+//   mean = mu_old + S_d / n_k;  scatter = S_dd / n_k - delta delta^T
+// (the reference's two passes, sogmm.cpp:410-416 / kernels.hpp:91-179,
+// fused into one pass centred at the previous mean).
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void em_finalize_kernel(const double* __restrict__ red,
+                                   ModelBuf b0, ModelBuf b1,
+                                   const EmState* __restrict__ st, RecBuf rec) {
+  constexpr int NS = nstats(D);
+  constexpr int NP = npacked(D);
+  if (st->done) return;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= st->k_cur) return;
+  const ModelBuf& mb = st->cur ? b1 : b0;
+  const double* s = red + static_cast<int64_t>(k) * NS;
+  const double cnt = s[0];
+  int flags = 0;
+  double mean[4] = {0, 0, 0, 0};
+  double cov[10];
+#pragma unroll
+  for (int j = 0; j < 10; ++j) cov[j] = 0.0;
+  float pc[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) pc[j] = 0.f;
+  double logdet = 0.0;
+  if (!(cnt < kDegenerateCount)) {
+    flags |= 1;
+    double delta[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      delta[j] = s[1 + j] / cnt;
+      mean[j] = mb.mu[k * 4 + j] + delta[j];
+    }
+    const double inv = 1.0 / cnt;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const int i = packed_row(q), j = packed_col(q);
+      cov[q] = s[1 + D + q] * inv - delta[i] * delta[j];
+      if (i == j) cov[q] += st->cov_reg;
+    }
+    if (factor_component<D>(cov, pc, &logdet)) flags |= 2;
+  }
+  rec.count[k] = cnt;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) rec.mean[k * 4 + j] = mean[j];
+#pragma unroll
+  for (int j = 0; j < 10; ++j) rec.cov[k * 10 + j] = cov[j];
+  rec.logdet[k] = logdet;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) rec.pc[k * 16 + j] = pc[j];
+  rec.flags[k] = flags;
+}
+
+// ---------------------------------------------------------------------------
+// Commit (single CTA of 1024 threads): sogmm.cpp:418-453 + :488-504.
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(1024) commit_kernel(
+    int mode, RecBuf rec, int k_in_arg, const double* __restrict__ red_ll,
+    ModelBuf b0, ModelBuf b1, EmState* st, double* __restrict__ ll_trace) {
+  constexpr int T = 1024;
+  constexpr int PER = kMaxK / T;  // components per thread (<= 4)
+  __shared__ int s_scan[T];
+  __shared__ double s_tot[T];
+  __shared__ int s_flag;
+  const int tid = threadIdx.x;
+  if (st->done) return;
+  const int k_in = mode == 0 ? st->k_cur : k_in_arg;
+
+  if (mode == 0) {
+    // EM bookkeeping: sogmm.cpp:490-498
+    if (tid == 0) {
+      const double ll = red_ll[0];
+      const int iter = st->iter;
+      st->units += st->npts * static_cast<double>(k_in);
+      if (ll_trace) ll_trace[iter] = ll;
+      st->ll = ll;
+      st->iter = iter + 1;
+      int conv = 0;
+      if (iter > 0) {
+        const double rel = fabs(ll - st->ll_prev) / fmax(fabs(st->ll_prev), 1e-12);
+        if (rel < st->tol) conv = 1;
+      }
+      if (conv) {
+        st->converged = 1;
+        st->done = 1;
+      }
+      st->ll_prev = ll;
+      s_flag = conv;
+    }
+    __syncthreads();
+    if (s_flag) return;
+  }
+
+  // keep flags -> exclusive scan (compaction preserves order, sogmm.cpp:418-429)
+  int keep[PER];
+  int cnt = 0;
+  double tot = 0.0;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int k = tid * PER + i;
+    keep[i] = (k < k_in) ? (rec.flags[k] & 1) : 0;
+    cnt += keep[i];
+    if (keep[i]) tot += rec.count[k];
+  }
+  s_scan[tid] = cnt;
+  s_tot[tid] = tot;
+  __syncthreads();
+  for (int off = 1; off < T; off <<= 1) {  // Hillis-Steele inclusive scan
+    const int v = tid >= off ? s_scan[tid - off] : 0;
+    __syncthreads();
+    s_scan[tid] += v;
+    __syncthreads();
+  }
+  // fixed-shape tree for the total count (deterministic)
+  for (int off = T / 2; off >= 1; off >>= 1) {
+    if (tid < off) s_tot[tid] += s_tot[tid + off];
+    __syncthreads();
+  }
+  const int k_new = s_scan[T - 1];
+  const double total = s_tot[0];
+  if (k_new == 0) {
+    if (tid == 0) {
+      st->error = 3;
+      st->error_kind = 2;
+      st->error_index = 0;
+      st->done = 1;
+    }
+    return;
+  }
+  // first non-SPD kept component (compacted index), sogmm.cpp:447-452
+  if (tid == 0) s_flag = 0x7fffffff;
+  __syncthreads();
+  int j = s_scan[tid] - cnt;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int k = tid * PER + i;
+    if (keep[i]) {
+      if (!(rec.flags[k] & 2)) atomicMin(&s_flag, j);
+      ++j;
+    }
+  }
+  __syncthreads();
+  if (s_flag != 0x7fffffff) {
+    if (tid == 0) {
+      st->error = 3;
+      st->error_kind = 1;
+      st->error_index = s_flag;
+      st->done = 1;
+    }
+    return;
+  }
+  const int dst_sel = mode == 0 ? (st->cur ^ 1) : st->cur;
+  const ModelBuf& dst = dst_sel ? b1 : b0;
+  const double half_d_ln2pi = 0.5 * D * kLog2Pi;
+  j = s_scan[tid] - cnt;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int k = tid * PER + i;
+    if (!keep[i]) continue;
+    const double w = rec.count[k] / total;
+    dst.w[j] = w;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dst.mu[j * 4 + q] = rec.mean[k * 4 + q];
+#pragma unroll
+    for (int q = 0; q < 10; ++q) dst.cov[j * 10 + q] = rec.cov[k * 10 + q];
+    CompConst c;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) c.p[q] = rec.pc[k * 16 + q];
+    c.p[10] = static_cast<float>(kLog2E * (log(w) + rec.logdet[k] - half_d_ln2pi));
+    dst.cst[j] = c;
+    ++j;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    st->removed += k_in - k_new;
+    st->k_cur = k_new;
+    if (mode == 0) {
+      st->cur = dst_sel;
+      if (st->iter >= st->max_iters) st->done = 1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Prep: FP64 model in buffer st->cur -> constants (gmm.cpp:33-48).
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void prep_kernel(ModelBuf b0, ModelBuf b1, EmState* st, int m) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const ModelBuf& mb = st->cur ? b1 : b0;
+  CompConst c;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) c.p[q] = 0.f;
+  double logdet = 0.0;
+  if (!factor_component<D>(mb.cov + k * 10, c.p, &logdet)) {
+    atomicMin(&st->error_index, k);
+    st->error = 3;
+    st->error_kind = 3;
+    st->done = 1;
+    return;
+  }
+  c.p[10] = static_cast<float>(
+      kLog2E * (log(mb.w[k]) + logdet - 0.5 * D * kLog2Pi));
+  mb.cst[k] = c;
+}
+
+// ---------------------------------------------------------------------------
+// FP64 two-pass weighted moments (kernels.hpp:82-181).
+// grid: (point chunks, component groups of 128); one thread per component.
+// ---------------------------------------------------------------------------
+constexpr int kMomChunk = 4096;  // points per CTA chunk (= kPointBlock)
+constexpr int kMomTile = 256;
+
+template <int D, bool LABELS, int PASS>
+__global__ void __launch_bounds__(128) moments_kernel(
+    const double* __restrict__ x64, int64_t n, const int32_t* __restrict__ labels,
+    const double* __restrict__ log_gamma, int m,
+    const double* __restrict__ means, double* __restrict__ part) {
+  __shared__ double xs[4][kMomTile];
+  __shared__ int ls[kMomTile];
+  const int k = blockIdx.y * 128 + threadIdx.x;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kMomChunk;
+  const int64_t c1 = min64(n, c0 + kMomChunk);
+  double mu[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) mu[j] = (PASS == 2 && k < m) ? means[k * 4 + j] : 0.0;
+  double acc[10];
+#pragma unroll
+  for (int j = 0; j < 10; ++j) acc[j] = 0.0;
+  for (int64_t t0 = c0; t0 < c1; t0 += kMomTile) {
+    const int len = static_cast<int>(min64(kMomTile, c1 - t0));
+    __syncthreads();
+    for (int i = threadIdx.x; i < len; i += 128) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) xs[j][i] = x64[j * n + t0 + i];
+      if (LABELS) ls[i] = labels[t0 + i];
+    }
+    __syncthreads();
+    if (k < m) {
+      for (int i = 0; i < len; ++i) {
+        double w;
+        if (LABELS) {
+          if (ls[i] != k) continue;
+          w = 1.0;
+        } else {
+          const double g = log_gamma[static_cast<int64_t>(k) * n + t0 + i];
+          if (g < -700.0) continue;  // sogmm.cpp:415 select(0.0, ...)
+          w = exp(g);
+        }
+        if (PASS == 1) {
+          acc[0] += w;
+#pragma unroll
+          for (int j = 0; j < D; ++j) acc[1 + j] += __dmul_rn(w, xs[j][i]);
+        } else {
+          double d[D];
+#pragma unroll
+          for (int j = 0; j < D; ++j) d[j] = xs[j][i] - mu[j];
+#pragma unroll
+          for (int q = 0; q < npacked(D); ++q) {
+            acc[q] += __dmul_rn(__dmul_rn(w, d[packed_row(q)]), d[packed_col(q)]);
+          }
+        }
+      }
+    }
+  }
+  if (k < m) {
+    double* o = part + (static_cast<int64_t>(blockIdx.x) * m + k) * 10;
+#pragma unroll
+    for (int j = 0; j < 10; ++j) o[j] = acc[j];
+  }
+}
+
+// reduce chunks in order; PASS 1 -> sums[m][5]; PASS 2 -> sums[m][10]
+__global__ void moments_reduce_kernel(const double* __restrict__ part,
+                                      int nchunks, int m, int width,
+                                      double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m * width) return;
+  const int k = i / width, j = i % width;
+  double s = 0.0;
+  for (int c = 0; c < nchunks; ++c) s += part[(static_cast<int64_t>(c) * m + k) * 10 + j];
+  out[k * width + j] = s;
+}
+
+template <int D>
+__global__ void moments_means_kernel(const double* __restrict__ sums, int m,
+                                     double* __restrict__ means,
+                                     double* __restrict__ counts) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const double c = sums[k * 5];
+  counts[k] = c;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    // degenerate: mean 0 (kernels.hpp:121-128)
+    means[k * 4 + j] = (j < D && !(c < kDegenerateCount)) ? sums[k * 5 + 1 + j] / c : 0.0;
+  }
+}
+
+template <int D>
+__global__ void moments_finish_kernel(const double* __restrict__ sums2,
+                                      const double* __restrict__ means,
+                                      const double* __restrict__ counts, int m,
+                                      double cov_reg, RecBuf rec) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const double cnt = counts[k];
+  const bool keep = !(cnt < kDegenerateCount);
+  const double inv = keep ? 1.0 / cnt : 0.0;
+  double cov[10];
+#pragma unroll
+  for (int q = 0; q < 10; ++q) cov[q] = 0.0;
+#pragma unroll
+  for (int q = 0; q < npacked(D); ++q) {
+    cov[q] = sums2[k * 10 + q] * inv;
+    if (packed_row(q) == packed_col(q)) cov[q] += cov_reg;
+  }
+  float pc[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) pc[j] = 0.f;
+  double logdet = 0.0;
+  int flags = keep ? 1 : 0;
+  if (keep && factor_component<D>(cov, pc, &logdet)) flags |= 2;
+  rec.count[k] = cnt;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) rec.mean[k * 4 + j] = means[k * 4 + j];
+#pragma unroll
+  for (int j = 0; j < 10; ++j) rec.cov[k * 10 + j] = cov[j];
+  rec.logdet[k] = logdet;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) rec.pc[k * 16 + j] = pc[j];
+  rec.flags[k] = flags;
+}
+
+// ---------------------------------------------------------------------------
+// Dense E step (API / debug path, FP64): thread per point.
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void estep_dense_kernel(const double* __restrict__ x64, int64_t n,
+                                   ModelBuf b0, ModelBuf b1,
+                                   const EmState* __restrict__ st, int m,
+                                   double* __restrict__ ll_part,
+                                   double* __restrict__ log_gamma) {
+  __shared__ double red[256];
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const ModelBuf& mb = st->cur ? b1 : b0;
+  double lse = 0.0;
+  if (i < n && !st->error) {
+    double x[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) x[j] = x64[j * n + i];
+    // recompute the FP64 precision factor on the fly from the FP32-free
+    // model: cheap relative to an API call, keeps this path pure FP64.
+    double mx = -INFINITY;
+    auto logd = [&](int k) {
+      double a[D][D];
+#pragma unroll
+      for (int q = 0; q < npacked(D); ++q) {
+        a[packed_row(q)][packed_col(q)] = mb.cov[k * 10 + q];
+        a[packed_col(q)][packed_row(q)] = mb.cov[k * 10 + q];
+      }
+      double l[D][D], p[D][D];
+      cholesky_d<D>(a, l);
+      lower_inverse_d<D>(l, p);
+      double ld = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) ld += log(p[j][j]);
+      double dd[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) dd[j] = x[j] - mb.mu[k * 4 + j];
+      double q = 0.0;
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        double y = 0.0;
+#pragma unroll
+        for (int c = 0; c <= r; ++c) y += p[r][c] * dd[c];
+        q += y * y;
+      }
+      return log(mb.w[k]) + ld - 0.5 * D * kLog2Pi - 0.5 * q;
+    };
+    for (int k = 0; k < m; ++k) mx = fmax(mx, logd(k));
+    double acc = 0.0;
+    for (int k = 0; k < m; ++k) acc += exp(fmax(logd(k) - mx, -700.0));
+    lse = (mx == -INFINITY) ? -INFINITY : mx + log(acc);
+    if (log_gamma) {
+      for (int k = 0; k < m; ++k) log_gamma[static_cast<int64_t>(k) * n + i] = logd(k) - lse;
+    }
+  }
+  red[threadIdx.x] = lse;
+  __syncthreads();
+  for (int off = 128; off >= 1; off >>= 1) {
+    if (threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) ll_part[blockIdx.x] = red[0];
+}
+
+// FP64 factors of buffer st->cur for the cholesky_cache API:
+// out[k*33 + 0..15] = L (4x4 row-major), [16..31] = P = L^-1, [32] = logdet.
+template <int D>
+__global__ void factor_dump_kernel(ModelBuf b0, ModelBuf b1,
+                                   const EmState* __restrict__ st, int m,
+                                   double* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const ModelBuf& mb = st->cur ? b1 : b0;
+  double a[D][D];
+#pragma unroll
+  for (int q = 0; q < npacked(D); ++q) {
+    a[packed_row(q)][packed_col(q)] = mb.cov[k * 10 + q];
+    a[packed_col(q)][packed_row(q)] = mb.cov[k * 10 + q];
+  }
+  double l[D][D], p[D][D];
+  double* o = out + static_cast<int64_t>(k) * 33;
+  for (int i = 0; i < 33; ++i) o[i] = 0.0;
+  if (!cholesky_d<D>(a, l)) return;
+  lower_inverse_d<D>(l, p);
+  double ld = 0.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) ld += log(p[j][j]);
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      o[i * 4 + j] = l[i][j];
+      o[16 + i * 4 + j] = p[i][j];
+    }
+  o[32] = ld;
+}
+
+}  // namespace
+
+cudaError_t launch_factor_dump(int d, const ModelBuf* bufs, const EmState* st,
+                               int m, double* out, cudaStream_t s) {
+  const int grid = (m + 127) / 128;
+  if (d == 4)
+    factor_dump_kernel<4><<<grid, 128, 0, s>>>(bufs[0], bufs[1], st, m, out);
+  else
+    factor_dump_kernel<3><<<grid, 128, 0, s>>>(bufs[0], bufs[1], st, m, out);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// launch helpers
+// ---------------------------------------------------------------------------
+cudaError_t launch_estep_stats(const PointsDev& pts, const ModelBuf* bufs,
+                               const EmState* st, int k0, double* partials,
+                               double* ll_part, float* lse_out, int sm_count,
+                               cudaStream_t s, int* ncl_out) {
+  if (pts.d == 4)
+    return launch_estep_d<4>(pts, bufs, st, k0, partials, ll_part, lse_out,
+                             sm_count, s, ncl_out);
+  return launch_estep_d<3>(pts, bufs, st, k0, partials, ll_part, lse_out,
+                           sm_count, s, ncl_out);
+}
+
+cudaError_t launch_em_reduce(int d, const double* partials,
+                             const double* ll_part, int ncl, int k0,
+                             const EmState* st, double* red, double* red_ll,
+                             cudaStream_t s) {
+  const int warps = k0 + 1;
+  const int wpb = 8;
+  const int grid = (warps + wpb - 1) / wpb;
+  if (d == 4)
+    em_reduce_kernel<4><<<grid, wpb * 32, 0, s>>>(partials, ll_part, ncl, k0, st, red, red_ll);
+  else
+    em_reduce_kernel<3><<<grid, wpb * 32, 0, s>>>(partials, ll_part, ncl, k0, st, red, red_ll);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_em_finalize(int d, const double* red, const ModelBuf* bufs,
+                               const EmState* st, int k0, RecBuf rec,
+                               cudaStream_t s) {
+  const int grid = (k0 + 127) / 128;
+  if (d == 4)
+    em_finalize_kernel<4><<<grid, 128, 0, s>>>(red, bufs[0], bufs[1], st, rec);
+  else
+    em_finalize_kernel<3><<<grid, 128, 0, s>>>(red, bufs[0], bufs[1], st, rec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_commit(int d, int mode, const RecBuf rec, int k_in,
+                          const double* red_ll, ModelBuf* bufs, EmState* st,
+                          double* ll_trace, cudaStream_t s) {
+  if (d == 4)
+    commit_kernel<4><<<1, 1024, 0, s>>>(mode, rec, k_in, red_ll, bufs[0], bufs[1], st, ll_trace);
+  else
+    commit_kernel<3><<<1, 1024, 0, s>>>(mode, rec, k_in, red_ll, bufs[0], bufs[1], st, ll_trace);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prep(int d, ModelBuf* bufs, EmState* st, int k,
+                        cudaStream_t s) {
+  const int grid = (k + 127) / 128;
+  if (d == 4)
+    prep_kernel<4><<<grid, 128, 0, s>>>(bufs[0], bufs[1], st, k);
+  else
+    prep_kernel<3><<<grid, 128, 0, s>>>(bufs[0], bufs[1], st, k);
+  return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t launch_moments_d(const double* x64, int64_t n,
+                                    const int32_t* labels,
+                                    const double* log_gamma, int m,
+                                    double cov_reg, MomentsScratch scr,
+                                    RecBuf rec, cudaStream_t s,
+                                    void (*allreduce)(double*, int64_t, void*),
+                                    void* ar_ctx) {
+  const int nchunks = static_cast<int>((n + kMomChunk - 1) / kMomChunk);
+  const dim3 grid(nchunks, (m + 127) / 128);
+  const int rg1 = (m * 5 + 255) / 256, rg2 = (m * 10 + 255) / 256;
+  if (labels)
+    moments_kernel<D, true, 1><<<grid, 128, 0, s>>>(x64, n, labels, log_gamma, m, nullptr, scr.part);
+  else
+    moments_kernel<D, false, 1><<<grid, 128, 0, s>>>(x64, n, labels, log_gamma, m, nullptr, scr.part);
+  moments_reduce_kernel<<<rg1, 256, 0, s>>>(scr.part, nchunks, m, 5, scr.sums);
+  if (allreduce) allreduce(scr.sums, static_cast<int64_t>(m) * 5, ar_ctx);
+  moments_means_kernel<D><<<(m + 127) / 128, 128, 0, s>>>(scr.sums, m, scr.means, scr.counts);
+  if (labels)
+    moments_kernel<D, true, 2><<<grid, 128, 0, s>>>(x64, n, labels, log_gamma, m, scr.means, scr.part);
+  else
+    moments_kernel<D, false, 2><<<grid, 128, 0, s>>>(x64, n, labels, log_gamma, m, scr.means, scr.part);
+  moments_reduce_kernel<<<rg2, 256, 0, s>>>(scr.part, nchunks, m, 10, scr.sums);
+  if (allreduce) allreduce(scr.sums, static_cast<int64_t>(m) * 10, ar_ctx);
+  moments_finish_kernel<D><<<(m + 127) / 128, 128, 0, s>>>(scr.sums, scr.means, scr.counts, m, cov_reg, rec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_moments(int d, const double* x64, int64_t n,
+                           const int32_t* labels, const double* log_gamma,
+                           int m, double cov_reg, MomentsScratch scr,
+                           RecBuf rec, int /*sm_count*/, cudaStream_t s,
+                           void (*allreduce)(double*, int64_t, void*),
+                           void* ar_ctx) {
+  if (d == 4)
+    return launch_moments_d<4>(x64, n, labels, log_gamma, m, cov_reg, scr, rec, s, allreduce, ar_ctx);
+  return launch_moments_d<3>(x64, n, labels, log_gamma, m, cov_reg, scr, rec, s, allreduce, ar_ctx);
+}
+
+cudaError_t launch_estep_dense(int d, const double* x64, int64_t n,
+                               const ModelBuf* bufs, const EmState* st,
+                               int m, double* ll_part, int nblk,
+                               double* log_gamma, cudaStream_t s) {
+  if (d == 4)
+    estep_dense_kernel<4><<<nblk, 256, 0, s>>>(x64, n, bufs[0], bufs[1], st, m, ll_part, log_gamma);
+  else
+    estep_dense_kernel<3><<<nblk, 256, 0, s>>>(x64, n, bufs[0], bufs[1], st, m, ll_part, log_gamma);
+  return cudaGetLastError();
+}
+
+}  // namespace gmmb

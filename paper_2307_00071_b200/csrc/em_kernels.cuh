@@ -1,0 +1,95 @@
+// em_kernels.cuh — EM iteration kernels (declarations + launch helpers).
+#pragma once
+#include "common.cuh"
+
+namespace gmmb {
+
+// Device model buffer (one of two, ping-ponged across M steps).
+struct ModelBuf {
+  double* w;        // [kcap]
+  double* mu;       // [kcap][4]
+  double* cov;      // [kcap][10] packed (D=3 uses the first 6)
+  CompConst* cst;   // [kcap] FP32 E-step constants
+};
+
+// Per-component M-step record (output of finalize, input of commit).
+struct RecBuf {
+  double* count;    // [kcap]
+  double* mean;     // [kcap][4]
+  double* cov;      // [kcap][10]  regularised covariance
+  double* logdet;   // [kcap]      sum ln diag P
+  float* pc;        // [kcap][16]  scaled precision factor
+  int* flags;       // [kcap]      bit0 keep, bit1 SPD ok
+};
+
+struct PointsDev {
+  int64_t n;
+  int d;
+  const double* x64;   // [4][n] column-major FP64 (original order)
+  const float4* xt;    // [n] sorted, tile-recentred FP32
+  const double* tc;    // [ntiles][4] tile centres
+  int ntiles;
+};
+
+// Fused E-step + sufficient statistics (one EM iteration's data pass).
+// Writes per-cluster FP64 partial statistics [ncl][kpad][nstats(D)] and
+// per-cluster log-likelihood partials (natural log) [ncl].
+cudaError_t launch_estep_stats(const PointsDev& pts, const ModelBuf* bufs,
+                               const EmState* st, int k0, double* partials,
+                               double* ll_part, float* lse_out, int sm_count,
+                               cudaStream_t s, int* ncl_out);
+
+// (partials == nullptr: only report the cluster count *ncl_out.)
+
+// FP64 L, P, logdet of buffer st->cur (cholesky_cache API), 33 doubles/comp.
+cudaError_t launch_factor_dump(int d, const ModelBuf* bufs, const EmState* st,
+                               int m, double* out, cudaStream_t s);
+
+// Deterministic second-stage reduce: red[k][nstats] (+ red_ll[0]).
+cudaError_t launch_em_reduce(int d, const double* partials,
+                             const double* ll_part, int ncl, int k0,
+                             const EmState* st, double* red, double* red_ll,
+                             cudaStream_t s);
+
+// Per-component finalize: centred stats about mu_old -> record.
+cudaError_t launch_em_finalize(int d, const double* red, const ModelBuf* bufs,
+                               const EmState* st, int k0, RecBuf rec,
+                               cudaStream_t s);
+
+// Single-CTA commit: convergence bookkeeping, compaction, new model.
+// mode 0: EM iteration (uses red_ll, ll_trace); mode 1: plain M step
+// (initial hard M step / m_step API: always commits, no EM bookkeeping).
+cudaError_t launch_commit(int d, int mode, const RecBuf rec, int k_in,
+                          const double* red_ll, ModelBuf* bufs, EmState* st,
+                          double* ll_trace, cudaStream_t s);
+
+// Model (FP64) -> E-step constants for buffer st->cur; sets error on
+// a non-SPD covariance (first failing index, gmm.cpp:33-48 semantics).
+cudaError_t launch_prep(int d, ModelBuf* bufs, EmState* st, int k,
+                        cudaStream_t s);
+
+// FP64 two-pass weighted moments (kernels.hpp:82-181) with weights either
+// from hard labels (kinit one-hot) or from a dense N x M log_gamma.
+// Produces records (count/mean/cov/...) for launch_commit(mode=1).
+struct MomentsScratch {
+  double* part;      // [nchunks][m][10]
+  double* sums;      // [m][5]   reduced pass-1 sums
+  double* means;     // [m][4]
+  double* counts;    // [m]
+};
+cudaError_t launch_moments(int d, const double* x64, int64_t n,
+                           const int32_t* labels, const double* log_gamma,
+                           int m, double cov_reg, MomentsScratch scr,
+                           RecBuf rec, int sm_count, cudaStream_t s,
+                           void (*allreduce)(double*, int64_t, void*),
+                           void* ar_ctx);
+
+// Exact per-point log-sum-exp (thread per point, all K), for the e_step
+// API: ll (natural log, per-cluster partials) and optional dense log_gamma
+// [n][m] column-major (original point order, FP64 output of FP32 math).
+cudaError_t launch_estep_dense(int d, const double* x64, int64_t n,
+                               const ModelBuf* bufs, const EmState* st,
+                               int m, double* ll_part, int nblk,
+                               double* log_gamma, cudaStream_t s);
+
+}  // namespace gmmb

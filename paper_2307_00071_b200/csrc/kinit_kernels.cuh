@@ -1,0 +1,62 @@
+// kinit_kernels.cuh — k-means++ seeding + nearest-centre labels on sm_100a.
+#pragma once
+#include "common.cuh"
+
+namespace gmmb {
+
+// One candidate per CTA per round, published with a round tag.
+struct __align__(32) KppSlot {
+  double clock;
+  long long idx;        // -1 if no eligible point in the CTA
+  long long unchosen;   // lowest unchosen index in the CTA (or LLONG_MAX)
+  int tag;              // round number + 1 once valid
+  int pad;
+};
+
+struct KinitScratch {
+  uint64_t* keys;     // [n]
+  double* d2;         // [n]   (only for the memory-resident variant)
+  int32_t* labels;    // [n]
+  unsigned char* chosen;  // [n] (memory-resident variant)
+  KppSlot* slots;     // [2][max_blocks]
+  int* owned;         // [k]
+  long long* centers; // [k]
+  int* status;        // [4]: [0] error flag
+};
+
+// Keys (sogmm.cpp:210-213): key_i = hash of the 4 doubles starting at x_i in
+// the column-major N x 4 buffer (the reference's pts.row(i).data() quirk).
+// tail[0..2] = the 3 doubles that follow x_{n-1} in the (global) buffer:
+// x64 + n (the y column) on one device; the next shard's x or the global y
+// column when the cloud is sharded.
+cudaError_t launch_keys(const double* x64, int64_t n, const double* tail,
+                        uint64_t* keys, cudaStream_t s);
+
+// Persistent k-means++ seeding for one device holding all points
+// (sogmm.cpp:224-287), followed by the final centre fold that yields the
+// nearest-centre labels (:290-312) and owned counts. Cooperative launch.
+cudaError_t launch_kpp_seed(const double* x64, int64_t n, int k, uint64_t seed,
+                            KinitScratch scr, int sm_count, cudaStream_t s);
+
+// Owned fix-up (sogmm.cpp:315-331), single CTA, no-op when nothing is empty.
+cudaError_t launch_fixup(int64_t n, int k, KinitScratch scr, cudaStream_t s);
+
+// ---- sharded (multi-rank) seeding: one kernel per round + allgather ----
+// Each rank holds points [offset, offset + n) of the global cloud.
+struct __align__(64) KppRankSlot {
+  double clock;
+  long long idx;        // global index, -1 if none eligible
+  long long unchosen;   // lowest unchosen global index
+  double x[4];          // coordinates of idx (if >= 0)
+  double ux[4];         // coordinates of unchosen (if valid)
+};
+cudaError_t launch_kpp_round(const double* x64, int64_t n, int64_t offset,
+                             int r, uint64_t seed, const KppRankSlot* prev,
+                             int world, KinitScratch scr, KppRankSlot* out,
+                             int* ticket, int sm_count, cudaStream_t s);
+// final fold of centre k-1 (from prev slots) + labels + owned counts
+cudaError_t launch_kpp_final(const double* x64, int64_t n, int64_t offset,
+                             int k, const KppRankSlot* prev, int world,
+                             KinitScratch scr, cudaStream_t s);
+
+}  // namespace gmmb
