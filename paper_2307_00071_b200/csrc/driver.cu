@@ -134,6 +134,7 @@ struct gmmb_ctx {
   DevBuf<long long> centers;
   DevBuf<KppRankSlot> rslots;  // [world] gathered + [1] own
   DevBuf<int> ticket;
+  DevBuf<int> kstatus;
   DevBuf<long long> ll64;      // sharded fix-up scratch
   // model
   DevBuf<double> mw[2], mmu[2], mcov[2];
@@ -320,9 +321,10 @@ KinitScratch kinit_scratch(gmmb_ctx* c, int k) {
   c->slots.ensure(static_cast<size_t>(c->sm_count) * 8 * 2);
   c->owned.ensure(std::max(k, 1));
   c->centers.ensure(std::max(k, 1));
-  c->flags.ensure(4);
+  c->kstatus.ensure(8);
   return KinitScratch{c->keys.p, c->kd2.p, c->labels.p, c->chosen.p,
-                      c->slots.p, c->owned.p, c->centers.p, c->flags.p};
+                      c->slots.p, c->owned.p, c->centers.p, c->kstatus.p,
+                      reinterpret_cast<unsigned*>(c->kstatus.p + 4)};
 }
 
 void run_kinit(gmmb_ctx* c, int k, uint64_t seed) {
@@ -331,7 +333,7 @@ void run_kinit(gmmb_ctx* c, int k, uint64_t seed) {
   ck(cudaMemsetAsync(c->owned.p, 0, sizeof(int) * k, c->s), "memset");
   if (c->world == 1) {
     ck(launch_keys(c->x64.p, n, c->x64.p + n, c->keys.p, c->s), "keys");
-    ck(cudaMemsetAsync(c->slots.p, 0, sizeof(KppSlot) * c->slots.cap, c->s), "memset");
+    ck(cudaMemsetAsync(c->kstatus.p, 0, sizeof(int) * 8, c->s), "memset");
     ck(launch_kpp_seed(c->x64.p, n, k, seed, ks, c->sm_count, c->s), "kpp_seed");
     ck(launch_fixup(n, k, ks, c->s), "fixup");
     return;
@@ -711,7 +713,7 @@ void gmmb_ctx_destroy(gmmb_ctx* c) {
   c->midx.release(); c->sort_tmp.release(); c->flags.release();
   c->keys.release(); c->kd2.release(); c->labels.release(); c->chosen.release();
   c->slots.release(); c->owned.release(); c->centers.release(); c->rslots.release();
-  c->ticket.release(); c->ll64.release();
+  c->ticket.release(); c->kstatus.release(); c->ll64.release();
   for (int b = 0; b < 2; ++b) {
     c->mw[b].release(); c->mmu[b].release(); c->mcov[b].release(); c->mcst[b].release();
   }

@@ -4,28 +4,31 @@
 
 namespace gmmb {
 
-// One candidate per CTA per round, published with a round tag.
-struct __align__(32) KppSlot {
-  double clock;
-  long long idx;        // -1 if no eligible point in the CTA
-  long long unchosen;   // lowest unchosen index in the CTA (or LLONG_MAX)
-  int tag;              // round number + 1 once valid
-  int pad;
+// One candidate per CTA per round, published with a round tag (64 B).
+struct __align__(64) KppSlot {
+  double clock;         // exact FP64 clock of the CTA's best candidate
+  long long idx;        // its global index, -1 if none eligible
+  long long unchosen;   // lowest unchosen global index in the CTA
+  int tag;              // round + 1 once valid
+  int owner;            // grid thread id owning idx (or -1)
+  double cx[4];         // coordinates of idx
 };
 
 struct KinitScratch {
-  uint64_t* keys;     // [n]
-  double* d2;         // [n]   (only for the memory-resident variant)
+  uint64_t* keys;     // [n]  key * golden (pre-multiplied hash counter)
+  double* d2;         // [n]  (memory-resident variant / sharded)
   int32_t* labels;    // [n]
-  unsigned char* chosen;  // [n] (memory-resident variant)
+  unsigned char* chosen;  // [n] (memory-resident variant / sharded)
   KppSlot* slots;     // [2][max_blocks]
   int* owned;         // [k]
   long long* centers; // [k]
-  int* status;        // [4]: [0] error flag
+  int* status;        // [4]
+  unsigned* counter;  // [1] grid-barrier arrival counter (zeroed per launch)
 };
 
 // Keys (sogmm.cpp:210-213): key_i = hash of the 4 doubles starting at x_i in
 // the column-major N x 4 buffer (the reference's pts.row(i).data() quirk).
+// Stored pre-multiplied by the golden ratio constant (rng.hpp:26).
 // tail[0..2] = the 3 doubles that follow x_{n-1} in the (global) buffer:
 // x64 + n (the y column) on one device; the next shard's x or the global y
 // column when the cloud is sharded.
