@@ -58,6 +58,9 @@ typedef struct {
   double ms_mstep0;            /* initial hard-assignment M step */
   double ms_em;                /* EM loop */
   double units;                /* sum over E steps of N * K_t */
+  double ms_total;             /* layout start -> EM end (device) */
+  double ms_estep;             /* fused E-step kernel, executed iterations */
+  long long launches;          /* kernels this library enqueued (CUB excluded) */
 } gmmb_fit_stats;
 
 const char* gmmb_last_error(void);
@@ -143,6 +146,19 @@ int gmmb_em_step(gmmb_ctx* ctx, const double* pts, int64_t n, int d, int m,
 int gmmb_cholesky_cache(gmmb_ctx* ctx, int d, int m, const double* covs,
                         double* lower, double* precision,
                         double* log_det_terms);
+
+/* Sharded k-means++ keys (sogmm.cpp:210-213 hash 4 contiguous doubles of
+ * the GLOBAL column-major buffer): the 3 doubles that follow shard `rank`'s
+ * last x value. heads[r*8 + 0..2] = first 3 x of shard r, [3..5] = its first
+ * 3 y, [6] = its point count. Host-only helper (no device needed). */
+int gmmb_shard_key_tail(const double* heads, int world, int rank,
+                        double* tail3);
+
+/* FP32 FFMA throughput microbenchmark (the E step's roofline denominator):
+ * runs ~`ms_target` ms of dependent-free FFMA chains on every SM and
+ * returns TFLOP/s (2 flops per FFMA) and the elapsed device ms. */
+int gmmb_ffma_peak(gmmb_ctx* ctx, double ms_target, double* tflops,
+                   double* ms);
 
 /* ---- synthetic inputs (synthetic.cpp / ingest.cpp restated, host) ------
  * make_synthetic_frame + image_pair_to_cloud (synthetic.cpp:9-72,

@@ -63,7 +63,8 @@ class _FitStats(ctypes.Structure):
                 ("k_init", ctypes.c_int), ("converged", ctypes.c_int),
                 ("ms_layout", ctypes.c_double), ("ms_kinit", ctypes.c_double),
                 ("ms_mstep0", ctypes.c_double), ("ms_em", ctypes.c_double),
-                ("units", ctypes.c_double)]
+                ("units", ctypes.c_double), ("ms_total", ctypes.c_double),
+                ("ms_estep", ctypes.c_double), ("launches", ctypes.c_longlong)]
 
 
 _lib = None
@@ -113,6 +114,8 @@ _SIGS = {
                                        ctypes.c_uint64, _D]),
     "gmmb_jitter_cloud": (ctypes.c_int, [_D, ctypes.c_int64, ctypes.c_double,
                                          ctypes.c_uint64]),
+    "gmmb_shard_key_tail": (ctypes.c_int, [_D, ctypes.c_int, ctypes.c_int, _D]),
+    "gmmb_ffma_peak": (ctypes.c_int, [_V, ctypes.c_double, _D, _D]),
 }
 
 
@@ -232,6 +235,9 @@ class FitResult:
     ms_kinit: float = 0.0
     ms_mstep0: float = 0.0
     ms_em: float = 0.0
+    ms_total: float = 0.0
+    ms_estep: float = 0.0
+    launches: int = 0
     labels: Optional[np.ndarray] = None
     centers: Optional[np.ndarray] = None
 
@@ -286,6 +292,12 @@ class Context:
     def handle(self):
         return self._h
 
+    def ffma_peak(self, ms_target: float = 50.0) -> tuple[float, float]:
+        """Measured FP32 FFMA TFLOP/s on this device (and the ms it took)."""
+        tf, ms = ctypes.c_double(), ctypes.c_double()
+        _check(load().gmmb_ffma_peak(self._h, ms_target, ctypes.byref(tf), ctypes.byref(ms)))
+        return tf.value, ms.value
+
     # -- device-resident fits (bench "value": inputs already in HBM) ------
     def upload(self, points, offset: int = 0, n_global: int = 0) -> None:
         p, n, d = _points(points)
@@ -319,7 +331,8 @@ def _result(out, ll, st: _FitStats, lab=None, cen=None) -> FitResult:
     return FitResult(model, st.em_iterations, st.final_log_likelihood,
                      st.removed_components, st.k_init, bool(st.converged),
                      ll[:st.em_iterations].copy(), st.units, st.ms_layout,
-                     st.ms_kinit, st.ms_mstep0, st.ms_em, lab, cen)
+                     st.ms_kinit, st.ms_mstep0, st.ms_em, st.ms_total, st.ms_estep,
+                     st.launches, lab, cen)
 
 
 _default_ctx: Optional[Context] = None
@@ -470,6 +483,16 @@ def blob_cloud(centers, sigma: float, per_blob: int, seed: int = 0) -> np.ndarra
     buf = np.zeros(4 * k * per_blob)
     _check(load().gmmb_blob_cloud(_ptr(c), k, sigma, per_blob, seed, _ptr(buf)))
     return buf.reshape(4, k * per_blob).T.copy()
+
+
+def shard_key_tail(heads: np.ndarray, rank: int) -> np.ndarray:
+    """The 3 doubles following shard `rank`'s last x in the global
+    column-major buffer (sharded k-means++ keys, sogmm.cpp:210-213).
+    heads: (world, 8) = first 3 x, first 3 y, point count, pad per shard."""
+    h = np.ascontiguousarray(heads, dtype=np.float64)
+    out = np.zeros(3)
+    _check(load().gmmb_shard_key_tail(_ptr(h), h.shape[0], rank, _ptr(out)))
+    return out
 
 
 def jitter_cloud(points: np.ndarray, sigma: float, seed: int) -> np.ndarray:

@@ -108,6 +108,8 @@ struct gmmb_ctx {
   int cc_major = 0, cc_minor = 0;
   cudaStream_t s = nullptr;
   cudaEvent_t ev[8] = {};
+  std::vector<cudaEvent_t> ev_e;  // [2*i], [2*i+1] bracket the E kernel of iteration i
+  long long launches = 0;         // kernels of this library enqueued by the current call
   // sharding
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
@@ -168,6 +170,13 @@ int guarded(F&& f) {
 }
 
 void set_device(gmmb_ctx* c) { ck(cudaSetDevice(c->device), "cudaSetDevice"); }
+
+// Copies ordered on the context's (non-blocking) stream: a plain cudaMemcpy
+// runs on the legacy stream, which does not wait for work on c->s.
+void copy_sync(gmmb_ctx* c, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+  ck(cudaMemcpyAsync(dst, src, bytes, kind, c->s), "cudaMemcpyAsync");
+  ck(cudaStreamSynchronize(c->s), "cudaStreamSynchronize");
+}
 
 void check_d(int d) {
   if (d != 3 && d != 4) throw Err{2, "dimension must be 3 (xyz) or 4 (xyz+intensity)"};
@@ -301,6 +310,7 @@ void layout(gmmb_ctx* c) {
                    c->sort_tmp.p, c->sort_tmp.cap};
   ck(launch_layout(c->x64.p, n, ls, c->xt.p, c->tc.p, c->perm.p, c->sm_count, c->s),
      "layout");
+  c->launches += 4;  // bbox, morton, tile + validate (CUB's sort kernels not counted)
 }
 
 void check_cloud_flags(gmmb_ctx* c) {
@@ -336,6 +346,7 @@ void run_kinit(gmmb_ctx* c, int k, uint64_t seed) {
     ck(cudaMemsetAsync(c->kstatus.p, 0, sizeof(int) * 8, c->s), "memset");
     ck(launch_kpp_seed(c->x64.p, n, k, seed, ks, c->sm_count, c->s), "kpp_seed");
     ck(launch_fixup(n, k, ks, c->s), "fixup");
+    c->launches += 3;  // keys, seed (persistent), fixup
     return;
   }
   // Sharded k-means++: local candidate per round -> allgather -> every rank
@@ -349,31 +360,22 @@ void run_kinit(gmmb_ctx* c, int k, uint64_t seed) {
     double* g = reinterpret_cast<double*>(c->ll64.p);  // [W][8]: 3 x, 3 y, n, pad
     std::vector<double> mine(8, 0.0);
     std::vector<double> hx(std::min<int64_t>(3, n)), hy(std::min<int64_t>(3, n));
-    ck(cudaMemcpy(hx.data(), c->x64.p, sizeof(double) * hx.size(), cudaMemcpyDeviceToHost), "D2H");
-    ck(cudaMemcpy(hy.data(), c->x64.p + n, sizeof(double) * hy.size(), cudaMemcpyDeviceToHost), "D2H");
+    copy_sync(c, hx.data(), c->x64.p, sizeof(double) * hx.size(), cudaMemcpyDeviceToHost);
+    copy_sync(c, hy.data(), c->x64.p + n, sizeof(double) * hy.size(), cudaMemcpyDeviceToHost);
     for (size_t q = 0; q < hx.size(); ++q) {
       mine[q] = hx[q];
       mine[3 + q] = hy[q];
     }
     mine[6] = static_cast<double>(n);
     c->dense.ensure(8);
-    ck(cudaMemcpy(c->dense.p, mine.data(), sizeof(double) * 8, cudaMemcpyHostToDevice), "H2D");
+    copy_sync(c, c->dense.p, mine.data(), sizeof(double) * 8, cudaMemcpyHostToDevice);
     nck(nccl().AllGather(c->dense.p, g, 8, ncclFloat64, c->comm, c->s), "ncclAllGather");
     std::vector<double> all(static_cast<size_t>(W) * 8);
     ck(cudaMemcpyAsync(all.data(), g, sizeof(double) * W * 8, cudaMemcpyDeviceToHost, c->s), "D2H");
     ck(cudaStreamSynchronize(c->s), "sync");
-    // flat global sequence after this shard's last x
     double tail[3] = {0, 0, 0};
-    int got = 0;
-    for (int r = c->rank + 1; r < W && got < 3; ++r) {
-      const int nr = static_cast<int>(std::min<double>(3.0, all[r * 8 + 6]));
-      for (int q = 0; q < nr && got < 3; ++q) tail[got++] = all[r * 8 + q];
-    }
-    for (int r = 0; r < W && got < 3; ++r) {  // wraps into the y column
-      const int nr = static_cast<int>(std::min<double>(3.0, all[r * 8 + 6]));
-      for (int q = 0; q < nr && got < 3; ++q) tail[got++] = all[r * 8 + 3 + q];
-    }
-    ck(cudaMemcpy(c->dense.p, tail, sizeof(tail), cudaMemcpyHostToDevice), "H2D");
+    if (gmmb_shard_key_tail(all.data(), W, c->rank, tail) != 0) throw Err{2, "bad shard layout"};
+    copy_sync(c, c->dense.p, tail, sizeof(tail), cudaMemcpyHostToDevice);
     ck(launch_keys(c->x64.p, n, c->dense.p, c->keys.p, c->s), "keys");
   }
   c->rslots.ensure(static_cast<size_t>(W) + 1);
@@ -403,7 +405,7 @@ void run_kinit(gmmb_ctx* c, int k, uint64_t seed) {
   for (int b = 0; b < k; ++b) any_empty |= owned[b] == 0;
   if (!any_empty) return;
   std::vector<int32_t> lab(n);
-  ck(cudaMemcpy(lab.data(), c->labels.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost), "D2H");
+  copy_sync(c, lab.data(), c->labels.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost);
   for (int b = 0; b < k; ++b) {
     if (owned[b] > 0) continue;
     int donor = 0;
@@ -416,7 +418,7 @@ void run_kinit(gmmb_ctx* c, int k, uint64_t seed) {
         break;
       }
     }
-    ck(cudaMemcpy(c->ll64.p, &lo, sizeof(lo), cudaMemcpyHostToDevice), "H2D");
+    copy_sync(c, c->ll64.p, &lo, sizeof(lo), cudaMemcpyHostToDevice);
     nck(nccl().AllReduce(c->ll64.p, c->ll64.p, 1, ncclInt64, ncclMin, c->comm, c->s),
         "ncclAllReduce");
     ck(cudaMemcpyAsync(&lo, c->ll64.p, sizeof(lo), cudaMemcpyDeviceToHost, c->s), "D2H");
@@ -427,7 +429,7 @@ void run_kinit(gmmb_ctx* c, int k, uint64_t seed) {
       owned[b]++;
     }
   }
-  ck(cudaMemcpy(c->labels.p, lab.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice), "H2D");
+  copy_sync(c, c->labels.p, lab.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice);
 }
 
 // ---- M step from labels / dense log_gamma -> model buffer st->cur -------
@@ -444,6 +446,7 @@ void run_moments_commit(gmmb_ctx* c, const int32_t* labels,
                     c->sm_count, c->s, c->world > 1 ? moments_allreduce_cb : nullptr, c),
      "moments");
   ck(launch_commit(c->d, 1, c->rec, m, nullptr, c->bufs, c->st.p, nullptr, c->s), "commit");
+  c->launches += 8;
 }
 
 // ---- model upload / download -------------------------------------------
@@ -480,14 +483,18 @@ void download_model(gmmb_ctx* c, int buf, int m, double* w, double* mu,
 }
 
 // ---- EM loop ----------------------------------------------------------
-void em_iteration(gmmb_ctx* c, int k0) {
+void em_iteration(gmmb_ctx* c, int k0, int it) {
   const int NS = nstats(c->d);
   PointsDev pts{c->n, c->d, c->x64.p, c->xt.p, c->tc.p,
                 static_cast<int>((c->n + kTile - 1) / kTile)};
   int ncl = 0;
+  const bool timed = it >= 0 && static_cast<size_t>(2 * it + 1) < c->ev_e.size();
+  if (timed) ck(cudaEventRecord(c->ev_e[2 * it], c->s), "event");
   ck(launch_estep_stats(pts, c->bufs, c->st.p, k0, c->partials.p, c->ll_part.p, nullptr,
                         c->sm_count, c->s, &ncl),
      "estep_stats");
+  if (timed) ck(cudaEventRecord(c->ev_e[2 * it + 1], c->s), "event");
+  c->launches += 4;
   double* red_ll = c->red.p + static_cast<size_t>(k0) * NS;
   ck(launch_em_reduce(c->d, c->partials.p, c->ll_part.p, ncl, k0, c->st.p, c->red.p, red_ll,
                       c->s),
@@ -516,12 +523,17 @@ void ensure_em_buffers(gmmb_ctx* c, int k0, int max_iters) {
 // final state.
 EmState run_em(gmmb_ctx* c, int k0, const gmmb_em_params* em) {
   ensure_em_buffers(c, k0, em->max_iters);
+  while (c->ev_e.size() < static_cast<size_t>(2 * em->max_iters)) {
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "cudaEventCreate");
+    c->ev_e.push_back(e);
+  }
   int launched = 0;
   int chunk = 2;
   EmState h{};
   while (true) {
     const int todo = std::min(chunk, em->max_iters - launched);
-    for (int i = 0; i < todo; ++i) em_iteration(c, k0);
+    for (int i = 0; i < todo; ++i) em_iteration(c, k0, launched + i);
     launched += todo;
     h = read_state(c);
     if (h.done || h.error || launched >= em->max_iters) break;
@@ -536,8 +548,7 @@ void finish_fit(gmmb_ctx* c, const EmState& h, const gmmb_em_params* em,
   raise_state_error(h);
   download_model(c, h.cur, h.k_cur, w_out, mu_out, cov_out);
   if (ll_trace && h.iter > 0) {
-    ck(cudaMemcpy(ll_trace, c->ll_trace.p, sizeof(double) * h.iter, cudaMemcpyDeviceToHost),
-       "ll D2H");
+    copy_sync(c, ll_trace, c->ll_trace.p, sizeof(double) * h.iter, cudaMemcpyDeviceToHost);
   }
   if (stats) {
     stats->em_iterations = h.iter;
@@ -546,6 +557,13 @@ void finish_fit(gmmb_ctx* c, const EmState& h, const gmmb_em_params* em,
     stats->k_out = h.k_cur;
     stats->converged = h.converged;
     stats->units = h.units;
+    double me = 0.0;
+    for (int i = 0; i < h.iter && static_cast<size_t>(2 * i + 1) < c->ev_e.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, c->ev_e[2 * i], c->ev_e[2 * i + 1]);
+      me += ms;
+    }
+    stats->ms_estep = me;
   }
   (void)em;
 }
@@ -567,6 +585,7 @@ void fit_k_resident(gmmb_ctx* c, int K, const gmmb_em_params* em, double* w_out,
   const int64_t ng = c->n_global;
   const int k = static_cast<int>(std::min<int64_t>(K, ng));  // sogmm.cpp:477
   if (k > kMaxK) throw Err{2, "K > 4096 is not supported by the fused E/M kernel"};
+  c->launches = 0;
   ck(cudaEventRecord(c->ev[0], c->s), "event");
   layout(c);
   ck(cudaEventRecord(c->ev[1], c->s), "event");
@@ -587,10 +606,10 @@ void fit_k_resident(gmmb_ctx* c, int K, const gmmb_em_params* em, double* w_out,
   check_cloud_flags(c);
   finish_fit(c, h, em, w_out, mu_out, cov_out, ll_trace, stats);
   if (labels_out)
-    ck(cudaMemcpy(labels_out, c->labels.p, sizeof(int32_t) * c->n, cudaMemcpyDeviceToHost), "D2H");
+    copy_sync(c, labels_out, c->labels.p, sizeof(int32_t) * c->n, cudaMemcpyDeviceToHost);
   if (centers_out) {
     std::vector<long long> cc(k);
-    ck(cudaMemcpy(cc.data(), c->centers.p, sizeof(long long) * k, cudaMemcpyDeviceToHost), "D2H");
+    copy_sync(c, cc.data(), c->centers.p, sizeof(long long) * k, cudaMemcpyDeviceToHost);
     for (int i = 0; i < k; ++i) centers_out[i] = cc[i];
   }
   if (stats) {
@@ -599,6 +618,8 @@ void fit_k_resident(gmmb_ctx* c, int K, const gmmb_em_params* em, double* w_out,
     stats->ms_kinit = elapsed(c, 1, 2);
     stats->ms_mstep0 = elapsed(c, 2, 3);
     stats->ms_em = elapsed(c, 4, 5);
+    stats->ms_total = elapsed(c, 0, 5);
+    stats->launches = c->launches;
   }
 }
 
@@ -611,6 +632,7 @@ void fit_from_resident(gmmb_ctx* c, int m, const double* w0, const double* mu0,
   if (m < 1) throw Err{2, "model has no components"};
   if (m > kMaxK) throw Err{2, "K > 4096 is not supported by the fused E/M kernel"};
   set_device(c);
+  c->launches = 0;
   ck(cudaEventRecord(c->ev[0], c->s), "event");
   layout(c);
   ck(cudaEventRecord(c->ev[1], c->s), "event");
@@ -618,6 +640,7 @@ void fit_from_resident(gmmb_ctx* c, int m, const double* w0, const double* mu0,
   upload_model(c, m, w0, mu0, cov0);
   reset_state(c, m, em, 0);
   ck(launch_prep(c->d, c->bufs, c->st.p, m, c->s), "prep");
+  c->launches += 1;
   ck(cudaEventRecord(c->ev[4], c->s), "event");
   EmState h = run_em(c, m, em);
   ck(cudaEventRecord(c->ev[5], c->s), "event");
@@ -630,6 +653,8 @@ void fit_from_resident(gmmb_ctx* c, int m, const double* w0, const double* mu0,
     stats->ms_kinit = 0.0;
     stats->ms_mstep0 = 0.0;
     stats->ms_em = elapsed(c, 4, 5);
+    stats->ms_total = elapsed(c, 0, 5);
+    stats->launches = c->launches;
   }
 }
 
@@ -640,6 +665,35 @@ void fit_from_resident(gmmb_ctx* c, int m, const double* w0, const double* mu0,
 extern "C" {
 
 const char* gmmb_last_error(void) { return g_err.c_str(); }
+
+int gmmb_ffma_peak_impl(int sm_count, void* stream, double ms_target, double* tflops,
+                        double* ms);
+
+int gmmb_ffma_peak(gmmb_ctx* c, double ms_target, double* tflops, double* ms) {
+  return guarded([&] {
+    if (!c || !tflops || !ms) throw Err{2, "null argument"};
+    set_device(c);
+    if (gmmb_ffma_peak_impl(c->sm_count, c->s, ms_target, tflops, ms) != 0)
+      throw Err{1, "ffma microbenchmark failed"};
+  });
+}
+
+int gmmb_shard_key_tail(const double* heads, int world, int rank, double* tail3) {
+  if (!heads || !tail3 || world < 1 || rank < 0 || rank >= world) return 2;
+  // flat global column-major sequence after this shard's last x: the next
+  // shards' x values, then (wrapping) the global y column = rank 0's y...
+  int got = 0;
+  for (int r = rank + 1; r < world && got < 3; ++r) {
+    const int nr = static_cast<int>(std::min(3.0, heads[r * 8 + 6]));
+    for (int q = 0; q < nr && got < 3; ++q) tail3[got++] = heads[r * 8 + q];
+  }
+  for (int r = 0; r < world && got < 3; ++r) {
+    const int nr = static_cast<int>(std::min(3.0, heads[r * 8 + 6]));
+    for (int q = 0; q < nr && got < 3; ++q) tail3[got++] = heads[r * 8 + 3 + q];
+  }
+  for (; got < 3; ++got) tail3[got] = 0.0;  // N < 3 overall: z column
+  return 0;
+}
 
 void gmmb_em_params_default(gmmb_em_params* p) {
   if (!p) return;
@@ -724,6 +778,7 @@ void gmmb_ctx_destroy(gmmb_ctx* c) {
   if (c->st_host) cudaFreeHost(c->st_host);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->ev_e) cudaEventDestroy(e);
   if (c->s) cudaStreamDestroy(c->s);
   delete c;
 }
@@ -779,7 +834,7 @@ int gmmb_fit_k(gmmb_ctx* c, const double* pts, int64_t n, int d, int K,
       c->ll64.ensure(static_cast<size_t>(c->world) + 1);
       std::vector<long long> sizes(c->world, 0);
       sizes[c->rank] = n;
-      ck(cudaMemcpy(c->ll64.p, sizes.data(), sizeof(long long) * c->world, cudaMemcpyHostToDevice), "H2D");
+      copy_sync(c, c->ll64.p, sizes.data(), sizeof(long long) * c->world, cudaMemcpyHostToDevice);
       nck(nccl().AllReduce(c->ll64.p, c->ll64.p, c->world, ncclInt64, ncclSum, c->comm, c->s), "allreduce");
       ck(cudaMemcpyAsync(sizes.data(), c->ll64.p, sizeof(long long) * c->world, cudaMemcpyDeviceToHost, c->s), "D2H");
       ck(cudaStreamSynchronize(c->s), "sync");
@@ -821,10 +876,10 @@ int gmmb_kinit(gmmb_ctx* c, const double* pts, int64_t n, int d, int k, uint64_t
     run_kinit(c, k, seed);
     ck(cudaStreamSynchronize(c->s), "sync");
     if (labels)
-      ck(cudaMemcpy(labels, c->labels.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost), "D2H");
+      copy_sync(c, labels, c->labels.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost);
     if (centers) {
       std::vector<long long> cc(k);
-      ck(cudaMemcpy(cc.data(), c->centers.p, sizeof(long long) * k, cudaMemcpyDeviceToHost), "D2H");
+      copy_sync(c, cc.data(), c->centers.p, sizeof(long long) * k, cudaMemcpyDeviceToHost);
       for (int i = 0; i < k; ++i) centers[i] = cc[i];
     }
   });
@@ -849,12 +904,12 @@ int gmmb_e_step(gmmb_ctx* c, const double* pts, int64_t n, int d, int m, const d
                           log_gamma_out ? c->dense.p : nullptr, c->s),
        "estep_dense");
     std::vector<double> parts(nblk);
-    ck(cudaMemcpy(parts.data(), c->ll_part.p, sizeof(double) * nblk, cudaMemcpyDeviceToHost), "D2H");
+    copy_sync(c, parts.data(), c->ll_part.p, sizeof(double) * nblk, cudaMemcpyDeviceToHost);
     double ll = 0.0;
     for (double p : parts) ll += p;
     if (ll_out) *ll_out = ll;
     if (log_gamma_out)
-      ck(cudaMemcpy(log_gamma_out, c->dense.p, sizeof(double) * n * m, cudaMemcpyDeviceToHost), "D2H");
+      copy_sync(c, log_gamma_out, c->dense.p, sizeof(double) * n * m, cudaMemcpyDeviceToHost);
   });
 }
 
@@ -897,7 +952,7 @@ int gmmb_em_step(gmmb_ctx* c, const double* pts, int64_t n, int d, int m, const 
     ck(launch_prep(c->d, c->bufs, c->st.p, m, c->s), "prep");
     raise_state_error(read_state(c));
     ensure_em_buffers(c, m, 1);
-    em_iteration(c, m);
+    em_iteration(c, m, -1);
     EmState h = read_state(c);
     raise_state_error(h);
     if (ll_out) *ll_out = h.ll;
@@ -927,7 +982,7 @@ int gmmb_cholesky_cache(gmmb_ctx* c, int d, int m, const double* covs, double* l
     c->dense.ensure(static_cast<size_t>(m) * 33);
     ck(launch_factor_dump(d, c->bufs, c->st.p, m, c->dense.p, c->s), "factor_dump");
     std::vector<double> f(static_cast<size_t>(m) * 33);
-    ck(cudaMemcpy(f.data(), c->dense.p, sizeof(double) * m * 33, cudaMemcpyDeviceToHost), "D2H");
+    copy_sync(c, f.data(), c->dense.p, sizeof(double) * m * 33, cudaMemcpyDeviceToHost);
     for (int k = 0; k < m; ++k) {
       for (int i = 0; i < d; ++i)
         for (int j = 0; j < d; ++j) {

@@ -1,0 +1,107 @@
+"""The C ABI library loads on a CPU-only host and exports every symbol
+include/gmmb.h declares; host-only helpers (generators, shard key tails)
+work without a GPU; device calls fail loudly (no CPU fallback)."""
+import math
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared():
+    src = open(os.path.join(ROOT, "include", "gmmb.h")).read()
+    return sorted(set(re.findall(r"\b(gmmb_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_symbols_exported(gm):
+    names = declared()
+    assert len(names) >= 20
+    out = subprocess.run(["nm", "-D", "--defined-only", gm.lib_path()], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r" T (gmmb_\w+)", out))
+    missing = [n for n in names if n not in exported]
+    assert not missing, missing
+    lib = gm.load()
+    for n in names:
+        assert getattr(lib, n) is not None
+
+
+def test_library_is_sm100a(gm):
+    out = subprocess.run(["cuobjdump", "--list-elf", gm.lib_path()], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_gpu_fails_loudly(gm):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises((gm.IoError, ValueError)):
+        gm.Context(0)
+
+
+def test_synthetic_frame_facts(gm):
+    p = gm.synthetic_frame_cloud()
+    assert p.shape == (307200, 4)
+    assert (p[:, 2] == 3.0).sum() == 129048
+    assert np.allclose(p.min(0), [-1.8257142857, -1.3685714286, 0.707, 0.2235294118], atol=1e-9)
+    assert np.allclose(p.max(0), [1.8257142857, 0.3225266667, 3.0, 0.9490196078], atol=1e-9)
+    # pixel (cx, cy) ray principle: row-major pixel order, intensities k/255
+    assert np.allclose(p[:, 3] * 255, np.round(p[:, 3] * 255))
+
+
+def test_structured_scene_matches_python_restatement(gm):
+    from test_rng_keys import bits
+    n, seed, noise = 50, 1, 0.005
+    p = gm.structured_scene(n, seed, noise)
+
+    def uni(s, st, c):
+        return (bits(s, st, c) >> 11) * 2.0**-53
+
+    def upos(s, st, c):
+        return ((bits(s, st, c) >> 11) + 1) * 2.0**-53
+
+    def npair(s, st, c):
+        u1, u2 = upos(s, st, c), uni(s, st, c + 1)
+        r = math.sqrt(-2 * math.log(u1))
+        return r * math.cos(2 * math.pi * u2), r * math.sin(2 * math.pi * u2)
+
+    for i in range(n):
+        u, v = uni(seed, 11, i * 8), uni(seed, 11, i * 8 + 1)
+        nz0, nz1 = npair(seed, 12, i * 8 + 2)
+        nz2, _ = npair(seed, 12, i * 8 + 4)
+        if i % 3 == 0:
+            q = [2 * u - 1, 2 * v - 1, 0.0]
+        elif i % 3 == 1:
+            q = [0.0, 2 * u - 1, 1.2 * v]
+        else:
+            a = 2 * math.pi * u
+            q = [0.55 + 0.3 * math.cos(a), -0.35 + 0.3 * math.sin(a), 1.1 * v]
+        q = [q[0] + noise * nz0, q[1] + noise * nz1, q[2] + noise * nz2]
+        inten = min(max(0.5 + 0.3 * math.sin(4 * q[0]) + 0.2 * math.cos(3 * q[1] + q[2]), 0), 1)
+        assert np.allclose(p[i], q + [inten], rtol=0, atol=1e-14)
+
+
+@pytest.mark.parametrize("sizes", [[5, 7, 3], [1, 1, 9], [2, 1, 1, 6], [400, 400]])
+def test_shard_key_tail(gm, sizes):
+    rng = np.random.default_rng(len(sizes))
+    n = sum(sizes)
+    x = np.column_stack([rng.normal(size=(n, 3)), rng.random(n)])
+    flat = np.asfortranarray(x).ravel(order="F")
+    heads = np.zeros((len(sizes), 8))
+    off = 0
+    for r, m in enumerate(sizes):
+        k = min(3, m)
+        heads[r, :k] = x[off:off + k, 0]
+        heads[r, 3:3 + k] = x[off:off + k, 1]
+        heads[r, 6] = m
+        off += m
+    off = 0
+    for r, m in enumerate(sizes):
+        last = off + m - 1
+        assert np.array_equal(gm.shard_key_tail(heads, r), flat[last + 1:last + 4])
+        off += m

@@ -1,0 +1,241 @@
+"""CUDA path (through the C ABI) vs the FP64 oracle on identical inputs.
+
+Bars (BASELINE.json north_star): kinit centres/labels, iteration counts and
+K bit-exact; per-iteration ll within 1e-5 relative; weights / means /
+covariances within 1e-4 (normalised metrics, tests/parity.py).
+"""
+import numpy as np
+import pytest
+
+from parity import LL_TOL, assert_model_close, ll_err
+
+pytestmark = pytest.mark.gpu
+
+
+def frame(gm):
+    return gm.synthetic_frame_cloud()
+
+
+def fixed_init(orc, pts, k, cov_reg=1e-6, seed=0):
+    lab, cen = orc.kinit(pts, k, seed)
+    w, mu, cov, _ = orc.m_step_labels(pts, lab, k, cov_reg)
+    d = pts.shape[1]
+    return w, mu[:, :d].copy(), cov[:, :d * (d + 1) // 2].copy()
+
+
+# ---- kinit: bit-exact -------------------------------------------------------
+@pytest.mark.parametrize("k,seed", [(1, 0), (7, 3), (64, 0), (512, 0), (512, 5)])
+def test_kinit_frame_exact(gm, orc, ctx, k, seed):
+    p = frame(gm)
+    lab, cen = gm.kinit(p, k, seed, ctx=ctx)
+    rl, rc = orc.kinit(p, k, seed)
+    assert np.array_equal(cen, rc)
+    assert np.array_equal(lab, rl)
+
+
+def test_kinit_3d_scene_exact(gm, orc, ctx):
+    p = gm.structured_scene(60000, 4, 0.005)[:, :3] * 25 + np.array([100.0, -40.0, 0.0])
+    lab, cen = gm.kinit(p, 256, 0, ctx=ctx)
+    rl, rc = orc.kinit(p, 256, 0)
+    assert np.array_equal(cen, rc) and np.array_equal(lab, rl)
+
+
+def test_kinit_duplicates_fallback_and_fixup(gm, orc, ctx):
+    base = np.array([[0, 0, 0, 0.1], [1, 0, 0, 0.2], [0, 1, 0, 0.3], [0, 0, 1, 0.4],
+                     [1, 1, 1, 0.5]], float)
+    p = np.repeat(base, 40, axis=0)
+    lab, cen = gm.kinit(p, 8, 0, ctx=ctx)
+    rl, rc = orc.kinit(p, 8, 0)
+    assert np.array_equal(cen, rc) and np.array_equal(lab, rl)
+    assert np.all(np.bincount(lab, minlength=8) >= 1)
+
+
+def test_kinit_k_equals_n(gm, orc, ctx):
+    rng = np.random.default_rng(4)
+    p = np.column_stack([rng.normal(size=(300, 3)), rng.random(300)])
+    lab, cen = gm.kinit(p, 300, 1, ctx=ctx)
+    rl, rc = orc.kinit(p, 300, 1)
+    assert np.array_equal(cen, rc) and np.array_equal(lab, rl)
+
+
+def test_kinit_large_cloud_memory_variant(gm, orc, ctx):
+    """N beyond the register-resident seeding kernel (148*384*8 = 454,656)."""
+    p = gm.structured_scene(600000, 7, 0.005)
+    lab, cen = gm.kinit(p, 32, 0, ctx=ctx)
+    rl, rc = orc.kinit(p, 32, 0)
+    assert np.array_equal(cen, rc) and np.array_equal(lab, rl)
+
+
+# ---- one production EM step, teacher forced ----------------------------------
+@pytest.mark.parametrize("k", [32, 256, 512, 1024, 2048])
+def test_em_step_teacher_forced_frame(gm, orc, ctx, k):
+    p = frame(gm)
+    if k > 512:  # cluster path (K > 512); keep the oracle quick
+        p = p[::2].copy()
+    w, mu, cov = fixed_init(orc, p, k)
+    ll, m1, rm = gm.em_step(p, gm.Gmm(w, mu, cov), 1e-6, ctx=ctx)
+    lg, rll = orc.e_step(p, w, mu, cov)
+    rw, rmu, rcov, rrm = orc.m_step(p, lg, 1e-6)
+    assert abs(ll - rll) / abs(rll) < LL_TOL
+    assert rm == rrm
+    assert_model_close(m1.weights, m1.means, m1.covariances, rw, rmu, rcov, tol=1e-5)
+
+
+def test_em_step_3d_offset_scene(gm, orc, ctx):
+    """cfg4-like coordinates (x25, offset (100,-40,0) m) stress the FP32
+    recentring; D = 3 native kernels."""
+    p = gm.structured_scene(100000, 4, 0.005)[:, :3] * 25 + np.array([100.0, -40.0, 0.0])
+    w, mu, cov = fixed_init(orc, p, 128)
+    ll, m1, rm = gm.em_step(p, gm.Gmm(w, mu, cov), 1e-6, ctx=ctx)
+    r = orc.fit_from(p, w, mu, cov, max_iters=1, ll_rel_tol=0.0, cov_reg=1e-6)
+    assert abs(ll - r["final_ll"]) / abs(r["final_ll"]) < LL_TOL
+    assert_model_close(m1.weights, m1.means, m1.covariances, r["w"], r["mu"], r["cov"], tol=1e-5)
+
+
+def test_em_step_removes_degenerate_component(gm, orc, ctx):
+    rng = np.random.default_rng(12)
+    p = np.column_stack([rng.normal(size=(20000, 3)) * 0.1, rng.random(20000)])
+    w = np.array([0.5, 0.4999, 0.0001])
+    mu = np.array([[0.05, 0, 0, 0.5], [-0.05, 0, 0, 0.5], [50.0, 50.0, 50.0, 0.5]])
+    cov = np.array([[0.01, 0, 0.01, 0, 0, 0.01, 0, 0, 0, 0.1]] * 3)
+    ll, m1, rm = gm.em_step(p, gm.Gmm(w, mu, cov), 1e-6, ctx=ctx)
+    lg, rll = orc.e_step(p, w, mu, cov)
+    rw, rmu, rcov, rrm = orc.m_step(p, lg, 1e-6)
+    assert rm == rrm == 1
+    assert_model_close(m1.weights, m1.means, m1.covariances, rw, rmu, rcov, tol=1e-5)
+
+
+# ---- end-to-end fits -----------------------------------------------------------
+def test_cfg1_fixed_init_50_iterations(gm, orc, ctx):
+    """BASELINE cfg1: 3D, N=20,000, K=32, fixed init, 50 EM iterations."""
+    p = gm.structured_scene(20000, 1, 0.005)[:, :3]
+    w, mu, cov = fixed_init(orc, p, 32)
+    res = gm.fit_from(p, gm.Gmm(w, mu, cov), gm.EmParams(50, 0.0, 1e-6), ctx=ctx)
+    ref = orc.fit_from(p, w, mu, cov, max_iters=50, ll_rel_tol=0.0, cov_reg=1e-6)
+    assert res.em_iterations == ref["em_iterations"] == 50
+    assert ll_err(res.ll_trace, ref["ll_trace"]) < LL_TOL
+    assert_model_close(res.model.weights, res.model.means, res.model.covariances,
+                       ref["w"], ref["mu"], ref["cov"])
+
+
+def test_cfg2_fit_k512_end_to_end(gm, orc, ctx):
+    """BASELINE cfg2: one 640x480 frame, K=512, k-means++ + EM to tol 1e-3."""
+    p = frame(gm)
+    em = gm.EmParams(100, 1e-3, 1e-6, 0)
+    res = gm.fit_k(p, 512, em, ctx=ctx, want_labels=True)
+    ref = orc.fit_k(p, 512, max_iters=100, ll_rel_tol=1e-3, cov_reg=1e-6, seed=0)
+    assert np.array_equal(res.centers, ref["centers"])
+    assert np.array_equal(res.labels, ref["labels"])
+    assert res.em_iterations == ref["em_iterations"]
+    assert res.removed_components == ref["removed"]
+    assert ll_err(res.ll_trace, ref["ll_trace"]) < LL_TOL
+    assert_model_close(res.model.weights, res.model.means, res.model.covariances,
+                       ref["w"], ref["mu"], ref["cov"])
+    assert res.units == pytest.approx(len(p) * 512 * res.em_iterations)
+
+
+def test_cfg3_jittered_frame_k256(gm, orc, ctx):
+    """BASELINE cfg3 frame f: xyz jittered by 2 mm (seed f), K=256, seed f."""
+    f = 3
+    p = gm.jitter_cloud(frame(gm), 0.002, f)
+    em = gm.EmParams(100, 1e-3, 1e-6, f)
+    res = gm.fit_k(p, 256, em, ctx=ctx)
+    ref = orc.fit_k(p, 256, max_iters=100, ll_rel_tol=1e-3, cov_reg=1e-6, seed=f)
+    assert res.em_iterations == ref["em_iterations"]
+    assert ll_err(res.ll_trace, ref["ll_trace"]) < LL_TOL
+    assert_model_close(res.model.weights, res.model.means, res.model.covariances,
+                       ref["w"], ref["mu"], ref["cov"])
+
+
+def test_blobs_3d_fit_converged_model(gm, orc, ctx):
+    c = np.array([[0.1, 0.1, 0.1, 0.0], [0.5, 0.5, 0.5, 0.0], [0.9, 0.9, 0.9, 0.0]])
+    p = gm.blob_cloud(c, 0.02, 2000, 7)[:, :3]
+    em = gm.EmParams(200, 1e-7, 1e-6, 0)
+    res = gm.fit_k(p, 5, em, ctx=ctx)
+    ref = orc.fit_k(p, 5, max_iters=200, ll_rel_tol=1e-7, cov_reg=1e-6, seed=0)
+    assert res.em_iterations == ref["em_iterations"]
+    assert ll_err(res.ll_trace, ref["ll_trace"]) < LL_TOL
+    assert_model_close(res.model.weights, res.model.means, res.model.covariances,
+                       ref["w"], ref["mu"], ref["cov"])
+
+
+def test_deterministic_bits(gm, ctx):
+    p = frame(gm)[::3].copy()
+    em = gm.EmParams(10, 0.0, 1e-6, 0)
+    a = gm.fit_k(p, 128, em, ctx=ctx)
+    b = gm.fit_k(p, 128, em, ctx=ctx)
+    assert np.array_equal(a.ll_trace, b.ll_trace)
+    assert np.array_equal(a.model.means, b.model.means)
+    assert np.array_equal(a.model.covariances, b.model.covariances)
+
+
+def test_resident_matches_host_api(gm, ctx):
+    p = frame(gm)[::4].copy()
+    em = gm.EmParams(20, 1e-4, 1e-6, 0)
+    a = gm.fit_k(p, 64, em, ctx=ctx)
+    ctx.upload(p)
+    b = ctx.fit_k_resident(64, em)
+    assert np.array_equal(a.ll_trace, b.ll_trace)
+    assert np.array_equal(a.model.weights, b.model.weights)
+
+
+# ---- single-step APIs ------------------------------------------------------------
+def test_e_step_api(gm, orc, ctx):
+    p = frame(gm)[::50].copy()
+    w, mu, cov = fixed_init(orc, p, 16)
+    lg, ll = gm.e_step(p, gm.Gmm(w, mu, cov), ctx=ctx)
+    rlg, rll = orc.e_step(p, w, mu, cov)
+    assert abs(ll - rll) / abs(rll) < 1e-12
+    big = rlg > -30
+    assert np.max(np.abs(lg[big] - rlg[big])) < 1e-8
+
+
+def test_m_step_api(gm, orc, ctx):
+    rng = np.random.default_rng(5)
+    p = frame(gm)[::40].copy()
+    lg = rng.normal(size=(len(p), 12)) * 3
+    lg -= np.log(np.exp(lg).sum(1, keepdims=True))
+    m, rm = gm.m_step(p, lg, 1e-6, ctx=ctx)
+    rw, rmu, rcov, rrm = orc.m_step(p, lg, 1e-6)
+    assert rm == rrm
+    assert_model_close(m.weights, m.means, m.covariances, rw, rmu, rcov, tol=1e-10)
+
+
+def test_cholesky_cache_api(gm, orc, ctx):
+    rng = np.random.default_rng(6)
+    a = rng.normal(size=(50, 4, 4))
+    s = np.einsum("mij,mkj->mik", a, a) + 1e-3 * np.eye(4)
+    r, c = np.array([0, 1, 1, 2, 2, 2, 3, 3, 3, 3]), np.array([0, 0, 1, 0, 1, 2, 0, 1, 2, 3])
+    cov = s[:, r, c]
+    cc = gm.cholesky_cache(gm.Gmm(np.full(50, 0.02), np.zeros((50, 4)), cov), ctx=ctx)
+    lo, pr, ld = orc.cholesky_cache(cov)
+    assert np.max(np.abs(cc.lower - lo)) < 1e-12
+    assert np.max(np.abs(cc.precision - pr)) < 1e-9
+    assert np.max(np.abs(cc.log_det_terms - ld)) < 1e-12
+
+
+# ---- error behaviour (gmmscape_cli.cpp:508-528 classes) --------------------------
+def test_errors(gm, ctx):
+    p = frame(gm)[::100].copy()
+    bad = p.copy()
+    bad[5, 2] = np.nan
+    with pytest.raises(gm.NumericalError):
+        gm.fit_k(bad, 4, gm.EmParams(5, 1e-3), ctx=ctx)
+    bad = p.copy()
+    bad[5, 3] = 1.5
+    with pytest.raises(gm.NumericalError, match="intensity"):
+        gm.fit_k(bad, 4, gm.EmParams(5, 1e-3), ctx=ctx)
+    with pytest.raises(ValueError):
+        gm.fit_k(p, 0, gm.EmParams(5, 1e-3), ctx=ctx)
+    with pytest.raises(ValueError):
+        gm.fit_k(p, 4, gm.EmParams(0, 1e-3), ctx=ctx)
+    with pytest.raises(ValueError):
+        gm.kinit(p, len(p) + 1, 0, ctx=ctx)
+    w = np.array([0.5, 0.5])
+    mu = np.zeros((2, 4))
+    cov = np.array([[1, 0, 1, 0, 0, 1, 0, 0, 0, 1.0], [-1, 0, 1, 0, 0, 1, 0, 0, 0, 1.0]])
+    with pytest.raises(gm.NumericalError, match="block 1"):
+        gm.fit_from(p, gm.Gmm(w, mu, cov), gm.EmParams(5, 1e-3), ctx=ctx)
+    # K > N is clamped to N (sogmm.cpp:477)
+    r = gm.fit_k(p[:20], 50, gm.EmParams(3, 0.0, 1e-3), ctx=ctx)
+    assert r.k_init == 20
