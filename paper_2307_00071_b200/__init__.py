@@ -40,7 +40,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def lib_path() -> str:
-    return os.path.join(_HERE, "libgmmb.so")
+    # GMMB_LIB: alternative build of the same library (precision experiments)
+    return os.environ.get("GMMB_LIB") or os.path.join(_HERE, "libgmmb.so")
 
 
 class NumericalError(RuntimeError):

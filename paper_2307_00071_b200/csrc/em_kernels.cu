@@ -23,6 +23,26 @@
 
 namespace cg = cooperative_groups;
 
+// Precision switches (defaults = production).
+#ifndef GMMB_SCALE_IEEE
+#define GMMB_SCALE_IEEE 0   // 1: IEEE 1/S instead of rcp.approx
+#endif
+#ifndef GMMB_BASE_HILO
+#define GMMB_BASE_HILO 0    // 1: log-normaliser as an FP32 hi + lo pair
+#endif
+#ifndef GMMB_FLUSH_SUBTILES
+#define GMMB_FLUSH_SUBTILES 2   // sub-tiles per FP32 -> FP64 promotion
+#endif
+#ifndef GMMB_FLUSH_LO
+#define GMMB_FLUSH_LO 0     // first statistic flushed at the fast cadence
+#endif
+#ifndef GMMB_FLUSH_HI
+#define GMMB_FLUSH_HI 99    // one past the last statistic flushed fast
+#endif
+#ifndef GMMB_MU_HILO
+#define GMMB_MU_HILO 0      // 1: tile-relative means as an FP32 hi + lo pair
+#endif
+
 namespace gmmb {
 
 namespace {
@@ -77,29 +97,80 @@ __device__ __forceinline__ float warp_reduce_scatter(float (&v)[P], int lane) {
 template <int D, int NW, int C, int P>
 struct EstepSmem {
   float4 xs[kTile];
-  float red[NW][P];
-  float bc_m[P];
-  float bc_s[P];
-  float xm[2][P];   // cluster exchange: CTA max per point
-  float xsum[2][P]; // cluster exchange: CTA sum per point
-  double ll[P];
-  double acc64[nstats(D)][NW * 32];
+  float sh[kTile];        // per-point shift (previous iteration's lse, log2)
+  float red[2][P][NW];    // per-warp partials per point, double-buffered
+  float xm[2][P];         // cluster exchange: CTA max per point
+  float xsum[2][P];       // cluster exchange: CTA sum per point
 };
 
-template <int D, int NW, int C, int P>
-__global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
+// Combines the NW per-warp partials of P points inside one warp: lane
+// (p = lane / 4, q = lane % 4) folds warps q, q+4, ... in order, then two
+// xor steps. Every warp computes the identical (order-fixed) value.
+template <int NW, int P, bool MAX>
+__device__ __forceinline__ float cta_combine(const float (&red)[P][NW], int lane) {
+  static_assert(P == 8, "lane mapping assumes 8 points per sub-tile");
+  const int p = lane >> 2, q = lane & 3;
+  float v = MAX ? -INFINITY : 0.f;
+#pragma unroll
+  for (int w = q; w < NW; w += 4) v = MAX ? fmaxf(v, red[p][w]) : v + red[p][w];
+#pragma unroll
+  for (int off = 1; off <= 2; off <<= 1) {
+    const float o = __shfl_xor_sync(0xffffffffu, v, off);
+    v = MAX ? fmaxf(v, o) : v + o;
+  }
+  return v;
+}
+
+// Cluster-wide combine of per-CTA values xs[p][rank]: lane (p, q) folds
+// ranks q, q+4, then two xor steps (fixed order on every CTA).
+template <int C, bool MAX>
+__device__ __forceinline__ float cluster_combine(float* local_slot, int lane) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int q = lane & 3;
+  float v = MAX ? -INFINITY : 0.f;
+#pragma unroll
+  for (int r = q; r < C; r += 4) {
+    const float o = *cl.map_shared_rank(local_slot, r);
+    v = MAX ? fmaxf(v, o) : v + o;
+  }
+#pragma unroll
+  for (int off = 1; off <= 2; off <<= 1) {
+    const float o = __shfl_xor_sync(0xffffffffu, v, off);
+    v = MAX ? fmaxf(v, o) : v + o;
+  }
+  return v;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ float rcpf(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// CPT components per thread: thread tid of CTA rank r owns components
+// r * kCtaComps + c * (32 NW) + tid, c < CPT. Per 8-point sub-tile: phase A
+// (log2 densities), phase B (normalise: one CTA barrier, every warp combines
+// the per-warp partials itself; clusters add one cluster barrier), phase C
+// (responsibilities + statistics centred at the previous means).
+template <int D, int NW, int C, int P, int CPT>
+__global__ void __launch_bounds__(NW * 32, 16 / NW)
     estep_stats_kernel(const float4* __restrict__ xt,
                        const double* __restrict__ tc, int64_t n, int ntiles,
                        ModelBuf b0, ModelBuf b1, const EmState* __restrict__ st,
                        int kpad, double* __restrict__ partials,
-                       double* __restrict__ ll_part,
-                       float* __restrict__ lse_out) {
+                       double* __restrict__ ll_part, float* lse, int exact_mode) {
   constexpr int NP = npacked(D);
   constexpr int NS = nstats(D);
   constexpr int T = NW * 32;
   using Smem = EstepSmem<D, NW, C, P>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  double* acc64 = reinterpret_cast<double*>(smem_raw + ((sizeof(Smem) + 15) & ~size_t(15)));
 
   if (st->done) return;
   const int tid = threadIdx.x;
@@ -111,41 +182,47 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
     cid = blockIdx.x / C;
     ncl = gridDim.x / C;
   }
-  const int k = rank * kCtaComps + tid;
   const int k_cur = st->k_cur;
-  const bool active = k < k_cur;
   const ModelBuf& mb = st->cur ? b1 : b0;
 
   // component constants in registers
-  float pp[NP];
-  float base2 = -INFINITY;
-  double mu64[D];
+  float pp[CPT][NP];
+  float base2[CPT];
+  float blo[CPT];
 #pragma unroll
-  for (int j = 0; j < NP; ++j) pp[j] = 0.f;
+  for (int c = 0; c < CPT; ++c) {
+    const int k = rank * kCtaComps + c * T + tid;
+    base2[c] = -INFINITY;
+    blo[c] = 0.f;
 #pragma unroll
-  for (int j = 0; j < D; ++j) mu64[j] = 0.0;
-  if (active) {
-    const float4* c4 = reinterpret_cast<const float4*>(mb.cst + k);
-    float cc[12];
-    const float4 a = c4[0], b = c4[1], c = c4[2];
-    cc[0] = a.x; cc[1] = a.y; cc[2] = a.z; cc[3] = a.w;
-    cc[4] = b.x; cc[5] = b.y; cc[6] = b.z; cc[7] = b.w;
-    cc[8] = c.x; cc[9] = c.y; cc[10] = c.z; cc[11] = c.w;
+    for (int j = 0; j < NP; ++j) pp[c][j] = 0.f;
+    if (k < k_cur) {
+      const float4* c4 = reinterpret_cast<const float4*>(mb.cst + k);
+      float cc[12];
+      const float4 a = c4[0], b = c4[1], e = c4[2];
+      cc[0] = a.x; cc[1] = a.y; cc[2] = a.z; cc[3] = a.w;
+      cc[4] = b.x; cc[5] = b.y; cc[6] = b.z; cc[7] = b.w;
+      cc[8] = e.x; cc[9] = e.y; cc[10] = e.z; cc[11] = e.w;
 #pragma unroll
-    for (int j = 0; j < NP; ++j) pp[j] = cc[j];
-    base2 = cc[10];
-#pragma unroll
-    for (int j = 0; j < D; ++j) mu64[j] = mb.mu[k * 4 + j];
+      for (int j = 0; j < NP; ++j) pp[c][j] = cc[j];
+      base2[c] = cc[10];
+      blo[c] = GMMB_BASE_HILO ? cc[11] : 0.f;
+    }
   }
 
-  float acc[NS];
+  float acc[CPT][NS];
 #pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    acc[s] = 0.f;
-    sm.acc64[s][tid] = 0.0;
-  }
-  if (tid < P) sm.ll[tid] = 0.0;
-  int parity = 0;
+  for (int c = 0; c < CPT; ++c)
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      acc[c][s] = 0.f;
+      acc64[(c * NS + s) * T + tid] = 0.0;
+    }
+  double ll_acc = 0.0;   // warp 0, lanes with lane % 4 == 0 (one point each)
+  int rb = 0;            // red[] buffer rotation (one flip per CTA barrier)
+  int xb = 0;            // cluster exchange buffer rotation
+  const bool finisher = warp == 0 && (lane & 3) == 0;
+  const int fp = lane >> 2;  // point of this lane's group
 
   for (int t = cid; t < ntiles; t += ncl) {
     const int64_t t0 = static_cast<int64_t>(t) * kTile;
@@ -153,158 +230,220 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
     __syncthreads();  // previous tile fully consumed
     for (int i = tid; i < kTile; i += T) {
       sm.xs[i] = i < npts ? xt[t0 + i] : make_float4(0.f, 0.f, 0.f, 0.f);
+      sm.sh[i] = (i < npts && !exact_mode) ? lse[t0 + i] : 0.f;
     }
-    float muf[D];
+    float muf[CPT][D];
+#if GMMB_MU_HILO
+    float mulo[CPT][D];
+#endif
 #pragma unroll
-    for (int j = 0; j < D; ++j) {
-      muf[j] = static_cast<float>(mu64[j] - tc[static_cast<int64_t>(t) * 4 + j]);
+    for (int c = 0; c < CPT; ++c) {
+      const int k = rank * kCtaComps + c * T + tid;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const double m = k < k_cur ? mb.mu[k * 4 + j] : 0.0;
+        const double rel = m - tc[static_cast<int64_t>(t) * 4 + j];
+        muf[c][j] = static_cast<float>(rel);
+#if GMMB_MU_HILO
+        mulo[c][j] = static_cast<float>(rel - static_cast<double>(muf[c][j]));
+#endif
+      }
     }
+#if GMMB_MU_HILO
+#define GMMB_D(xc, c, j) (((xc) - muf[c][j]) - mulo[c][j])
+#else
+#define GMMB_D(xc, c, j) ((xc) - muf[c][j])
+#endif
     __syncthreads();
 
     for (int q = 0; q < npts; q += P) {
-      // ---- phase A: log2 densities, d kept in registers ----
-      float dd[P][D];
-      float l[P];
+      // ---- phase A: log2 densities ----
+      // l = base2 - |P'd|^2 (GMMB_BASE_HILO keeps q = |P'd|^2 and forms
+      // ((hi - shift) + lo) - q so the ~30-unit normaliser is never rounded)
+      float l[CPT][P], e[CPT][P];
 #pragma unroll
       for (int p = 0; p < P; ++p) {
         const float4 x = sm.xs[q + p];
-        dd[p][0] = x.x - muf[0];
-        dd[p][1] = x.y - muf[1];
-        dd[p][2] = x.z - muf[2];
-        if constexpr (D == 4) dd[p][3] = x.w - muf[3];
-        float y0 = pp[0] * dd[p][0];
-        float y1 = fmaf(pp[2], dd[p][1], pp[1] * dd[p][0]);
-        float y2 = fmaf(pp[5], dd[p][2], fmaf(pp[4], dd[p][1], pp[3] * dd[p][0]));
-        float qf = fmaf(y0, y0, fmaf(y1, y1, y2 * y2));
-        if constexpr (D == 4) {
-          float y3 = fmaf(pp[9], dd[p][3],
-                          fmaf(pp[8], dd[p][2],
-                               fmaf(pp[7], dd[p][1], pp[6] * dd[p][0])));
-          qf = fmaf(y3, y3, qf);
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+          const float d0 = GMMB_D(x.x, c, 0), d1 = GMMB_D(x.y, c, 1), d2 = GMMB_D(x.z, c, 2);
+          const float y0 = pp[c][0] * d0;
+          const float y1 = fmaf(pp[c][2], d1, pp[c][1] * d0);
+          const float y2 = fmaf(pp[c][5], d2, fmaf(pp[c][4], d1, pp[c][3] * d0));
+#if GMMB_BASE_HILO
+          float lv = fmaf(y2, y2, fmaf(y1, y1, y0 * y0));
+          if constexpr (D == 4) {
+            const float d3 = GMMB_D(x.w, c, 3);
+            const float y3 = fmaf(pp[c][9], d3, fmaf(pp[c][8], d2, fmaf(pp[c][7], d1, pp[c][6] * d0)));
+            lv = fmaf(y3, y3, lv);
+          }
+          l[c][p] = base2[c] == -INFINITY ? INFINITY : lv;  // holds q
+#else
+          float lv = fmaf(-y2, y2, fmaf(-y1, y1, fmaf(-y0, y0, base2[c])));
+          if constexpr (D == 4) {
+            const float d3 = GMMB_D(x.w, c, 3);
+            const float y3 = fmaf(pp[c][9], d3, fmaf(pp[c][8], d2, fmaf(pp[c][7], d1, pp[c][6] * d0)));
+            lv = fmaf(-y3, y3, lv);
+          }
+          l[c][p] = lv;
+#endif
         }
-        l[p] = (q + p < npts) ? base2 - qf : 0.f;
       }
-      // ---- phase B1: per-point max over the CTA's components ----
-      {
-        float v[P];
-#pragma unroll
-        for (int p = 0; p < P; ++p) v[p] = l[p];
-        const float r = warp_reduce_scatter<P, true>(v, lane);
-        if ((lane & (32 / P - 1)) == 0) sm.red[warp][lane >> (5 - Log2<P>::v)] = r;
-      }
-      __syncthreads();
-      if (tid < P) {
-        float m = sm.red[0][tid];
-#pragma unroll
-        for (int w = 1; w < NW; ++w) m = fmaxf(m, sm.red[w][tid]);
-        sm.bc_m[tid] = m;
-      }
-      __syncthreads();
-      // ---- phase B2: shifted exponentials and their sum ----
-      float e[P];
-      {
+#if GMMB_BASE_HILO
+#define GMMB_ARG(c, p, m) (((base2[c] - (m)) + blo[c]) - l[c][p])
+#define GMMB_LV(c, p) (base2[c] - l[c][p])
+#else
+#define GMMB_ARG(c, p, m) (l[c][p] - (m))
+#define GMMB_LV(c, p) (l[c][p])
+#endif
+      const bool valid_g = q + fp < npts;  // this lane group's point
+      float S = 1.f, M = 0.f;              // lane group's sum and shift
+      bool exact = exact_mode != 0;
+      if (!exact) {
+        // ---- phase B: normalise by the previous iteration's lse ----
+        const float4 h0 = *reinterpret_cast<const float4*>(&sm.sh[q]);
+        const float4 h1 = *reinterpret_cast<const float4*>(&sm.sh[q + 4]);
+        const float shp[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
         float v[P];
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-          float m = sm.bc_m[p];
-          m = (m == -INFINITY) ? 0.f : m;
-          e[p] = ex2f(l[p] - m);
-          v[p] = e[p];
+          v[p] = 0.f;
+#pragma unroll
+          for (int c = 0; c < CPT; ++c) {
+            e[c][p] = ex2f(GMMB_ARG(c, p, shp[p]));
+            v[p] += e[c][p];
+          }
         }
         const float r = warp_reduce_scatter<P, false>(v, lane);
-        if ((lane & (32 / P - 1)) == 0) sm.red[warp][lane >> (5 - Log2<P>::v)] = r;
-      }
-      __syncthreads();
-      float s_cta = 0.f;
-      if (tid < P) {
-#pragma unroll
-        for (int w = 0; w < NW; ++w) s_cta += sm.red[w][tid];
+        if ((lane & 3) == 0) sm.red[rb][lane >> 2][warp] = r;
+        __syncthreads();
+        S = cta_combine<NW, P, false>(sm.red[rb], lane);
+        rb ^= 1;
         if constexpr (C > 1) {
-          sm.xm[parity][tid] = sm.bc_m[tid];
-          sm.xsum[parity][tid] = s_cta;
+          if (finisher) sm.xsum[xb][fp] = S;
+          cluster_sync_all();
+          S = cluster_combine<C, false>(&sm.xsum[xb][fp], lane);
+          xb ^= 1;
         }
+        M = sm.sh[q + fp];
+        // identical inputs in every warp => warp-, CTA- and cluster-uniform
+        exact = __any_sync(0xffffffffu, valid_g && !(S >= 0x1p-64f && S <= 0x1p64f));
       }
-      if constexpr (C > 1) {
-        // cluster-wide combine of (max, sum) per point; the release/acquire
-        // barrier orders the partial writes above before the DSMEM reads.
-        asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-        asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-      }
-      if (tid < P) {
-        const float mc = sm.bc_m[tid];
-        float M = mc, S = 0.f;
+      if (exact) {
+        // ---- exact max-shift path (first iteration, or the shift failed) ----
+        float v[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          v[p] = GMMB_LV(0, p);
+#pragma unroll
+          for (int c = 1; c < CPT; ++c) v[p] = fmaxf(v[p], GMMB_LV(c, p));
+        }
+        float r = warp_reduce_scatter<P, true>(v, lane);
+        if ((lane & 3) == 0) sm.red[rb][lane >> 2][warp] = r;
+        __syncthreads();
+        M = cta_combine<NW, P, true>(sm.red[rb], lane);
+        rb ^= 1;
         if constexpr (C > 1) {
-          cg::cluster_group cl = cg::this_cluster();
-          float mr[C], sr[C];
-#pragma unroll
-          for (int r = 0; r < C; ++r) {
-            mr[r] = *cl.map_shared_rank(&sm.xm[parity][tid], r);
-            sr[r] = *cl.map_shared_rank(&sm.xsum[parity][tid], r);
-          }
-          M = mr[0];
-#pragma unroll
-          for (int r = 1; r < C; ++r) M = fmaxf(M, mr[r]);
-#pragma unroll
-          for (int r = 0; r < C; ++r) {
-            if (mr[r] != -INFINITY) S += sr[r] * ex2f(mr[r] - M);
-          }
-        } else {
-          S = s_cta;
+          if (finisher) sm.xm[xb][fp] = M;
+          cluster_sync_all();
+          M = cluster_combine<C, true>(&sm.xm[xb][fp], lane);
+          xb ^= 1;
         }
-        const bool valid = q + tid < npts;
-        const float mloc = (mc == -INFINITY) ? 0.f : mc;
-        float scale = 0.f;
-        if (valid) {
-          scale = (C > 1 ? ex2f(mloc - M) : 1.f) / S;
-          const float lse2 = M + lg2f(S);
-          if (rank == 0) {
-            sm.ll[tid] += static_cast<double>(lse2);
-            if (lse_out) lse_out[t0 + q + tid] = lse2;
+        M = M == -INFINITY ? 0.f : M;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const float mp = __shfl_sync(0xffffffffu, M, p * 4);
+          v[p] = 0.f;
+#pragma unroll
+          for (int c = 0; c < CPT; ++c) {
+            e[c][p] = ex2f(GMMB_ARG(c, p, mp));
+            v[p] += e[c][p];
           }
         }
-        sm.bc_s[tid] = scale;
+        r = warp_reduce_scatter<P, false>(v, lane);
+        if ((lane & 3) == 0) sm.red[rb][lane >> 2][warp] = r;
+        __syncthreads();
+        S = cta_combine<NW, P, false>(sm.red[rb], lane);
+        rb ^= 1;
+        if constexpr (C > 1) {
+          if (finisher) sm.xsum[xb][fp] = S;
+          cluster_sync_all();
+          S = cluster_combine<C, false>(&sm.xsum[xb][fp], lane);
+          xb ^= 1;
+        }
       }
-      parity ^= 1;
-      __syncthreads();
-      // ---- phase C: responsibilities and centred statistics ----
+      if (finisher && valid_g && rank == 0) {
+        const float lse2 = M + lg2f(S);
+        ll_acc += static_cast<double>(lse2);
+        lse[t0 + q + fp] = lse2;
+      }
+      const float scale_g = valid_g ? (GMMB_SCALE_IEEE ? 1.f / S : rcpf(S)) : 0.f;
+      // ---- phase C: responsibilities and statistics centred at mu_old ----
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        const float r = e[p] * sm.bc_s[p];
-        float w[D];
+        const float sc = __shfl_sync(0xffffffffu, scale_g, p * 4);
+        const float4 x = sm.xs[q + p];
+        const float xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-        for (int j = 0; j < D; ++j) w[j] = r * dd[p][j];
-        acc[0] += r;
+        for (int c = 0; c < CPT; ++c) {
+          const float r = e[c][p] * sc;
+          float dd[D], w[D];
 #pragma unroll
-        for (int j = 0; j < D; ++j) acc[1 + j] += w[j];
-        int s = 1 + D;
+          for (int j = 0; j < D; ++j) {
+            dd[j] = GMMB_D(xv[j], c, j);
+            w[j] = r * dd[j];
+          }
+          acc[c][0] += r;
 #pragma unroll
-        for (int i = 0; i < D; ++i) {
+          for (int j = 0; j < D; ++j) acc[c][1 + j] += w[j];
+          int s = 1 + D;
 #pragma unroll
-          for (int j = 0; j <= i; ++j) {
-            acc[s] = fmaf(w[i], dd[p][j], acc[s]);
-            ++s;
+          for (int i = 0; i < D; ++i) {
+#pragma unroll
+            for (int j = 0; j <= i; ++j) {
+              acc[c][s] = fmaf(w[i], dd[j], acc[c][s]);
+              ++s;
+            }
           }
         }
+      }
+      if (GMMB_FLUSH_SUBTILES < 16 && ((q / P + 1) % GMMB_FLUSH_SUBTILES) == 0) {
+#pragma unroll
+        for (int c = 0; c < CPT; ++c)
+#pragma unroll
+          for (int s = (GMMB_FLUSH_LO); s < (NS < GMMB_FLUSH_HI ? NS : GMMB_FLUSH_HI); ++s) {
+            acc64[(c * NS + s) * T + tid] += static_cast<double>(acc[c][s]);
+            acc[c][s] = 0.f;
+          }
       }
     }
     // promote the tile's FP32 partial sums to FP64
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      sm.acc64[s][tid] += static_cast<double>(acc[s]);
-      acc[s] = 0.f;
-    }
+    for (int c = 0; c < CPT; ++c)
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        acc64[(c * NS + s) * T + tid] += static_cast<double>(acc[c][s]);
+        acc[c][s] = 0.f;
+      }
+#undef GMMB_D
+#undef GMMB_ARG
+#undef GMMB_LV
   }
   __syncthreads();
-  if (k < kpad) {
-    double* out = partials + (static_cast<int64_t>(cid) * kpad + k) * NS;
 #pragma unroll
-    for (int s = 0; s < NS; ++s) out[s] = sm.acc64[s][tid];
+  for (int c = 0; c < CPT; ++c) {
+    const int k = rank * kCtaComps + c * T + tid;
+    if (k < kpad) {
+      double* out = partials + (static_cast<int64_t>(cid) * kpad + k) * NS;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) out[s] = acc64[(c * NS + s) * T + tid];
+    }
   }
-  if (rank == 0 && tid == 0) {
+  if (warp == 0) {  // ll partial of this cluster: the 8 finisher lanes, in order
     double s = 0.0;
 #pragma unroll
-    for (int p = 0; p < P; ++p) s += sm.ll[p];
-    ll_part[cid] = s * kLn2;
+    for (int p = 0; p < P; ++p) s += __shfl_sync(0xffffffffu, ll_acc, p * 4);
+    if (lane == 0 && rank == 0) ll_part[cid] = s * kLn2;
   }
   if constexpr (C > 1) {
     // keep smem alive until every CTA of the cluster finished its DSMEM reads
@@ -312,14 +451,15 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
   }
 }
 
-template <int D, int NW, int C, int P>
+template <int D, int NW, int C, int P, int CPT>
 cudaError_t launch_estep_t(const PointsDev& pts, const ModelBuf* bufs,
                            const EmState* st, int kpad, double* partials,
-                           double* ll_part, float* lse_out, int sm_count,
+                           double* ll_part, float* lse, int exact_mode, int sm_count,
                            cudaStream_t s, int* ncl_out) {
   using Smem = EstepSmem<D, NW, C, P>;
-  auto kern = estep_stats_kernel<D, NW, C, P>;
-  const size_t smem = sizeof(Smem);
+  auto kern = estep_stats_kernel<D, NW, C, P, CPT>;
+  const size_t smem = ((sizeof(Smem) + 15) & ~size_t(15)) +
+                      sizeof(double) * nstats(D) * CPT * NW * 32;
   static int per_sm_dev[64] = {0};  // per template instance and device
   int dev = 0;
   cudaGetDevice(&dev);
@@ -355,27 +495,27 @@ cudaError_t launch_estep_t(const PointsDev& pts, const ModelBuf* bufs,
   cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, kern, pts.xt, pts.tc, pts.n, pts.ntiles,
                             bufs[0], bufs[1], st, kpad, partials, ll_part,
-                            lse_out);
+                            lse, exact_mode);
 }
 
 template <int D>
 cudaError_t launch_estep_d(const PointsDev& pts, const ModelBuf* bufs,
                            const EmState* st, int k0, double* partials,
-                           double* ll_part, float* lse_out, int sm_count,
+                           double* ll_part, float* lse, int exact_mode, int sm_count,
                            cudaStream_t s, int* ncl) {
   constexpr int P = 8;
   const int kpad = k0;
-#define GMMB_L(NW, C) \
-  return launch_estep_t<D, NW, C, P>(pts, bufs, st, kpad, partials, ll_part, \
-                                     lse_out, sm_count, s, ncl)
-  if (k0 <= 32) GMMB_L(1, 1);
-  if (k0 <= 64) GMMB_L(2, 1);
-  if (k0 <= 128) GMMB_L(4, 1);
-  if (k0 <= 256) GMMB_L(8, 1);
-  if (k0 <= 512) GMMB_L(16, 1);
-  if (k0 <= 1024) GMMB_L(16, 2);
-  if (k0 <= 2048) GMMB_L(16, 4);
-  if (k0 <= 4096) GMMB_L(16, 8);
+#define GMMB_L(NW, C, CPT) \
+  return launch_estep_t<D, NW, C, P, CPT>(pts, bufs, st, kpad, partials, ll_part, \
+                                          lse, exact_mode, sm_count, s, ncl)
+  if (k0 <= 32) GMMB_L(1, 1, 1);
+  if (k0 <= 64) GMMB_L(2, 1, 1);
+  if (k0 <= 128) GMMB_L(4, 1, 1);
+  if (k0 <= 256) GMMB_L(8, 1, 1);
+  if (k0 <= 512) GMMB_L(8, 1, 2);
+  if (k0 <= 1024) GMMB_L(8, 2, 2);
+  if (k0 <= 2048) GMMB_L(8, 4, 2);
+  if (k0 <= 4096) GMMB_L(8, 8, 2);
 #undef GMMB_L
   return cudaErrorInvalidValue;
 }
@@ -669,7 +809,9 @@ __global__ void __launch_bounds__(1024) commit_kernel(
     CompConst c;
 #pragma unroll
     for (int q = 0; q < 16; ++q) c.p[q] = rec.pc[k * 16 + q];
-    c.p[10] = static_cast<float>(kLog2E * (log(w) + rec.logdet[k] - half_d_ln2pi));
+    const double b2 = kLog2E * (log(w) + rec.logdet[k] - half_d_ln2pi);
+    c.p[10] = static_cast<float>(b2);
+    c.p[11] = static_cast<float>(b2 - static_cast<double>(c.p[10]));
     dst.cst[j] = c;
     ++j;
   }
@@ -703,8 +845,9 @@ __global__ void prep_kernel(ModelBuf b0, ModelBuf b1, EmState* st, int m) {
     st->done = 1;
     return;
   }
-  c.p[10] = static_cast<float>(
-      kLog2E * (log(mb.w[k]) + logdet - 0.5 * D * kLog2Pi));
+  const double b2 = kLog2E * (log(mb.w[k]) + logdet - 0.5 * D * kLog2Pi);
+  c.p[10] = static_cast<float>(b2);
+  c.p[11] = static_cast<float>(b2 - static_cast<double>(c.p[10]));
   mb.cst[k] = c;
 }
 
@@ -949,12 +1092,12 @@ cudaError_t launch_factor_dump(int d, const ModelBuf* bufs, const EmState* st,
 // ---------------------------------------------------------------------------
 cudaError_t launch_estep_stats(const PointsDev& pts, const ModelBuf* bufs,
                                const EmState* st, int k0, double* partials,
-                               double* ll_part, float* lse_out, int sm_count,
-                               cudaStream_t s, int* ncl_out) {
+                               double* ll_part, float* lse, int exact_mode,
+                               int sm_count, cudaStream_t s, int* ncl_out) {
   if (pts.d == 4)
-    return launch_estep_d<4>(pts, bufs, st, k0, partials, ll_part, lse_out,
+    return launch_estep_d<4>(pts, bufs, st, k0, partials, ll_part, lse, exact_mode,
                              sm_count, s, ncl_out);
-  return launch_estep_d<3>(pts, bufs, st, k0, partials, ll_part, lse_out,
+  return launch_estep_d<3>(pts, bufs, st, k0, partials, ll_part, lse, exact_mode,
                            sm_count, s, ncl_out);
 }
 
