@@ -105,3 +105,24 @@ def test_shard_key_tail(gm, sizes):
         last = off + m - 1
         assert np.array_equal(gm.shard_key_tail(heads, r), flat[last + 1:last + 4])
         off += m
+
+
+def build_cpp_example(gm, tmp_path):
+    exe = tmp_path / "fit_blobs"
+    libdir = os.path.dirname(gm.lib_path())
+    subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "fit_blobs.cpp"), "-L", libdir, "-lgmmb",
+                    "-Wl,-rpath," + libdir, "-o", str(exe)], check=True)
+    return exe
+
+
+def test_cpp_api_builds_and_reports_device_errors(gm, tmp_path):
+    """The reference-shaped C++ API compiles against libgmmb.so; without a
+    GPU the example exits with the CLI's I/O class (1), not a fallback."""
+    import torch
+    exe = build_cpp_example(gm, tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    if torch.cuda.is_available():
+        assert r.returncode == 0, r.stderr
+    else:
+        assert r.returncode == 1 and "device error" in r.stderr

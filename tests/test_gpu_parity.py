@@ -239,3 +239,12 @@ def test_errors(gm, ctx):
     # K > N is clamped to N (sogmm.cpp:477)
     r = gm.fit_k(p[:20], 50, gm.EmParams(3, 0.0, 1e-3), ctx=ctx)
     assert r.k_init == 20
+
+
+def test_cpp_example_fits_blobs(gm, tmp_path):
+    import subprocess
+    from test_abi import build_cpp_example
+    exe = build_cpp_example(gm, tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    assert "K=3" in r.stdout
