@@ -146,7 +146,6 @@ struct gmmb_ctx {
   DevBuf<int> rflags;
   DevBuf<double> mpart, msums, mmeans, mcounts;
   DevBuf<double> partials, ll_part, red, ll_trace;
-  DevBuf<float> lse;     // per-point log2-sum-exp of the last E step (sorted order)
   DevBuf<double> dense;  // log_gamma staging for m_step / e_step
   DevBuf<EmState> st;
   EmState* st_host = nullptr;  // pinned
@@ -491,10 +490,8 @@ void em_iteration(gmmb_ctx* c, int k0, int it) {
   int ncl = 0;
   const bool timed = it >= 0 && static_cast<size_t>(2 * it + 1) < c->ev_e.size();
   if (timed) ck(cudaEventRecord(c->ev_e[2 * it], c->s), "event");
-  // first E step of a run: exact max shift; later ones shift by the
-  // previous iteration's per-point lse (exact fallback inside the kernel)
-  ck(launch_estep_stats(pts, c->bufs, c->st.p, k0, c->partials.p, c->ll_part.p, c->lse.p,
-                        it <= 0 ? 1 : 0, c->sm_count, c->s, &ncl),
+  ck(launch_estep_stats(pts, c->bufs, c->st.p, k0, c->partials.p, c->ll_part.p, 0,
+                        c->sm_count, c->s, &ncl),
      "estep_stats");
   if (timed) ck(cudaEventRecord(c->ev_e[2 * it + 1], c->s), "event");
   c->launches += 4;
@@ -513,10 +510,9 @@ void ensure_em_buffers(gmmb_ctx* c, int k0, int max_iters) {
   PointsDev pts{c->n, c->d, c->x64.p, c->xt.p, c->tc.p,
                 static_cast<int>((c->n + kTile - 1) / kTile)};
   int ncl = 0;
-  ck(launch_estep_stats(pts, c->bufs, c->st.p, k0, nullptr, nullptr, nullptr, 1,
+  ck(launch_estep_stats(pts, c->bufs, c->st.p, k0, nullptr, nullptr, 0,
                         c->sm_count, c->s, &ncl),
      "estep query");
-  c->lse.ensure(static_cast<size_t>(pts.ntiles) * kTile);
   c->partials.ensure(static_cast<size_t>(ncl) * k0 * NS);
   c->ll_part.ensure(ncl);
   c->red.ensure(static_cast<size_t>(k0) * NS + 1);
@@ -778,7 +774,7 @@ void gmmb_ctx_destroy(gmmb_ctx* c) {
   c->rcount.release(); c->rmean.release(); c->rcov.release(); c->rlogdet.release();
   c->rpc.release(); c->rflags.release(); c->mpart.release(); c->msums.release();
   c->mmeans.release(); c->mcounts.release(); c->partials.release(); c->ll_part.release();
-  c->red.release(); c->ll_trace.release(); c->lse.release(); c->dense.release(); c->st.release();
+  c->red.release(); c->ll_trace.release(); c->dense.release(); c->st.release();
   if (c->st_host) cudaFreeHost(c->st_host);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);

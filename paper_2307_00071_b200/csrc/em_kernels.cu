@@ -19,28 +19,21 @@
 // kernel, so results are bit-reproducible run to run.
 #include <cooperative_groups.h>
 
+#include <type_traits>
+
 #include "em_kernels.cuh"
 
 namespace cg = cooperative_groups;
 
-// Precision switches (defaults = production).
-#ifndef GMMB_SCALE_IEEE
-#define GMMB_SCALE_IEEE 0   // 1: IEEE 1/S instead of rcp.approx
-#endif
-#ifndef GMMB_BASE_HILO
-#define GMMB_BASE_HILO 0    // 1: log-normaliser as an FP32 hi + lo pair
-#endif
+// Precision / schedule switches (defaults = production).
 #ifndef GMMB_FLUSH_SUBTILES
 #define GMMB_FLUSH_SUBTILES 2   // sub-tiles per FP32 -> FP64 promotion
 #endif
-#ifndef GMMB_FLUSH_LO
-#define GMMB_FLUSH_LO 0     // first statistic flushed at the fast cadence
+#ifndef GMMB_PIPE
+#define GMMB_PIPE 1             // 1: software-pipelined kernel when one CTA holds all components
 #endif
-#ifndef GMMB_FLUSH_HI
-#define GMMB_FLUSH_HI 99    // one past the last statistic flushed fast
-#endif
-#ifndef GMMB_MU_HILO
-#define GMMB_MU_HILO 0      // 1: tile-relative means as an FP32 hi + lo pair
+#ifndef GMMB_PXB
+#define GMMB_PXB 1              // 1: y = P'x - P'mu (FFMA chains); 0: y = P'(x - mu)
 #endif
 
 namespace gmmb {
@@ -97,7 +90,6 @@ __device__ __forceinline__ float warp_reduce_scatter(float (&v)[P], int lane) {
 template <int D, int NW, int C, int P>
 struct EstepSmem {
   float4 xs[kTile];
-  float sh[kTile];        // per-point shift (previous iteration's lse, log2)
   float red[2][P][NW];    // per-warp partials per point, double-buffered
   float xm[2][P];         // cluster exchange: CTA max per point
   float xsum[2][P];       // cluster exchange: CTA sum per point
@@ -157,26 +149,51 @@ __device__ __forceinline__ float rcpf(float x) {
 // (log2 densities), phase B (normalise: one CTA barrier, every warp combines
 // the per-warp partials itself; clusters add one cluster barrier), phase C
 // (responsibilities + statistics centred at the previous means).
+//
+// Phase A evaluates y = P'x - P'mu' as FFMA chains (P'mu' is formed once
+// per tile in FP64), so a unit costs 10 + D FFMA (D = 4) instead of
+// D FADD + D FMUL + 6 FFMA + D FFMA. Phase B sums ex2(l) with no shift: the
+// log2 densities of any point that matters lie far inside FP32's exponent
+// range; a sub-tile whose sum leaves [2^-64, 2^64] (outliers far from every
+// component) is redone with the exact max shift.
 template <int D, int NW, int C, int P, int CPT>
 __global__ void __launch_bounds__(NW * 32, 16 / NW)
     estep_stats_kernel(const float4* __restrict__ xt,
                        const double* __restrict__ tc, int64_t n, int ntiles,
                        ModelBuf b0, ModelBuf b1, const EmState* __restrict__ st,
                        int kpad, double* __restrict__ partials,
-                       double* __restrict__ ll_part, float* lse, int exact_mode) {
+                       double* __restrict__ ll_part, int exact_mode) {
   constexpr int NP = npacked(D);
   constexpr int NS = nstats(D);
   constexpr int T = NW * 32;
   using Smem = EstepSmem<D, NW, C, P>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-  double* acc64 = reinterpret_cast<double*>(smem_raw + ((sizeof(Smem) + 15) & ~size_t(15)));
+
 
   if (st->done) return;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  int rank = 0, cid = blockIdx.x, ncl = gridDim.x;
+  // FP64 accumulators, stat pairs as double2 [(c * NSP + s / 2) * T + tid]:
+  // conflict-free 16-byte shared loads/stores when promoting
+  constexpr int NSP = (NS + 1) / 2;
+  double2* acc64 = reinterpret_cast<double2*>(smem_raw + ((sizeof(Smem) + 15) & ~size_t(15)));
+  auto promote = [&](float (&a)[CPT][NS]) {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c)
+#pragma unroll
+      for (int s2 = 0; s2 < NSP; ++s2) {
+        double2 v = acc64[(c * NSP + s2) * T + tid];
+        v.x += static_cast<double>(a[c][2 * s2]);
+        a[c][2 * s2] = 0.f;
+        if (2 * s2 + 1 < NS) {
+          v.y += static_cast<double>(a[c][2 * s2 + 1]);
+          a[c][2 * s2 + 1] = 0.f;
+        }
+        acc64[(c * NSP + s2) * T + tid] = v;
+      }
+  };  int rank = 0, cid = blockIdx.x, ncl = gridDim.x;
   if constexpr (C > 1) {
     rank = static_cast<int>(cg::this_cluster().block_rank());
     cid = blockIdx.x / C;
@@ -188,12 +205,10 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW)
   // component constants in registers
   float pp[CPT][NP];
   float base2[CPT];
-  float blo[CPT];
 #pragma unroll
   for (int c = 0; c < CPT; ++c) {
     const int k = rank * kCtaComps + c * T + tid;
     base2[c] = -INFINITY;
-    blo[c] = 0.f;
 #pragma unroll
     for (int j = 0; j < NP; ++j) pp[c][j] = 0.f;
     if (k < k_cur) {
@@ -206,7 +221,6 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW)
 #pragma unroll
       for (int j = 0; j < NP; ++j) pp[c][j] = cc[j];
       base2[c] = cc[10];
-      blo[c] = GMMB_BASE_HILO ? cc[11] : 0.f;
     }
   }
 
@@ -214,10 +228,9 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW)
 #pragma unroll
   for (int c = 0; c < CPT; ++c)
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      acc[c][s] = 0.f;
-      acc64[(c * NS + s) * T + tid] = 0.0;
-    }
+    for (int s = 0; s < NS; ++s) acc[c][s] = 0.f;
+#pragma unroll
+  for (int i = 0; i < CPT * NSP; ++i) acc64[i * T + tid] = make_double2(0.0, 0.0);
   double ll_acc = 0.0;   // warp 0, lanes with lane % 4 == 0 (one point each)
   int rb = 0;            // red[] buffer rotation (one flip per CTA barrier)
   int xb = 0;            // cluster exchange buffer rotation
@@ -230,87 +243,77 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW)
     __syncthreads();  // previous tile fully consumed
     for (int i = tid; i < kTile; i += T) {
       sm.xs[i] = i < npts ? xt[t0 + i] : make_float4(0.f, 0.f, 0.f, 0.f);
-      sm.sh[i] = (i < npts && !exact_mode) ? lse[t0 + i] : 0.f;
     }
+    // tile-relative means mu' = fp32(mu - c_t) and nb = -P' mu' (FP64 dot)
     float muf[CPT][D];
-#if GMMB_MU_HILO
-    float mulo[CPT][D];
-#endif
+    float nb[CPT][D];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
       const int k = rank * kCtaComps + c * T + tid;
+      double rel[D];
 #pragma unroll
       for (int j = 0; j < D; ++j) {
         const double m = k < k_cur ? mb.mu[k * 4 + j] : 0.0;
-        const double rel = m - tc[static_cast<int64_t>(t) * 4 + j];
-        muf[c][j] = static_cast<float>(rel);
-#if GMMB_MU_HILO
-        mulo[c][j] = static_cast<float>(rel - static_cast<double>(muf[c][j]));
-#endif
+        rel[j] = m - tc[static_cast<int64_t>(t) * 4 + j];
+        muf[c][j] = static_cast<float>(rel[j]);
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j <= i; ++j) {
+          s = fma(static_cast<double>(pp[c][i * (i + 1) / 2 + j]),
+                  static_cast<double>(muf[c][j]), s);
+        }
+        nb[c][i] = static_cast<float>(-s);
       }
     }
-#if GMMB_MU_HILO
-#define GMMB_D(xc, c, j) (((xc) - muf[c][j]) - mulo[c][j])
-#else
-#define GMMB_D(xc, c, j) ((xc) - muf[c][j])
-#endif
     __syncthreads();
 
     for (int q = 0; q < npts; q += P) {
-      // ---- phase A: log2 densities ----
-      // l = base2 - |P'd|^2 (GMMB_BASE_HILO keeps q = |P'd|^2 and forms
-      // ((hi - shift) + lo) - q so the ~30-unit normaliser is never rounded)
+      // ---- phase A: log2 densities l = base2 - |y|^2 ----
       float l[CPT][P], e[CPT][P];
 #pragma unroll
       for (int p = 0; p < P; ++p) {
         const float4 x = sm.xs[q + p];
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
-          const float d0 = GMMB_D(x.x, c, 0), d1 = GMMB_D(x.y, c, 1), d2 = GMMB_D(x.z, c, 2);
+#if GMMB_PXB
+          const float y0 = fmaf(pp[c][0], x.x, nb[c][0]);
+          const float y1 = fmaf(pp[c][2], x.y, fmaf(pp[c][1], x.x, nb[c][1]));
+          const float y2 = fmaf(pp[c][5], x.z, fmaf(pp[c][4], x.y, fmaf(pp[c][3], x.x, nb[c][2])));
+#else
+          const float d0 = x.x - muf[c][0], d1 = x.y - muf[c][1], d2 = x.z - muf[c][2];
           const float y0 = pp[c][0] * d0;
           const float y1 = fmaf(pp[c][2], d1, pp[c][1] * d0);
           const float y2 = fmaf(pp[c][5], d2, fmaf(pp[c][4], d1, pp[c][3] * d0));
-#if GMMB_BASE_HILO
-          float lv = fmaf(y2, y2, fmaf(y1, y1, y0 * y0));
-          if constexpr (D == 4) {
-            const float d3 = GMMB_D(x.w, c, 3);
-            const float y3 = fmaf(pp[c][9], d3, fmaf(pp[c][8], d2, fmaf(pp[c][7], d1, pp[c][6] * d0)));
-            lv = fmaf(y3, y3, lv);
-          }
-          l[c][p] = base2[c] == -INFINITY ? INFINITY : lv;  // holds q
-#else
+#endif
           float lv = fmaf(-y2, y2, fmaf(-y1, y1, fmaf(-y0, y0, base2[c])));
           if constexpr (D == 4) {
-            const float d3 = GMMB_D(x.w, c, 3);
+#if GMMB_PXB
+            const float y3 = fmaf(pp[c][9], x.w, fmaf(pp[c][8], x.z,
+                                  fmaf(pp[c][7], x.y, fmaf(pp[c][6], x.x, nb[c][3]))));
+#else
+            const float d3 = x.w - muf[c][3];
             const float y3 = fmaf(pp[c][9], d3, fmaf(pp[c][8], d2, fmaf(pp[c][7], d1, pp[c][6] * d0)));
+#endif
             lv = fmaf(-y3, y3, lv);
           }
           l[c][p] = lv;
-#endif
         }
       }
-#if GMMB_BASE_HILO
-#define GMMB_ARG(c, p, m) (((base2[c] - (m)) + blo[c]) - l[c][p])
-#define GMMB_LV(c, p) (base2[c] - l[c][p])
-#else
-#define GMMB_ARG(c, p, m) (l[c][p] - (m))
-#define GMMB_LV(c, p) (l[c][p])
-#endif
       const bool valid_g = q + fp < npts;  // this lane group's point
       float S = 1.f, M = 0.f;              // lane group's sum and shift
       bool exact = exact_mode != 0;
       if (!exact) {
-        // ---- phase B: normalise by the previous iteration's lse ----
-        const float4 h0 = *reinterpret_cast<const float4*>(&sm.sh[q]);
-        const float4 h1 = *reinterpret_cast<const float4*>(&sm.sh[q + 4]);
-        const float shp[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+        // ---- phase B: unshifted sum of 2^l over all components ----
         float v[P];
 #pragma unroll
         for (int p = 0; p < P; ++p) {
           v[p] = 0.f;
 #pragma unroll
           for (int c = 0; c < CPT; ++c) {
-            e[c][p] = ex2f(GMMB_ARG(c, p, shp[p]));
+            e[c][p] = ex2f(l[c][p]);
             v[p] += e[c][p];
           }
         }
@@ -325,18 +328,17 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW)
           S = cluster_combine<C, false>(&sm.xsum[xb][fp], lane);
           xb ^= 1;
         }
-        M = sm.sh[q + fp];
         // identical inputs in every warp => warp-, CTA- and cluster-uniform
         exact = __any_sync(0xffffffffu, valid_g && !(S >= 0x1p-64f && S <= 0x1p64f));
       }
       if (exact) {
-        // ---- exact max-shift path (first iteration, or the shift failed) ----
+        // ---- exact max-shift path (forced, or the plain sum left range) ----
         float v[P];
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-          v[p] = GMMB_LV(0, p);
+          v[p] = l[0][p];
 #pragma unroll
-          for (int c = 1; c < CPT; ++c) v[p] = fmaxf(v[p], GMMB_LV(c, p));
+          for (int c = 1; c < CPT; ++c) v[p] = fmaxf(v[p], l[c][p]);
         }
         float r = warp_reduce_scatter<P, true>(v, lane);
         if ((lane & 3) == 0) sm.red[rb][lane >> 2][warp] = r;
@@ -356,7 +358,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW)
           v[p] = 0.f;
 #pragma unroll
           for (int c = 0; c < CPT; ++c) {
-            e[c][p] = ex2f(GMMB_ARG(c, p, mp));
+            e[c][p] = ex2f(l[c][p] - mp);
             v[p] += e[c][p];
           }
         }
@@ -372,12 +374,8 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW)
           xb ^= 1;
         }
       }
-      if (finisher && valid_g && rank == 0) {
-        const float lse2 = M + lg2f(S);
-        ll_acc += static_cast<double>(lse2);
-        lse[t0 + q + fp] = lse2;
-      }
-      const float scale_g = valid_g ? (GMMB_SCALE_IEEE ? 1.f / S : rcpf(S)) : 0.f;
+      if (finisher && valid_g && rank == 0) ll_acc += static_cast<double>(M + lg2f(S));
+      const float scale_g = valid_g ? rcpf(S) : 0.f;
       // ---- phase C: responsibilities and statistics centred at mu_old ----
 #pragma unroll
       for (int p = 0; p < P; ++p) {
@@ -390,7 +388,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW)
           float dd[D], w[D];
 #pragma unroll
           for (int j = 0; j < D; ++j) {
-            dd[j] = GMMB_D(xv[j], c, j);
+            dd[j] = xv[j] - muf[c][j];
             w[j] = r * dd[j];
           }
           acc[c][0] += r;
@@ -407,27 +405,9 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW)
           }
         }
       }
-      if (GMMB_FLUSH_SUBTILES < 16 && ((q / P + 1) % GMMB_FLUSH_SUBTILES) == 0) {
-#pragma unroll
-        for (int c = 0; c < CPT; ++c)
-#pragma unroll
-          for (int s = (GMMB_FLUSH_LO); s < (NS < GMMB_FLUSH_HI ? NS : GMMB_FLUSH_HI); ++s) {
-            acc64[(c * NS + s) * T + tid] += static_cast<double>(acc[c][s]);
-            acc[c][s] = 0.f;
-          }
-      }
+      if (GMMB_FLUSH_SUBTILES < 16 && ((q / P + 1) % GMMB_FLUSH_SUBTILES) == 0) promote(acc);
     }
-    // promote the tile's FP32 partial sums to FP64
-#pragma unroll
-    for (int c = 0; c < CPT; ++c)
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        acc64[(c * NS + s) * T + tid] += static_cast<double>(acc[c][s]);
-        acc[c][s] = 0.f;
-      }
-#undef GMMB_D
-#undef GMMB_ARG
-#undef GMMB_LV
+    promote(acc);  // the tile's remaining FP32 partial sums
   }
   __syncthreads();
 #pragma unroll
@@ -436,7 +416,11 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW)
     if (k < kpad) {
       double* out = partials + (static_cast<int64_t>(cid) * kpad + k) * NS;
 #pragma unroll
-      for (int s = 0; s < NS; ++s) out[s] = acc64[(c * NS + s) * T + tid];
+      for (int s2 = 0; s2 < NSP; ++s2) {
+        const double2 v = acc64[(c * NSP + s2) * T + tid];
+        out[2 * s2] = v.x;
+        if (2 * s2 + 1 < NS) out[2 * s2 + 1] = v.y;
+      }
     }
   }
   if (warp == 0) {  // ll partial of this cluster: the 8 finisher lanes, in order
@@ -450,16 +434,328 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW)
     cg::this_cluster().sync();
   }
 }
+// ---------------------------------------------------------------------------
+// Software-pipelined variant for one CTA per component set (K <= 512).
+//
+// The normaliser of sub-tile s needs a CTA-wide sum; instead of a
+// __syncthreads per sub-tile, each thread posts its warp's partials for
+// sub-tile s to a ring slot and arrives on that slot's mbarrier, then goes
+// on to the log densities of sub-tile s+1 before waiting for s. The warp
+// shuffle chain of s+1 and the statistics of s are one basic block, so the
+// shuffle and barrier latencies hide behind FFMA work of the same warp.
+// Three slots suffice: a thread that writes slot s % 3 has passed the wait
+// for s - 1, so every thread has finished reading sub-tile s - 3.
+// ---------------------------------------------------------------------------
+constexpr int kRing = 3;
+
+template <int NW, int P>
+struct PipeSmem {
+  float4 xs[kTile];
+  float red[kRing][P][NW];  // per-warp partials per point, one ring slot per sub-tile
+  float xred[2][P][NW];     // exact-path scratch (max, then sum), __syncthreads-ordered
+  unsigned long long bar[kRing];
+};
+
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(b));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(b));
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(a)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(b));
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+template <int D, int NW, int P, int CPT>
+__global__ void __launch_bounds__(NW * 32, 16 / NW)
+    estep_stats_pipe_kernel(const float4* __restrict__ xt,
+                            const double* __restrict__ tc, int64_t n, int ntiles,
+                            ModelBuf b0, ModelBuf b1, const EmState* __restrict__ st,
+                            int kpad, double* __restrict__ partials,
+                            double* __restrict__ ll_part, int exact_mode) {
+  constexpr int NP = npacked(D);
+  constexpr int NS = nstats(D);
+  constexpr int NSP = (NS + 1) / 2;
+  constexpr int T = NW * 32;
+  using Smem = PipeSmem<NW, P>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  double2* acc64 = reinterpret_cast<double2*>(smem_raw + ((sizeof(Smem) + 15) & ~size_t(15)));
+
+  if (st->done) return;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int k_cur = st->k_cur;
+  const ModelBuf& mb = st->cur ? b1 : b0;
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < kRing; ++i) mbar_init(&sm.bar[i], T);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+
+  float pp[CPT][NP];
+  float base2[CPT];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    const int k = c * T + tid;
+    base2[c] = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < NP; ++j) pp[c][j] = 0.f;
+    if (k < k_cur) {
+      const float4* c4 = reinterpret_cast<const float4*>(mb.cst + k);
+      float cc[12];
+      const float4 a = c4[0], b = c4[1], e = c4[2];
+      cc[0] = a.x; cc[1] = a.y; cc[2] = a.z; cc[3] = a.w;
+      cc[4] = b.x; cc[5] = b.y; cc[6] = b.z; cc[7] = b.w;
+      cc[8] = e.x; cc[9] = e.y; cc[10] = e.z; cc[11] = e.w;
+#pragma unroll
+      for (int j = 0; j < NP; ++j) pp[c][j] = cc[j];
+      base2[c] = cc[10];
+    }
+  }
+  float acc[CPT][NS];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c)
+#pragma unroll
+    for (int s = 0; s < NS; ++s) acc[c][s] = 0.f;
+#pragma unroll
+  for (int i = 0; i < CPT * NSP; ++i) acc64[i * T + tid] = make_double2(0.0, 0.0);
+  auto promote = [&]() {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c)
+#pragma unroll
+      for (int s2 = 0; s2 < NSP; ++s2) {
+        double2 v = acc64[(c * NSP + s2) * T + tid];
+        v.x += static_cast<double>(acc[c][2 * s2]);
+        acc[c][2 * s2] = 0.f;
+        if (2 * s2 + 1 < NS) {
+          v.y += static_cast<double>(acc[c][2 * s2 + 1]);
+          acc[c][2 * s2 + 1] = 0.f;
+        }
+        acc64[(c * NSP + s2) * T + tid] = v;
+      }
+  };
+
+  double ll_acc = 0.0;  // warp 0, lanes with lane % 4 == 0 (one point each)
+  const bool finisher = warp == 0 && (lane & 3) == 0;
+  const int fp = lane >> 2;  // point of this lane's group
+  unsigned gsub = 0;         // global sub-tile counter (ring slot / parity)
+  int xb = 0;                // exact-path scratch rotation
+  float muf[CPT][D], nb[CPT][D];
+
+  // log2 densities of the P points at q (sm.xs) for this thread's components
+  auto dens = [&](int q, float (&l)[CPT][P]) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const float4 x = sm.xs[q + p];
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const float y0 = fmaf(pp[c][0], x.x, nb[c][0]);
+        const float y1 = fmaf(pp[c][2], x.y, fmaf(pp[c][1], x.x, nb[c][1]));
+        const float y2 = fmaf(pp[c][5], x.z, fmaf(pp[c][4], x.y, fmaf(pp[c][3], x.x, nb[c][2])));
+        float lv = fmaf(-y2, y2, fmaf(-y1, y1, fmaf(-y0, y0, base2[c])));
+        if constexpr (D == 4) {
+          const float y3 = fmaf(pp[c][9], x.w, fmaf(pp[c][8], x.z,
+                                fmaf(pp[c][7], x.y, fmaf(pp[c][6], x.x, nb[c][3]))));
+          lv = fmaf(-y3, y3, lv);
+        }
+        l[c][p] = lv;
+      }
+    }
+  };
+  // phase A + the warp part of phase B: e = 2^l, warp reduce-scatter
+  auto stage_a = [&](int q, float (&e)[CPT][P]) -> float {
+    dens(q, e);
+    float v[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      v[p] = 0.f;
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        e[c][p] = ex2f(e[c][p]);
+        v[p] += e[c][p];
+      }
+    }
+    return warp_reduce_scatter<P, false>(v, lane);
+  };
+  auto post = [&](float r) {
+    const int slot = gsub % kRing;
+    if ((lane & 3) == 0) sm.red[slot][lane >> 2][warp] = r;
+    mbar_arrive(&sm.bar[slot]);
+    ++gsub;
+  };
+  // CTA combine of sub-tile gs (posted), exact fallback, statistics
+  auto stage_c = [&](int q, int npts, unsigned gs, float (&e)[CPT][P]) {
+    const int slot = gs % kRing;
+    mbar_wait(&sm.bar[slot], (gs / kRing) & 1u);
+    float S = cta_combine<NW, P, false>(sm.red[slot], lane);
+    float M = 0.f;
+    const bool valid_g = q + fp < npts;
+    const bool exact = __any_sync(0xffffffffu, valid_g && (exact_mode != 0 ||
+                                                           !(S >= 0x1p-64f && S <= 0x1p64f)));
+    if (exact) {  // CTA-uniform: identical S in every warp
+      float v[P];
+      dens(q, e);
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        v[p] = e[0][p];
+#pragma unroll
+        for (int c = 1; c < CPT; ++c) v[p] = fmaxf(v[p], e[c][p]);
+      }
+      float r = warp_reduce_scatter<P, true>(v, lane);
+      if ((lane & 3) == 0) sm.xred[xb][lane >> 2][warp] = r;
+      __syncthreads();
+      M = cta_combine<NW, P, true>(sm.xred[xb], lane);
+      xb ^= 1;
+      M = M == -INFINITY ? 0.f : M;
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const float mp = __shfl_sync(0xffffffffu, M, p * 4);
+        v[p] = 0.f;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+          e[c][p] = ex2f(e[c][p] - mp);
+          v[p] += e[c][p];
+        }
+      }
+      r = warp_reduce_scatter<P, false>(v, lane);
+      if ((lane & 3) == 0) sm.xred[xb][lane >> 2][warp] = r;
+      __syncthreads();
+      S = cta_combine<NW, P, false>(sm.xred[xb], lane);
+      xb ^= 1;
+    }
+    if (finisher && valid_g) ll_acc += static_cast<double>(M + lg2f(S));
+    const float scale_g = valid_g ? rcpf(S) : 0.f;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const float sc = __shfl_sync(0xffffffffu, scale_g, p * 4);
+      const float4 x = sm.xs[q + p];
+      const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const float r = e[c][p] * sc;
+        float dd[D], w[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          dd[j] = xv[j] - muf[c][j];
+          w[j] = r * dd[j];
+        }
+        acc[c][0] += r;
+#pragma unroll
+        for (int j = 0; j < D; ++j) acc[c][1 + j] += w[j];
+        int s = 1 + D;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+#pragma unroll
+          for (int j = 0; j <= i; ++j) {
+            acc[c][s] = fmaf(w[i], dd[j], acc[c][s]);
+            ++s;
+          }
+        }
+      }
+    }
+    if (GMMB_FLUSH_SUBTILES < 16 && ((q / P + 1) % GMMB_FLUSH_SUBTILES) == 0) promote();
+  };
+
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t t0 = static_cast<int64_t>(t) * kTile;
+    const int npts = static_cast<int>(min64(kTile, n - t0));
+    __syncthreads();  // previous tile fully consumed (and barrier init visible)
+    for (int i = tid; i < kTile; i += T) {
+      sm.xs[i] = i < npts ? xt[t0 + i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const int k = c * T + tid;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const double m = k < k_cur ? mb.mu[k * 4 + j] : 0.0;
+        muf[c][j] = static_cast<float>(m - tc[static_cast<int64_t>(t) * 4 + j]);
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j <= i; ++j) {
+          s = fma(static_cast<double>(pp[c][i * (i + 1) / 2 + j]),
+                  static_cast<double>(muf[c][j]), s);
+        }
+        nb[c][i] = static_cast<float>(-s);
+      }
+    }
+    __syncthreads();
+    // pipeline over the tile's sub-tiles: A(s) | C(s-1) + post(s)
+    float ea[CPT][P], eb[CPT][P];
+    post(stage_a(0, ea));
+    int q = P;
+    while (true) {
+      if (q >= npts) {
+        stage_c(q - P, npts, gsub - 1, ea);
+        break;
+      }
+      {
+        const float r = stage_a(q, eb);
+        stage_c(q - P, npts, gsub - 1, ea);
+        post(r);
+      }
+      q += P;
+      if (q >= npts) {
+        stage_c(q - P, npts, gsub - 1, eb);
+        break;
+      }
+      {
+        const float r = stage_a(q, ea);
+        stage_c(q - P, npts, gsub - 1, eb);
+        post(r);
+      }
+      q += P;
+    }
+    promote();  // the tile's remaining FP32 partial sums
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    const int k = c * T + tid;
+    if (k < kpad) {
+      double* out = partials + (static_cast<int64_t>(blockIdx.x) * kpad + k) * NS;
+#pragma unroll
+      for (int s2 = 0; s2 < NSP; ++s2) {
+        const double2 v = acc64[(c * NSP + s2) * T + tid];
+        out[2 * s2] = v.x;
+        if (2 * s2 + 1 < NS) out[2 * s2 + 1] = v.y;
+      }
+    }
+  }
+  if (warp == 0) {  // ll partial of this CTA: the 8 finisher lanes, in order
+    double s = 0.0;
+#pragma unroll
+    for (int p = 0; p < P; ++p) s += __shfl_sync(0xffffffffu, ll_acc, p * 4);
+    if (lane == 0) ll_part[blockIdx.x] = s * kLn2;
+  }
+}
 
 template <int D, int NW, int C, int P, int CPT>
 cudaError_t launch_estep_t(const PointsDev& pts, const ModelBuf* bufs,
                            const EmState* st, int kpad, double* partials,
-                           double* ll_part, float* lse, int exact_mode, int sm_count,
+                           double* ll_part, int exact_mode, int sm_count,
                            cudaStream_t s, int* ncl_out) {
-  using Smem = EstepSmem<D, NW, C, P>;
-  auto kern = estep_stats_kernel<D, NW, C, P, CPT>;
+  using Smem = typename std::conditional<C == 1 && GMMB_PIPE, PipeSmem<NW, P>,
+                                         EstepSmem<D, NW, C, P>>::type;
+  auto kern = (C == 1 && GMMB_PIPE) ? estep_stats_pipe_kernel<D, NW, P, CPT>
+                                    : estep_stats_kernel<D, NW, C, P, CPT>;
   const size_t smem = ((sizeof(Smem) + 15) & ~size_t(15)) +
-                      sizeof(double) * nstats(D) * CPT * NW * 32;
+                      sizeof(double2) * ((nstats(D) + 1) / 2) * CPT * NW * 32;
   static int per_sm_dev[64] = {0};  // per template instance and device
   int dev = 0;
   cudaGetDevice(&dev);
@@ -495,19 +791,19 @@ cudaError_t launch_estep_t(const PointsDev& pts, const ModelBuf* bufs,
   cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, kern, pts.xt, pts.tc, pts.n, pts.ntiles,
                             bufs[0], bufs[1], st, kpad, partials, ll_part,
-                            lse, exact_mode);
+                            exact_mode);
 }
 
 template <int D>
 cudaError_t launch_estep_d(const PointsDev& pts, const ModelBuf* bufs,
                            const EmState* st, int k0, double* partials,
-                           double* ll_part, float* lse, int exact_mode, int sm_count,
+                           double* ll_part, int exact_mode, int sm_count,
                            cudaStream_t s, int* ncl) {
   constexpr int P = 8;
   const int kpad = k0;
 #define GMMB_L(NW, C, CPT) \
   return launch_estep_t<D, NW, C, P, CPT>(pts, bufs, st, kpad, partials, ll_part, \
-                                          lse, exact_mode, sm_count, s, ncl)
+                                          exact_mode, sm_count, s, ncl)
   if (k0 <= 32) GMMB_L(1, 1, 1);
   if (k0 <= 64) GMMB_L(2, 1, 1);
   if (k0 <= 128) GMMB_L(4, 1, 1);
@@ -1092,12 +1388,12 @@ cudaError_t launch_factor_dump(int d, const ModelBuf* bufs, const EmState* st,
 // ---------------------------------------------------------------------------
 cudaError_t launch_estep_stats(const PointsDev& pts, const ModelBuf* bufs,
                                const EmState* st, int k0, double* partials,
-                               double* ll_part, float* lse, int exact_mode,
+                               double* ll_part, int exact_mode,
                                int sm_count, cudaStream_t s, int* ncl_out) {
   if (pts.d == 4)
-    return launch_estep_d<4>(pts, bufs, st, k0, partials, ll_part, lse, exact_mode,
+    return launch_estep_d<4>(pts, bufs, st, k0, partials, ll_part, exact_mode,
                              sm_count, s, ncl_out);
-  return launch_estep_d<3>(pts, bufs, st, k0, partials, ll_part, lse, exact_mode,
+  return launch_estep_d<3>(pts, bufs, st, k0, partials, ll_part, exact_mode,
                            sm_count, s, ncl_out);
 }
 

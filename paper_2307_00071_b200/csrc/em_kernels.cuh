@@ -33,13 +33,11 @@ struct PointsDev {
 
 // Fused E-step + sufficient statistics (one EM iteration's data pass).
 // Writes per-cluster FP64 partial statistics [ncl][kpad][nstats(D)] and
-// per-cluster log-likelihood partials (natural log) [ncl]. lse[n] (sorted
-// point order, log2 units) holds the previous iteration's per-point
-// log-sum-exp on entry (the normalising shift, unless exact_mode) and this
-// iteration's on exit.
+// per-cluster log-likelihood partials (natural log) [ncl]. exact_mode = 1
+// forces the max-shifted normalisation on every sub-tile (validation).
 cudaError_t launch_estep_stats(const PointsDev& pts, const ModelBuf* bufs,
                                const EmState* st, int k0, double* partials,
-                               double* ll_part, float* lse, int exact_mode,
+                               double* ll_part, int exact_mode,
                                int sm_count, cudaStream_t s, int* ncl_out);
 
 // (partials == nullptr: only report the cluster count *ncl_out.)

@@ -13,4 +13,6 @@ p = gm.synthetic_frame_cloud()
 ctx.upload(p)
 for _ in range(args.reps):
     r = ctx.fit_k_resident(args.k, gm.EmParams(100, args.tol, 1e-6, 0))
-    print(f"iters {r.em_iterations} kinit {r.ms_kinit:.3f} em {r.ms_em:.3f} ms", flush=True)
+    print(f"iters {r.em_iterations} kinit {r.ms_kinit:.3f} m0 {r.ms_mstep0:.3f} em {r.ms_em:.3f} "
+          f"estep {r.ms_estep:.3f} ms ({r.ms_estep / max(r.em_iterations, 1) * 1e3:.1f} us/iter) "
+          f"total {r.ms_total:.3f}", flush=True)
