@@ -36,6 +36,9 @@ METRIC = "EM point*component*iters/sec and ms per GMM fit"
 UNIT = "point*component*iter/s"
 FLOP_PER_UNIT = {4: 62.0, 3: 42.0}     # 2D^2 + 6D + 6
 NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+# DRAM traffic of one fused-E launch at cfg2 K=512 (ncu --set full capture)
+TRAFFIC_BYTES = 5.12e6
+TRAFFIC_SRC = "profiles/r1_estep_ncu.txt"
 
 
 def parse():
@@ -289,15 +292,17 @@ def main():
                      "em": statistics.mean(r.ms_em for r in res),
                      "estep_kernel": est_ms / args.steps},
         "em_only_value": units / (sum(r.ms_em for r in res) * 1e-3),
-        "roofline": {"bound": "fp32", "kernel": "estep_stats_kernel (fused E step + "
-                     "sufficient statistics)", "achieved": achieved_tf, "peak": peak_tf,
+        "roofline": {"bound": "fp32", "kernel": "estep_ws_kernel (warp-specialised fused E "
+                     "step + sufficient statistics)", "achieved": achieved_tf, "peak": peak_tf,
                      "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
                      "flop_per_unit": FLOP_PER_UNIT[d],
-                     "peak_source": "measured FFMA microbenchmark in this run "
-                                    "(MEASURED_PEAKS.json has no FP32 figure); nominal %.1f"
+                     "peak_source": "measured packed-FP32 (fma.rn.f32x2) microbenchmark in this "
+                                    "run (MEASURED_PEAKS.json has no FP32 figure); nominal %.1f"
                                     % NOMINAL_FP32_TFLOPS,
-                     "traffic": None,
-                     "traffic_note": "DRAM bytes/launch from ncu --set full in profiles/"},
+                     "traffic": TRAFFIC_BYTES,
+                     "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch, "
+                                     "ncu --set full (%s); algorithmic %.0f B (points 16 B each "
+                                     "+ FP64 partials)" % (TRAFFIC_SRC, 16 * n)},
         "clocks": clocks,
         "wall_s": wall,
         "device": {"sm_count": sm, "cc": "%d.%d" % (cc_major, cc_minor)},

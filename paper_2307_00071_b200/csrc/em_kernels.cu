@@ -30,7 +30,13 @@ namespace cg = cooperative_groups;
 #define GMMB_FLUSH_SUBTILES 2   // sub-tiles per FP32 -> FP64 promotion
 #endif
 #ifndef GMMB_PIPE
-#define GMMB_PIPE 1             // 1: software-pipelined kernel when one CTA holds all components
+#define GMMB_PIPE 1             // 1: warp-specialised packed kernel when one CTA holds all K
+#endif
+#ifndef GMMB_WS_P
+#define GMMB_WS_P 16            // points per sub-tile of the warp-specialised kernel
+#endif
+#ifndef GMMB_F2F_ALU
+#define GMMB_F2F_ALU 0          // 1: FP32 -> FP64 widening on the integer ALU
 #endif
 #ifndef GMMB_PXB
 #define GMMB_PXB 1              // 1: y = P'x - P'mu (FFMA chains); 0: y = P'(x - mu)
@@ -96,17 +102,18 @@ struct EstepSmem {
 };
 
 // Combines the NW per-warp partials of P points inside one warp: lane
-// (p = lane / 4, q = lane % 4) folds warps q, q+4, ... in order, then two
-// xor steps. Every warp computes the identical (order-fixed) value.
+// (p = lane / G, q = lane % G), G = 32 / P, folds warps q, q+G, ... in
+// order, then log2(G) xor steps. Every warp computes the identical
+// (order-fixed) value.
 template <int NW, int P, bool MAX>
 __device__ __forceinline__ float cta_combine(const float (&red)[P][NW], int lane) {
-  static_assert(P == 8, "lane mapping assumes 8 points per sub-tile");
-  const int p = lane >> 2, q = lane & 3;
+  constexpr int G = 32 / P;  // lanes per point
+  const int p = lane / G, q = lane % G;
   float v = MAX ? -INFINITY : 0.f;
 #pragma unroll
-  for (int w = q; w < NW; w += 4) v = MAX ? fmaxf(v, red[p][w]) : v + red[p][w];
+  for (int w = q; w < NW; w += G) v = MAX ? fmaxf(v, red[p][w]) : v + red[p][w];
 #pragma unroll
-  for (int off = 1; off <= 2; off <<= 1) {
+  for (int off = 1; off < G; off <<= 1) {
     const float o = __shfl_xor_sync(0xffffffffu, v, off);
     v = MAX ? fmaxf(v, o) : v + o;
   }
@@ -435,27 +442,25 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW)
   }
 }
 // ---------------------------------------------------------------------------
-// Software-pipelined variant for one CTA per component set (K <= 512).
+// Packed, software-pipelined fused E step (one CTA holds all K <= 512
+// components; thread tid owns the component pair (tid, T + tid)).
 //
-// The normaliser of sub-tile s needs a CTA-wide sum; instead of a
-// __syncthreads per sub-tile, each thread posts its warp's partials for
-// sub-tile s to a ring slot and arrives on that slot's mbarrier, then goes
-// on to the log densities of sub-tile s+1 before waiting for s. The warp
-// shuffle chain of s+1 and the statistics of s are one basic block, so the
-// shuffle and barrier latencies hide behind FFMA work of the same warp.
-// Three slots suffice: a thread that writes slot s % 3 has passed the wait
-// for s - 1, so every thread has finished reading sub-tile s - 3.
+// * Packed FP32: every per-(point, component) operation is identical for the
+//   thread's two components, so phases A and C run on f32x2 register pairs
+//   (FFMA2 / FADD2 / FMUL2: 64 lane-operations per warp instruction; B200
+//   reaches its 74 TFLOP/s FP32 peak only through this form, and it issues
+//   half the instructions). Points enter as scalar broadcast operands.
+// * Phase A evaluates q - base = |P'x - P'mu'|^2 - base with FFMA chains
+//   (P'mu' formed once per tile in FP64); e = 2^-(q - base) on the MUFU.
+// * Phase B sums e with no shift: log2 densities of any point that matters
+//   lie far inside FP32's exponent range; a sub-tile whose sum leaves
+//   [2^-64, 2^64] is redone with the exact max shift (CTA-uniform decision).
+// * Software pipelining: the CTA-wide sum of sub-tile s is posted to a ring
+//   slot + mbarrier, and the thread computes the densities of s+1 before
+//   waiting for s, so shuffle/barrier latency hides behind FFMA work. Three
+//   slots suffice: a thread that writes slot s % 3 has passed the wait for
+//   s - 1, so every thread has finished reading sub-tile s - 3.
 // ---------------------------------------------------------------------------
-constexpr int kRing = 3;
-
-template <int NW, int P>
-struct PipeSmem {
-  float4 xs[kTile];
-  float red[kRing][P][NW];  // per-warp partials per point, one ring slot per sub-tile
-  float xred[2][P][NW];     // exact-path scratch (max, then sum), __syncthreads-ordered
-  unsigned long long bar[kRing];
-};
-
 __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
   const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(b));
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
@@ -476,273 +481,469 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
       : "memory");
 }
 
-template <int D, int NW, int P, int CPT>
-__global__ void __launch_bounds__(NW * 32, 16 / NW)
-    estep_stats_pipe_kernel(const float4* __restrict__ xt,
-                            const double* __restrict__ tc, int64_t n, int ntiles,
-                            ModelBuf b0, ModelBuf b1, const EmState* __restrict__ st,
-                            int kpad, double* __restrict__ partials,
-                            double* __restrict__ ll_part, int exact_mode) {
+// f32x2 register pairs (lo = component tid, hi = component T + tid)
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t pk(float a, float b) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float lo2(f2_t v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return a;
+}
+__device__ __forceinline__ float hi2(f2_t v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return b;
+}
+__device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) {
+  f2_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2_t add2(f2_t a, f2_t b) {
+  f2_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) {
+  f2_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float ex2n(float x) {  // 2^-x
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(-x));
+  return y;
+}
+
+// FP32 -> FP64 widening. The XU pipe (F2F) also carries the ex2 of every
+// unit; GMMB_F2F_ALU = 1 widens on the integer ALU instead (exact for
+// normal numbers; FP32 subnormals, ~1e-38, flush to zero).
+__device__ __forceinline__ double f32_to_f64(float f) {
+#if GMMB_F2F_ALU
+  const unsigned b = __float_as_uint(f);
+  const unsigned e = b & 0x7f800000u;
+  const unsigned hi = e ? (((b >> 3) & 0x0fffffffu) + 0x38000000u) | (b & 0x80000000u) : 0u;
+  const unsigned lo = e ? (b << 29) : 0u;
+  return __hiloint2double(static_cast<int>(hi), static_cast<int>(lo));
+#else
+  return static_cast<double>(f);
+#endif
+}
+
+// ---------------------------------------------------------------------------
+// Warp-specialised fused E step (one CTA holds all K <= 512 components).
+//
+// Producer warps own the log densities, consumer warps own the statistics:
+//   producer thread j (component pair j, T + j), per P-point sub-tile:
+//     Q = |P'x - P'mu'|^2 - base2 (FFMA chains; P'mu' = P'mu - P'c_t per
+//     tile in FP64), e = 2^-Q (MUFU), e pairs -> e ring slot, a warp
+//     reduce-scatter of the per-point sums -> red ring slot, arrive full;
+//   consumer thread j: wait full, combine the per-warp partials (fixed
+//     order) into S, copy its e pairs, arrive empty, then r = e / S and the
+//     centred statistics sum r, sum r d, sum r d d^T (d = x - mu_old) in FP32
+//     pairs, promoted to FP64 shared memory every GMMB_FLUSH_SUBTILES
+//     sub-tiles.
+// Point tiles (2 KB) and tile centres arrive by TMA bulk copies into a
+// double buffer, issued a tile ahead by one producer thread.
+// Every per-(point, component) operation is identical for a thread's two
+// components, so both roles run on f32x2 register pairs (FFMA2 / FADD2 /
+// FMUL2): B200 reaches its FP32 peak only through that form, and it issues
+// half the instructions. Splitting the roles halves each thread's live
+// registers, which keeps enough independent FFMA2 chains in flight.
+//
+// The normaliser is an unshifted sum: the log2 densities of any point that
+// matters lie far inside FP32's exponent range. A sub-tile whose sum leaves
+// [2^-64, 2^64] (outliers far from every component) is redone by the
+// consumers with the exact max shift (uniform decision: S is identical in
+// every consumer warp), reloading the constants from global memory.
+// ---------------------------------------------------------------------------
+constexpr int kRing = 3;  // sub-tile slots in flight between the roles
+
+template <int NWH, int P>
+struct WsSmem {
+  float4 xs[2][kTile];                   // point tiles (TMA destination)
+  double tcs[2][4];                      // tile centres (TMA destination)
+  float4 ering[kRing][P / 2][NWH * 32];  // e pairs: [slot][point pair][thread]
+  float red[kRing][P][NWH];              // producer per-warp partial sums
+  float xred[2][P][NWH];                 // consumer exact-path scratch
+  double mu[4][2 * NWH * 32];            // mu (FP64), [q][component]
+  unsigned long long full[kRing], empty[kRing], xs_full[2], xs_free[2];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+
+template <int D, int NWH, int P>
+__global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
+    estep_ws_kernel(const float4* __restrict__ xt, const double* __restrict__ tc,
+                    int64_t n, int ntiles, ModelBuf b0, ModelBuf b1,
+                    const EmState* __restrict__ st, int kpad,
+                    double* __restrict__ partials, double* __restrict__ ll_part,
+                    int exact_mode) {
   constexpr int NP = npacked(D);
   constexpr int NS = nstats(D);
-  constexpr int NSP = (NS + 1) / 2;
-  constexpr int T = NW * 32;
-  using Smem = PipeSmem<NW, P>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int T = NWH * 32;  // threads per role
+  constexpr int G = 32 / P;    // lanes per point after the warp reduce-scatter
+  using Smem = WsSmem<NWH, P>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  // consumer FP64 accumulators: acc64[s * T + j] = (component j, component T + j)
   double2* acc64 = reinterpret_cast<double2*>(smem_raw + ((sizeof(Smem) + 15) & ~size_t(15)));
 
   if (st->done) return;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int warp = tid >> 5;
+  const bool producer = threadIdx.x < T;
+  const int j = static_cast<int>(threadIdx.x) % T;  // component pair (j, T + j)
+  const int lane = j & 31;
+  const int warp = j >> 5;
   const int k_cur = st->k_cur;
   const ModelBuf& mb = st->cur ? b1 : b0;
-  if (tid == 0) {
+  constexpr unsigned kTileBytes = kTile * sizeof(float4) + 4 * sizeof(double);
+  auto issue_tile = [&](int t, int buf) {  // one thread: TMA bulk copy of tile t
+    mbar_expect_tx(&sm.xs_full[buf], kTileBytes);
+    bulk_g2s(sm.xs[buf], xt + static_cast<int64_t>(t) * kTile, kTile * sizeof(float4),
+             &sm.xs_full[buf]);
+    bulk_g2s(sm.tcs[buf], tc + static_cast<int64_t>(t) * 4, 4 * sizeof(double), &sm.xs_full[buf]);
+  };
+  if (threadIdx.x == 0) {
 #pragma unroll
-    for (int i = 0; i < kRing; ++i) mbar_init(&sm.bar[i], T);
+    for (int i = 0; i < kRing; ++i) {
+      mbar_init(&sm.full[i], T);
+      mbar_init(&sm.empty[i], T);
+    }
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.xs_full[b], 1);
+      mbar_init(&sm.xs_free[b], T);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (static_cast<int>(blockIdx.x) < ntiles) issue_tile(blockIdx.x, 0);
   }
 
-  float pp[CPT][NP];
-  float base2[CPT];
+  // component constants as pairs (lo = component j, hi = component T + j)
+  auto load_consts = [&](f2_t (&PP)[NP], f2_t& NBASE) {
+    float pp[2][NP], base2[2];
 #pragma unroll
-  for (int c = 0; c < CPT; ++c) {
-    const int k = c * T + tid;
-    base2[c] = -INFINITY;
+    for (int c = 0; c < 2; ++c) {
+      const int k = c * T + j;
+      base2[c] = -INFINITY;
 #pragma unroll
-    for (int j = 0; j < NP; ++j) pp[c][j] = 0.f;
-    if (k < k_cur) {
-      const float4* c4 = reinterpret_cast<const float4*>(mb.cst + k);
-      float cc[12];
-      const float4 a = c4[0], b = c4[1], e = c4[2];
-      cc[0] = a.x; cc[1] = a.y; cc[2] = a.z; cc[3] = a.w;
-      cc[4] = b.x; cc[5] = b.y; cc[6] = b.z; cc[7] = b.w;
-      cc[8] = e.x; cc[9] = e.y; cc[10] = e.z; cc[11] = e.w;
+      for (int q = 0; q < NP; ++q) pp[c][q] = 0.f;
+      if (k < k_cur) {
+        const float4* c4 = reinterpret_cast<const float4*>(mb.cst + k);
+        float cc[12];
+        const float4 a = c4[0], b = c4[1], e = c4[2];
+        cc[0] = a.x; cc[1] = a.y; cc[2] = a.z; cc[3] = a.w;
+        cc[4] = b.x; cc[5] = b.y; cc[6] = b.z; cc[7] = b.w;
+        cc[8] = e.x; cc[9] = e.y; cc[10] = e.z; cc[11] = e.w;
 #pragma unroll
-      for (int j = 0; j < NP; ++j) pp[c][j] = cc[j];
-      base2[c] = cc[10];
-    }
-  }
-  float acc[CPT][NS];
-#pragma unroll
-  for (int c = 0; c < CPT; ++c)
-#pragma unroll
-    for (int s = 0; s < NS; ++s) acc[c][s] = 0.f;
-#pragma unroll
-  for (int i = 0; i < CPT * NSP; ++i) acc64[i * T + tid] = make_double2(0.0, 0.0);
-  auto promote = [&]() {
-#pragma unroll
-    for (int c = 0; c < CPT; ++c)
-#pragma unroll
-      for (int s2 = 0; s2 < NSP; ++s2) {
-        double2 v = acc64[(c * NSP + s2) * T + tid];
-        v.x += static_cast<double>(acc[c][2 * s2]);
-        acc[c][2 * s2] = 0.f;
-        if (2 * s2 + 1 < NS) {
-          v.y += static_cast<double>(acc[c][2 * s2 + 1]);
-          acc[c][2 * s2 + 1] = 0.f;
-        }
-        acc64[(c * NSP + s2) * T + tid] = v;
+        for (int q = 0; q < NP; ++q) pp[c][q] = cc[q];
+        base2[c] = cc[10];
       }
+    }
+#pragma unroll
+    for (int q = 0; q < NP; ++q) PP[q] = pk(pp[0][q], pp[1][q]);
+    NBASE = pk(-base2[0], -base2[1]);
   };
-
-  double ll_acc = 0.0;  // warp 0, lanes with lane % 4 == 0 (one point each)
-  const bool finisher = warp == 0 && (lane & 3) == 0;
-  const int fp = lane >> 2;  // point of this lane's group
-  unsigned gsub = 0;         // global sub-tile counter (ring slot / parity)
-  int xb = 0;                // exact-path scratch rotation
-  float muf[CPT][D], nb[CPT][D];
-
-  // log2 densities of the P points at q (sm.xs) for this thread's components
-  auto dens = [&](int q, float (&l)[CPT][P]) {
+  // NB = -P'(mu - c_t): FP64 dot of the FP32 factor with the FP32-rounded
+  // tile-relative mean (the same mu' the consumers centre on), rounded once
+  auto tile_nb = [&](const double* ct, const f2_t (&PP)[NP], f2_t (&NB)[D]) {
+    float nbf[2][D];
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-      const float4 x = sm.xs[q + p];
+    for (int c = 0; c < 2; ++c) {
+      float muf[D];
 #pragma unroll
-      for (int c = 0; c < CPT; ++c) {
-        const float y0 = fmaf(pp[c][0], x.x, nb[c][0]);
-        const float y1 = fmaf(pp[c][2], x.y, fmaf(pp[c][1], x.x, nb[c][1]));
-        const float y2 = fmaf(pp[c][5], x.z, fmaf(pp[c][4], x.y, fmaf(pp[c][3], x.x, nb[c][2])));
-        float lv = fmaf(-y2, y2, fmaf(-y1, y1, fmaf(-y0, y0, base2[c])));
-        if constexpr (D == 4) {
-          const float y3 = fmaf(pp[c][9], x.w, fmaf(pp[c][8], x.z,
-                                fmaf(pp[c][7], x.y, fmaf(pp[c][6], x.x, nb[c][3]))));
-          lv = fmaf(-y3, y3, lv);
-        }
-        l[c][p] = lv;
-      }
-    }
-  };
-  // phase A + the warp part of phase B: e = 2^l, warp reduce-scatter
-  auto stage_a = [&](int q, float (&e)[CPT][P]) -> float {
-    dens(q, e);
-    float v[P];
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      v[p] = 0.f;
-#pragma unroll
-      for (int c = 0; c < CPT; ++c) {
-        e[c][p] = ex2f(e[c][p]);
-        v[p] += e[c][p];
-      }
-    }
-    return warp_reduce_scatter<P, false>(v, lane);
-  };
-  auto post = [&](float r) {
-    const int slot = gsub % kRing;
-    if ((lane & 3) == 0) sm.red[slot][lane >> 2][warp] = r;
-    mbar_arrive(&sm.bar[slot]);
-    ++gsub;
-  };
-  // CTA combine of sub-tile gs (posted), exact fallback, statistics
-  auto stage_c = [&](int q, int npts, unsigned gs, float (&e)[CPT][P]) {
-    const int slot = gs % kRing;
-    mbar_wait(&sm.bar[slot], (gs / kRing) & 1u);
-    float S = cta_combine<NW, P, false>(sm.red[slot], lane);
-    float M = 0.f;
-    const bool valid_g = q + fp < npts;
-    const bool exact = __any_sync(0xffffffffu, valid_g && (exact_mode != 0 ||
-                                                           !(S >= 0x1p-64f && S <= 0x1p64f)));
-    if (exact) {  // CTA-uniform: identical S in every warp
-      float v[P];
-      dens(q, e);
-#pragma unroll
-      for (int p = 0; p < P; ++p) {
-        v[p] = e[0][p];
-#pragma unroll
-        for (int c = 1; c < CPT; ++c) v[p] = fmaxf(v[p], e[c][p]);
-      }
-      float r = warp_reduce_scatter<P, true>(v, lane);
-      if ((lane & 3) == 0) sm.xred[xb][lane >> 2][warp] = r;
-      __syncthreads();
-      M = cta_combine<NW, P, true>(sm.xred[xb], lane);
-      xb ^= 1;
-      M = M == -INFINITY ? 0.f : M;
-#pragma unroll
-      for (int p = 0; p < P; ++p) {
-        const float mp = __shfl_sync(0xffffffffu, M, p * 4);
-        v[p] = 0.f;
-#pragma unroll
-        for (int c = 0; c < CPT; ++c) {
-          e[c][p] = ex2f(e[c][p] - mp);
-          v[p] += e[c][p];
-        }
-      }
-      r = warp_reduce_scatter<P, false>(v, lane);
-      if ((lane & 3) == 0) sm.xred[xb][lane >> 2][warp] = r;
-      __syncthreads();
-      S = cta_combine<NW, P, false>(sm.xred[xb], lane);
-      xb ^= 1;
-    }
-    if (finisher && valid_g) ll_acc += static_cast<double>(M + lg2f(S));
-    const float scale_g = valid_g ? rcpf(S) : 0.f;
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      const float sc = __shfl_sync(0xffffffffu, scale_g, p * 4);
-      const float4 x = sm.xs[q + p];
-      const float xv[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-      for (int c = 0; c < CPT; ++c) {
-        const float r = e[c][p] * sc;
-        float dd[D], w[D];
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-          dd[j] = xv[j] - muf[c][j];
-          w[j] = r * dd[j];
-        }
-        acc[c][0] += r;
-#pragma unroll
-        for (int j = 0; j < D; ++j) acc[c][1 + j] += w[j];
-        int s = 1 + D;
-#pragma unroll
-        for (int i = 0; i < D; ++i) {
-#pragma unroll
-          for (int j = 0; j <= i; ++j) {
-            acc[c][s] = fmaf(w[i], dd[j], acc[c][s]);
-            ++s;
-          }
-        }
-      }
-    }
-    if (GMMB_FLUSH_SUBTILES < 16 && ((q / P + 1) % GMMB_FLUSH_SUBTILES) == 0) promote();
-  };
-
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t t0 = static_cast<int64_t>(t) * kTile;
-    const int npts = static_cast<int>(min64(kTile, n - t0));
-    __syncthreads();  // previous tile fully consumed (and barrier init visible)
-    for (int i = tid; i < kTile; i += T) {
-      sm.xs[i] = i < npts ? xt[t0 + i] : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-      const int k = c * T + tid;
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        const double m = k < k_cur ? mb.mu[k * 4 + j] : 0.0;
-        muf[c][j] = static_cast<float>(m - tc[static_cast<int64_t>(t) * 4 + j]);
-      }
+      for (int q = 0; q < D; ++q) muf[q] = static_cast<float>(sm.mu[q][c * T + j] - ct[q]);
 #pragma unroll
       for (int i = 0; i < D; ++i) {
         double s = 0.0;
 #pragma unroll
-        for (int j = 0; j <= i; ++j) {
-          s = fma(static_cast<double>(pp[c][i * (i + 1) / 2 + j]),
-                  static_cast<double>(muf[c][j]), s);
+        for (int q = 0; q <= i; ++q) {
+          const f2_t pij = PP[i * (i + 1) / 2 + q];
+          s = fma(static_cast<double>(c ? hi2(pij) : lo2(pij)), static_cast<double>(muf[q]), s);
         }
-        nb[c][i] = static_cast<float>(-s);
+        nbf[c][i] = static_cast<float>(-s);
       }
     }
-    __syncthreads();
-    // pipeline over the tile's sub-tiles: A(s) | C(s-1) + post(s)
-    float ea[CPT][P], eb[CPT][P];
-    post(stage_a(0, ea));
-    int q = P;
-    while (true) {
-      if (q >= npts) {
-        stage_c(q - P, npts, gsub - 1, ea);
-        break;
+#pragma unroll
+    for (int q = 0; q < D; ++q) NB[q] = pk(nbf[0][q], nbf[1][q]);
+  };
+  // Q = q - base2 = -(log2 density) of the P points at xs, both components
+  auto dens = [&](const float4* xs, const f2_t (&PP)[NP], const f2_t (&NB)[D], f2_t NBASE,
+                  f2_t (&Q)[P]) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const float4 x = xs[p];
+      const f2_t X0 = pk(x.x, x.x), X1 = pk(x.y, x.y), X2 = pk(x.z, x.z);
+      const f2_t Y0 = fma2(PP[0], X0, NB[0]);
+      const f2_t Y1 = fma2(PP[2], X1, fma2(PP[1], X0, NB[1]));
+      const f2_t Y2 = fma2(PP[5], X2, fma2(PP[4], X1, fma2(PP[3], X0, NB[2])));
+      f2_t qv = fma2(Y2, Y2, fma2(Y1, Y1, fma2(Y0, Y0, NBASE)));
+      if constexpr (D == 4) {
+        const f2_t X3 = pk(x.w, x.w);
+        const f2_t Y3 = fma2(PP[9], X3, fma2(PP[8], X2, fma2(PP[7], X1, fma2(PP[6], X0, NB[3]))));
+        qv = fma2(Y3, Y3, qv);
       }
-      {
-        const float r = stage_a(q, eb);
-        stage_c(q - P, npts, gsub - 1, ea);
-        post(r);
-      }
-      q += P;
-      if (q >= npts) {
-        stage_c(q - P, npts, gsub - 1, eb);
-        break;
-      }
-      {
-        const float r = stage_a(q, ea);
-        stage_c(q - P, npts, gsub - 1, eb);
-        post(r);
-      }
-      q += P;
+      Q[p] = qv;
     }
-    promote();  // the tile's remaining FP32 partial sums
+  };
+
+  if (!producer) {  // mu (FP64) of both components, read by both roles
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int k = c * T + j;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sm.mu[q][k] = k < k_cur ? mb.mu[k * 4 + q] : 0.0;
+    }
   }
   __syncthreads();
+  if (producer) {
+    // ======================= producer warps =======================
+    f2_t PP[NP], NBASE, NB[D];
+    load_consts(PP, NBASE);
+    unsigned g = 0;  // global sub-tile counter
+    int ti = 0;      // tile iteration
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++ti) {
+      const int npts = static_cast<int>(min64(kTile, n - static_cast<int64_t>(t) * kTile));
+      const int nsub = (npts + P - 1) / P;
+      const int tb = ti & 1;
+      mbar_wait(&sm.xs_full[tb], (ti >> 1) & 1u);
+      {
+        double ct[4];
 #pragma unroll
-  for (int c = 0; c < CPT; ++c) {
-    const int k = c * T + tid;
+        for (int q = 0; q < 4; ++q) ct[q] = sm.tcs[tb][q];
+        tile_nb(ct, PP, NB);
+      }
+      for (int s = 0; s < nsub; ++s, ++g) {
+        if (j == 0 && s == min(kRing, nsub - 1)) {
+          // prefetch the next tile: consumers have started this tile (they
+          // read sub-tile g - kRing), so they released the other buffer
+          const int tn = t + gridDim.x;
+          if (tn < ntiles) {
+            if (ti >= 1) mbar_wait(&sm.xs_free[tb ^ 1], ((ti - 1) >> 1) & 1u);
+            issue_tile(tn, tb ^ 1);
+          }
+        }
+        const int slot = g % kRing;
+        if (g >= kRing) mbar_wait(&sm.empty[slot], ((g / kRing) - 1) & 1u);
+        f2_t E[P];
+        dens(&sm.xs[tb][s * P], PP, NB, NBASE, E);
+        float v[P];
+#pragma unroll
+        for (int p = 0; p < P; p += 2) {
+          const float e0 = ex2n(lo2(E[p])), e1 = ex2n(hi2(E[p]));
+          const float e2 = ex2n(lo2(E[p + 1])), e3 = ex2n(hi2(E[p + 1]));
+          sm.ering[slot][p / 2][j] = make_float4(e0, e1, e2, e3);
+          v[p] = e0 + e1;
+          v[p + 1] = e2 + e3;
+        }
+        const float r = warp_reduce_scatter<P, false>(v, lane);
+        if ((lane % G) == 0) sm.red[slot][lane / G][warp] = r;
+        mbar_arrive(&sm.full[slot]);
+      }
+    }
+    return;  // producers hold no statistics
+  }
+
+  // ======================= consumer warps =======================
+  f2_t ACC[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    ACC[s] = 0ull;
+    acc64[s * T + j] = make_double2(0.0, 0.0);
+  }
+  // FP32 register sums are widened into the FP64 shared accumulators every
+  // GMMB_FLUSH_SUBTILES x 8 points (a second FP32 level, or a
+  // longer cadence, costs accuracy that EM amplifies ~25x).
+  auto promote = [&]() {  // registers -> acc64
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      double2 v = acc64[s * T + j];
+      v.x += f32_to_f64(lo2(ACC[s]));
+      v.y += f32_to_f64(hi2(ACC[s]));
+      ACC[s] = 0ull;
+      acc64[s * T + j] = v;
+    }
+  };
+  double ll_acc = 0.0;  // consumer warp 0, lanes with lane % G == 0 (one point each)
+  const bool finisher = warp == 0 && (lane % G) == 0;
+  const int fp = lane / G;
+  int xb = 0;
+  unsigned g = 0;
+  int ti = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++ti) {
+    const int npts = static_cast<int>(min64(kTile, n - static_cast<int64_t>(t) * kTile));
+    const int nsub = (npts + P - 1) / P;
+    const int tb = ti & 1;
+    mbar_wait(&sm.xs_full[tb], (ti >> 1) & 1u);
+    f2_t NMU[D];  // -(mu - c_t) as FP32 pairs
+    {
+      float nm[2][D];
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int q = 0; q < D; ++q)
+          nm[c][q] = static_cast<float>(-(sm.mu[q][c * T + j] - sm.tcs[tb][q]));
+#pragma unroll
+      for (int q = 0; q < D; ++q) NMU[q] = pk(nm[0][q], nm[1][q]);
+    }
+    for (int s = 0; s < nsub; ++s, ++g) {
+      const int q0 = s * P;
+      const int slot = g % kRing;
+      mbar_wait(&sm.full[slot], (g / kRing) & 1u);
+      float S = cta_combine<NWH, P, false>(sm.red[slot], lane);
+      f2_t E[P];
+#pragma unroll
+      for (int p = 0; p < P; p += 2) {
+        const float4 v = sm.ering[slot][p / 2][j];
+        E[p] = pk(v.x, v.y);
+        E[p + 1] = pk(v.z, v.w);
+      }
+      mbar_arrive(&sm.empty[slot]);
+      float M = 0.f;
+      const bool valid_g = q0 + fp < npts;
+      const bool exact = __any_sync(0xffffffffu, valid_g && (exact_mode != 0 ||
+                                                             !(S >= 0x1p-64f && S <= 0x1p64f)));
+      if (exact) {  // uniform over consumer warps: identical S everywhere
+        f2_t PP[NP], NBASE, NB[D];
+        load_consts(PP, NBASE);
+        float nbf[2][D];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q <= i; ++q) {
+              const f2_t pij = PP[i * (i + 1) / 2 + q];
+              acc = fma(static_cast<double>(c ? hi2(pij) : lo2(pij)),
+                        sm.mu[q][c * T + j] - sm.tcs[tb][q], acc);
+            }
+            nbf[c][i] = static_cast<float>(-acc);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < D; ++q) NB[q] = pk(nbf[0][q], nbf[1][q]);
+        dens(&sm.xs[tb][q0], PP, NB, NBASE, E);
+        float v[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) v[p] = fmaxf(-lo2(E[p]), -hi2(E[p]));
+        float r = warp_reduce_scatter<P, true>(v, lane);
+        if ((lane % G) == 0) sm.xred[xb][lane / G][warp] = r;
+        asm volatile("bar.sync 2, %0;" ::"r"(T) : "memory");
+        M = cta_combine<NWH, P, true>(sm.xred[xb], lane);
+        xb ^= 1;
+        M = M == -INFINITY ? 0.f : M;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const float mp = __shfl_sync(0xffffffffu, M, p * G);
+          const float e0 = ex2n(lo2(E[p]) + mp), e1 = ex2n(hi2(E[p]) + mp);
+          E[p] = pk(e0, e1);
+          v[p] = e0 + e1;
+        }
+        r = warp_reduce_scatter<P, false>(v, lane);
+        if ((lane % G) == 0) sm.xred[xb][lane / G][warp] = r;
+        asm volatile("bar.sync 2, %0;" ::"r"(T) : "memory");
+        S = cta_combine<NWH, P, false>(sm.xred[xb], lane);
+        xb ^= 1;
+      }
+      if (finisher && valid_g) ll_acc += static_cast<double>(M + lg2f(S));
+      const float scale_g = valid_g ? rcpf(S) : 0.f;
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const float sc = __shfl_sync(0xffffffffu, scale_g, p * G);
+        const float4 x = sm.xs[tb][q0 + p];
+        const float xv[4] = {x.x, x.y, x.z, x.w};
+        const f2_t R = mul2(E[p], pk(sc, sc));
+        f2_t DD[D], W[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          DD[i] = add2(pk(xv[i], xv[i]), NMU[i]);
+          W[i] = mul2(R, DD[i]);
+        }
+        ACC[0] = add2(ACC[0], R);
+#pragma unroll
+        for (int i = 0; i < D; ++i) ACC[1 + i] = add2(ACC[1 + i], W[i]);
+        int q = 1 + D;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+#pragma unroll
+          for (int c = 0; c <= i; ++c) {
+            ACC[q] = fma2(W[i], DD[c], ACC[q]);
+            ++q;
+          }
+        }
+        if (GMMB_FLUSH_SUBTILES < 16 && ((q0 + p + 1) % (GMMB_FLUSH_SUBTILES * 8)) == 0) promote();
+      }
+    }
+    promote();  // the tile's remaining FP32 partial sums
+    mbar_arrive(&sm.xs_free[tb]);  // this consumer is done with tile buffer tb
+  }
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int k = c * T + j;
     if (k < kpad) {
       double* out = partials + (static_cast<int64_t>(blockIdx.x) * kpad + k) * NS;
 #pragma unroll
-      for (int s2 = 0; s2 < NSP; ++s2) {
-        const double2 v = acc64[(c * NSP + s2) * T + tid];
-        out[2 * s2] = v.x;
-        if (2 * s2 + 1 < NS) out[2 * s2 + 1] = v.y;
+      for (int s = 0; s < NS; ++s) {
+        const double2 v = acc64[s * T + j];
+        out[s] = c ? v.y : v.x;
       }
     }
   }
-  if (warp == 0) {  // ll partial of this CTA: the 8 finisher lanes, in order
+  if (warp == 0) {  // ll partial of this CTA: the P finisher lanes, in order
     double s = 0.0;
 #pragma unroll
-    for (int p = 0; p < P; ++p) s += __shfl_sync(0xffffffffu, ll_acc, p * 4);
+    for (int p = 0; p < P; ++p) s += __shfl_sync(0xffffffffu, ll_acc, p * G);
     if (lane == 0) ll_part[blockIdx.x] = s * kLn2;
   }
+}
+
+template <int D, int NWH>
+cudaError_t launch_estep_ws(const PointsDev& pts, const ModelBuf* bufs, const EmState* st,
+                            int kpad, double* partials, double* ll_part, int exact_mode,
+                            int sm_count, cudaStream_t s, int* ncl_out) {
+  constexpr int P = GMMB_WS_P;
+  using Smem = WsSmem<NWH, P>;
+  auto kern = estep_ws_kernel<D, NWH, P>;
+  const size_t smem = ((sizeof(Smem) + 15) & ~size_t(15)) + sizeof(double2) * nstats(D) * NWH * 32;
+  static int per_sm_dev[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& per_sm = per_sm_dev[dev & 63];
+  if (per_sm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 2 * NWH * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+  }
+  int ncl = sm_count * per_sm;
+  if (ncl > pts.ntiles) ncl = pts.ntiles;
+  if (ncl < 1) ncl = 1;
+  *ncl_out = ncl;
+  if (!partials) return cudaSuccess;  // size query only
+  kern<<<ncl, 2 * NWH * 32, smem, s>>>(pts.xt, pts.tc, pts.n, pts.ntiles, bufs[0], bufs[1], st,
+                                       kpad, partials, ll_part, exact_mode);
+  return cudaGetLastError();
 }
 
 template <int D, int NW, int C, int P, int CPT>
@@ -750,10 +951,8 @@ cudaError_t launch_estep_t(const PointsDev& pts, const ModelBuf* bufs,
                            const EmState* st, int kpad, double* partials,
                            double* ll_part, int exact_mode, int sm_count,
                            cudaStream_t s, int* ncl_out) {
-  using Smem = typename std::conditional<C == 1 && GMMB_PIPE, PipeSmem<NW, P>,
-                                         EstepSmem<D, NW, C, P>>::type;
-  auto kern = (C == 1 && GMMB_PIPE) ? estep_stats_pipe_kernel<D, NW, P, CPT>
-                                    : estep_stats_kernel<D, NW, C, P, CPT>;
+  using Smem = EstepSmem<D, NW, C, P>;
+  auto kern = estep_stats_kernel<D, NW, C, P, CPT>;
   const size_t smem = ((sizeof(Smem) + 15) & ~size_t(15)) +
                       sizeof(double2) * ((nstats(D) + 1) / 2) * CPT * NW * 32;
   static int per_sm_dev[64] = {0};  // per template instance and device
@@ -804,11 +1003,23 @@ cudaError_t launch_estep_d(const PointsDev& pts, const ModelBuf* bufs,
 #define GMMB_L(NW, C, CPT) \
   return launch_estep_t<D, NW, C, P, CPT>(pts, bufs, st, kpad, partials, ll_part, \
                                           exact_mode, sm_count, s, ncl)
+#define GMMB_W(NWH) \
+  return launch_estep_ws<D, NWH>(pts, bufs, st, kpad, partials, ll_part, exact_mode, \
+                                 sm_count, s, ncl)
+#if GMMB_PIPE
+  // warp-specialised packed kernel: K <= 64 NWH
+  if (k0 <= 64) GMMB_W(1);
+  if (k0 <= 128) GMMB_W(2);
+  if (k0 <= 256) GMMB_W(4);
+  if (k0 <= 512) GMMB_W(8);
+#undef GMMB_W
+#else
   if (k0 <= 32) GMMB_L(1, 1, 1);
   if (k0 <= 64) GMMB_L(2, 1, 1);
   if (k0 <= 128) GMMB_L(4, 1, 1);
   if (k0 <= 256) GMMB_L(8, 1, 1);
   if (k0 <= 512) GMMB_L(8, 1, 2);
+#endif
   if (k0 <= 1024) GMMB_L(8, 2, 2);
   if (k0 <= 2048) GMMB_L(8, 4, 2);
   if (k0 <= 4096) GMMB_L(8, 8, 2);

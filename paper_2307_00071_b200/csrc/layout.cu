@@ -141,10 +141,10 @@ __global__ void __launch_bounds__(kTile)
 #pragma unroll
   for (int j = 0; j < 4; ++j) c[j] = red[j][0] / cnt;
   if (tid < 4) tc[static_cast<int64_t>(t) * 4 + tid] = c[tid];
-  if (v) {
-    xt[i] = make_float4(static_cast<float>(x[0] - c[0]), static_cast<float>(x[1] - c[1]),
-                        static_cast<float>(x[2] - c[2]), static_cast<float>(x[3] - c[3]));
-  }
+  // padding points of the last tile are zero (the E kernel copies whole tiles)
+  xt[i] = v ? make_float4(static_cast<float>(x[0] - c[0]), static_cast<float>(x[1] - c[1]),
+                          static_cast<float>(x[2] - c[2]), static_cast<float>(x[3] - c[3]))
+            : make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 }  // namespace
