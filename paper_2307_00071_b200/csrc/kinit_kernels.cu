@@ -13,17 +13,22 @@
 // Work per point per round is cut three ways:
 //  * the (seed, round) half of the counter hash is hoisted out of the point
 //    loop and keys are stored pre-multiplied, leaving one mix64 per point;
-//  * clocks are first evaluated in FP32 with a proven relative error bound
-//    (< 1e-4); only points within 4e-4 of their warp's approximate minimum
-//    (typically one per warp) get the exact FP64 log and division, which
-//    therefore decide the argmin exactly;
+//  * clocks are evaluated in FP32 with a proven relative error bound
+//    (< 3e-5); the grid exchanges the top-2 approximate clocks, and only
+//    when the runner-up lies within the 4e-4 band of the best (round-0 key
+//    duplicates, near-ties) do the points inside the band get the exact
+//    FP64 log and division, which then decide the argmin exactly;
+//  * the draws of round r + 1 are computed while the round-r exchange is in
+//    flight (a dedicated communication warp per CTA holds no points);
 //  * the nearest-centre pass (sogmm.cpp:290-312) is folded into the rounds:
 //    round r already evaluates d(x, c_{r-1}), so the running argmin with
 //    strict < over ascending centre index gives the labels for free.
-// The per-round grid exchange: each CTA publishes one 64-byte slot, arrives
-// on a monotonic counter with a release reduction, one thread per CTA polls
-// the counter (relaxed loads, one acquire fence), then every CTA reduces all
-// slots in the same order.
+// The per-round grid exchange uses the LL protocol: each CTA publishes its
+// top-2 as 8-byte (payload, round tag) words, which are single-copy atomic,
+// and the communication warp of every CTA polls all CTAs' words (each lane
+// its slots concurrently) and reduces them in a fixed order — no fence, no
+// arrival counter (scripts/micro/ll_bench.cu: 2.2 us per exchange against
+// 2.5 us for counter + fence, 3.5 us through a master CTA).
 #include <climits>
 
 #include "kinit_kernels.cuh"
@@ -117,6 +122,38 @@ __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// LL-protocol words: (payload, tag) written and read as one 8-byte access
+__device__ __forceinline__ void st_ll(uint2* p, unsigned v, unsigned tag) {
+  asm volatile("st.relaxed.gpu.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(v), "r"(tag)
+               : "memory");
+}
+__device__ __forceinline__ unsigned ld_ll(const uint2* p, unsigned tag) {
+  unsigned v, t;
+  do {
+    asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(v), "=r"(t) : "l"(p)
+                 : "memory");
+  } while (t != tag);
+  return v;
+}
+// N consecutive LL words polled together: all loads issue back to back,
+// then every tag is checked (one L2 round trip per attempt, not N)
+template <int N>
+__device__ __forceinline__ void ld_ll_n(const uint2* p, unsigned tag, unsigned (&v)[N]) {
+  static_assert(N % 2 == 0, "pairs of words (16-byte loads)");
+  bool ok;
+  do {
+    ok = true;
+#pragma unroll
+    for (int i = 0; i < N; i += 2) {
+      unsigned t0, t1;
+      asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(v[i]), "=r"(t0), "=r"(v[i + 1]), "=r"(t1)
+                   : "l"(p + i)
+                   : "memory");
+      ok = ok && t0 == tag && t1 == tag;
+    }
+  } while (!ok);
+}
 __device__ __forceinline__ void fence_acq_rel() {
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
@@ -140,23 +177,6 @@ constexpr int kSeedThreads = 384;
 constexpr int kSeedWarps = kSeedThreads / 32;
 constexpr int kMaxSeedBlocks = 1024;
 
-struct SeedSmem {
-  double wc[kSeedWarps];
-  long long wi[kSeedWarps];
-  int wo[kSeedWarps];
-  double wx[kSeedWarps][4];
-  double gc[kMaxSeedBlocks / 32];
-  long long gi[kMaxSeedBlocks / 32];
-  int gs[kMaxSeedBlocks / 32];
-  long long gu[kMaxSeedBlocks / 32];
-  long long win;
-  int win_owner;
-  int fallbacks;
-  double cx[4];
-  double scx[kMaxSeedBlocks][4];   // gathered slot coordinates
-  int sown[kMaxSeedBlocks];
-};
-
 __device__ __forceinline__ void shfl_cand(double& c, long long& i, int& s,
                                           int off) {
   const double c2 = __shfl_xor_sync(0xffffffffu, c, off);
@@ -169,6 +189,66 @@ __device__ __forceinline__ void shfl_cand(double& c, long long& i, int& s,
   }
 }
 
+// top-2 merge of approximate clocks: (a1, i1) best (lowest index on ties),
+// a2 the smallest value that is not the best entry
+__device__ __forceinline__ void merge_top2(float& a1, int& i1, float& a2, float b1, int j1,
+                                           float b2) {
+  const bool take = j1 >= 0 && (i1 < 0 || b1 < a1 || (b1 == a1 && j1 < i1));
+  if (take) {
+    a2 = fminf(a1, b2);
+    a1 = b1;
+    i1 = j1;
+  } else {
+    a2 = fminf(a2, b1);
+  }
+}
+
+// Grid top-2 over nblk LL slots (a1, i1, a2, pad) by one warp: a lane polls
+// its slots (lane, lane + 32, ...) concurrently, one L2 round trip per
+// attempt; the result (identical in every lane) does not depend on arrival
+// order.
+__device__ __forceinline__ void gather_top2(const uint2* slots, int nblk, unsigned tag, int lane,
+                                            float& g1, int& gi, float& g2) {
+  for (int base = 0; base < nblk; base += 256) {
+    unsigned pend = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (base + lane + 32 * q < nblk) pend |= 1u << q;
+    while (pend) {
+      unsigned v[8][4];
+      bool ok[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        ok[q] = false;
+        if ((pend >> q) & 1) {
+          const uint2* w = slots + (base + lane + 32 * q) * 4;
+          unsigned t0, t1, t2, t3;
+          asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(v[q][0]), "=r"(t0), "=r"(v[q][1]), "=r"(t1) : "l"(w) : "memory");
+          asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(v[q][2]), "=r"(t2), "=r"(v[q][3]), "=r"(t3) : "l"(w + 2) : "memory");
+          ok[q] = t0 == tag && t1 == tag && t2 == tag && t3 == tag;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (ok[q]) {
+          merge_top2(g1, gi, g2, __uint_as_float(v[q][0]), static_cast<int>(v[q][1]),
+                     __uint_as_float(v[q][2]));
+          pend &= ~(1u << q);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const float b1 = __shfl_xor_sync(0xffffffffu, g1, off);
+    const int k1 = __shfl_xor_sync(0xffffffffu, gi, off);
+    const float b2 = __shfl_xor_sync(0xffffffffu, g2, off);
+    merge_top2(g1, gi, g2, b1, k1, b2);
+  }
+}
+
 // arrive on a monotonic grid counter and wait for all CTAs (one thread)
 __device__ __forceinline__ void grid_exchange(unsigned* counter, unsigned target) {
   red_release_add(counter, 1u);
@@ -177,7 +257,47 @@ __device__ __forceinline__ void grid_exchange(unsigned* counter, unsigned target
   fence_acq_rel();
 }
 
-// Each thread keeps PPT points (stride = grid threads) in registers.
+// Each compute thread keeps PPT points (stride = grid compute threads) in
+// registers. Warp 0 of every CTA holds no points: it is the communication
+// warp. Per round:
+//   compute warps: fold centre r-1 into d2 / labels, approximate clocks
+//     a = -ln(u) / d2 from precomputed draws, warp top-2 -> shared memory;
+//   barrier;
+//   warp 0: CTA top-2, publish (LL slot); CTA 0's warp 0 gathers every
+//     slot, decides and publishes the winner record (16 spread copies);
+//     every warp 0 polls its copy;
+//   compute warps meanwhile draw -ln(u) for round r+1 (off the critical
+//     path);
+//   barrier.
+// The approximate argmin is exact unless the grid runner-up lies within the
+// FP32 error band (round 0 ties on duplicate keys, near-ties): then every
+// point inside the band gets the exact FP64 clock and a second exchange
+// decides on (clock, index), as the reference's strict-< scan does.
+constexpr int kCompWarps = kSeedWarps - 1;
+constexpr int kCompThreads = kCompWarps * 32;
+constexpr int kSlotWords = 4;  // approx: a1, i1, a2, pad; exact: clock lo, hi, idx, pad
+
+struct SeedSmem {
+  float wa1[kSeedWarps];
+  int wi1[kSeedWarps];
+  float wa2[kSeedWarps];
+  double ec[kSeedWarps];
+  long long ei[kSeedWarps];
+  long long gu[kSeedWarps];
+  double cx[4];
+  long long win;
+  float thr;
+  int exact_rounds;
+};
+
+__device__ __forceinline__ unsigned long long dbits(double v) {
+  return static_cast<unsigned long long>(__double_as_longlong(v));
+}
+__device__ __forceinline__ double bitsd(unsigned lo, unsigned hi) {
+  return __longlong_as_double(
+      static_cast<long long>((static_cast<unsigned long long>(hi) << 32) | lo));
+}
+
 __global__ void __launch_bounds__(kSeedThreads, 1)
     kpp_seed_kernel(const double* __restrict__ x64, int64_t n, int k,
                     uint64_t seed, KinitScratch scr) {
@@ -185,17 +305,20 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
   __shared__ SeedSmem sm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nblk = gridDim.x;
-  const long long G = static_cast<long long>(nblk) * kSeedThreads;
-  const long long g0 = static_cast<long long>(blockIdx.x) * kSeedThreads + tid;
+  const bool comm = warp == 0;
+  const long long G = static_cast<long long>(nblk) * kCompThreads;
+  const long long g0 = comm ? -1 : static_cast<long long>(blockIdx.x) * kCompThreads + tid - 32;
+  // LL regions (uint2 words): approx slots [2][nblk], exact slots [2][nblk]
+  uint2* llw = reinterpret_cast<uint2*>(scr.slots);
   double px[PPT][4], d2[PPT];
-  float inv[PPT];  // ~1/d2 in FP32 (approximate clocks only)
+  float inv[PPT], na[PPT];
   uint64_t kp[PPT];
   int lab[PPT];
   unsigned chosen = 0, valid = 0;
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
     const long long i = g0 + j * G;
-    const bool v = i < n;
+    const bool v = !comm && i < n;
     if (v) valid |= 1u << j;
 #pragma unroll
     for (int q = 0; q < 4; ++q) px[j][q] = v ? x64[q * n + i] : 0.0;
@@ -203,160 +326,171 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
     d2[j] = INFINITY;
     inv[j] = 0.f;
     lab[j] = 0;
+    na[j] = INFINITY;
   }
   // slots beyond the warp's last valid point are skipped (warp-uniform)
   const unsigned wvalid = __reduce_or_sync(0xffffffffu, valid);
-  if (tid == 0) sm.fallbacks = 0;
-  double c[4] = {0, 0, 0, 0};
-  unsigned epoch = 0;  // completed grid exchanges
-  for (int r = 0; r <= k; ++r) {
+  if (tid == 0) sm.exact_rounds = 0;
+  auto draw = [&](int r) {  // -ln(u) of round r, FP32 approximation
     const uint64_t pre = round_prefix(seed, r);
-    float a[PPT];
-    float amin = INFINITY;
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      a[j] = INFINITY;
-      if (!((wvalid >> j) & 1)) continue;
-      if (r > 0) {  // fold c_{r-1} (sogmm.cpp:229-238) + running label
-        const double dd = dist2(px[j][0], px[j][1], px[j][2], px[j][3], c);
-        if (dd < d2[j]) {
-          d2[j] = dd;
-          lab[j] = r - 1;
-          // 1/d2 for the approximate clock; d2 == 0 (a chosen point or a
-          // duplicate) is ineligible (sogmm.cpp:254)
-          const float f = __double2float_rn(dd);
-          inv[j] = dd > 0.0 ? (isinf(f) ? 1e-38f : rcp_approx(f)) : 0.f;
-        }
-      }
-      if (r == k) continue;
-      const float na = nlu_approx(mix64(pre + kp[j]));
-      const float aj = r == 0 ? na : (inv[j] > 0.f ? na * inv[j] : INFINITY);
-      a[j] = ((valid >> j) & 1) ? aj : INFINITY;
-      amin = fminf(amin, a[j]);
+      if ((wvalid >> j) & 1) na[j] = nlu_approx(mix64(pre + kp[j]));
     }
-    if (r == k) break;
-    // warp filter, then exact FP64 clocks for the few candidates
-    float wmin = amin;
+  };
+  if (!comm) draw(0);
+  double c[4] = {0, 0, 0, 0};
+  unsigned epoch = 0;  // completed counter-based grid exchanges (fallback)
+  for (int r = 0; r <= k; ++r) {
+    const unsigned tag = static_cast<unsigned>(r) + 1u;
+    const int par = r & 1;
+    uint2* slot_a = llw + par * nblk * kSlotWords;
+    uint2* slot_e = llw + (2 + par) * nblk * kSlotWords;
+    float a[PPT];
+    if (!comm) {
+      // ---- fold centre r-1 (sogmm.cpp:229-238), approximate clocks ----
+      float a1 = INFINITY, a2 = INFINITY;
+      int i1 = -1;
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1)
-      wmin = fminf(wmin, __shfl_xor_sync(0xffffffffu, wmin, off));
-    const float thr = wmin * kBand;
-    double bc = INFINITY;
-    long long bi = -1;
-    int bj = 0;
-#pragma unroll
-    for (int j = 0; j < PPT; ++j) {
-      if (!((wvalid >> j) & 1)) continue;
-      const bool cj = ((valid >> j) & 1) && (r == 0 || d2[j] > 0.0) && !(a[j] > thr);
-      if (__any_sync(0xffffffffu, cj)) {
-        if (cj) {
-          const double nl = nlu_exact(mix64(pre + kp[j]));
-          const double clk = r == 0 ? nl : nl / d2[j];
-          const long long i = g0 + j * G;
-          if (clk < INFINITY && cand_better(clk, i, bc, bi)) {
-            bc = clk;
-            bi = i;
-            bj = j;
+      for (int j = 0; j < PPT; ++j) {
+        a[j] = INFINITY;
+        if (!((wvalid >> j) & 1)) continue;
+        if (r > 0) {
+          const double dd = dist2(px[j][0], px[j][1], px[j][2], px[j][3], c);
+          if (dd < d2[j]) {
+            d2[j] = dd;
+            lab[j] = r - 1;
+            // d2 == 0 (a chosen point or a duplicate) is ineligible (:254)
+            const float f = __double2float_rn(dd);
+            inv[j] = dd > 0.0 ? (isinf(f) ? 1e-38f : rcp_approx(f)) : 0.f;
           }
         }
+        if (r == k) continue;
+        const float aj = r == 0 ? na[j] : (inv[j] > 0.f ? na[j] * inv[j] : INFINITY);
+        a[j] = ((valid >> j) & 1) ? aj : INFINITY;
+        if (a[j] < INFINITY) merge_top2(a1, i1, a2, a[j], static_cast<int>(g0 + j * G), INFINITY);
       }
-    }
-    // warp argmin: usually a single lane holds a candidate
-    const unsigned has = __ballot_sync(0xffffffffu, bi >= 0);
-    int src = has ? __ffs(has) - 1 : 0;
-    if (__popc(has) > 1) {
-      double wc = bc;
-      long long wi = bi;
-      int ws = lane;
+      if (r == k) break;
 #pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) shfl_cand(wc, wi, ws, off);
-      src = ws;
+      for (int off = 16; off >= 1; off >>= 1) {
+        const float b1 = __shfl_xor_sync(0xffffffffu, a1, off);
+        const int k1 = __shfl_xor_sync(0xffffffffu, i1, off);
+        const float b2 = __shfl_xor_sync(0xffffffffu, a2, off);
+        merge_top2(a1, i1, a2, b1, k1, b2);
+      }
+      if (lane == 0) {
+        sm.wa1[warp] = a1;
+        sm.wi1[warp] = i1;
+        sm.wa2[warp] = a2;
+      }
+    } else if (r == k) {
+      break;
     }
-    if (has && lane == src) {
-      double x0 = px[0][0], x1 = px[0][1], x2 = px[0][2], x3 = px[0][3];
+    __syncthreads();
+    if (comm) {
+      // ---- CTA top-2 -> LL slot (8-byte (payload, tag) words) ----
+      float c1 = lane >= 1 && lane < kSeedWarps ? sm.wa1[lane] : INFINITY;
+      int j1 = lane >= 1 && lane < kSeedWarps ? sm.wi1[lane] : -1;
+      float c2 = lane >= 1 && lane < kSeedWarps ? sm.wa2[lane] : INFINITY;
 #pragma unroll
-      for (int j = 1; j < PPT; ++j) {
-        if (bj == j) {
-          x0 = px[j][0]; x1 = px[j][1]; x2 = px[j][2]; x3 = px[j][3];
+      for (int off = 16; off >= 1; off >>= 1) {
+        const float b1 = __shfl_xor_sync(0xffffffffu, c1, off);
+        const int k1 = __shfl_xor_sync(0xffffffffu, j1, off);
+        const float b2 = __shfl_xor_sync(0xffffffffu, c2, off);
+        merge_top2(c1, j1, c2, b1, k1, b2);
+      }
+      if (lane == 0) {
+        uint2* w = slot_a + blockIdx.x * kSlotWords;
+        st_ll(w + 0, __float_as_uint(c1), tag);
+        st_ll(w + 1, static_cast<unsigned>(j1), tag);
+        st_ll(w + 2, __float_as_uint(c2), tag);
+        st_ll(w + 3, 0u, tag);
+      }
+      // ---- grid top-2: every CTA gathers every slot (all of a lane's
+      // slots polled concurrently), reduces in a fixed order ----
+      float g1 = INFINITY, g2 = INFINITY;
+      int gi = -1;
+      gather_top2(slot_a, nblk, tag, lane, g1, gi, g2);
+      // exact unless the runner-up lies within the FP32 error band
+      const bool need_exact = gi >= 0 && !(g2 > g1 * kBand);
+      const long long wi = need_exact ? -2 : gi;
+      if (lane < 4 && wi >= 0) sm.cx[lane] = __ldg(x64 + lane * n + wi);  // read-only cloud
+      if (lane == 0) {
+        sm.win = wi;
+        sm.thr = need_exact ? g1 * kBand : -1.f;
+      }
+    } else if (r + 1 < k) {
+      draw(r + 1);  // overlaps the exchange
+    }
+    __syncthreads();
+    if (sm.win == -2) {
+      // ---- exact resolution among the points inside the band (rare) ----
+      if (!comm) {
+        const float thr = sm.thr;
+        const uint64_t pre = round_prefix(seed, r);
+        double bc = INFINITY;
+        long long bi = -1;
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          if (!((wvalid >> j) & 1)) continue;
+          if (((valid >> j) & 1) && (r == 0 || d2[j] > 0.0) && !(a[j] > thr)) {
+            const double nl = nlu_exact(mix64(pre + kp[j]));
+            const double clk = r == 0 ? nl : nl / d2[j];
+            const long long i = g0 + j * G;
+            if (clk < INFINITY && cand_better(clk, i, bc, bi)) {
+              bc = clk;
+              bi = i;
+            }
+          }
+        }
+        int bs = 0;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) shfl_cand(bc, bi, bs, off);
+        if (lane == 0) {
+          sm.ec[warp] = bc;
+          sm.ei[warp] = bi;
         }
       }
-      sm.wc[warp] = bc;
-      sm.wi[warp] = bi;
-      sm.wo[warp] = static_cast<int>(g0);
-      sm.wx[warp][0] = x0; sm.wx[warp][1] = x1; sm.wx[warp][2] = x2; sm.wx[warp][3] = x3;
-    } else if (!has && lane == 0) {
-      sm.wc[warp] = INFINITY;
-      sm.wi[warp] = -1;
-      sm.wo[warp] = -1;
-    }
-    __syncthreads();
-    KppSlot* slots = scr.slots + (r & 1) * nblk;
-    if (warp == 0) {
-      double c1 = lane < kSeedWarps ? sm.wc[lane] : INFINITY;
-      long long i1 = lane < kSeedWarps ? sm.wi[lane] : -1;
-      int s1 = lane;
+      __syncthreads();
+      if (comm) {
+        double c1 = lane >= 1 && lane < kSeedWarps ? sm.ec[lane] : INFINITY;
+        long long j1 = lane >= 1 && lane < kSeedWarps ? sm.ei[lane] : -1;
+        int src = lane;
 #pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) shfl_cand(c1, i1, s1, off);
-      if (lane == 0) {
-        KppSlot& sl = slots[blockIdx.x];
-        sl.clock = c1;
-        sl.idx = i1;
-        sl.owner = i1 >= 0 ? sm.wo[s1] : -1;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) sl.cx[q] = i1 >= 0 ? sm.wx[s1][q] : 0.0;
-        ++epoch;
-        grid_exchange(scr.counter, static_cast<unsigned>(nblk) * epoch);
-      }
-    }
-    __syncthreads();
-    // every CTA reduces every CTA's slot in the same order => same winner
-    if (tid < ((nblk + 31) & ~31)) {
-      double gc = INFINITY;
-      long long gi = -1;
-      int gs = -1;
-      for (int b = tid; b < nblk; b += kSeedThreads) {
-        const volatile KppSlot& vs = slots[b];
-        const double c2 = vs.clock;
-        const long long i2 = vs.idx;
-        sm.sown[b] = vs.owner;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) sm.scx[b][q] = vs.cx[q];
-        if (cand_better(c2, i2, gc, gi)) {
-          gc = c2;
-          gi = i2;
-          gs = b;
+        for (int off = 16; off >= 1; off >>= 1) shfl_cand(c1, j1, src, off);
+        if (lane == 0) {
+          uint2* w = slot_e + blockIdx.x * kSlotWords;
+          const unsigned long long cb = dbits(c1);
+          st_ll(w + 0, static_cast<unsigned>(cb), tag);
+          st_ll(w + 1, static_cast<unsigned>(cb >> 32), tag);
+          st_ll(w + 2, static_cast<unsigned>(static_cast<int>(j1)), tag);
+          st_ll(w + 3, 0u, tag);
         }
-      }
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) shfl_cand(gc, gi, gs, off);
-      if (lane == 0) {
-        sm.gc[warp] = gc;
-        sm.gi[warp] = gi;
-        sm.gs[warp] = gs;
-      }
-    }
-    __syncthreads();
-    if (warp == 0) {
-      const int nw = (nblk + 31) >> 5;
-      double c1 = lane < nw ? sm.gc[lane] : INFINITY;
-      long long i1 = lane < nw ? sm.gi[lane] : -1;
-      int s1 = lane < nw ? sm.gs[lane] : -1;
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) shfl_cand(c1, i1, s1, off);
-      if (lane == 0) {
-        if (i1 >= 0 && c1 < INFINITY) {
-          sm.win = i1;
-          sm.win_owner = sm.sown[s1];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) sm.cx[q] = sm.scx[s1][q];
-        } else {
-          sm.win = -1;  // no eligible point anywhere: fallback below
+        double gc = INFINITY;
+        long long gj = -1;
+        for (int b = lane; b < nblk; b += 32) {
+          unsigned wv[4];
+          ld_ll_n<4>(slot_e + b * kSlotWords, tag, wv);
+          const double c2 = bitsd(wv[0], wv[1]);
+          const long long j2 = static_cast<int>(wv[2]);
+          if (cand_better(c2, j2, gc, gj)) {
+            gc = c2;
+            gj = j2;
+          }
         }
+        int bs2 = 0;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) shfl_cand(gc, gj, bs2, off);
+        const long long wi = (gj >= 0 && gc < INFINITY) ? gj : -1;
+        if (lane < 4 && wi >= 0) sm.cx[lane] = __ldg(x64 + lane * n + wi);
+        if (lane == 0) sm.win = wi;
       }
+      __syncthreads();
+      if (tid == 0) sm.exact_rounds += 1;
     }
-    __syncthreads();
     if (sm.win < 0) {
-      // sogmm.cpp:276-284: lowest unchosen index (rare; a second exchange)
+      // sogmm.cpp:276-284: no eligible point anywhere -> lowest unchosen
+      // index (rare; counter-based exchange)
       const unsigned freem = valid & ~chosen;
       long long bu = freem ? g0 + static_cast<long long>(__ffs(freem) - 1) * G : LLONG_MAX;
 #pragma unroll
@@ -369,7 +503,7 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
       if (tid == 0) {
         long long m = LLONG_MAX;
         for (int w = 0; w < kSeedWarps; ++w) m = sm.gu[w] < m ? sm.gu[w] : m;
-        KppSlot* fs = scr.slots + 2 * nblk;
+        KppSlot* fs = reinterpret_cast<KppSlot*>(llw + 4 * nblk * kSlotWords);
         fs[blockIdx.x].unchosen = m;
         ++epoch;
         grid_exchange(scr.counter, static_cast<unsigned>(nblk) * epoch);
@@ -379,28 +513,28 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
           m = u2 < m ? u2 : m;
         }
         sm.win = m;
-        sm.win_owner = static_cast<int>(m % G);
 #pragma unroll
         for (int q = 0; q < 4; ++q) sm.cx[q] = x64[q * n + m];
       }
       __syncthreads();
     }
-    if (blockIdx.x == 0 && tid == 0) scr.centers[r] = sm.win;
+    const long long win = sm.win;
+    if (blockIdx.x == 0 && tid == 0) scr.centers[r] = win;
 #pragma unroll
     for (int q = 0; q < 4; ++q) c[q] = sm.cx[q];
-    if (sm.win_owner == static_cast<int>(g0)) {
-      chosen |= 1u << static_cast<int>((sm.win - g0) / G);
-    }
-    // sm.win / sm.cx are rewritten only after the next round's exchange,
-    // which every thread reaches after these reads (two barriers later)
+    if (!comm && win % G == g0) chosen |= 1u << static_cast<int>(win / G);
+    // sm.win / sm.cx are rewritten by warp 0 only after the next round's
+    // first barrier, which every thread reaches after these reads
   }
   // labels + owned counts (every point's final nearest centre)
+  if (!comm) {
 #pragma unroll
-  for (int j = 0; j < PPT; ++j) {
-    const long long i = g0 + j * G;
-    if (i >= n) continue;
-    scr.labels[i] = lab[j];
-    atomicAdd(&scr.owned[lab[j]], 1);
+    for (int j = 0; j < PPT; ++j) {
+      const long long i = g0 + j * G;
+      if (i >= n) continue;
+      scr.labels[i] = lab[j];
+      atomicAdd(&scr.owned[lab[j]], 1);
+    }
   }
 }
 
@@ -721,7 +855,7 @@ cudaError_t launch_kpp_seed(const double* x64, int64_t n, int k, uint64_t seed,
                             KinitScratch scr, int sm_count, cudaStream_t s) {
   // one CTA per SM, points register-resident while they fit
   const int nblk = sm_count < kMaxSeedBlocks ? sm_count : kMaxSeedBlocks;
-  if (n <= static_cast<int64_t>(nblk) * kSeedThreads * kSeedPPT) {
+  if (n <= static_cast<int64_t>(nblk) * kCompThreads * kSeedPPT) {
     void* args[] = {(void*)&x64, (void*)&n, (void*)&k, (void*)&seed, (void*)&scr};
     return cudaLaunchCooperativeKernel((void*)kpp_seed_kernel, dim3(nblk),
                                        dim3(kSeedThreads), args, 0, s);
