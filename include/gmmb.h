@@ -77,6 +77,13 @@ int gmmb_nccl_unique_id(void* out128);
 int gmmb_ctx_create_sharded(int device, int rank, int world,
                             const void* nccl_id128, gmmb_ctx** out);
 void gmmb_ctx_destroy(gmmb_ctx* ctx);
+/* EM loop execution mode (no reference counterpart; measurement aid).
+ * 0 (default): the EM loop of a fit is one CUDA graph with a conditional
+ * WHILE node, the loop condition set on the device — no host round trip.
+ * 1: iterations are enqueued in chunks with CUDA events around every fused
+ * E kernel (gmmb_fit_stats.ms_estep), for kernel timing. Same results. */
+int gmmb_ctx_set_timing(gmmb_ctx* ctx, int per_kernel_events);
+
 int gmmb_device_info(gmmb_ctx* ctx, int* sm_count, int* cc_major,
                      int* cc_minor);
 

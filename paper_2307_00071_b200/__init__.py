@@ -117,6 +117,7 @@ _SIGS = {
                                          ctypes.c_uint64]),
     "gmmb_shard_key_tail": (ctypes.c_int, [_D, ctypes.c_int, ctypes.c_int, _D]),
     "gmmb_ffma_peak": (ctypes.c_int, [_V, ctypes.c_double, _D, _D]),
+    "gmmb_ctx_set_timing": (ctypes.c_int, [_V, ctypes.c_int]),
 }
 
 
@@ -292,6 +293,12 @@ class Context:
     @property
     def handle(self):
         return self._h
+
+    def set_timing(self, per_kernel_events: bool) -> None:
+        """EM loop mode: False (default) = one CUDA graph per fit (conditional
+        WHILE node, no host round trip); True = chunked launches with CUDA
+        events around every fused E kernel (FitResult.ms_estep)."""
+        _check(load().gmmb_ctx_set_timing(self._h, 1 if per_kernel_events else 0))
 
     def ffma_peak(self, ms_target: float = 50.0) -> tuple[float, float]:
         """Measured FP32 FFMA TFLOP/s on this device (and the ms it took)."""

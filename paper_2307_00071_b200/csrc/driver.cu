@@ -100,6 +100,19 @@ struct DevBuf {
   }
 };
 
+// Shape + buffer identity of a built EM graph (rebuild when any differs).
+struct EmGraphKey {
+  int k0, d, world;
+  int64_t n;
+  const void* p[12];
+  bool operator==(const EmGraphKey& o) const {
+    if (k0 != o.k0 || d != o.d || n != o.n || world != o.world) return false;
+    for (int i = 0; i < 12; ++i)
+      if (p[i] != o.p[i]) return false;
+    return true;
+  }
+};
+
 }  // namespace
 
 struct gmmb_ctx {
@@ -149,6 +162,10 @@ struct gmmb_ctx {
   DevBuf<double> dense;  // log_gamma staging for m_step / e_step
   DevBuf<EmState> st;
   EmState* st_host = nullptr;  // pinned
+  int timing = 0;                // 1: chunked EM loop with per-iteration E-kernel events
+  bool last_timed = false;       // the last EM run recorded those events
+  cudaGraphExec_t em_graph = nullptr;
+  EmGraphKey em_key{};
   ModelBuf bufs[2];
   RecBuf rec;
 };
@@ -485,7 +502,8 @@ void download_model(gmmb_ctx* c, int buf, int m, double* w, double* mu,
 }
 
 // ---- EM loop ----------------------------------------------------------
-void em_iteration(gmmb_ctx* c, int k0, int it) {
+void em_iteration(gmmb_ctx* c, int k0, int it,
+                  const cudaGraphConditionalHandle* cond = nullptr) {
   const int NS = nstats(c->d);
   PointsDev pts{c->n, c->d, c->x64.p, c->xt.p, c->tc.p,
                 static_cast<int>((c->n + kTile - 1) / kTile)};
@@ -497,14 +515,80 @@ void em_iteration(gmmb_ctx* c, int k0, int it) {
      "estep_stats");
   if (timed) ck(cudaEventRecord(c->ev_e[2 * it + 1], c->s), "event");
   c->launches += 4;
+  if (c->world == 1) {
+    c->launches += -1;  // fused reduce + finalize
+    ck(launch_em_reduce_finalize(c->d, c->partials.p, ncl, k0, c->bufs, c->st.p, c->rec, c->s),
+       "em_reduce_finalize");
+    ck(launch_commit(c->d, 0, c->rec, k0, nullptr, c->bufs, c->st.p, c->ll_trace.p, c->s, cond,
+                     c->ll_part.p, ncl),
+       "commit");
+    return;
+  }
   double* red_ll = c->red.p + static_cast<size_t>(k0) * NS;
   ck(launch_em_reduce(c->d, c->partials.p, c->ll_part.p, ncl, k0, c->st.p, c->red.p, red_ll,
                       c->s),
      "em_reduce");
-  if (c->world > 1) allreduce_sum(c, c->red.p, static_cast<int64_t>(k0) * NS + 1);
+  allreduce_sum(c, c->red.p, static_cast<int64_t>(k0) * NS + 1);
   ck(launch_em_finalize(c->d, c->red.p, c->bufs, c->st.p, k0, c->rec, c->s), "em_finalize");
-  ck(launch_commit(c->d, 0, c->rec, k0, red_ll, c->bufs, c->st.p, c->ll_trace.p, c->s),
+  ck(launch_commit(c->d, 0, c->rec, k0, red_ll, c->bufs, c->st.p, c->ll_trace.p, c->s, cond),
      "commit");
+}
+
+// The whole EM loop as one CUDA graph: a conditional WHILE node whose body
+// is one iteration (E+stats -> reduce -> finalize -> commit); the commit
+// kernel sets the loop condition from the device state, so a fit's EM loop
+// is one graph launch with no host round trip. Rebuilt only when the
+// problem shape or a device buffer changes.
+EmGraphKey em_graph_key(gmmb_ctx* c, int k0) {
+  EmGraphKey k{};
+  k.k0 = k0;
+  k.d = c->d;
+  k.n = c->n;
+  k.world = c->world;
+  const void* ps[12] = {c->xt.p, c->tc.p, c->partials.p, c->ll_part.p, c->red.p, c->ll_trace.p,
+                        c->st.p, c->bufs[0].w, c->bufs[1].w, c->rec.count, c->bufs[0].cst,
+                        c->bufs[1].cst};
+  for (int i = 0; i < 12; ++i) k.p[i] = ps[i];
+  return k;
+}
+
+void launch_em_graph(gmmb_ctx* c, int k0) {
+  const EmGraphKey key = em_graph_key(c, k0);
+  if (!c->em_graph || !(key == c->em_key)) {
+    if (c->em_graph) cudaGraphExecDestroy(c->em_graph);
+    c->em_graph = nullptr;
+    cudaGraph_t g = nullptr;
+    ck(cudaGraphCreate(&g, 0), "cudaGraphCreate");
+    cudaGraphConditionalHandle h;
+    ck(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault),
+       "cudaGraphConditionalHandleCreate");
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    ck(cudaGraphAddNode(&node, g, nullptr, 0, &cp), "cudaGraphAddNode");
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    ck(cudaStreamBeginCaptureToGraph(c->s, body, nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeRelaxed),
+       "cudaStreamBeginCaptureToGraph");
+    const long long launches = c->launches;
+    try {
+      em_iteration(c, k0, -1, &h);
+      c->launches = launches;
+    } catch (...) {
+      cudaGraph_t dummy;
+      cudaStreamEndCapture(c->s, &dummy);
+      cudaGraphDestroy(g);
+      throw;
+    }
+    ck(cudaStreamEndCapture(c->s, &body), "cudaStreamEndCapture");
+    ck(cudaGraphInstantiate(&c->em_graph, g, 0), "cudaGraphInstantiate");
+    cudaGraphDestroy(g);
+    c->em_key = key;
+  }
+  ck(cudaGraphLaunch(c->em_graph, c->s), "cudaGraphLaunch");
 }
 
 void ensure_em_buffers(gmmb_ctx* c, int k0, int max_iters) {
@@ -529,6 +613,13 @@ EmState run_em(gmmb_ctx* c, int k0, const gmmb_em_params* em) {
     cudaEvent_t e;
     ck(cudaEventCreate(&e), "cudaEventCreate");
     c->ev_e.push_back(e);
+  }
+  c->last_timed = !(c->world == 1 && !c->timing);
+  if (!c->last_timed) {
+    launch_em_graph(c, k0);
+    EmState h = read_state(c);
+    c->launches += 3LL * h.iter;
+    return h;
   }
   int launched = 0;
   int chunk = 2;
@@ -560,12 +651,12 @@ void finish_fit(gmmb_ctx* c, const EmState& h, const gmmb_em_params* em,
     stats->converged = h.converged;
     stats->units = h.units;
     double me = 0.0;
-    for (int i = 0; i < h.iter && static_cast<size_t>(2 * i + 1) < c->ev_e.size(); ++i) {
+    for (int i = 0; c->last_timed && i < h.iter && static_cast<size_t>(2 * i + 1) < c->ev_e.size(); ++i) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, c->ev_e[2 * i], c->ev_e[2 * i + 1]);
       me += ms;
     }
-    stats->ms_estep = me;
+    stats->ms_estep = c->last_timed ? me : 0.0;  // per-kernel events only in timing mode
   }
   (void)em;
 }
@@ -777,12 +868,19 @@ void gmmb_ctx_destroy(gmmb_ctx* c) {
   c->rpc.release(); c->rflags.release(); c->mpart.release(); c->msums.release();
   c->mmeans.release(); c->mcounts.release(); c->partials.release(); c->ll_part.release();
   c->red.release(); c->ll_trace.release(); c->dense.release(); c->st.release();
+  if (c->em_graph) cudaGraphExecDestroy(c->em_graph);
   if (c->st_host) cudaFreeHost(c->st_host);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->ev_e) cudaEventDestroy(e);
   if (c->s) cudaStreamDestroy(c->s);
   delete c;
+}
+
+int gmmb_ctx_set_timing(gmmb_ctx* c, int per_kernel_events) {
+  if (!c) return 2;
+  c->timing = per_kernel_events ? 1 : 0;
+  return 0;
 }
 
 int gmmb_device_info(gmmb_ctx* c, int* sm_count, int* cc_major, int* cc_minor) {

@@ -1151,17 +1151,12 @@ __device__ bool factor_component(const double* cov_packed, float* pc,
 // (the reference's two passes, sogmm.cpp:410-416 / kernels.hpp:91-179,
 // fused into one pass centred at the previous mean).
 // ---------------------------------------------------------------------------
+// Finalize one component from its reduced statistics s[NS] (centred at the
+// old mean): mean, covariance + cov_reg, FP64 Cholesky / precision factor.
 template <int D>
-__global__ void em_finalize_kernel(const double* __restrict__ red,
-                                   ModelBuf b0, ModelBuf b1,
-                                   const EmState* __restrict__ st, RecBuf rec) {
-  constexpr int NS = nstats(D);
+__device__ __forceinline__ void finalize_component(const double* s, int k, const ModelBuf& mb,
+                                                   double cov_reg, RecBuf& rec) {
   constexpr int NP = npacked(D);
-  if (st->done) return;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= st->k_cur) return;
-  const ModelBuf& mb = st->cur ? b1 : b0;
-  const double* s = red + static_cast<int64_t>(k) * NS;
   const double cnt = s[0];
   int flags = 0;
   double mean[4] = {0, 0, 0, 0};
@@ -1185,7 +1180,7 @@ __global__ void em_finalize_kernel(const double* __restrict__ red,
     for (int q = 0; q < NP; ++q) {
       const int i = packed_row(q), j = packed_col(q);
       cov[q] = s[1 + D + q] * inv - delta[i] * delta[j];
-      if (i == j) cov[q] += st->cov_reg;
+      if (i == j) cov[q] += cov_reg;
     }
     if (factor_component<D>(cov, pc, &logdet)) flags |= 2;
   }
@@ -1200,26 +1195,84 @@ __global__ void em_finalize_kernel(const double* __restrict__ red,
   rec.flags[k] = flags;
 }
 
+template <int D>
+__global__ void em_finalize_kernel(const double* __restrict__ red,
+                                   ModelBuf b0, ModelBuf b1,
+                                   const EmState* __restrict__ st, RecBuf rec) {
+  if (st->done) return;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= st->k_cur) return;
+  const ModelBuf& mb = st->cur ? b1 : b0;
+  finalize_component<D>(red + static_cast<int64_t>(k) * nstats(D), k, mb, st->cov_reg, rec);
+}
+
+// Single-device fused second stage: one warp per component reduces the
+// per-CTA partials in a fixed order (lane-strided sums, fixed butterfly) and
+// its lane 0 finalizes the component.
+template <int D>
+__global__ void __launch_bounds__(128) em_reduce_finalize_kernel(
+    const double* __restrict__ partials, int ncl, int kpad, ModelBuf b0, ModelBuf b1,
+    const EmState* __restrict__ st, RecBuf rec) {
+  constexpr int NS = nstats(D);
+  if (st->done) return;
+  const int lane = threadIdx.x & 31;
+  const int k = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (k >= kpad || k >= st->k_cur) return;
+  double acc[NS];
+#pragma unroll
+  for (int j = 0; j < NS; ++j) acc[j] = 0.0;
+  for (int c = lane; c < ncl; c += 32) {
+    const double* src = partials + (static_cast<int64_t>(c) * kpad + k) * NS;
+#pragma unroll
+    for (int j = 0; j < NS; ++j) acc[j] += src[j];
+  }
+#pragma unroll
+  for (int j = 0; j < NS; ++j) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
+  }
+  if (lane == 0) {
+    const ModelBuf& mb = st->cur ? b1 : b0;
+    finalize_component<D>(acc, k, mb, st->cov_reg, rec);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Commit (single CTA of 1024 threads): sogmm.cpp:418-453 + :488-504.
 // ---------------------------------------------------------------------------
 template <int D>
-__global__ void __launch_bounds__(1024) commit_kernel(
-    int mode, RecBuf rec, int k_in_arg, const double* __restrict__ red_ll,
-    ModelBuf b0, ModelBuf b1, EmState* st, double* __restrict__ ll_trace) {
+__device__ __forceinline__ void commit_body(
+    int mode, const RecBuf& rec, int k_in_arg, const double* __restrict__ red_ll,
+    const double* __restrict__ ll_part, int ncl,
+    const ModelBuf& b0, const ModelBuf& b1, EmState* st, double* __restrict__ ll_trace) {
   constexpr int T = 1024;
   constexpr int PER = kMaxK / T;  // components per thread (<= 4)
-  __shared__ int s_scan[T];
-  __shared__ double s_tot[T];
+  __shared__ int s_wcnt[32];
+  __shared__ double s_wtot[32];
+  __shared__ int s_woff[32];
+  __shared__ int s_knew;
+  __shared__ double s_total;
   __shared__ int s_flag;
-  const int tid = threadIdx.x;
+  static_assert(T == 1024, "one CTA of 1024 threads");
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (st->done) return;
   const int k_in = mode == 0 ? st->k_cur : k_in_arg;
 
   if (mode == 0) {
+    // log-likelihood: the per-CTA partials of the fused E kernel in a fixed
+    // order (lane-strided sums, then a fixed butterfly), or a reduced value
+    double ll = 0.0;
+    if (warp == 0) {
+      if (ll_part) {
+        for (int c = lane; c < ncl; c += 32) ll += ll_part[c];
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) ll += __shfl_xor_sync(0xffffffffu, ll, off);
+      } else {
+        ll = red_ll[0];
+      }
+    }
     // EM bookkeeping: sogmm.cpp:490-498
     if (tid == 0) {
-      const double ll = red_ll[0];
       const int iter = st->iter;
       st->units += st->npts * static_cast<double>(k_in);
       if (ll_trace) ll_trace[iter] = ll;
@@ -1241,7 +1294,9 @@ __global__ void __launch_bounds__(1024) commit_kernel(
     if (s_flag) return;
   }
 
-  // keep flags -> exclusive scan (compaction preserves order, sogmm.cpp:418-429)
+  // keep flags -> exclusive scan (compaction preserves order, sogmm.cpp:418-429):
+  // warp scans + one warp over the 32 warp totals; total kept count with a
+  // fixed-shape reduction (deterministic)
   int keep[PER];
   int cnt = 0;
   double tot = 0.0;
@@ -1252,22 +1307,37 @@ __global__ void __launch_bounds__(1024) commit_kernel(
     cnt += keep[i];
     if (keep[i]) tot += rec.count[k];
   }
-  s_scan[tid] = cnt;
-  s_tot[tid] = tot;
+  int incl = cnt;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += v;
+  }
+  double wt = tot;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) wt += __shfl_xor_sync(0xffffffffu, wt, off);
+  if (lane == 31) s_wcnt[warp] = incl;
+  if (lane == 0) s_wtot[warp] = wt;
   __syncthreads();
-  for (int off = 1; off < T; off <<= 1) {  // Hillis-Steele inclusive scan
-    const int v = tid >= off ? s_scan[tid - off] : 0;
-    __syncthreads();
-    s_scan[tid] += v;
-    __syncthreads();
+  if (warp == 0) {
+    const int wc = s_wcnt[lane];
+    int wi = wc;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, wi, off);
+      if (lane >= off) wi += v;
+    }
+    s_woff[lane] = wi - wc;
+    double t = s_wtot[lane];
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    if (lane == 31) s_knew = wi;
+    if (lane == 0) s_total = t;
   }
-  // fixed-shape tree for the total count (deterministic)
-  for (int off = T / 2; off >= 1; off >>= 1) {
-    if (tid < off) s_tot[tid] += s_tot[tid + off];
-    __syncthreads();
-  }
-  const int k_new = s_scan[T - 1];
-  const double total = s_tot[0];
+  __syncthreads();
+  const int excl = s_woff[warp] + incl - cnt;
+  const int k_new = s_knew;
+  const double total = s_total;
   if (k_new == 0) {
     if (tid == 0) {
       st->error = 3;
@@ -1280,7 +1350,7 @@ __global__ void __launch_bounds__(1024) commit_kernel(
   // first non-SPD kept component (compacted index), sogmm.cpp:447-452
   if (tid == 0) s_flag = 0x7fffffff;
   __syncthreads();
-  int j = s_scan[tid] - cnt;
+  int j = excl;
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
     const int k = tid * PER + i;
@@ -1302,7 +1372,7 @@ __global__ void __launch_bounds__(1024) commit_kernel(
   const int dst_sel = mode == 0 ? (st->cur ^ 1) : st->cur;
   const ModelBuf& dst = dst_sel ? b1 : b0;
   const double half_d_ln2pi = 0.5 * D * kLog2Pi;
-  j = s_scan[tid] - cnt;
+  j = excl;
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
     const int k = tid * PER + i;
@@ -1330,6 +1400,22 @@ __global__ void __launch_bounds__(1024) commit_kernel(
       st->cur = dst_sel;
       if (st->iter >= st->max_iters) st->done = 1;
     }
+  }
+}
+
+// Commit kernel. Inside the EM while-graph (use_cond = 1) it also sets the
+// loop condition from the device state: the whole EM loop runs without a
+// host round trip (CUDA conditional graph node).
+template <int D>
+__global__ void __launch_bounds__(1024) commit_kernel(
+    int mode, RecBuf rec, int k_in_arg, const double* __restrict__ red_ll,
+    const double* __restrict__ ll_part, int ncl,
+    ModelBuf b0, ModelBuf b1, EmState* st, double* __restrict__ ll_trace,
+    cudaGraphConditionalHandle cond, int use_cond) {
+  commit_body<D>(mode, rec, k_in_arg, red_ll, ll_part, ncl, b0, b1, st, ll_trace);
+  if (use_cond) {
+    __syncthreads();
+    if (threadIdx.x == 0) cudaGraphSetConditional(cond, st->done ? 0u : 1u);
   }
 }
 
@@ -1622,6 +1708,17 @@ cudaError_t launch_em_reduce(int d, const double* partials,
   return cudaGetLastError();
 }
 
+cudaError_t launch_em_reduce_finalize(int d, const double* partials, int ncl, int k0,
+                                     const ModelBuf* bufs, const EmState* st, RecBuf rec,
+                                     cudaStream_t s) {
+  const int grid = (k0 + 3) / 4;
+  if (d == 4)
+    em_reduce_finalize_kernel<4><<<grid, 128, 0, s>>>(partials, ncl, k0, bufs[0], bufs[1], st, rec);
+  else
+    em_reduce_finalize_kernel<3><<<grid, 128, 0, s>>>(partials, ncl, k0, bufs[0], bufs[1], st, rec);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_em_finalize(int d, const double* red, const ModelBuf* bufs,
                                const EmState* st, int k0, RecBuf rec,
                                cudaStream_t s) {
@@ -1635,11 +1732,17 @@ cudaError_t launch_em_finalize(int d, const double* red, const ModelBuf* bufs,
 
 cudaError_t launch_commit(int d, int mode, const RecBuf rec, int k_in,
                           const double* red_ll, ModelBuf* bufs, EmState* st,
-                          double* ll_trace, cudaStream_t s) {
+                          double* ll_trace, cudaStream_t s,
+                          const cudaGraphConditionalHandle* cond,
+                          const double* ll_part, int ncl) {
+  const cudaGraphConditionalHandle h = cond ? *cond : cudaGraphConditionalHandle{};
+  const int use = cond ? 1 : 0;
   if (d == 4)
-    commit_kernel<4><<<1, 1024, 0, s>>>(mode, rec, k_in, red_ll, bufs[0], bufs[1], st, ll_trace);
+    commit_kernel<4><<<1, 1024, 0, s>>>(mode, rec, k_in, red_ll, ll_part, ncl, bufs[0], bufs[1],
+                                        st, ll_trace, h, use);
   else
-    commit_kernel<3><<<1, 1024, 0, s>>>(mode, rec, k_in, red_ll, bufs[0], bufs[1], st, ll_trace);
+    commit_kernel<3><<<1, 1024, 0, s>>>(mode, rec, k_in, red_ll, ll_part, ncl, bufs[0], bufs[1],
+                                        st, ll_trace, h, use);
   return cudaGetLastError();
 }
 

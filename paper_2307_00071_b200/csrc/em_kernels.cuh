@@ -60,9 +60,20 @@ cudaError_t launch_em_finalize(int d, const double* red, const ModelBuf* bufs,
 // Single-CTA commit: convergence bookkeeping, compaction, new model.
 // mode 0: EM iteration (uses red_ll, ll_trace); mode 1: plain M step
 // (initial hard M step / m_step API: always commits, no EM bookkeeping).
+// cond != nullptr: the launch is the tail of the EM while-graph body and
+// sets the loop condition (1 = run another iteration) from st->done.
 cudaError_t launch_commit(int d, int mode, const RecBuf rec, int k_in,
                           const double* red_ll, ModelBuf* bufs, EmState* st,
-                          double* ll_trace, cudaStream_t s);
+                          double* ll_trace, cudaStream_t s,
+                          const cudaGraphConditionalHandle* cond = nullptr,
+                          const double* ll_part = nullptr, int ncl = 0);
+// (mode 0: the log-likelihood comes from ll_part[ncl] if given, else red_ll[0])
+
+// Single-device fused reduce of the per-CTA partials + finalize (replaces
+// launch_em_reduce + launch_em_finalize when there is no cross-rank sum).
+cudaError_t launch_em_reduce_finalize(int d, const double* partials, int ncl, int k0,
+                                     const ModelBuf* bufs, const EmState* st, RecBuf rec,
+                                     cudaStream_t s);
 
 // Model (FP64) -> E-step constants for buffer st->cur; sets error on
 // a non-SPD covariance (first failing index, gmm.cpp:33-48 semantics).

@@ -9,6 +9,8 @@ ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--tol", type=float, default=1e-3)
 args = ap.parse_args()
 ctx = gm.Context(0)
+if os.environ.get("GMMB_TIMING", "0") == "1":
+    ctx.set_timing(True)
 p = gm.synthetic_frame_cloud()
 ctx.upload(p)
 for _ in range(args.reps):
