@@ -24,6 +24,7 @@
 #include "em_kernels.cuh"
 #include "kinit_kernels.cuh"
 #include "layout.cuh"
+#include "mstep_hard.cuh"
 
 using namespace gmmb;
 
@@ -138,6 +139,7 @@ struct gmmb_ctx {
   DevBuf<uint64_t> mkeys_in, mkeys_out;
   DevBuf<int32_t> midx;
   DevBuf<unsigned char> sort_tmp;
+  DevBuf<int32_t> hidx;           // hard M step: [3][n] sort indices / keys
   DevBuf<int> flags;
   // kinit
   DevBuf<uint64_t> keys;
@@ -455,6 +457,18 @@ void run_kinit(gmmb_ctx* c, int k, uint64_t seed) {
 void run_moments_commit(gmmb_ctx* c, const int32_t* labels,
                         const double* log_gamma, int m, double cov_reg) {
   const int64_t n = c->n;
+  if (labels && c->world == 1) {
+    // hard labels on one device: stable sort by label + segmented moments
+    c->hidx.ensure(static_cast<size_t>(n) * 3);
+    const size_t tb = hard_moments_temp_bytes(n, m);
+    c->sort_tmp.ensure(tb);
+    HardScratch hs{c->hidx.p, c->hidx.p + n, c->hidx.p + 2 * n, c->sort_tmp.p, c->sort_tmp.cap};
+    ck(launch_hard_moments(c->d, c->x64.p, n, labels, m, cov_reg, hs, c->rec, c->s),
+       "hard_moments");
+    ck(launch_commit(c->d, 1, c->rec, m, nullptr, c->bufs, c->st.p, nullptr, c->s), "commit");
+    c->launches += 3;  // iota, moments, commit (CUB's sort kernels not counted)
+    return;
+  }
   const int nchunks = static_cast<int>((n + 4095) / 4096);
   c->mpart.ensure(static_cast<size_t>(nchunks) * m * 10);
   c->msums.ensure(static_cast<size_t>(m) * 10);
@@ -857,7 +871,7 @@ void gmmb_ctx_destroy(gmmb_ctx* c) {
   if (c->comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
   c->x64.release(); c->xt.release(); c->tc.release(); c->perm.release();
   c->bbox_part.release(); c->mkeys_in.release(); c->mkeys_out.release();
-  c->midx.release(); c->sort_tmp.release(); c->flags.release();
+  c->midx.release(); c->sort_tmp.release(); c->flags.release(); c->hidx.release();
   c->keys.release(); c->kd2.release(); c->labels.release(); c->chosen.release();
   c->slots.release(); c->owned.release(); c->centers.release(); c->rslots.release();
   c->ticket.release(); c->kstatus.release(); c->ll64.release();
