@@ -347,7 +347,10 @@ KinitScratch kinit_scratch(gmmb_ctx* c, int k) {
   c->kd2.ensure(n);
   c->labels.ensure(n);
   c->chosen.ensure(n);
-  c->slots.ensure(static_cast<size_t>(c->sm_count) * 8 * 2);
+  // persistent kernel: LL words + fallback slots; memory-resident rounds:
+  // one slot per CTA (n / 8192 CTAs beyond 4 per SM)
+  c->slots.ensure(std::max<size_t>(static_cast<size_t>(c->sm_count) * 8 * 2,
+                                   static_cast<size_t>(n / 8192 + 1)));
   c->owned.ensure(std::max(k, 1));
   c->centers.ensure(std::max(k, 1));
   c->kstatus.ensure(8);

@@ -538,74 +538,116 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
   }
 }
 
-// Memory-resident variant (N beyond the register budget): plain exact FP64
-// clocks, state in global memory, one launch per round (grid barrier =
-// kernel boundary), CTA slots reduced by the last CTA to finish.
-__global__ void __launch_bounds__(512)
+// Memory-resident variant (N beyond the register budget): state in global
+// memory, one launch per round (grid barrier = kernel boundary). Per round a
+// CTA streams its points, folds centre r-1 into d2 / labels (exact FP64),
+// keeps FP32 clocks in shared memory, and computes the exact FP64 clock only
+// for its points within the error band of its own best approximate clock:
+// any point inside the global band is inside the local band of its CTA
+// (the global best is no larger than the local best), so each CTA's exact
+// (clock, index) best contains the global winner. The last CTA to finish
+// reduces every CTA's slot in parallel, in a fixed order.
+constexpr int kMemThreads = 512;
+constexpr int kMemPPT = 16;  // points per thread held as FP32 clocks in shared memory
+
+__global__ void __launch_bounds__(kMemThreads)
     kpp_mem_round_kernel(const double* __restrict__ x64, int64_t n, int r,
                          int k, uint64_t seed, KinitScratch scr, int* ticket,
                          long long* win_io) {
-  __shared__ double s_c[16];
-  __shared__ long long s_i[16];
-  __shared__ long long s_u[16];
+  __shared__ float s_a[kMemPPT * kMemThreads];
+  __shared__ double s_c[kMemThreads / 32];
+  __shared__ long long s_i[kMemThreads / 32];
+  __shared__ long long s_u[kMemThreads / 32];
+  __shared__ float s_f[kMemThreads / 32];
   __shared__ int s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t G = static_cast<int64_t>(gridDim.x) * 512;
+  constexpr int NW = kMemThreads / 32;
+  const int64_t G = static_cast<int64_t>(gridDim.x) * kMemThreads;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kMemThreads + tid;
   const long long win = r > 0 ? win_io[0] : -1;
   double c[4] = {0, 0, 0, 0};
   if (r > 0)
     for (int q = 0; q < 4; ++q) c[q] = x64[q * n + win];
   const uint64_t pre = round_prefix(seed, r);
-  double bc = INFINITY;
-  long long bi = -1, bu = LLONG_MAX;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * 512 + tid; i < n; i += G) {
-    double dcur;
-    if (r > 0) {
-      dcur = scr.d2[i];
-      const double dd = dist2(x64[i], x64[n + i], x64[2 * n + i], x64[3 * n + i], c);
-      if (dd < dcur) {
-        dcur = dd;
-        scr.d2[i] = dd;
-        scr.labels[i] = r - 1;
+  long long bu = LLONG_MAX;
+  float amin = INFINITY;
+  // phase 1: fold centre r-1, FP32 clocks
+#pragma unroll 4
+  for (int m = 0; m < kMemPPT; ++m) {
+    const int64_t i = base + m * G;
+    float a = INFINITY;
+    if (i < n) {
+      double dcur;
+      if (r > 0) {
+        dcur = scr.d2[i];
+        const double dd = dist2(x64[i], x64[n + i], x64[2 * n + i], x64[3 * n + i], c);
+        if (dd < dcur) {
+          dcur = dd;
+          scr.d2[i] = dd;
+          scr.labels[i] = r - 1;
+        }
+        if (i == win) scr.chosen[i] = 1;
+      } else {
+        dcur = INFINITY;
+        scr.d2[i] = INFINITY;
+        scr.labels[i] = 0;
+        scr.chosen[i] = 0;
       }
-      if (i == win) scr.chosen[i] = 1;
-    } else {
-      dcur = INFINITY;
-      scr.d2[i] = INFINITY;
-      scr.labels[i] = 0;
-      scr.chosen[i] = 0;
+      if (r < k) {
+        const float na = nlu_approx(mix64(pre + scr.keys[i]));
+        if (r == 0) {
+          a = na;
+        } else if (dcur > 0.0) {
+          const float f = __double2float_rn(dcur);
+          a = na * (isinf(f) ? 1e-38f : rcp_approx(f));
+        }
+        if (!scr.chosen[i] && i < bu) bu = i;
+      }
     }
-    if (r == k) continue;
-    const double nl = nlu_exact(mix64(pre + scr.keys[i]));
-    if (r == 0) {
-      if (cand_better(nl, i, bc, bi)) { bc = nl; bi = i; }
-    } else if (dcur > 0.0) {
-      const double clk = nl / dcur;
-      if (clk < INFINITY && cand_better(clk, i, bc, bi)) { bc = clk; bi = i; }
-    }
-    if (!scr.chosen[i] && i < bu) bu = i;
+    s_a[m * kMemThreads + tid] = a;
+    amin = fminf(amin, a);
   }
   if (r == k) return;
 #pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) amin = fminf(amin, __shfl_xor_sync(0xffffffffu, amin, off));
+  if (lane == 0) s_f[warp] = amin;
+  __syncthreads();
+  float cmin = INFINITY;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) cmin = fminf(cmin, s_f[w]);
+  const float thr = cmin * kBand;
+  // phase 2: exact FP64 clocks inside the CTA's band (sogmm.cpp:240-275)
+  double bc = INFINITY;
+  long long bi = -1;
+  if (cmin < INFINITY) {
+    for (int m = 0; m < kMemPPT; ++m) {
+      const int64_t i = base + m * G;
+      if (i >= n || !(s_a[m * kMemThreads + tid] <= thr)) continue;
+      const double nl = nlu_exact(mix64(pre + scr.keys[i]));
+      const double clk = r == 0 ? nl : nl / scr.d2[i];
+      if (clk < INFINITY && cand_better(clk, i, bc, bi)) {
+        bc = clk;
+        bi = i;
+      }
+    }
+  }
+  int bs = 0;
+#pragma unroll
   for (int off = 16; off >= 1; off >>= 1) {
-    const double c2 = __shfl_xor_sync(0xffffffffu, bc, off);
-    const long long i2 = __shfl_xor_sync(0xffffffffu, bi, off);
+    shfl_cand(bc, bi, bs, off);
     const long long u2 = __shfl_xor_sync(0xffffffffu, bu, off);
-    if (cand_better(c2, i2, bc, bi)) { bc = c2; bi = i2; }
     bu = u2 < bu ? u2 : bu;
   }
   if (lane == 0) { s_c[warp] = bc; s_i[warp] = bi; s_u[warp] = bu; }
   __syncthreads();
   if (warp == 0) {
-    bc = lane < 16 ? s_c[lane] : INFINITY;
-    bi = lane < 16 ? s_i[lane] : -1;
-    bu = lane < 16 ? s_u[lane] : LLONG_MAX;
+    bc = lane < NW ? s_c[lane] : INFINITY;
+    bi = lane < NW ? s_i[lane] : -1;
+    bu = lane < NW ? s_u[lane] : LLONG_MAX;
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
-      const double c2 = __shfl_xor_sync(0xffffffffu, bc, off);
-      const long long i2 = __shfl_xor_sync(0xffffffffu, bi, off);
+      shfl_cand(bc, bi, bs, off);
       const long long u2 = __shfl_xor_sync(0xffffffffu, bu, off);
-      if (cand_better(c2, i2, bc, bi)) { bc = c2; bi = i2; }
       bu = u2 < bu ? u2 : bu;
     }
     if (lane == 0) {
@@ -618,19 +660,43 @@ __global__ void __launch_bounds__(512)
     }
   }
   __syncthreads();
-  if (!s_last || tid != 0) return;
+  if (!s_last) return;
+  // last CTA: every slot, in parallel, fixed order
   __threadfence();
   double gc = INFINITY;
   long long gi = -1, gu = LLONG_MAX;
-  for (int b = 0; b < static_cast<int>(gridDim.x); ++b) {
+  for (int b = tid; b < static_cast<int>(gridDim.x); b += kMemThreads) {
     const volatile KppSlot& sl = scr.slots[b];
-    if (cand_better(sl.clock, sl.idx, gc, gi)) { gc = sl.clock; gi = sl.idx; }
-    gu = sl.unchosen < gu ? sl.unchosen : gu;
+    const double c2 = sl.clock;
+    const long long i2 = sl.idx, u2 = sl.unchosen;
+    if (cand_better(c2, i2, gc, gi)) { gc = c2; gi = i2; }
+    gu = u2 < gu ? u2 : gu;
   }
-  const long long w = (gi >= 0 && gc < INFINITY) ? gi : gu;
-  win_io[0] = w;
-  scr.centers[r] = w;
-  *ticket = 0;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    shfl_cand(gc, gi, bs, off);
+    const long long u2 = __shfl_xor_sync(0xffffffffu, gu, off);
+    gu = u2 < gu ? u2 : gu;
+  }
+  if (lane == 0) { s_c[warp] = gc; s_i[warp] = gi; s_u[warp] = gu; }
+  __syncthreads();
+  if (warp == 0) {
+    gc = lane < NW ? s_c[lane] : INFINITY;
+    gi = lane < NW ? s_i[lane] : -1;
+    gu = lane < NW ? s_u[lane] : LLONG_MAX;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      shfl_cand(gc, gi, bs, off);
+      const long long u2 = __shfl_xor_sync(0xffffffffu, gu, off);
+      gu = u2 < gu ? u2 : gu;
+    }
+    if (lane == 0) {
+      const long long w = (gi >= 0 && gc < INFINITY) ? gi : gu;  // :276-284 fallback
+      win_io[0] = w;
+      scr.centers[r] = w;
+      *ticket = 0;
+    }
+  }
 }
 
 __global__ void owned_kernel(int64_t n, const int32_t* __restrict__ labels,
@@ -860,14 +926,18 @@ cudaError_t launch_kpp_seed(const double* x64, int64_t n, int k, uint64_t seed,
     return cudaLaunchCooperativeKernel((void*)kpp_seed_kernel, dim3(nblk),
                                        dim3(kSeedThreads), args, 0, s);
   }
-  // memory-resident fallback: one launch per round
-  const int grid = sm_count * 4;
+  // memory-resident fallback: one launch per round; a thread holds up to
+  // kMemPPT points (n > sm_count * 4 * 512 * kMemPPT: more CTAs)
+  const int64_t cap = static_cast<int64_t>(sm_count) * 4 * kMemThreads * kMemPPT;
+  const int grid = static_cast<int>(
+      n <= cap ? sm_count * 4 : (n + static_cast<int64_t>(kMemThreads) * kMemPPT - 1) /
+                                    (static_cast<int64_t>(kMemThreads) * kMemPPT));
   int* ticket = scr.status;
   long long* win = reinterpret_cast<long long*>(scr.status + 2);
   cudaError_t e = cudaMemsetAsync(scr.status, 0, sizeof(int) * 4, s);
   if (e != cudaSuccess) return e;
   for (int r = 0; r <= k; ++r) {
-    kpp_mem_round_kernel<<<grid, 512, 0, s>>>(x64, n, r, k, seed, scr, ticket, win);
+    kpp_mem_round_kernel<<<grid, kMemThreads, 0, s>>>(x64, n, r, k, seed, scr, ticket, win);
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
