@@ -193,14 +193,13 @@ __device__ __forceinline__ void shfl_cand(double& c, long long& i, int& s,
 // a2 the smallest value that is not the best entry
 __device__ __forceinline__ void merge_top2(float& a1, int& i1, float& a2, float b1, int j1,
                                            float b2) {
-  const bool take = j1 >= 0 && (i1 < 0 || b1 < a1 || (b1 == a1 && j1 < i1));
-  if (take) {
-    a2 = fminf(a1, b2);
-    a1 = b1;
-    i1 = j1;
-  } else {
-    a2 = fminf(a2, b1);
-  }
+  // branch-free (selects): the communication warp's code stays small and
+  // straight, which keeps it resident in the instruction cache
+  const bool take = (j1 >= 0) & ((i1 < 0) | (b1 < a1) | ((b1 == a1) & (j1 < i1)));
+  const float n2 = take ? fminf(a1, b2) : fminf(a2, b1);
+  a1 = take ? b1 : a1;
+  i1 = take ? j1 : i1;
+  a2 = n2;
 }
 
 // Grid top-2 over nblk LL slots (a1, i1, a2, pad) by one warp: a lane polls
@@ -258,36 +257,47 @@ __device__ __forceinline__ void grid_exchange(unsigned* counter, unsigned target
 }
 
 // Each compute thread keeps PPT points (stride = grid compute threads) in
-// registers. Warp 0 of every CTA holds no points: it is the communication
-// warp. Per round:
-//   compute warps: fold centre r-1 into d2 / labels, approximate clocks
-//     a = -ln(u) / d2 from precomputed draws, warp top-2 -> shared memory;
-//   barrier;
-//   warp 0: CTA top-2, publish (LL slot); CTA 0's warp 0 gathers every
-//     slot, decides and publishes the winner record (16 spread copies);
-//     every warp 0 polls its copy;
-//   compute warps meanwhile draw -ln(u) for round r+1 (off the critical
-//     path);
+// registers. The last warp of every CTA holds no points: it is the
+// communication warp. The rounds run two at a time ("epochs"), speculatively:
+//   compute warps: fold the centres decided in the previous epoch into d2 /
+//     labels (in centre order, strict <), then for round r the FP32 clocks
+//     a = -ln(u_r) / d2 and for round r + 1 the speculative clocks
+//     b = -ln(u_{r+1}) / d2 with the same (pre-c_r) d2; a warp top-2 of each
+//     (the level-1 best carries its FP64 d2) -> shared memory; barrier;
+//   comm warp: CTA top-2s -> one LL slot; every comm warp gathers every slot,
+//     reduces in a fixed order and decides: c_r is the level-0 winner (exact
+//     unless the runner-up lies within the FP32 error band, then the exact
+//     FP64 resolution below), and the level-1 winner s is round r + 1's
+//     centre iff its clock is out of band and c_r leaves its d2 unchanged
+//     (exact FP64 test): every other point's true clock can only be larger
+//     than its speculative one, d2 only shrinks. Otherwise round r + 1 runs
+//     normally in the next epoch (on cfg2 the speculation holds in 99.4 % of
+//     the rounds, so the exchanges halve);
+//   compute warps meanwhile draw -ln(u) for rounds r + 2 and r + 3;
 //   barrier.
-// The approximate argmin is exact unless the grid runner-up lies within the
-// FP32 error band (round 0 ties on duplicate keys, near-ties): then every
-// point inside the band gets the exact FP64 clock and a second exchange
-// decides on (clock, index), as the reference's strict-< scan does.
+// The exact resolution (round-0 key duplicates, near-ties): every point
+// inside the band gets the exact FP64 clock and a second exchange decides on
+// (clock, index), as the reference's strict-< scan does.
 constexpr int kCompWarps = kSeedWarps - 1;
 constexpr int kCompThreads = kCompWarps * 32;
-constexpr int kSlotWords = 4;  // approx: a1, i1, a2, pad; exact: clock lo, hi, idx, pad
+constexpr int kSlotWords = 8;  // approx: a1 i1 a2 b1 j1 b2 d2lo d2hi; exact: clock lo hi, idx, pad
 
 struct SeedSmem {
   float wa1[kSeedWarps];
   int wi1[kSeedWarps];
   float wa2[kSeedWarps];
+  float wb1[kSeedWarps];
+  int wj1[kSeedWarps];
+  float wb2[kSeedWarps];
+  double wd2[kSeedWarps];
   double ec[kSeedWarps];
   long long ei[kSeedWarps];
   long long gu[kSeedWarps];
-  double cx[4];
-  long long win;
+  double cx[2][4];
+  long long win[2];  // round r winner; round r + 1 speculative winner (-1: rejected)
   float thr;
   int exact_rounds;
+  int spec_hits;
 };
 
 __device__ __forceinline__ unsigned long long dbits(double v) {
@@ -297,21 +307,30 @@ __device__ __forceinline__ double bitsd(unsigned lo, unsigned hi) {
   return __longlong_as_double(
       static_cast<long long>((static_cast<unsigned long long>(hi) << 32) | lo));
 }
+// top-2 merge whose best entry carries a payload (its d2)
+__device__ __forceinline__ void merge_top2d(float& a1, int& i1, float& a2, double& d, float b1,
+                                            int j1, float b2, double e) {
+  const bool take = (j1 >= 0) & ((i1 < 0) | (b1 < a1) | ((b1 == a1) & (j1 < i1)));
+  merge_top2(a1, i1, a2, b1, j1, b2);
+  d = take ? e : d;
+}
 
+template <int PPT>
 __global__ void __launch_bounds__(kSeedThreads, 1)
     kpp_seed_kernel(const double* __restrict__ x64, int64_t n, int k,
                     uint64_t seed, KinitScratch scr) {
-  constexpr int PPT = kSeedPPT;
   __shared__ SeedSmem sm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nblk = gridDim.x;
-  const bool comm = warp == 0;
+  // the communication warp is the CTA's last warp: the scheduler favours
+  // high warp ids, so its exchange is not starved by the draws
+  const bool comm = warp == kSeedWarps - 1;
   const long long G = static_cast<long long>(nblk) * kCompThreads;
-  const long long g0 = comm ? -1 : static_cast<long long>(blockIdx.x) * kCompThreads + tid - 32;
+  const long long g0 = comm ? -1 : static_cast<long long>(blockIdx.x) * kCompThreads + tid;
   // LL regions (uint2 words): approx slots [2][nblk], exact slots [2][nblk]
   uint2* llw = reinterpret_cast<uint2*>(scr.slots);
   double px[PPT][4], d2[PPT];
-  float inv[PPT], na[PPT];
+  float inv[PPT], na0[PPT], na1[PPT], nb0[PPT], nb1[PPT];
   uint64_t kp[PPT];
   int lab[PPT];
   unsigned chosen = 0, valid = 0;
@@ -326,104 +345,202 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
     d2[j] = INFINITY;
     inv[j] = 0.f;
     lab[j] = 0;
-    na[j] = INFINITY;
+    na0[j] = na1[j] = nb0[j] = nb1[j] = INFINITY;
   }
   // slots beyond the warp's last valid point are skipped (warp-uniform)
   const unsigned wvalid = __reduce_or_sync(0xffffffffu, valid);
-  if (tid == 0) sm.exact_rounds = 0;
-  auto draw = [&](int r) {  // -ln(u) of round r, FP32 approximation
+  if (tid == 0) {
+    sm.exact_rounds = 0;
+    sm.spec_hits = 0;
+  }
+  auto draw = [&](int r, float (&out)[PPT]) {  // -ln(u) of round r, FP32 approximation
+    if (r >= k) return;
     const uint64_t pre = round_prefix(seed, r);
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      if ((wvalid >> j) & 1) na[j] = nlu_approx(mix64(pre + kp[j]));
+      if ((wvalid >> j) & 1) out[j] = nlu_approx(mix64(pre + kp[j]));
     }
   };
-  if (!comm) draw(0);
-  double c[4] = {0, 0, 0, 0};
+  if (!comm) {
+    draw(0, na0);
+    draw(1, na1);
+  }
+  double cf[2][4];   // centres to fold at the start of the epoch, in order
+  int nf = 0, rf = 0;  // how many, and the round of the first
   unsigned epoch = 0;  // completed counter-based grid exchanges (fallback)
-  for (int r = 0; r <= k; ++r) {
-    const unsigned tag = static_cast<unsigned>(r) + 1u;
-    const int par = r & 1;
+  unsigned xtag = 0;   // LL tag (one per epoch)
+  int r = 0;
+  while (true) {
+    const unsigned tag = ++xtag;
+    const int par = tag & 1;
     uint2* slot_a = llw + par * nblk * kSlotWords;
     uint2* slot_e = llw + (2 + par) * nblk * kSlotWords;
+    const bool lvl1 = r > 0 && r + 1 < k;  // round r + 1 can be speculated
     float a[PPT];
     if (!comm) {
-      // ---- fold centre r-1 (sogmm.cpp:229-238), approximate clocks ----
-      float a1 = INFINITY, a2 = INFINITY;
-      int i1 = -1;
+      // ---- fold the new centres (sogmm.cpp:229-238), clocks of r, r + 1 ----
+      float a1 = INFINITY, a2 = INFINITY, b1 = INFINITY, b2 = INFINITY;
+      int i1 = -1, j1 = -1;
+      double bd = 0.0;
 #pragma unroll
       for (int j = 0; j < PPT; ++j) {
         a[j] = INFINITY;
         if (!((wvalid >> j) & 1)) continue;
-        if (r > 0) {
-          const double dd = dist2(px[j][0], px[j][1], px[j][2], px[j][3], c);
+        for (int f = 0; f < nf; ++f) {
+          const double dd = dist2(px[j][0], px[j][1], px[j][2], px[j][3], cf[f]);
           if (dd < d2[j]) {
             d2[j] = dd;
-            lab[j] = r - 1;
+            lab[j] = rf + f;
             // d2 == 0 (a chosen point or a duplicate) is ineligible (:254)
-            const float f = __double2float_rn(dd);
-            inv[j] = dd > 0.0 ? (isinf(f) ? 1e-38f : rcp_approx(f)) : 0.f;
+            const float fl = __double2float_rn(dd);
+            inv[j] = dd > 0.0 ? (isinf(fl) ? 1e-38f : rcp_approx(fl)) : 0.f;
           }
         }
-        if (r == k) continue;
-        const float aj = r == 0 ? na[j] : (inv[j] > 0.f ? na[j] * inv[j] : INFINITY);
-        a[j] = ((valid >> j) & 1) ? aj : INFINITY;
-        if (a[j] < INFINITY) merge_top2(a1, i1, a2, a[j], static_cast<int>(g0 + j * G), INFINITY);
+        if (r >= k || !((valid >> j) & 1)) continue;
+        const int ij = static_cast<int>(g0 + j * G);
+        const float aj = r == 0 ? na0[j] : (inv[j] > 0.f ? na0[j] * inv[j] : INFINITY);
+        a[j] = aj;
+        if (aj < INFINITY) merge_top2(a1, i1, a2, aj, ij, INFINITY);
+        if (lvl1 && inv[j] > 0.f) merge_top2d(b1, j1, b2, bd, na1[j] * inv[j], ij, INFINITY, d2[j]);
       }
-      if (r == k) break;
+      if (r >= k) break;
 #pragma unroll
       for (int off = 16; off >= 1; off >>= 1) {
-        const float b1 = __shfl_xor_sync(0xffffffffu, a1, off);
-        const int k1 = __shfl_xor_sync(0xffffffffu, i1, off);
-        const float b2 = __shfl_xor_sync(0xffffffffu, a2, off);
-        merge_top2(a1, i1, a2, b1, k1, b2);
+        const float o1 = __shfl_xor_sync(0xffffffffu, a1, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, i1, off);
+        const float o2 = __shfl_xor_sync(0xffffffffu, a2, off);
+        merge_top2(a1, i1, a2, o1, oi, o2);
+        const float p1 = __shfl_xor_sync(0xffffffffu, b1, off);
+        const int pj = __shfl_xor_sync(0xffffffffu, j1, off);
+        const float p2 = __shfl_xor_sync(0xffffffffu, b2, off);
+        const double pd = __shfl_xor_sync(0xffffffffu, bd, off);
+        merge_top2d(b1, j1, b2, bd, p1, pj, p2, pd);
       }
       if (lane == 0) {
-        sm.wa1[warp] = a1;
-        sm.wi1[warp] = i1;
-        sm.wa2[warp] = a2;
+        sm.wa1[warp] = a1; sm.wi1[warp] = i1; sm.wa2[warp] = a2;
+        sm.wb1[warp] = b1; sm.wj1[warp] = j1; sm.wb2[warp] = b2; sm.wd2[warp] = bd;
       }
-    } else if (r == k) {
+    } else if (r >= k) {
       break;
     }
     __syncthreads();
     if (comm) {
-      // ---- CTA top-2 -> LL slot (8-byte (payload, tag) words) ----
-      float c1 = lane >= 1 && lane < kSeedWarps ? sm.wa1[lane] : INFINITY;
-      int j1 = lane >= 1 && lane < kSeedWarps ? sm.wi1[lane] : -1;
-      float c2 = lane >= 1 && lane < kSeedWarps ? sm.wa2[lane] : INFINITY;
-#pragma unroll
+      // ---- CTA top-2s -> one LL slot of 8-byte (payload, tag) words ----
+      const bool w = lane < kCompWarps;
+      float c1 = w ? sm.wa1[lane] : INFINITY, c2 = w ? sm.wa2[lane] : INFINITY;
+      int k1 = w ? sm.wi1[lane] : -1;
+      float e1 = w ? sm.wb1[lane] : INFINITY, e2 = w ? sm.wb2[lane] : INFINITY;
+      int l1 = w ? sm.wj1[lane] : -1;
+      double ed = w ? sm.wd2[lane] : 0.0;
+#pragma unroll 1
       for (int off = 16; off >= 1; off >>= 1) {
-        const float b1 = __shfl_xor_sync(0xffffffffu, c1, off);
-        const int k1 = __shfl_xor_sync(0xffffffffu, j1, off);
-        const float b2 = __shfl_xor_sync(0xffffffffu, c2, off);
-        merge_top2(c1, j1, c2, b1, k1, b2);
+        const float o1 = __shfl_xor_sync(0xffffffffu, c1, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, k1, off);
+        const float o2 = __shfl_xor_sync(0xffffffffu, c2, off);
+        merge_top2(c1, k1, c2, o1, oi, o2);
+        const float p1 = __shfl_xor_sync(0xffffffffu, e1, off);
+        const int pj = __shfl_xor_sync(0xffffffffu, l1, off);
+        const float p2 = __shfl_xor_sync(0xffffffffu, e2, off);
+        const double pd = __shfl_xor_sync(0xffffffffu, ed, off);
+        merge_top2d(e1, l1, e2, ed, p1, pj, p2, pd);
       }
-      if (lane == 0) {
-        uint2* w = slot_a + blockIdx.x * kSlotWords;
-        st_ll(w + 0, __float_as_uint(c1), tag);
-        st_ll(w + 1, static_cast<unsigned>(j1), tag);
-        st_ll(w + 2, __float_as_uint(c2), tag);
-        st_ll(w + 3, 0u, tag);
+      if (lane < kSlotWords) {
+        const unsigned long long db = dbits(ed);
+        const unsigned v = lane == 0 ? __float_as_uint(c1) : lane == 1 ? static_cast<unsigned>(k1)
+                         : lane == 2 ? __float_as_uint(c2) : lane == 3 ? __float_as_uint(e1)
+                         : lane == 4 ? static_cast<unsigned>(l1) : lane == 5 ? __float_as_uint(e2)
+                         : lane == 6 ? static_cast<unsigned>(db) : static_cast<unsigned>(db >> 32);
+        st_ll(slot_a + blockIdx.x * kSlotWords + lane, v, tag);
       }
-      // ---- grid top-2: every CTA gathers every slot (all of a lane's
-      // slots polled concurrently), reduces in a fixed order ----
-      float g1 = INFINITY, g2 = INFINITY;
-      int gi = -1;
-      gather_top2(slot_a, nblk, tag, lane, g1, gi, g2);
-      // exact unless the runner-up lies within the FP32 error band
+      // ---- grid top-2s: every CTA gathers every slot (a lane's slots
+      // polled concurrently), reduces in a fixed order ----
+      float g1 = INFINITY, g2 = INFINITY, h1 = INFINITY, h2 = INFINITY;
+      int gi = -1, hj = -1;
+      double hd = 0.0;
+      constexpr int kQ = 5;  // slots per lane per pass (one pass covers 160 CTAs)
+      for (int base = 0; base < nblk; base += 32 * kQ) {
+        unsigned pend = 0;
+#pragma unroll
+        for (int q = 0; q < kQ; ++q)
+          if (base + lane + 32 * q < nblk) pend |= 1u << q;
+        while (pend) {
+          unsigned v[kQ][8];
+          bool ok[kQ];
+#pragma unroll
+          for (int q = 0; q < kQ; ++q) {
+            ok[q] = false;
+            if ((pend >> q) & 1) {
+              const uint2* wp = slot_a + (base + lane + 32 * q) * kSlotWords;
+              bool good = true;
+#pragma unroll
+              for (int h = 0; h < 4; ++h) {
+                unsigned t0, t1;
+                asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(v[q][2 * h]), "=r"(t0), "=r"(v[q][2 * h + 1]), "=r"(t1)
+                             : "l"(wp + 2 * h)
+                             : "memory");
+                good = good && t0 == tag && t1 == tag;
+              }
+              ok[q] = good;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < kQ; ++q) {
+            if (ok[q]) {
+              merge_top2(g1, gi, g2, __uint_as_float(v[q][0]), static_cast<int>(v[q][1]),
+                         __uint_as_float(v[q][2]));
+              merge_top2d(h1, hj, h2, hd, __uint_as_float(v[q][3]), static_cast<int>(v[q][4]),
+                          __uint_as_float(v[q][5]), bitsd(v[q][6], v[q][7]));
+              pend &= ~(1u << q);
+            }
+          }
+        }
+      }
+#pragma unroll 1
+      for (int off = 16; off >= 1; off >>= 1) {
+        const float o1 = __shfl_xor_sync(0xffffffffu, g1, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, gi, off);
+        const float o2 = __shfl_xor_sync(0xffffffffu, g2, off);
+        merge_top2(g1, gi, g2, o1, oi, o2);
+        const float p1 = __shfl_xor_sync(0xffffffffu, h1, off);
+        const int pj = __shfl_xor_sync(0xffffffffu, hj, off);
+        const float p2 = __shfl_xor_sync(0xffffffffu, h2, off);
+        const double pd = __shfl_xor_sync(0xffffffffu, hd, off);
+        merge_top2d(h1, hj, h2, hd, p1, pj, p2, pd);
+      }
+      // level 0: exact unless the runner-up lies within the FP32 error band
       const bool need_exact = gi >= 0 && !(g2 > g1 * kBand);
       const long long wi = need_exact ? -2 : gi;
-      if (lane < 4 && wi >= 0) sm.cx[lane] = __ldg(x64 + lane * n + wi);  // read-only cloud
+      // level 1: out of band, and c_r leaves the speculative winner's d2 as is
+      long long si = -1;
+      double xs[4] = {0, 0, 0, 0}, xc[4] = {0, 0, 0, 0};
+      if (lvl1 && wi >= 0 && hj >= 0 && h2 > h1 * kBand) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          xc[q] = __ldg(x64 + q * n + wi);
+          xs[q] = __ldg(x64 + q * n + hj);
+        }
+        const double dd = dist2(xs[0], xs[1], xs[2], xs[3], xc);
+        if (!(dd < hd)) si = hj;
+      } else if (wi >= 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) xc[q] = __ldg(x64 + q * n + wi);
+      }
+      if (lane < 4) {
+        sm.cx[0][lane] = xc[lane == 0 ? 0 : lane == 1 ? 1 : lane == 2 ? 2 : 3];
+        sm.cx[1][lane] = xs[lane == 0 ? 0 : lane == 1 ? 1 : lane == 2 ? 2 : 3];
+      }
       if (lane == 0) {
-        sm.win = wi;
+        sm.win[0] = wi;
+        sm.win[1] = si;
         sm.thr = need_exact ? g1 * kBand : -1.f;
       }
-    } else if (r + 1 < k) {
-      draw(r + 1);  // overlaps the exchange
+    } else {
+      draw(r + 2, nb0);  // overlaps the exchange
+      draw(r + 3, nb1);
     }
     __syncthreads();
-    if (sm.win == -2) {
+    if (sm.win[0] == -2) {
       // ---- exact resolution among the points inside the band (rare) ----
       if (!comm) {
         const float thr = sm.thr;
@@ -453,8 +570,8 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
       }
       __syncthreads();
       if (comm) {
-        double c1 = lane >= 1 && lane < kSeedWarps ? sm.ec[lane] : INFINITY;
-        long long j1 = lane >= 1 && lane < kSeedWarps ? sm.ei[lane] : -1;
+        double c1 = lane < kCompWarps ? sm.ec[lane] : INFINITY;
+        long long j1 = lane < kCompWarps ? sm.ei[lane] : -1;
         int src = lane;
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) shfl_cand(c1, j1, src, off);
@@ -482,13 +599,16 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) shfl_cand(gc, gj, bs2, off);
         const long long wi = (gj >= 0 && gc < INFINITY) ? gj : -1;
-        if (lane < 4 && wi >= 0) sm.cx[lane] = __ldg(x64 + lane * n + wi);
-        if (lane == 0) sm.win = wi;
+        if (lane < 4 && wi >= 0) sm.cx[0][lane] = __ldg(x64 + lane * n + wi);
+        if (lane == 0) {
+          sm.win[0] = wi;
+          sm.win[1] = -1;  // no speculation across an exact round
+        }
       }
       __syncthreads();
       if (tid == 0) sm.exact_rounds += 1;
     }
-    if (sm.win < 0) {
+    if (sm.win[0] < 0) {
       // sogmm.cpp:276-284: no eligible point anywhere -> lowest unchosen
       // index (rare; counter-based exchange)
       const unsigned freem = valid & ~chosen;
@@ -500,9 +620,9 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
       }
       if (lane == 0) sm.gu[warp] = bu;
       __syncthreads();
-      if (tid == 0) {
+      if (tid == 32 * (kSeedWarps - 1)) {
         long long m = LLONG_MAX;
-        for (int w = 0; w < kSeedWarps; ++w) m = sm.gu[w] < m ? sm.gu[w] : m;
+        for (int w = 0; w < kCompWarps; ++w) m = sm.gu[w] < m ? sm.gu[w] : m;
         KppSlot* fs = reinterpret_cast<KppSlot*>(llw + 4 * nblk * kSlotWords);
         fs[blockIdx.x].unchosen = m;
         ++epoch;
@@ -512,18 +632,46 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
           const long long u2 = reinterpret_cast<volatile KppSlot*>(fs)[b].unchosen;
           m = u2 < m ? u2 : m;
         }
-        sm.win = m;
+        sm.win[0] = m;
+        sm.win[1] = -1;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) sm.cx[q] = x64[q * n + m];
+        for (int q = 0; q < 4; ++q) sm.cx[0][q] = x64[q * n + m];
       }
       __syncthreads();
     }
-    const long long win = sm.win;
-    if (blockIdx.x == 0 && tid == 0) scr.centers[r] = win;
+    // ---- commit this epoch's centres (1 or 2) ----
+    const long long w0 = sm.win[0], w1 = sm.win[1];
+    if (blockIdx.x == 0 && tid == 0) {  // (a compute thread)
+      scr.centers[r] = w0;
+      if (w1 >= 0) {
+        scr.centers[r + 1] = w1;
+        sm.spec_hits += 1;
+      }
+    }
+    rf = r;
+    nf = w1 >= 0 ? 2 : 1;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) c[q] = sm.cx[q];
-    if (!comm && win % G == g0) chosen |= 1u << static_cast<int>(win / G);
-    // sm.win / sm.cx are rewritten by warp 0 only after the next round's
+    for (int q = 0; q < 4; ++q) {
+      cf[0][q] = sm.cx[0][q];
+      cf[1][q] = sm.cx[1][q];
+    }
+    if (!comm) {
+      if (w0 % G == g0) chosen |= 1u << static_cast<int>(w0 / G);
+      if (w1 >= 0 && w1 % G == g0) chosen |= 1u << static_cast<int>(w1 / G);
+      // draws of the next epoch's two rounds
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        if (w1 >= 0) {
+          na0[j] = nb0[j];
+          na1[j] = nb1[j];
+        } else {
+          na0[j] = na1[j];
+          na1[j] = nb0[j];
+        }
+      }
+    }
+    r += nf;
+    // sm.win / sm.cx are rewritten by warp 0 only after the next epoch's
     // first barrier, which every thread reaches after these reads
   }
   // labels + owned counts (every point's final nearest centre)
@@ -921,11 +1069,13 @@ cudaError_t launch_kpp_seed(const double* x64, int64_t n, int k, uint64_t seed,
                             KinitScratch scr, int sm_count, cudaStream_t s) {
   // one CTA per SM, points register-resident while they fit
   const int nblk = sm_count < kMaxSeedBlocks ? sm_count : kMaxSeedBlocks;
-  if (n <= static_cast<int64_t>(nblk) * kCompThreads * kSeedPPT) {
-    void* args[] = {(void*)&x64, (void*)&n, (void*)&k, (void*)&seed, (void*)&scr};
-    return cudaLaunchCooperativeKernel((void*)kpp_seed_kernel, dim3(nblk),
+  void* args[] = {(void*)&x64, (void*)&n, (void*)&k, (void*)&seed, (void*)&scr};
+  if (n <= static_cast<int64_t>(nblk) * kCompThreads * 6)
+    return cudaLaunchCooperativeKernel((void*)kpp_seed_kernel<6>, dim3(nblk), dim3(kSeedThreads),
+                                       args, 0, s);
+  if (n <= static_cast<int64_t>(nblk) * kCompThreads * kSeedPPT)
+    return cudaLaunchCooperativeKernel((void*)kpp_seed_kernel<kSeedPPT>, dim3(nblk),
                                        dim3(kSeedThreads), args, 0, s);
-  }
   // memory-resident fallback: one launch per round; a thread holds up to
   // kMemPPT points (n > sm_count * 4 * 512 * kMemPPT: more CTAs)
   const int64_t cap = static_cast<int64_t>(sm_count) * 4 * kMemThreads * kMemPPT;
