@@ -134,6 +134,27 @@ int gmmb_e_step(gmmb_ctx* ctx, const double* pts, int64_t n, int d, int m,
                 const double* w, const double* mu, const double* cov,
                 double* ll_out, double* log_gamma_out);
 
+/* score (inference.hpp:33, inference.cpp:141-172): average log-likelihood
+ * of the cloud under the model (natural log, FP64); point_ll_out (n,
+ * optional) receives each point's log-sum-exp. D = 3 or 4; 4 is the
+ * reference's Gmm4. */
+int gmmb_score(gmmb_ctx* ctx, const double* pts, int64_t n, int d, int m, const double* w,
+               const double* mu, const double* cov, double* avg_ll_out, double* point_ll_out);
+
+/* joint_dist_sample (inference.hpp:13-14, inference.cpp:17-54): n draws,
+ * out = n x d column-major; draw i depends only on (seed, i) through the
+ * reference's counter RNG (component: rng::uniform(seed, 0, i); normals:
+ * rng::normal_pair(seed, 1, 4i) and (seed, 1, 4i + 2)). */
+int gmmb_sample(gmmb_ctx* ctx, int d, int m, const double* w, const double* mu,
+                const double* cov, int64_t n, uint64_t seed, double* out);
+
+/* color_conditional (inference.hpp:25-27, inference.cpp:56-139): expected
+ * intensity and variance at n 3D locations (locs n x 3 column-major) under
+ * a 4D model; clamp != 0 clamps the expectation to [0, 1]. */
+int gmmb_color_conditional(gmmb_ctx* ctx, int m, const double* w, const double* mu,
+                           const double* cov, const double* locs, int64_t n, int clamp,
+                           double* expected, double* variance);
+
 /* m_step (sogmm.hpp:62-63, sogmm.cpp:399-463) from an N x M log_gamma.
  * Outputs sized for m; *m_out = kept components; *removed = m - *m_out. */
 int gmmb_m_step(gmmb_ctx* ctx, const double* pts, int64_t n, int d,

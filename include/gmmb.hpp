@@ -220,4 +220,41 @@ inline CholeskyCache cholesky_cache(Context& ctx, const Gmm& model) {
   return c;
 }
 
+// score (inference.cpp:141-172): average log-likelihood.
+inline double score(Context& ctx, const Gmm& model, const PointCloud& cloud) {
+  double avg = 0.0;
+  check(gmmb_score(ctx.get(), cloud.points.data(), cloud.size(), cloud.dim, model.components(),
+                   model.weights.data(), model.means.data(), model.covariances.data(), &avg,
+                   nullptr));
+  return avg;
+}
+
+// joint_dist_sample (inference.cpp:17-54).
+inline PointCloud joint_dist_sample(Context& ctx, const Gmm& model, std::int64_t n,
+                                    std::uint64_t seed) {
+  PointCloud out;
+  out.dim = model.dim;
+  out.points.resize(static_cast<size_t>(n > 0 ? n : 0) * model.dim);
+  check(gmmb_sample(ctx.get(), model.dim, model.components(), model.weights.data(),
+                    model.means.data(), model.covariances.data(), n, seed, out.points.data()));
+  return out;
+}
+
+// color_conditional (inference.cpp:56-139); locs is N x 3 column-major.
+struct ConditionalResult {
+  std::vector<double> expected_intensity;
+  std::vector<double> variance;
+};
+inline ConditionalResult color_conditional(Context& ctx, const Gmm& model,
+                                           const std::vector<double>& locs, bool clamp = true) {
+  const std::int64_t n = static_cast<std::int64_t>(locs.size() / 3);
+  ConditionalResult r;
+  r.expected_intensity.resize(n);
+  r.variance.resize(n);
+  check(gmmb_color_conditional(ctx.get(), model.components(), model.weights.data(),
+                               model.means.data(), model.covariances.data(), locs.data(), n,
+                               clamp ? 1 : 0, r.expected_intensity.data(), r.variance.data()));
+  return r;
+}
+
 }  // namespace gmmb

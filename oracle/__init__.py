@@ -88,6 +88,11 @@ def load():
                                                       ctypes.POINTER(_Stats)]),
             "orc_fit_k": (ctypes.c_int, [D, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(_Em),
                                          D, D, D, D, ctypes.POINTER(_Stats), I64, I32]),
+            "orc_score": (ctypes.c_int, [D, ctypes.c_int64, ctypes.c_int, D, D, D, D]),
+            "orc_sample": (ctypes.c_int, [ctypes.c_int, D, D, D, ctypes.c_int64,
+                                          ctypes.c_uint64, D]),
+            "orc_color_conditional": (ctypes.c_int, [ctypes.c_int, D, D, D, D, ctypes.c_int64,
+                                                     ctypes.c_int, D, D]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -273,3 +278,36 @@ def fit_k(points, K, max_iters=100, ll_rel_tol=1e-5, cov_reg=1e-6, seed=0):
     return dict(w=w, mu=mu, cov=cov, ll_trace=ll[:st.em_iterations],
                 em_iterations=st.em_iterations, final_ll=st.final_log_likelihood,
                 removed=st.removed_components, k_init=st.k_init, centers=cen, labels=lab)
+
+
+def _model4(w, mu, cov):
+    return (np.ascontiguousarray(w, dtype=np.float64), np.ascontiguousarray(mu, dtype=np.float64),
+            np.ascontiguousarray(cov, dtype=np.float64))
+
+
+def score(points, w, mu, cov):
+    """inference.cpp:141-172: average log-likelihood (4D model)."""
+    p = embed3(points)
+    w, mu, cov = _model4(w, mu, cov)
+    out = ctypes.c_double()
+    _check(load().orc_score(_p(p), p.shape[0], len(w), _p(w), _p(mu), _p(cov), ctypes.byref(out)))
+    return out.value
+
+
+def sample(w, mu, cov, n, seed=0):
+    """inference.cpp:17-54: (n, 4) draws."""
+    w, mu, cov = _model4(w, mu, cov)
+    out = np.zeros((n, 4), order="F")
+    _check(load().orc_sample(len(w), _p(w), _p(mu), _p(cov), n, seed, _p(out)))
+    return out
+
+
+def color_conditional(w, mu, cov, locs, clamp=True):
+    """inference.cpp:56-139: (expected intensity, variance) at (n, 3) locations."""
+    w, mu, cov = _model4(w, mu, cov)
+    loc = np.asfortranarray(np.asarray(locs, dtype=np.float64)[:, :3])
+    n = loc.shape[0]
+    e, v = np.zeros(n), np.zeros(n)
+    _check(load().orc_color_conditional(len(w), _p(w), _p(mu), _p(cov), _p(loc), n,
+                                        1 if clamp else 0, _p(e), _p(v)))
+    return e, v

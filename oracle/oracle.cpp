@@ -711,6 +711,185 @@ int guarded(F&& f) {
 
 }  // namespace
 
+// ---- inference.cpp restatements (score, joint_dist_sample, color_conditional)
+
+// 3x3 Cholesky (Eigen LLT semantics: column algorithm) and L L^T x = b solve
+bool cholesky3(const double* a, double* l) {  // a, l column-major 3x3
+  for (int i = 0; i < 9; ++i) l[i] = 0.0;
+  for (int j = 0; j < 3; ++j) {
+    double d = a[j * 3 + j];
+    for (int k = 0; k < j; ++k) d -= l[k * 3 + j] * l[k * 3 + j];
+    if (!(d > 0.0) || !std::isfinite(d)) return false;
+    const double ljj = std::sqrt(d);
+    l[j * 3 + j] = ljj;
+    for (int i = j + 1; i < 3; ++i) {
+      double s2 = a[j * 3 + i];
+      for (int k = 0; k < j; ++k) s2 -= l[k * 3 + i] * l[k * 3 + j];
+      l[j * 3 + i] = s2 / ljj;
+    }
+  }
+  return true;
+}
+void llt_solve3(const double* l, const double* b, double* x) {
+  double y[3];
+  for (int i = 0; i < 3; ++i) {
+    double s2 = b[i];
+    for (int k = 0; k < i; ++k) s2 -= l[k * 3 + i] * y[k];
+    y[i] = s2 / l[i * 3 + i];
+  }
+  for (int i = 2; i >= 0; --i) {
+    double s2 = y[i];
+    for (int k = i + 1; k < 3; ++k) s2 -= l[i * 3 + k] * x[k];
+    x[i] = s2 / l[i * 3 + i];
+  }
+}
+
+// inference.cpp:141-172: average log-likelihood
+double score(const double* pts, int64_t n, const Model& md) {
+  const Cache c = cholesky_cache(md);
+  const int m = md.m();
+  std::vector<double> base(m);
+  for (int b = 0; b < m; ++b) base[b] = std::log(md.w[b]) + c.logdet[b] - 2.0 * kLog2Pi;
+  const int64_t nb = num_blocks(n);
+  std::vector<double> partials(nb, 0.0);
+  parallel_for_blocks(nb, [&](int64_t blk) {
+    const int64_t r0 = blk * kPointBlock;
+    const int64_t len = std::min<int64_t>(n, r0 + kPointBlock) - r0;
+    std::vector<double> block(static_cast<size_t>(len) * m), lse(len);
+    for (int b = 0; b < m; ++b) {
+      const double* mu = &md.mu[b * 4];
+      const double* p = &c.prec[b * 16];
+      for (int64_t i = 0; i < len; ++i) {
+        const int64_t g = r0 + i;
+        block[b * len + i] = log_density(p, base[b], pts[g] - mu[0], pts[n + g] - mu[1],
+                                         pts[2 * n + g] - mu[2], pts[3 * n + g] - mu[3]);
+      }
+    }
+    logsumexp_rows(block.data(), len, m, lse.data());
+    double s2 = 0.0;
+    for (int64_t i = 0; i < len; ++i) s2 += lse[i];
+    partials[blk] = s2;
+  });
+  double total = 0.0;
+  for (double p : partials) total += p;
+  return total / static_cast<double>(n);
+}
+
+// inference.cpp:17-54: draws (n x 4 column-major)
+void joint_dist_sample(const Model& md, int64_t n, uint64_t seed, double* out) {
+  const Cache c = cholesky_cache(md);
+  const int m = md.m();
+  std::vector<double> cdf(m);
+  double acc = 0.0;
+  for (int b = 0; b < m; ++b) {
+    acc += md.w[b];
+    cdf[b] = acc;
+  }
+  cdf[m - 1] = 1.0;
+  parallel_for_blocks(num_blocks(n), [&](int64_t blk) {
+    const int64_t r0 = blk * kPointBlock;
+    const int64_t r1 = std::min<int64_t>(n, r0 + kPointBlock);
+    for (int64_t i = r0; i < r1; ++i) {
+      const double u = orc_uniform(seed, 0, static_cast<uint64_t>(i));
+      int b = 0;
+      while (b < m - 1 && u >= cdf[b]) ++b;
+      double z[4];
+      orc_normal_pair(seed, 1, static_cast<uint64_t>(i) * 4, &z[0], &z[1]);
+      orc_normal_pair(seed, 1, static_cast<uint64_t>(i) * 4 + 2, &z[2], &z[3]);
+      const double* L = &c.lower[b * 16];
+      for (int r = 0; r < 4; ++r) {
+        double v = at(L, r, 0) * z[0];
+        for (int j = 1; j < 4; ++j) v = v + at(L, r, j) * z[j];
+        out[r * n + i] = md.mu[b * 4 + r] + v;
+      }
+    }
+  });
+}
+
+// inference.cpp:56-139: E[intensity | xyz] and Var
+void color_conditional(const Model& md, const double* locs, int64_t n, int clamp,
+                       double* expected, double* variance) {
+  const int m = md.m();
+  std::vector<double> xx_inv(m * 9), mux(m * 3), reg(m * 3), mui(m), cvar(m), gbase(m);
+  for (int b = 0; b < m; ++b) {
+    double cov[16];
+    unpack_symmetric4(&md.cov[b * 10], cov);
+    double sxx[9], sxi[3], l[9];
+    for (int i = 0; i < 3; ++i) {
+      for (int j = 0; j < 3; ++j) sxx[j * 3 + i] = at(cov, i, j);
+      sxi[i] = at(cov, i, 3);
+    }
+    if (!cholesky3(sxx, l)) {
+      throw NumError{"spatial covariance of component " + std::to_string(b) +
+                     " is not positive definite"};
+    }
+    for (int col = 0; col < 3; ++col) {
+      double e[3] = {0, 0, 0}, x[3];
+      e[col] = 1.0;
+      llt_solve3(l, e, x);
+      for (int i = 0; i < 3; ++i) xx_inv[b * 9 + col * 3 + i] = x[i];
+    }
+    llt_solve3(l, sxi, &reg[b * 3]);
+    for (int i = 0; i < 3; ++i) mux[b * 3 + i] = md.mu[b * 4 + i];
+    mui[b] = md.mu[b * 4 + 3];
+    cvar[b] = at(cov, 3, 3) - (sxi[0] * reg[b * 3] + sxi[1] * reg[b * 3 + 1] + sxi[2] * reg[b * 3 + 2]);
+    const double log_det = 2.0 * ((std::log(l[0]) + std::log(l[4])) + std::log(l[8]));
+    gbase[b] = std::log(md.w[b]) - 0.5 * (3.0 * kLog2Pi + log_det);
+  }
+  std::atomic<int> bad{0};
+  std::atomic<int64_t> bad_idx{-1};
+  std::vector<double> vbad(1, 0.0);
+  parallel_for_blocks(num_blocks(n), [&](int64_t blk) {
+    const int64_t r0 = blk * kPointBlock;
+    const int64_t r1 = std::min<int64_t>(n, r0 + kPointBlock);
+    std::vector<double> lg(m), cm(m), mh(m);
+    for (int64_t i = r0; i < r1; ++i) {
+      const double x[3] = {locs[i], locs[n + i], locs[2 * n + i]};
+      double mx = kNegInf;
+      for (int b = 0; b < m; ++b) {
+        const double d[3] = {x[0] - mux[b * 3], x[1] - mux[b * 3 + 1], x[2] - mux[b * 3 + 2]};
+        const double* A = &xx_inv[b * 9];
+        double q = 0.0;
+        for (int r = 0; r < 3; ++r) {
+          const double ad = A[0 * 3 + r] * d[0] + A[1 * 3 + r] * d[1] + A[2 * 3 + r] * d[2];
+          q += d[r] * ad;
+        }
+        mh[b] = q;
+        lg[b] = gbase[b] - 0.5 * q;
+        cm[b] = mui[b] + (reg[b * 3] * d[0] + reg[b * 3 + 1] * d[1] + reg[b * 3 + 2] * d[2]);
+        if (lg[b] > mx) mx = lg[b];
+      }
+      double e = 0.0, second = 0.0;
+      if (mx == kNegInf || !std::isfinite(mx)) {
+        int b = 0;
+        for (int q = 1; q < m; ++q)
+          if (mh[q] < mh[b]) b = q;
+        e = cm[b];
+        second = cvar[b] + e * e;
+      } else {
+        double norm = 0.0;
+        for (int b = 0; b < m; ++b) {
+          const double w = std::exp(lg[b] - mx);
+          norm += w;
+          e += w * cm[b];
+          second += w * (cvar[b] + cm[b] * cm[b]);
+        }
+        e /= norm;
+        second /= norm;
+      }
+      double v = second - e * e;
+      if (v < -1e-12) {
+        bad = 1;
+        bad_idx = i;
+      }
+      if (v < 0.0) v = 0.0;
+      variance[i] = v;
+      expected[i] = clamp ? std::min(std::max(e, 0.0), 1.0) : e;
+    }
+  });
+  if (bad) throw NumError{"conditional variance below tolerance"};
+}
+
 extern "C" {
 
 const char* orc_last_error(void) { return g_err.c_str(); }
@@ -938,4 +1117,31 @@ int orc_fit_k(const double* pts, int64_t n, int K, const orc_em_params* em,
   });
 }
 
+
+int orc_score(const double* pts, int64_t n, int m, const double* w, const double* mu,
+              const double* cov, double* out) {
+  return guarded([&] {
+    if (n < 1) throw ArgError{"empty cloud"};
+    Model md = model_from(m, w, mu, cov);
+    *out = score(pts, n, md);
+  });
+}
+
+int orc_sample(int m, const double* w, const double* mu, const double* cov, int64_t n,
+               uint64_t seed, double* out) {
+  return guarded([&] {
+    if (n < 1) throw ArgError{"sample count must be >= 1"};
+    Model md = model_from(m, w, mu, cov);
+    joint_dist_sample(md, n, seed, out);
+  });
+}
+
+int orc_color_conditional(int m, const double* w, const double* mu, const double* cov,
+                          const double* locs, int64_t n, int clamp, double* expected,
+                          double* variance) {
+  return guarded([&] {
+    Model md = model_from(m, w, mu, cov);
+    color_conditional(md, locs, n, clamp, expected, variance);
+  });
+}
 }  // extern "C"

@@ -124,6 +124,17 @@ int orc_fit_from_streaming(const double* pts, int64_t n, int m0,
                            double* w_out, double* mu_out, double* cov_out,
                            double* ll_trace, orc_fit_stats* stats);
 
+/* inference.cpp:141-172 score (average ll), :17-54 joint_dist_sample
+ * (n x 4 column-major out), :56-139 color_conditional (locs n x 3
+ * column-major). */
+int orc_score(const double* pts, int64_t n, int m, const double* w, const double* mu,
+              const double* cov, double* out);
+int orc_sample(int m, const double* w, const double* mu, const double* cov, int64_t n,
+               uint64_t seed, double* out);
+int orc_color_conditional(int m, const double* w, const double* mu, const double* cov,
+                          const double* locs, int64_t n, int clamp, double* expected,
+                          double* variance);
+
 #ifdef __cplusplus
 }
 #endif

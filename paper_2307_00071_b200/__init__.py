@@ -118,6 +118,12 @@ _SIGS = {
     "gmmb_shard_key_tail": (ctypes.c_int, [_D, ctypes.c_int, ctypes.c_int, _D]),
     "gmmb_ffma_peak": (ctypes.c_int, [_V, ctypes.c_double, _D, _D]),
     "gmmb_ctx_set_timing": (ctypes.c_int, [_V, ctypes.c_int]),
+    "gmmb_score": (ctypes.c_int, [_V, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _D, _D, _D,
+                                  _D, _D]),
+    "gmmb_sample": (ctypes.c_int, [_V, ctypes.c_int, ctypes.c_int, _D, _D, _D, ctypes.c_int64,
+                                   ctypes.c_uint64, _D]),
+    "gmmb_color_conditional": (ctypes.c_int, [_V, ctypes.c_int, _D, _D, _D, _D, ctypes.c_int64,
+                                              ctypes.c_int, _D, _D]),
 }
 
 
@@ -420,6 +426,42 @@ def e_step(points, model: Gmm, want_log_gamma: bool = True,
     _check(load().gmmb_e_step(c.handle, _ptr(p), n, d, m, _ptr(w), _ptr(mu), _ptr(cov),
                               ctypes.byref(ll), _ptr(lg)))
     return lg, ll.value
+
+
+def score(points, model: Gmm, ctx: Optional[Context] = None, per_point: bool = False):
+    """inference.cpp:141-172: average log-likelihood of the cloud (and, with
+    per_point, each point's log-sum-exp)."""
+    c = _ctx(ctx)
+    p, n, d = _points(points)
+    w, mu, cov, m = _model_arrays(model, d)
+    avg = ctypes.c_double()
+    pp = np.zeros(n) if per_point else None
+    _check(load().gmmb_score(c.handle, _ptr(p), n, d, m, _ptr(w), _ptr(mu), _ptr(cov),
+                             ctypes.byref(avg), _ptr(pp)))
+    return (avg.value, pp) if per_point else avg.value
+
+
+def joint_dist_sample(model: Gmm, n: int, seed: int = 0, ctx: Optional[Context] = None):
+    """inference.cpp:17-54: (n, D) draws; draw i depends only on (seed, i)."""
+    c = _ctx(ctx)
+    d = np.asarray(model.means).shape[1]
+    w, mu, cov, m = _model_arrays(model, d)
+    out = np.zeros((n, d), order="F")
+    _check(load().gmmb_sample(c.handle, d, m, _ptr(w), _ptr(mu), _ptr(cov), n, seed, _ptr(out)))
+    return out
+
+
+def color_conditional(model: Gmm, locs, clamp: bool = True, ctx: Optional[Context] = None):
+    """inference.cpp:56-139: (expected intensity, variance) at (n, 3) locations
+    under a 4D model."""
+    c = _ctx(ctx)
+    w, mu, cov, m = _model_arrays(model, 4)
+    loc = np.asfortranarray(np.asarray(locs, dtype=np.float64)[:, :3])
+    n = loc.shape[0]
+    e, v = np.zeros(n), np.zeros(n)
+    _check(load().gmmb_color_conditional(c.handle, m, _ptr(w), _ptr(mu), _ptr(cov), _ptr(loc), n,
+                                         1 if clamp else 0, _ptr(e), _ptr(v)))
+    return e, v
 
 
 def m_step(points, log_gamma, cov_reg: float = 1e-6, ctx: Optional[Context] = None):

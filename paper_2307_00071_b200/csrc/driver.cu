@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <climits>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -25,6 +26,7 @@
 #include "kinit_kernels.cuh"
 #include "layout.cuh"
 #include "mstep_hard.cuh"
+#include "inference.cuh"
 
 using namespace gmmb;
 
@@ -140,6 +142,9 @@ struct gmmb_ctx {
   DevBuf<int32_t> midx;
   DevBuf<unsigned char> sort_tmp;
   DevBuf<int32_t> hidx;           // hard M step: [3][n] sort indices / keys
+  // inference (score / sample / conditional / e_step API)
+  DevBuf<double> iw, imu, icov, ifac, ilow, iout, iout2;
+  DevBuf<int> ierr;
   DevBuf<int> flags;
   // kinit
   DevBuf<uint64_t> keys;
@@ -769,6 +774,51 @@ void fit_from_resident(gmmb_ctx* c, int m, const double* w0, const double* mu0,
 }
 
 
+// ---- inference helpers ----------------------------------------------------
+// gmm.cpp:8-31 Gmm4::validate (host part: sizes, finiteness, weights); the
+// SPD check runs on the device (factors kernel).
+void validate_model(int m, int d, const double* w, const double* mu, const double* cov) {
+  if (m < 1) throw Err{3, "model has no components"};
+  if (!w || !mu || !cov) throw Err{2, "null model buffer"};
+  const int np = d * (d + 1) / 2;
+  double sum = 0.0, wmin = INFINITY;
+  bool finite = true;
+  for (int k = 0; k < m; ++k) {
+    finite = finite && std::isfinite(w[k]);
+    for (int j = 0; j < d; ++j) finite = finite && std::isfinite(mu[k * d + j]);
+    for (int j = 0; j < np; ++j) finite = finite && std::isfinite(cov[k * np + j]);
+    sum += w[k];
+    wmin = std::min(wmin, w[k]);
+  }
+  if (!finite) throw Err{3, "model contains non-finite values"};
+  if (wmin <= 0.0) throw Err{3, "model weights must be positive"};
+  if (std::abs(sum - 1.0) > 1e-9) throw Err{3, "model weights sum to " + std::to_string(sum)};
+}
+
+// model -> device, FP64 factors; returns the first non-SPD component or -1
+int upload_factors(gmmb_ctx* c, int m, int d, const double* w, const double* mu,
+                   const double* cov, bool want_lower) {
+  set_device(c);
+  const int np = d * (d + 1) / 2;
+  c->iw.ensure(m);
+  c->imu.ensure(static_cast<size_t>(m) * d);
+  c->icov.ensure(static_cast<size_t>(m) * np);
+  c->ifac.ensure(static_cast<size_t>(m) * 16);
+  if (want_lower) c->ilow.ensure(static_cast<size_t>(m) * 10);
+  c->ierr.ensure(4);
+  ck(cudaMemcpyAsync(c->iw.p, w, sizeof(double) * m, cudaMemcpyHostToDevice, c->s), "H2D");
+  ck(cudaMemcpyAsync(c->imu.p, mu, sizeof(double) * m * d, cudaMemcpyHostToDevice, c->s), "H2D");
+  ck(cudaMemcpyAsync(c->icov.p, cov, sizeof(double) * m * np, cudaMemcpyHostToDevice, c->s), "H2D");
+  const int init[4] = {INT_MAX, INT_MAX, INT_MAX, INT_MAX};
+  ck(cudaMemcpyAsync(c->ierr.p, init, sizeof(init), cudaMemcpyHostToDevice, c->s), "H2D");
+  ck(launch_factors(d, c->iw.p, c->imu.p, c->icov.p, m, c->ifac.p,
+                    want_lower ? c->ilow.p : nullptr, c->ierr.p, c->s),
+     "factors");
+  int err[4];
+  copy_sync(c, err, c->ierr.p, sizeof(err), cudaMemcpyDeviceToHost);
+  return err[0] == INT_MAX ? -1 : err[0];
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -875,6 +925,8 @@ void gmmb_ctx_destroy(gmmb_ctx* c) {
   c->x64.release(); c->xt.release(); c->tc.release(); c->perm.release();
   c->bbox_part.release(); c->mkeys_in.release(); c->mkeys_out.release();
   c->midx.release(); c->sort_tmp.release(); c->flags.release(); c->hidx.release();
+  c->iw.release(); c->imu.release(); c->icov.release(); c->ifac.release(); c->ilow.release();
+  c->iout.release(); c->iout2.release(); c->ierr.release();
   c->keys.release(); c->kd2.release(); c->labels.release(); c->chosen.release();
   c->slots.release(); c->owned.release(); c->centers.release(); c->rslots.release();
   c->ticket.release(); c->kstatus.release(); c->ll64.release();
@@ -1007,19 +1059,19 @@ int gmmb_e_step(gmmb_ctx* c, const double* pts, int64_t n, int d, int m, const d
   return guarded([&] {
     if (!c) throw Err{2, "null context"};
     upload(c, pts, n, d, 0, n);
-    layout(c);
+    validate(c);
     check_cloud_flags(c);
-    ensure_model(c, m);
-    upload_model(c, m, w, mu, cov);
-    reset_state(c, m, nullptr, 0);
-    ck(launch_prep(c->d, c->bufs, c->st.p, m, c->s), "prep");
-    raise_state_error(read_state(c));
-    const int nblk = static_cast<int>((n + 255) / 256);
+    if (m < 1 || !w || !mu || !cov) throw Err{2, "model has no components"};
+    // cholesky_cache semantics (gmm.cpp:33-48, kernels.cpp:71-75)
+    const int bad = upload_factors(c, m, d, w, mu, cov, false);
+    if (bad >= 0)
+      throw Err{3, "cholesky failed: block " + std::to_string(bad) + " is not positive definite"};
+    const int nblk = dense_blocks(n);
     c->ll_part.ensure(nblk);
     if (log_gamma_out) c->dense.ensure(static_cast<size_t>(n) * m);
-    ck(launch_estep_dense(c->d, c->x64.p, n, c->bufs, c->st.p, m, c->ll_part.p, nblk,
-                          log_gamma_out ? c->dense.p : nullptr, c->s),
-       "estep_dense");
+    ck(launch_dense(d, c->x64.p, n, c->ifac.p, m, nullptr, c->ll_part.p,
+                    log_gamma_out ? c->dense.p : nullptr, c->s),
+       "dense");
     std::vector<double> parts(nblk);
     copy_sync(c, parts.data(), c->ll_part.p, sizeof(double) * nblk, cudaMemcpyDeviceToHost);
     double ll = 0.0;
@@ -1027,6 +1079,87 @@ int gmmb_e_step(gmmb_ctx* c, const double* pts, int64_t n, int d, int m, const d
     if (ll_out) *ll_out = ll;
     if (log_gamma_out)
       copy_sync(c, log_gamma_out, c->dense.p, sizeof(double) * n * m, cudaMemcpyDeviceToHost);
+  });
+}
+
+int gmmb_score(gmmb_ctx* c, const double* pts, int64_t n, int d, int m, const double* w,
+               const double* mu, const double* cov, double* avg_ll_out, double* point_ll_out) {
+  return guarded([&] {
+    if (!c) throw Err{2, "null context"};
+    check_d(d);
+    if (n < 1) throw Err{2, "empty cloud"};  // inference.cpp:143
+    validate_model(m, d, w, mu, cov);
+    upload(c, pts, n, d, 0, n);
+    validate(c);
+    check_cloud_flags(c);
+    const int bad = upload_factors(c, m, d, w, mu, cov, false);
+    if (bad >= 0)
+      throw Err{3, "covariance of component " + std::to_string(bad) + " is not positive definite"};
+    const int nblk = dense_blocks(n);
+    c->ll_part.ensure(nblk);
+    if (point_ll_out) c->iout.ensure(n);
+    ck(launch_dense(d, c->x64.p, n, c->ifac.p, m, point_ll_out ? c->iout.p : nullptr,
+                    c->ll_part.p, nullptr, c->s),
+       "dense");
+    std::vector<double> parts(nblk);
+    copy_sync(c, parts.data(), c->ll_part.p, sizeof(double) * nblk, cudaMemcpyDeviceToHost);
+    double ll = 0.0;
+    for (double p : parts) ll += p;
+    if (avg_ll_out) *avg_ll_out = ll / static_cast<double>(n);
+    if (point_ll_out)
+      copy_sync(c, point_ll_out, c->iout.p, sizeof(double) * n, cudaMemcpyDeviceToHost);
+  });
+}
+
+int gmmb_sample(gmmb_ctx* c, int d, int m, const double* w, const double* mu, const double* cov,
+                int64_t n, uint64_t seed, double* out) {
+  return guarded([&] {
+    if (!c) throw Err{2, "null context"};
+    check_d(d);
+    if (n < 1) throw Err{2, "sample count must be >= 1"};  // inference.cpp:19
+    if (!out) throw Err{2, "null output"};
+    validate_model(m, d, w, mu, cov);
+    const int bad = upload_factors(c, m, d, w, mu, cov, true);
+    if (bad >= 0)
+      throw Err{3, "covariance of component " + std::to_string(bad) + " is not positive definite"};
+    c->iout.ensure(static_cast<size_t>(n) * d);
+    c->iout2.ensure(m);
+    ck(launch_sample(d, c->iw.p, c->ifac.p, c->ilow.p, m, n, seed, c->iout2.p, c->iout.p, c->s),
+       "sample");
+    copy_sync(c, out, c->iout.p, sizeof(double) * n * d, cudaMemcpyDeviceToHost);
+  });
+}
+
+int gmmb_color_conditional(gmmb_ctx* c, int m, const double* w, const double* mu,
+                           const double* cov, const double* locs, int64_t n, int clamp,
+                           double* expected, double* variance) {
+  return guarded([&] {
+    if (!c) throw Err{2, "null context"};
+    validate_model(m, 4, w, mu, cov);
+    if (n < 1) return;
+    if (!locs || !expected || !variance) throw Err{2, "null buffer"};
+    const int bad = upload_factors(c, m, 4, w, mu, cov, false);
+    if (bad >= 0)
+      throw Err{3, "covariance of component " + std::to_string(bad) + " is not positive definite"};
+    c->iout.ensure(static_cast<size_t>(n) * 5 + static_cast<size_t>(m) * 20);
+    double* dl = c->iout.p;                 // locs n x 3
+    double* de = dl + 3 * n;                // expected
+    double* dv = de + n;                    // variance
+    double* cnd = dv + n;                   // [m][20]
+    ck(cudaMemcpyAsync(dl, locs, sizeof(double) * n * 3, cudaMemcpyHostToDevice, c->s), "H2D");
+    const int init[4] = {INT_MAX, INT_MAX, INT_MAX, INT_MAX};
+    ck(cudaMemcpyAsync(c->ierr.p, init, sizeof(init), cudaMemcpyHostToDevice, c->s), "H2D");
+    ck(launch_conditional(c->iw.p, c->imu.p, c->icov.p, m, dl, n, clamp, cnd, de, dv, c->ierr.p,
+                          c->s),
+       "conditional");
+    int err[4];
+    copy_sync(c, err, c->ierr.p, sizeof(err), cudaMemcpyDeviceToHost);
+    if (err[0] != INT_MAX)
+      throw Err{3, "spatial covariance of component " + std::to_string(err[0]) +
+                       " is not positive definite"};
+    if (err[1] != INT_MAX) throw Err{3, "conditional variance below tolerance"};
+    copy_sync(c, expected, de, sizeof(double) * n, cudaMemcpyDeviceToHost);
+    copy_sync(c, variance, dv, sizeof(double) * n, cudaMemcpyDeviceToHost);
   });
 }
 

@@ -564,7 +564,10 @@ __device__ __forceinline__ double f32_to_f64(float f) {
 // consumers with the exact max shift (uniform decision: S is identical in
 // every consumer warp), reloading the constants from global memory.
 // ---------------------------------------------------------------------------
-constexpr int kRing = 3;  // sub-tile slots in flight between the roles
+#ifndef GMMB_RING
+#define GMMB_RING 3
+#endif
+constexpr int kRing = GMMB_RING;  // sub-tile slots in flight between the roles
 
 template <int NWH, int P, int C>
 struct WsSmem {
@@ -1626,69 +1629,6 @@ __global__ void moments_finish_kernel(const double* __restrict__ sums2,
   rec.flags[k] = flags;
 }
 
-// ---------------------------------------------------------------------------
-// Dense E step (API / debug path, FP64): thread per point.
-// ---------------------------------------------------------------------------
-template <int D>
-__global__ void estep_dense_kernel(const double* __restrict__ x64, int64_t n,
-                                   ModelBuf b0, ModelBuf b1,
-                                   const EmState* __restrict__ st, int m,
-                                   double* __restrict__ ll_part,
-                                   double* __restrict__ log_gamma) {
-  __shared__ double red[256];
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const ModelBuf& mb = st->cur ? b1 : b0;
-  double lse = 0.0;
-  if (i < n && !st->error) {
-    double x[D];
-#pragma unroll
-    for (int j = 0; j < D; ++j) x[j] = x64[j * n + i];
-    // recompute the FP64 precision factor on the fly from the FP32-free
-    // model: cheap relative to an API call, keeps this path pure FP64.
-    double mx = -INFINITY;
-    auto logd = [&](int k) {
-      double a[D][D];
-#pragma unroll
-      for (int q = 0; q < npacked(D); ++q) {
-        a[packed_row(q)][packed_col(q)] = mb.cov[k * 10 + q];
-        a[packed_col(q)][packed_row(q)] = mb.cov[k * 10 + q];
-      }
-      double l[D][D], p[D][D];
-      cholesky_d<D>(a, l);
-      lower_inverse_d<D>(l, p);
-      double ld = 0.0;
-#pragma unroll
-      for (int j = 0; j < D; ++j) ld += log(p[j][j]);
-      double dd[D];
-#pragma unroll
-      for (int j = 0; j < D; ++j) dd[j] = x[j] - mb.mu[k * 4 + j];
-      double q = 0.0;
-#pragma unroll
-      for (int r = 0; r < D; ++r) {
-        double y = 0.0;
-#pragma unroll
-        for (int c = 0; c <= r; ++c) y += p[r][c] * dd[c];
-        q += y * y;
-      }
-      return log(mb.w[k]) + ld - 0.5 * D * kLog2Pi - 0.5 * q;
-    };
-    for (int k = 0; k < m; ++k) mx = fmax(mx, logd(k));
-    double acc = 0.0;
-    for (int k = 0; k < m; ++k) acc += exp(fmax(logd(k) - mx, -700.0));
-    lse = (mx == -INFINITY) ? -INFINITY : mx + log(acc);
-    if (log_gamma) {
-      for (int k = 0; k < m; ++k) log_gamma[static_cast<int64_t>(k) * n + i] = logd(k) - lse;
-    }
-  }
-  red[threadIdx.x] = lse;
-  __syncthreads();
-  for (int off = 128; off >= 1; off >>= 1) {
-    if (threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) ll_part[blockIdx.x] = red[0];
-}
-
 // FP64 factors of buffer st->cur for the cholesky_cache API:
 // out[k*33 + 0..15] = L (4x4 row-major), [16..31] = P = L^-1, [32] = logdet.
 template <int D>
@@ -1849,15 +1789,6 @@ cudaError_t launch_moments(int d, const double* x64, int64_t n,
   return launch_moments_d<3>(x64, n, labels, log_gamma, m, cov_reg, scr, rec, s, allreduce, ar_ctx);
 }
 
-cudaError_t launch_estep_dense(int d, const double* x64, int64_t n,
-                               const ModelBuf* bufs, const EmState* st,
-                               int m, double* ll_part, int nblk,
-                               double* log_gamma, cudaStream_t s) {
-  if (d == 4)
-    estep_dense_kernel<4><<<nblk, 256, 0, s>>>(x64, n, bufs[0], bufs[1], st, m, ll_part, log_gamma);
-  else
-    estep_dense_kernel<3><<<nblk, 256, 0, s>>>(x64, n, bufs[0], bufs[1], st, m, ll_part, log_gamma);
-  return cudaGetLastError();
-}
+
 
 }  // namespace gmmb

@@ -96,12 +96,6 @@ cudaError_t launch_moments(int d, const double* x64, int64_t n,
                            void (*allreduce)(double*, int64_t, void*),
                            void* ar_ctx);
 
-// Exact per-point log-sum-exp (thread per point, all K), for the e_step
-// API: ll (natural log, per-cluster partials) and optional dense log_gamma
-// [n][m] column-major (original point order, FP64 output of FP32 math).
-cudaError_t launch_estep_dense(int d, const double* x64, int64_t n,
-                               const ModelBuf* bufs, const EmState* st,
-                               int m, double* ll_part, int nblk,
-                               double* log_gamma, cudaStream_t s);
+
 
 }  // namespace gmmb
