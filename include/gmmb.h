@@ -134,6 +134,19 @@ int gmmb_e_step(gmmb_ctx* ctx, const double* pts, int64_t n, int d, int m,
                 const double* w, const double* mu, const double* cov,
                 double* ll_out, double* log_gamma_out);
 
+/* Device ingest (ingest.hpp:27-35, ingest.cpp:27-75): decimate(depth, f),
+ * decimate(intensity, f) and image_pair_to_cloud with intrinsics.decimated(f),
+ * on the GPU. Images are width x height row-major uint16; the resulting
+ * N x 4 cloud (row-major pixel order, zero depths dropped) becomes the
+ * context's resident cloud for gmmb_fit_k_resident; pts_out (optional, N x 4
+ * column-major, capacity (width/f)*(height/f)*4) receives a copy, n_out its
+ * size. Errors: invalid_argument (2) for bad factor / intrinsics,
+ * NumericalError (3) when every depth is zero. */
+int gmmb_ingest_images(gmmb_ctx* ctx, const uint16_t* depth, const uint16_t* intensity, int width,
+                       int height, double intensity_max, double fx, double fy, double cx,
+                       double cy, double depth_scale, int factor, double* pts_out,
+                       int64_t* n_out);
+
 /* score (inference.hpp:33, inference.cpp:141-172): average log-likelihood
  * of the cloud under the model (natural log, FP64); point_ll_out (n,
  * optional) receives each point's log-sum-exp. D = 3 or 4; 4 is the
@@ -188,12 +201,35 @@ int gmmb_shard_key_tail(const double* heads, int world, int rank,
 int gmmb_ffma_peak(gmmb_ctx* ctx, double ms_target, double* tflops,
                    double* ms);
 
+/* ---- model I/O (gmm_io.hpp:21-33, gmm_io.cpp:71-177), host ------------
+ * Binary "SGMM4D01" (f32 payload) and the JSON mirror (full precision), 4D
+ * models (means m x 4, covariances m x 10 packed). Load applies the
+ * reference's checks (finalize_loaded): returns 1 for format / truncation /
+ * open errors (GmmFormatError / GmmTruncatedError / IoError), 3 for
+ * non-finite, non-positive or non-normalised weights and non-SPD
+ * covariances, 2 if capacity < M (*m_out still set). Messages via
+ * gmmb_io_last_error. */
+const char* gmmb_io_last_error(void);
+int gmmb_save_model(const char* path, int m, const double* w, const double* mu,
+                    const double* cov);
+int gmmb_load_model(const char* path, int capacity, double* w, double* mu, double* cov,
+                    int* m_out);
+int gmmb_save_model_json(const char* path, int m, const double* w, const double* mu,
+                         const double* cov);
+int gmmb_load_model_json(const char* path, int capacity, double* w, double* mu, double* cov,
+                         int* m_out);
+
 /* ---- synthetic inputs (synthetic.cpp / ingest.cpp restated, host) ------
  * make_synthetic_frame + image_pair_to_cloud (synthetic.cpp:9-72,
  * ingest.cpp:27-57): writes up to width*height points (col-major, D=4,
  * capacity width*height rows, leading dimension = *n_out). */
 int gmmb_synthetic_frame_cloud(int width, int height, double depth_scale,
                                double* pts_out, int64_t* n_out);
+/* make_synthetic_frame (synthetic.cpp:9-72): the depth (depth_scale units)
+ * and 8-bit intensity images, width x height row-major; intr_out (optional)
+ * = fx, fy, cx, cy. */
+int gmmb_synthetic_frame_images(int width, int height, double depth_scale, uint16_t* depth_out,
+                                uint16_t* intensity_out, double* intr_out);
 /* make_structured_scene (synthetic.cpp:94-129): N x 4 col-major. */
 int gmmb_structured_scene(int64_t n, uint64_t seed, double noise_sigma,
                           double* pts_out);

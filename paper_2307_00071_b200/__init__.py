@@ -118,6 +118,22 @@ _SIGS = {
     "gmmb_shard_key_tail": (ctypes.c_int, [_D, ctypes.c_int, ctypes.c_int, _D]),
     "gmmb_ffma_peak": (ctypes.c_int, [_V, ctypes.c_double, _D, _D]),
     "gmmb_ctx_set_timing": (ctypes.c_int, [_V, ctypes.c_int]),
+    "gmmb_ingest_images": (ctypes.c_int, [_V, ctypes.POINTER(ctypes.c_uint16),
+                                          ctypes.POINTER(ctypes.c_uint16), ctypes.c_int,
+                                          ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                          ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                          ctypes.c_double, ctypes.c_int, _D,
+                                          ctypes.POINTER(ctypes.c_int64)]),
+    "gmmb_synthetic_frame_images": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                                   ctypes.POINTER(ctypes.c_uint16),
+                                                   ctypes.POINTER(ctypes.c_uint16), _D]),
+    "gmmb_io_last_error": (ctypes.c_char_p, []),
+    "gmmb_save_model": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _D, _D, _D]),
+    "gmmb_load_model": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _D, _D, _D,
+                                       ctypes.POINTER(ctypes.c_int)]),
+    "gmmb_save_model_json": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _D, _D, _D]),
+    "gmmb_load_model_json": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _D, _D, _D,
+                                            ctypes.POINTER(ctypes.c_int)]),
     "gmmb_score": (ctypes.c_int, [_V, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _D, _D, _D,
                                   _D, _D]),
     "gmmb_sample": (ctypes.c_int, [_V, ctypes.c_int, ctypes.c_int, _D, _D, _D, ctypes.c_int64,
@@ -317,6 +333,30 @@ class Context:
         p, n, d = _points(points)
         self._n, self._d = n, d
         _check(load().gmmb_upload(self._h, _ptr(p), n, d, offset, n_global))
+
+    def ingest_images(self, depth, intensity, intrinsics, intensity_max: float = 255.0,
+                      depth_scale: float = 1000.0, factor: int = 1, want_points: bool = False):
+        """Device ingest (ingest.cpp:27-75): decimate + image_pair_to_cloud on
+        the GPU; the cloud becomes this context's resident cloud. intrinsics =
+        (fx, fy, cx, cy) of the full-resolution image. Returns N, or (N,
+        (N, 4) points) with want_points."""
+        dep = np.ascontiguousarray(depth, dtype=np.uint16)
+        inten = np.ascontiguousarray(intensity, dtype=np.uint16)
+        if dep.shape != inten.shape or dep.ndim != 2:
+            raise ValueError("depth and intensity dimensions differ")
+        h, w = dep.shape
+        fx, fy, cx, cy = (float(v) for v in intrinsics)
+        cap = (w // max(factor, 1)) * (h // max(factor, 1))
+        buf = np.zeros(4 * max(cap, 1)) if want_points else None
+        n = ctypes.c_int64()
+        U16 = ctypes.POINTER(ctypes.c_uint16)
+        _check(load().gmmb_ingest_images(self._h, dep.ctypes.data_as(U16), inten.ctypes.data_as(U16),
+                                         w, h, intensity_max, fx, fy, cx, cy, depth_scale, factor,
+                                         _ptr(buf), ctypes.byref(n)))
+        self._n, self._d = n.value, 4
+        if not want_points:
+            return n.value
+        return n.value, buf[:4 * n.value].reshape(4, n.value).T.copy()
 
     def fit_k_resident(self, k: int, em: EmParams = EmParams(),
                        want_labels: bool = False) -> FitResult:
@@ -519,6 +559,59 @@ def synthetic_frame_cloud(width: int = 640, height: int = 480,
                                              ctypes.byref(n)))
     nn = n.value
     return buf[:4 * nn].reshape(4, nn).T.copy()
+
+
+class GmmFormatError(IoError):
+    """gmm_io.hpp:10-13 — wrong magic or malformed structure."""
+
+
+def _io_check(code: int) -> None:
+    if code == 0:
+        return
+    msg = load().gmmb_io_last_error().decode(errors="replace")
+    if code == 2:
+        raise ValueError(msg)
+    if code == 3:
+        raise NumericalError(msg)
+    if "magic" in msg or "malformed" in msg or "missing" in msg or "truncated" in msg \
+            or "inconsistent" in msg or "bad row" in msg or "zero components" in msg:
+        raise GmmFormatError(msg)
+    raise IoError(msg)
+
+
+def save_gmm(model: Gmm, path: str, json: bool = False) -> None:
+    """gmm_io.cpp:71-85 (binary SGMM4D01, f32) / :120-141 (JSON mirror)."""
+    w, mu, cov, m = _model_arrays(model, 4)
+    fn = load().gmmb_save_model_json if json else load().gmmb_save_model
+    _io_check(fn(path.encode(), m, _ptr(w), _ptr(mu), _ptr(cov)))
+
+
+def load_gmm(path: str, json: bool = False) -> Gmm:
+    """gmm_io.cpp:87-118 / :143-177 with finalize_loaded's checks."""
+    fn = load().gmmb_load_model_json if json else load().gmmb_load_model
+    m = ctypes.c_int()
+    cap = 1
+    while True:
+        w, mu, cov = np.zeros(cap), np.zeros((cap, 4)), np.zeros((cap, 10))
+        code = fn(path.encode(), cap, _ptr(w), _ptr(mu), _ptr(cov), ctypes.byref(m))
+        if code == 2 and m.value > cap:
+            cap = m.value
+            continue
+        _io_check(code)
+        k = m.value
+        return Gmm(w[:k].copy(), mu[:k].copy(), cov[:k].copy())
+
+
+def synthetic_frame_images(width: int = 640, height: int = 480, depth_scale: float = 1000.0):
+    """make_synthetic_frame (synthetic.cpp:9-72): (depth uint16 (H, W),
+    intensity uint16 (H, W), (fx, fy, cx, cy))."""
+    dep = np.zeros((height, width), np.uint16)
+    inten = np.zeros((height, width), np.uint16)
+    intr = np.zeros(4)
+    U16 = ctypes.POINTER(ctypes.c_uint16)
+    _check(load().gmmb_synthetic_frame_images(width, height, depth_scale, dep.ctypes.data_as(U16),
+                                              inten.ctypes.data_as(U16), _ptr(intr)))
+    return dep, inten, tuple(intr)
 
 
 def structured_scene(n: int, seed: int = 0, noise_sigma: float = 0.005) -> np.ndarray:

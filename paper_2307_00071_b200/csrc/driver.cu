@@ -27,6 +27,7 @@
 #include "layout.cuh"
 #include "mstep_hard.cuh"
 #include "inference.cuh"
+#include "ingest.cuh"
 
 using namespace gmmb;
 
@@ -145,6 +146,9 @@ struct gmmb_ctx {
   // inference (score / sample / conditional / e_step API)
   DevBuf<double> iw, imu, icov, ifac, ilow, iout, iout2;
   DevBuf<int> ierr;
+  DevBuf<uint16_t> img;        // ingest: depth + intensity images
+  DevBuf<int> iflags;          // ingest: flags + offsets
+  DevBuf<int64_t> in_n;
   DevBuf<int> flags;
   // kinit
   DevBuf<uint64_t> keys;
@@ -926,7 +930,8 @@ void gmmb_ctx_destroy(gmmb_ctx* c) {
   c->bbox_part.release(); c->mkeys_in.release(); c->mkeys_out.release();
   c->midx.release(); c->sort_tmp.release(); c->flags.release(); c->hidx.release();
   c->iw.release(); c->imu.release(); c->icov.release(); c->ifac.release(); c->ilow.release();
-  c->iout.release(); c->iout2.release(); c->ierr.release();
+  c->iout.release(); c->iout2.release(); c->ierr.release(); c->img.release();
+  c->iflags.release(); c->in_n.release();
   c->keys.release(); c->kd2.release(); c->labels.release(); c->chosen.release();
   c->slots.release(); c->owned.release(); c->centers.release(); c->rslots.release();
   c->ticket.release(); c->kstatus.release(); c->ll64.release();
@@ -1079,6 +1084,58 @@ int gmmb_e_step(gmmb_ctx* c, const double* pts, int64_t n, int d, int m, const d
     if (ll_out) *ll_out = ll;
     if (log_gamma_out)
       copy_sync(c, log_gamma_out, c->dense.p, sizeof(double) * n * m, cudaMemcpyDeviceToHost);
+  });
+}
+
+int gmmb_ingest_images(gmmb_ctx* c, const uint16_t* depth, const uint16_t* intensity, int width,
+                       int height, double intensity_max, double fx, double fy, double cx,
+                       double cy, double depth_scale, int factor, double* pts_out,
+                       int64_t* n_out) {
+  return guarded([&] {
+    if (!c) throw Err{2, "null context"};
+    if (!depth || !intensity) throw Err{2, "null image"};
+    // decimate (ingest.cpp:59-63)
+    if (factor < 1) throw Err{2, "decimation factor must be >= 1"};
+    if (factor > width || factor > height)
+      throw Err{2, "decimation factor exceeds image dimensions"};
+    if (!(intensity_max > 0.0)) throw Err{2, "intensity max_value must be > 0"};
+    // CameraIntrinsics::decimated + validate (ingest.cpp:7-25)
+    const int wd = width / factor, hd = height / factor;
+    IngestParams ip{fx / factor, fy / factor, cx / factor, cy / factor, 1.0 / depth_scale,
+                    1.0 / intensity_max};
+    if (ip.fx <= 0.0 || ip.fy <= 0.0 || depth_scale <= 0.0)
+      throw Err{2, "intrinsics: fx, fy, depth_scale must be > 0"};
+    if (!(ip.cx > 0.0 && ip.cx < wd) || !(ip.cy > 0.0 && ip.cy < hd))
+      throw Err{2, "intrinsics: principal point outside image"};
+    set_device(c);
+    const int64_t npx = static_cast<int64_t>(width) * height;
+    const int64_t np = static_cast<int64_t>(wd) * hd;
+    c->img.ensure(static_cast<size_t>(npx) * 2);
+    c->iflags.ensure(static_cast<size_t>(np) * 2);
+    c->in_n.ensure(1);
+    const size_t tb = ingest_temp_bytes(np);
+    c->sort_tmp.ensure(tb);
+    c->x64.ensure(static_cast<size_t>(np) * 4 + 4);
+    ck(cudaMemcpyAsync(c->img.p, depth, sizeof(uint16_t) * npx, cudaMemcpyHostToDevice, c->s),
+       "depth H2D");
+    ck(cudaMemcpyAsync(c->img.p + npx, intensity, sizeof(uint16_t) * npx, cudaMemcpyHostToDevice,
+                       c->s),
+       "intensity H2D");
+    IngestScratch is{c->iflags.p, c->iflags.p + np, c->sort_tmp.p, c->sort_tmp.cap};
+    ck(launch_ingest(c->img.p, c->img.p + npx, width, wd, hd, factor, ip, is, c->x64.p,
+                     c->in_n.p, c->s),
+       "ingest");
+    int64_t n = 0;
+    copy_sync(c, &n, c->in_n.p, sizeof(n), cudaMemcpyDeviceToHost);
+    if (n == 0) throw Err{3, "all depth pixels are zero: empty cloud"};
+    c->n = n;
+    c->d = 4;
+    c->offset = 0;
+    c->n_global = n;
+    c->have_cloud = true;
+    if (n_out) *n_out = n;
+    if (pts_out)
+      copy_sync(c, pts_out, c->x64.p, sizeof(double) * n * 4, cudaMemcpyDeviceToHost);
   });
 }
 

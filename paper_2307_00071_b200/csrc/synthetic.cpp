@@ -36,13 +36,19 @@ void normal_pair(uint64_t seed, uint64_t stream, uint64_t counter, double& z0,
 
 extern "C" {
 
-int gmmb_synthetic_frame_cloud(int width, int height, double depth_scale,
-                               double* pts_out, int64_t* n_out) {
-  if (width < 1 || height < 1 || !(depth_scale > 0.0) || !pts_out || !n_out) return 2;
+int gmmb_synthetic_frame_images(int width, int height, double depth_scale, uint16_t* depth_out,
+                                uint16_t* intensity_out, double* intr_out) {
+  if (width < 1 || height < 1 || !(depth_scale > 0.0) || !depth_out || !intensity_out) return 2;
   const double fx = 525.0 * width / 640.0, fy = 525.0 * width / 640.0;
   const double cx = width * 0.5 - 0.5, cy = height * 0.5 - 0.5;
-  const size_t np = static_cast<size_t>(width) * height;
-  std::vector<uint16_t> depth(np), inten(np);
+  uint16_t* depth = depth_out;
+  uint16_t* inten = intensity_out;
+  if (intr_out) {
+    intr_out[0] = fx;
+    intr_out[1] = fy;
+    intr_out[2] = cx;
+    intr_out[3] = cy;
+  }
   const double sc[3] = {0.35, -0.1, 2.1};
   const double sr = 0.35;
   for (int v = 0; v < height; ++v) {
@@ -76,6 +82,17 @@ int gmmb_synthetic_frame_cloud(int width, int height, double depth_scale,
           static_cast<uint16_t>(std::lround(in * 255.0));
     }
   }
+  return 0;
+}
+
+int gmmb_synthetic_frame_cloud(int width, int height, double depth_scale,
+                               double* pts_out, int64_t* n_out) {
+  if (width < 1 || height < 1 || !(depth_scale > 0.0) || !pts_out || !n_out) return 2;
+  const size_t np = static_cast<size_t>(width) * height;
+  std::vector<uint16_t> depth(np), inten(np);
+  double intr[4];
+  gmmb_synthetic_frame_images(width, height, depth_scale, depth.data(), inten.data(), intr);
+  const double fx = intr[0], fy = intr[1], cx = intr[2], cy = intr[3];
   // image_pair_to_cloud (ingest.cpp:27-57): row-major pixels, drop zero depth
   int64_t n = 0;
   for (uint16_t d : depth) n += d > 0;
