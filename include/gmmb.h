@@ -147,6 +147,29 @@ int gmmb_ingest_images(gmmb_ctx* ctx, const uint16_t* depth, const uint16_t* int
                        double cy, double depth_scale, int factor, double* pts_out,
                        int64_t* n_out);
 
+/* GbmsParams (sogmm.hpp:12-22). */
+typedef struct gmmb_gbms_params {
+  double bandwidth;        /* in (0, 1], normalised units; default 0.015 */
+  int max_iters;           /* default 100 */
+  double convergence_tol;  /* mean seed displacement; default 1e-5 */
+  double merge_radius;     /* <= 0: bandwidth / 2 */
+} gmmb_gbms_params;
+void gmmb_gbms_params_default(gmmb_gbms_params* p);
+
+/* gbms_estimate_components (sogmm.hpp:33-34, sogmm.cpp:22-195) on the
+ * device: binned seeding, blurring mean shift with seed folding, single-
+ * linkage merge. modes (optional): components x 4 row-major, original
+ * coordinates, up to modes_capacity rows. D = 3 runs on the 4D embedding. */
+int gmmb_gbms(gmmb_ctx* ctx, const double* pts, int64_t n, int d, const gmmb_gbms_params* gp,
+              int* components, int* iterations, double* modes, int modes_capacity);
+
+/* fit (sogmm.hpp:74-75, sogmm.cpp:465-510): GBMS decides K, then the fit of
+ * gmmb_fit_k. Outputs sized for capacity components (returns 2 with
+ * *gbms_components set when K exceeds it). */
+int gmmb_fit(gmmb_ctx* ctx, const double* pts, int64_t n, int d, const gmmb_gbms_params* gp,
+             const gmmb_em_params* em, int capacity, double* w_out, double* mu_out,
+             double* cov_out, double* ll_trace, gmmb_fit_stats* stats, int* gbms_components);
+
 /* score (inference.hpp:33, inference.cpp:141-172): average log-likelihood
  * of the cloud under the model (natural log, FP64); point_ll_out (n,
  * optional) receives each point's log-sum-exp. D = 3 or 4; 4 is the

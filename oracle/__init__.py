@@ -88,6 +88,9 @@ def load():
                                                       ctypes.POINTER(_Stats)]),
             "orc_fit_k": (ctypes.c_int, [D, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(_Em),
                                          D, D, D, D, ctypes.POINTER(_Stats), I64, I32]),
+            "orc_gbms": (ctypes.c_int, [D, ctypes.c_int64, ctypes.c_double, ctypes.c_int,
+                                        ctypes.c_double, ctypes.c_double, I, I, I, D,
+                                        ctypes.c_int]),
             "orc_score": (ctypes.c_int, [D, ctypes.c_int64, ctypes.c_int, D, D, D, D]),
             "orc_sample": (ctypes.c_int, [ctypes.c_int, D, D, D, ctypes.c_int64,
                                           ctypes.c_uint64, D]),
@@ -311,3 +314,14 @@ def color_conditional(w, mu, cov, locs, clamp=True):
     _check(load().orc_color_conditional(len(w), _p(w), _p(mu), _p(cov), _p(loc), n,
                                         1 if clamp else 0, _p(e), _p(v)))
     return e, v
+
+
+def gbms(points, bandwidth=0.015, max_iters=100, tol=1e-5, merge_radius=-1.0):
+    """sogmm.cpp:22-195: (components, iterations, initial seed count, modes (c, 4))."""
+    p = embed3(points)
+    comp, it, s0 = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    cap = 65536
+    modes = np.zeros((cap, 4))
+    _check(load().orc_gbms(_p(p), p.shape[0], bandwidth, max_iters, tol, merge_radius,
+                           ctypes.byref(comp), ctypes.byref(it), ctypes.byref(s0), _p(modes), cap))
+    return comp.value, it.value, s0.value, modes[:comp.value].copy()

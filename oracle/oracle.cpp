@@ -31,6 +31,9 @@
 #include <string>
 #include <thread>
 #include <vector>
+#include <array>
+#include <numeric>
+#include <map>
 
 namespace {
 
@@ -890,6 +893,224 @@ void color_conditional(const Model& md, const double* locs, int64_t n, int clamp
   if (bad) throw NumError{"conditional variance below tolerance"};
 }
 
+// ---- GBMS component estimation (sogmm.cpp:22-195, kdtree.hpp:13-99) -------
+
+// KdTree4 (kdtree.hpp): median split on the widest axis, leaf size 16,
+// std::nth_element partitions — restated verbatim so radius queries visit
+// points in the reference's order (it fixes the FP summation order).
+class KdTree4 {
+ public:
+  KdTree4(const std::vector<double>& pts, int n, int leaf = 16)
+      : pts_(pts), n_(n), leaf_(leaf) {
+    idx_.resize(n);
+    std::iota(idx_.begin(), idx_.end(), 0);
+    if (n > 0) {
+      nodes_.reserve(2 * n / leaf_ + 2);
+      build(0, n);
+    }
+  }
+  template <typename V>
+  void for_each_in_radius(const double* q, double r, V&& visit) const {
+    if (!nodes_.empty()) search(0, q, r * r, r, visit);
+  }
+
+ private:
+  struct Node {
+    int begin, end, axis = -1;
+    double split = 0.0;
+    int left = -1, right = -1;
+  };
+  double at(int row, int d) const { return pts_[static_cast<size_t>(row) * 4 + d]; }
+  int build(int begin, int end) {
+    const int id = static_cast<int>(nodes_.size());
+    nodes_.push_back({begin, end});
+    if (end - begin <= leaf_) return id;
+    double lo[4], hi[4];
+    for (int d = 0; d < 4; ++d) lo[d] = hi[d] = at(idx_[begin], d);
+    for (int i = begin + 1; i < end; ++i)
+      for (int d = 0; d < 4; ++d) {
+        lo[d] = std::min(lo[d], at(idx_[i], d));
+        hi[d] = std::max(hi[d], at(idx_[i], d));
+      }
+    int axis = 0;  // Eigen maxCoeff: first maximum
+    for (int d = 1; d < 4; ++d)
+      if (hi[d] - lo[d] > hi[axis] - lo[axis]) axis = d;
+    if (hi[axis] - lo[axis] <= 0.0) return id;
+    const int mid = begin + (end - begin) / 2;
+    std::nth_element(idx_.begin() + begin, idx_.begin() + mid, idx_.begin() + end,
+                     [&](int a, int b) { return at(a, axis) < at(b, axis); });
+    nodes_[id].axis = axis;
+    nodes_[id].split = at(idx_[mid], axis);
+    const int l = build(begin, mid);
+    const int r = build(mid, end);
+    nodes_[id].left = l;
+    nodes_[id].right = r;
+    return id;
+  }
+  template <typename V>
+  void search(int id, const double* q, double r2, double r, V&& visit) const {
+    const Node& nd = nodes_[id];
+    if (nd.axis < 0) {
+      for (int i = nd.begin; i < nd.end; ++i) {
+        const int p = idx_[i];
+        const double e0 = at(p, 0) - q[0], e1 = at(p, 1) - q[1], e2 = at(p, 2) - q[2],
+                     e3 = at(p, 3) - q[3];
+        if (((e0 * e0 + e1 * e1) + e2 * e2) + e3 * e3 <= r2) visit(p);
+      }
+      return;
+    }
+    const double d = q[nd.axis] - nd.split;
+    if (d <= r) search(nd.left, q, r2, r, visit);
+    if (d >= -r) search(nd.right, q, r2, r, visit);
+  }
+  const std::vector<double>& pts_;
+  int n_, leaf_;
+  std::vector<int> idx_;
+  std::vector<Node> nodes_;
+};
+
+struct GbmsOut {
+  int components = 0, iterations = 0, seeds0 = 0;
+  std::vector<double> modes;  // components x 4 row-major
+};
+
+GbmsOut gbms(const double* pts, int64_t n, double bw, int max_iters, double tol, double merge_r) {
+  if (!(bw > 0.0) || bw > 1.0) throw ArgError{"bandwidth must be in (0, 1]"};
+  if (max_iters < 1) throw ArgError{"max_iters must be >= 1"};
+  if (!(tol > 0.0)) throw ArgError{"convergence_tol must be > 0"};
+  validate_cloud(pts, n);
+  double mins[4], ranges[4];
+  for (int d = 0; d < 4; ++d) {
+    double lo = pts[d * n], hi = pts[d * n];
+    for (int64_t i = 1; i < n; ++i) {
+      lo = std::min(lo, pts[d * n + i]);
+      hi = std::max(hi, pts[d * n + i]);
+    }
+    mins[d] = lo;
+    ranges[d] = hi - lo;
+  }
+  auto norm = [&](int64_t i, int d) {
+    return ranges[d] > 0.0 ? (pts[d * n + i] - mins[d]) / ranges[d] : 0.0;
+  };
+  std::map<uint64_t, std::pair<std::array<double, 4>, int>> bins;
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t key = 0;
+    double v[4];
+    for (int d = 0; d < 4; ++d) {
+      v[d] = norm(i, d);
+      const auto cell = static_cast<uint64_t>(v[d] / bw);
+      key = (key << 16) | (cell & 0xffff);
+    }
+    auto it = bins.try_emplace(key, std::array<double, 4>{0, 0, 0, 0}, 0).first;
+    for (int d = 0; d < 4; ++d) it->second.first[d] += v[d];
+    it->second.second += 1;
+  }
+  int S = static_cast<int>(bins.size());
+  std::vector<double> seeds(static_cast<size_t>(S) * 4), weights(S, 1.0);
+  {
+    int s = 0;
+    for (const auto& kv : bins) {
+      for (int d = 0; d < 4; ++d) seeds[s * 4 + d] = kv.second.first[d] / kv.second.second;
+      ++s;
+    }
+  }
+  GbmsOut out;
+  out.seeds0 = S;
+  double total_weight = 0.0;
+  for (double w : weights) total_weight += w;
+  const double fold_eps = std::max(1e-12, tol * 1e-3);
+  for (int iter = 0; iter < max_iters; ++iter) {
+    ++out.iterations;
+    std::vector<double> next(static_cast<size_t>(S) * 4);
+    KdTree4 tree(seeds, S);
+    parallel_for_blocks(num_blocks(S), [&](int64_t blk) {
+      const int64_t r0 = blk * kPointBlock, r1 = std::min<int64_t>(S, r0 + kPointBlock);
+      for (int64_t s = r0; s < r1; ++s) {
+        double sum[4] = {0, 0, 0, 0}, mass = 0.0;
+        tree.for_each_in_radius(&seeds[s * 4], bw, [&](int j) {
+          for (int d = 0; d < 4; ++d) sum[d] += weights[j] * seeds[j * 4 + d];
+          mass += weights[j];
+        });
+        for (int d = 0; d < 4; ++d) next[s * 4 + d] = sum[d] / mass;
+      }
+    });
+    double shift = 0.0;
+    for (int s = 0; s < S; ++s) {
+      double q = 0.0;
+      for (int d = 0; d < 4; ++d) {
+        const double e = next[s * 4 + d] - seeds[s * 4 + d];
+        q += e * e;
+      }
+      shift += weights[s] * std::sqrt(q);
+    }
+    shift /= total_weight;
+    seeds.swap(next);
+    std::vector<uint64_t> keys(S);
+    std::map<uint64_t, std::pair<int, double>> fold;
+    std::vector<int> keep;
+    for (int s = 0; s < S; ++s) {
+      uint64_t key = 0;
+      for (int d = 0; d < 4; ++d) {
+        const auto cell = static_cast<uint64_t>((seeds[s * 4 + d] + 1.0) / fold_eps);
+        key = orc_mix64(key ^ cell);
+      }
+      keys[s] = key;
+      auto [it, ins] = fold.try_emplace(key, s, 0.0);
+      if (ins) keep.push_back(s);
+      it->second.second += weights[s];
+    }
+    if (static_cast<int>(keep.size()) < S) {
+      std::vector<double> fs(keep.size() * 4), fw(keep.size());
+      for (size_t o = 0; o < keep.size(); ++o) {
+        for (int d = 0; d < 4; ++d) fs[o * 4 + d] = seeds[keep[o] * 4 + d];
+        fw[o] = fold.at(keys[keep[o]]).second;
+      }
+      seeds.swap(fs);
+      weights.swap(fw);
+      S = static_cast<int>(keep.size());
+    }
+    if (shift < tol) break;
+  }
+  const double mr = merge_r > 0.0 ? merge_r : bw * 0.5;
+  std::vector<int> parent(S);
+  std::iota(parent.begin(), parent.end(), 0);
+  auto find = [&](int a) {
+    while (parent[a] != a) {
+      parent[a] = parent[parent[a]];
+      a = parent[a];
+    }
+    return a;
+  };
+  KdTree4 tree(seeds, S);
+  for (int s = 0; s < S; ++s) {
+    tree.for_each_in_radius(&seeds[s * 4], mr, [&](int j) {
+      const int ra = find(s), rb = find(j);
+      if (ra != rb) parent[std::max(ra, rb)] = std::min(ra, rb);
+    });
+  }
+  std::vector<int> root_to_mode(S, -1);
+  std::vector<std::array<double, 4>> sums;
+  std::vector<double> masses;
+  for (int s = 0; s < S; ++s) {
+    const int r = find(s);
+    if (root_to_mode[r] < 0) {
+      root_to_mode[r] = static_cast<int>(sums.size());
+      sums.push_back({0, 0, 0, 0});
+      masses.push_back(0.0);
+    }
+    for (int d = 0; d < 4; ++d) sums[root_to_mode[r]][d] += weights[s] * seeds[s * 4 + d];
+    masses[root_to_mode[r]] += weights[s];
+  }
+  out.components = static_cast<int>(sums.size());
+  out.modes.resize(sums.size() * 4);
+  for (size_t m = 0; m < sums.size(); ++m)
+    for (int d = 0; d < 4; ++d) {
+      const double y = sums[m][d] / masses[m];
+      out.modes[m * 4 + d] = ranges[d] > 0.0 ? y * ranges[d] + mins[d] : mins[d];
+    }
+  return out;
+}
+
 extern "C" {
 
 const char* orc_last_error(void) { return g_err.c_str(); }
@@ -1142,6 +1363,20 @@ int orc_color_conditional(int m, const double* w, const double* mu, const double
   return guarded([&] {
     Model md = model_from(m, w, mu, cov);
     color_conditional(md, locs, n, clamp, expected, variance);
+  });
+}
+
+int orc_gbms(const double* pts, int64_t n, double bandwidth, int max_iters, double tol,
+             double merge_radius, int* components, int* iterations, int* seeds0,
+             double* modes, int modes_capacity) {
+  return guarded([&] {
+    GbmsOut g = gbms(pts, n, bandwidth, max_iters, tol, merge_radius);
+    *components = g.components;
+    *iterations = g.iterations;
+    if (seeds0) *seeds0 = g.seeds0;
+    if (modes)
+      std::memcpy(modes, g.modes.data(),
+                  sizeof(double) * 4 * std::min(g.components, modes_capacity));
   });
 }
 }  // extern "C"

@@ -135,6 +135,13 @@ int orc_color_conditional(int m, const double* w, const double* mu, const double
                           const double* locs, int64_t n, int clamp, double* expected,
                           double* variance);
 
+/* gbms_estimate_components (sogmm.cpp:22-195) with the reference's kd-tree
+ * (kdtree.hpp); points N x 4 column-major; modes (optional) components x 4
+ * row-major, up to modes_capacity rows. */
+int orc_gbms(const double* pts, int64_t n, double bandwidth, int max_iters, double tol,
+             double merge_radius, int* components, int* iterations, int* seeds0,
+             double* modes, int modes_capacity);
+
 #ifdef __cplusplus
 }
 #endif

@@ -57,6 +57,11 @@ class _EmParams(ctypes.Structure):
                 ("cov_reg", ctypes.c_double), ("seed", ctypes.c_uint64)]
 
 
+class _GbmsParams(ctypes.Structure):  # gmmb_gbms_params (sogmm.hpp:12-22)
+    _fields_ = [("bandwidth", ctypes.c_double), ("max_iters", ctypes.c_int),
+                ("convergence_tol", ctypes.c_double), ("merge_radius", ctypes.c_double)]
+
+
 class _FitStats(ctypes.Structure):
     _fields_ = [("em_iterations", ctypes.c_int),
                 ("final_log_likelihood", ctypes.c_double),
@@ -134,6 +139,12 @@ _SIGS = {
     "gmmb_save_model_json": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _D, _D, _D]),
     "gmmb_load_model_json": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _D, _D, _D,
                                             ctypes.POINTER(ctypes.c_int)]),
+    "gmmb_gbms": (ctypes.c_int, [_V, _D, ctypes.c_int64, ctypes.c_int,
+                                 ctypes.POINTER(_GbmsParams), ctypes.POINTER(ctypes.c_int),
+                                 ctypes.POINTER(ctypes.c_int), _D, ctypes.c_int]),
+    "gmmb_fit": (ctypes.c_int, [_V, _D, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(_GbmsParams),
+                                ctypes.POINTER(_EmParams), ctypes.c_int, _D, _D, _D, _D,
+                                ctypes.POINTER(_FitStats), ctypes.POINTER(ctypes.c_int)]),
     "gmmb_score": (ctypes.c_int, [_V, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _D, _D, _D,
                                   _D, _D]),
     "gmmb_sample": (ctypes.c_int, [_V, ctypes.c_int, ctypes.c_int, _D, _D, _D, ctypes.c_int64,
@@ -264,6 +275,7 @@ class FitResult:
     launches: int = 0
     labels: Optional[np.ndarray] = None
     centers: Optional[np.ndarray] = None
+    gbms_components: int = 0      # fit(): GBMS's component estimate
 
 
 @dataclasses.dataclass
@@ -416,6 +428,52 @@ def fit_k(points, k: int, em: EmParams = EmParams(), ctx: Optional[Context] = No
                              _ptr(out[0]), _ptr(out[1]), _ptr(out[2]), _ptr(ll),
                              ctypes.byref(st), _ptr(lab, _I32), _ptr(cen, _I64)))
     return _result(out, ll, st, lab, cen)
+
+
+@dataclasses.dataclass
+class GbmsParams:
+    """GbmsParams (sogmm.hpp:12-22)."""
+    bandwidth: float = 0.015
+    max_iters: int = 100
+    convergence_tol: float = 1e-5
+    merge_radius: float = -1.0
+
+    def _c(self):
+        return _GbmsParams(self.bandwidth, self.max_iters, self.convergence_tol, self.merge_radius)
+
+
+def gbms(points, params: GbmsParams = GbmsParams(), ctx: Optional[Context] = None):
+    """gbms_estimate_components (sogmm.cpp:22-195): (components, iterations,
+    modes (components, 4) in the original coordinates)."""
+    c = _ctx(ctx)
+    p, n, d = _points(points)
+    comp, it = ctypes.c_int(), ctypes.c_int()
+    cap = 8192
+    while True:
+        modes = np.zeros((cap, 4))
+        _check(load().gmmb_gbms(c.handle, _ptr(p), n, d, ctypes.byref(params._c()),
+                                ctypes.byref(comp), ctypes.byref(it), _ptr(modes), cap))
+        if comp.value <= cap:
+            return comp.value, it.value, modes[:comp.value].copy()
+        cap = comp.value
+
+
+def fit(points, params: GbmsParams = GbmsParams(), em: EmParams = EmParams(),
+        ctx: Optional[Context] = None) -> FitResult:
+    """fit (sogmm.cpp:465-510): GBMS decides K, then k-means++ -> m_step -> EM."""
+    c = _ctx(ctx)
+    p, n, d = _points(points)
+    cap = 4096
+    out = _alloc_model(cap, d)
+    ll = np.zeros(max(em.max_iters, 1))
+    st = _FitStats()
+    comp = ctypes.c_int()
+    _check(load().gmmb_fit(c.handle, _ptr(p), n, d, ctypes.byref(params._c()),
+                           ctypes.byref(em._c()), cap, _ptr(out[0]), _ptr(out[1]), _ptr(out[2]),
+                           _ptr(ll), ctypes.byref(st), ctypes.byref(comp)))
+    r = _result(out, ll, st, None, None)
+    r.gbms_components = comp.value
+    return r
 
 
 def _model_arrays(model: Gmm, d: int):

@@ -28,6 +28,7 @@
 #include "mstep_hard.cuh"
 #include "inference.cuh"
 #include "ingest.cuh"
+#include "gbms.cuh"
 
 using namespace gmmb;
 
@@ -149,6 +150,7 @@ struct gmmb_ctx {
   DevBuf<uint16_t> img;        // ingest: depth + intensity images
   DevBuf<int> iflags;          // ingest: flags + offsets
   DevBuf<int64_t> in_n;
+  DevBuf<unsigned char> gb;    // GBMS scratch (one allocation)
   DevBuf<int> flags;
   // kinit
   DevBuf<uint64_t> keys;
@@ -823,6 +825,55 @@ int upload_factors(gmmb_ctx* c, int m, int d, const double* w, const double* mu,
   return err[0] == INT_MAX ? -1 : err[0];
 }
 
+// GBMS on the resident cloud (sogmm.cpp:22-195); modes copied to the host
+GbmsResultHost run_gbms(gmmb_ctx* c, const gmmb_gbms_params* gp, double* modes, int capacity) {
+  if (!gp) throw Err{2, "null GBMS parameters"};
+  // GbmsParams::validate (sogmm.cpp:22-30)
+  if (!(gp->bandwidth > 0.0) || gp->bandwidth > 1.0) throw Err{2, "bandwidth must be in (0, 1]"};
+  if (gp->max_iters < 1) throw Err{2, "max_iters must be >= 1"};
+  if (!(gp->convergence_tol > 0.0)) throw Err{2, "convergence_tol must be > 0"};
+  const int64_t n = c->n;
+  if (n > (int64_t{1} << 31) - 2) throw Err{2, "too many points for GBMS on one device"};
+  // carve the scratch: 8 + 5n*4... doubles, uint64 and int32 arrays
+  const size_t nn = static_cast<size_t>(n) + 1;
+  const size_t tb = gbms_temp_bytes(n);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  const size_t o_mm = take(8 * 8), o_norm = take(nn * 32), o_seeds = take(nn * 32),
+               o_next = take(nn * 32), o_w = take(nn * 8), o_w2 = take(nn * 8),
+               o_terms = take(nn * 8), o_scal = take(8), o_modes = take(nn * 32),
+               o_k0 = take(nn * 8), o_k1 = take(nn * 8), o_uk = take(nn * 8), o_i0 = take(nn * 4),
+               o_i1 = take(nn * 4), o_i2 = take(nn * 4), o_i3 = take(nn * 4),
+               o_cnt = take(nn * 4), o_off = take(nn * 4), o_nr = take(4), o_fl = take(4),
+               o_tmp = take(tb);
+  c->gb.ensure(off);
+  unsigned char* b = c->gb.p;
+  GbmsScratch g{reinterpret_cast<double*>(b + o_mm), reinterpret_cast<double*>(b + o_norm),
+                reinterpret_cast<double*>(b + o_seeds), reinterpret_cast<double*>(b + o_next),
+                reinterpret_cast<double*>(b + o_w), reinterpret_cast<double*>(b + o_w2),
+                reinterpret_cast<double*>(b + o_terms), reinterpret_cast<double*>(b + o_scal),
+                reinterpret_cast<double*>(b + o_modes), reinterpret_cast<uint64_t*>(b + o_k0),
+                reinterpret_cast<uint64_t*>(b + o_k1), reinterpret_cast<uint64_t*>(b + o_uk),
+                reinterpret_cast<int32_t*>(b + o_i0), reinterpret_cast<int32_t*>(b + o_i1),
+                reinterpret_cast<int32_t*>(b + o_i2), reinterpret_cast<int32_t*>(b + o_i3),
+                reinterpret_cast<int*>(b + o_cnt), reinterpret_cast<int*>(b + o_off),
+                reinterpret_cast<int*>(b + o_nr), reinterpret_cast<int*>(b + o_fl),
+                b + o_tmp, tb};
+  const double mr = gp->merge_radius > 0.0 ? gp->merge_radius : gp->bandwidth * 0.5;
+  GbmsParamsDev prm{gp->bandwidth, gp->convergence_tol, mr, gp->max_iters};
+  GbmsResultHost res{};
+  ck(gbms_run(c->x64.p, n, prm, g, &res, c->s), "gbms");
+  if (modes && capacity > 0) {
+    const int m = std::min(res.components, capacity);
+    copy_sync(c, modes, g.modes, sizeof(double) * 4 * m, cudaMemcpyDeviceToHost);
+  }
+  return res;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -857,6 +908,14 @@ int gmmb_shard_key_tail(const double* heads, int world, int rank, double* tail3)
   }
   for (; got < 3; ++got) tail3[got] = 0.0;  // N < 3 overall: z column
   return 0;
+}
+
+void gmmb_gbms_params_default(gmmb_gbms_params* p) {
+  if (!p) return;
+  p->bandwidth = 0.015;
+  p->max_iters = 100;
+  p->convergence_tol = 1e-5;
+  p->merge_radius = -1.0;
 }
 
 void gmmb_em_params_default(gmmb_em_params* p) {
@@ -931,7 +990,7 @@ void gmmb_ctx_destroy(gmmb_ctx* c) {
   c->midx.release(); c->sort_tmp.release(); c->flags.release(); c->hidx.release();
   c->iw.release(); c->imu.release(); c->icov.release(); c->ifac.release(); c->ilow.release();
   c->iout.release(); c->iout2.release(); c->ierr.release(); c->img.release();
-  c->iflags.release(); c->in_n.release();
+  c->iflags.release(); c->in_n.release(); c->gb.release();
   c->keys.release(); c->kd2.release(); c->labels.release(); c->chosen.release();
   c->slots.release(); c->owned.release(); c->centers.release(); c->rslots.release();
   c->ticket.release(); c->kstatus.release(); c->ll64.release();
@@ -1136,6 +1195,37 @@ int gmmb_ingest_images(gmmb_ctx* c, const uint16_t* depth, const uint16_t* inten
     if (n_out) *n_out = n;
     if (pts_out)
       copy_sync(c, pts_out, c->x64.p, sizeof(double) * n * 4, cudaMemcpyDeviceToHost);
+  });
+}
+
+int gmmb_gbms(gmmb_ctx* c, const double* pts, int64_t n, int d, const gmmb_gbms_params* gp,
+              int* components, int* iterations, double* modes, int modes_capacity) {
+  return guarded([&] {
+    if (!c) throw Err{2, "null context"};
+    upload(c, pts, n, d, 0, n);
+    validate(c);
+    check_cloud_flags(c);  // cloud.validate() (sogmm.cpp:36)
+    const GbmsResultHost r = run_gbms(c, gp, modes, modes_capacity);
+    if (components) *components = r.components;
+    if (iterations) *iterations = r.iterations;
+  });
+}
+
+int gmmb_fit(gmmb_ctx* c, const double* pts, int64_t n, int d, const gmmb_gbms_params* gp,
+             const gmmb_em_params* em, int capacity, double* w_out, double* mu_out,
+             double* cov_out, double* ll_trace, gmmb_fit_stats* stats, int* gbms_components) {
+  return guarded([&] {
+    if (!c) throw Err{2, "null context"};
+    if (c->world > 1) throw Err{2, "gmmb_fit is single-device; use gmmb_fit_k when sharded"};
+    upload(c, pts, n, d, 0, n);
+    validate(c);
+    check_cloud_flags(c);  // sogmm.cpp:466
+    check_em(em);          // :468-470
+    const GbmsResultHost r = run_gbms(c, gp, nullptr, 0);  // :472-475
+    if (gbms_components) *gbms_components = r.components;
+    const int k = static_cast<int>(std::min<int64_t>(r.components, n));  // :477
+    if (k > capacity) throw Err{2, "output capacity smaller than the GBMS component count"};
+    fit_k_resident(c, k, em, w_out, mu_out, cov_out, ll_trace, stats, nullptr, nullptr);
   });
 }
 
