@@ -315,11 +315,28 @@ __device__ __forceinline__ void merge_top2d(float& a1, int& i1, float& a2, doubl
   d = take ? e : d;
 }
 
-template <int PPT>
+// Per-point state lives in shared memory (SoA by compute thread) and every
+// per-point loop is rolled: the compute warps' executed code stays a few KB,
+// so the communication warp's exchange code is not evicted from the
+// instruction cache every epoch (it was, with register-resident points and
+// fully unrolled loops: ~7k-cycle exchange phases of `no_instruction` stalls).
+struct PointState {
+  double* x;      // [4][ppt][kCompThreads]
+  double* d2;     // [ppt][kCompThreads]
+  uint64_t* kp;   // pre-multiplied keys
+  float *inv, *na0, *na1, *nb0, *nb1, *a;
+  int* lab;
+};
+__host__ __device__ constexpr size_t point_state_bytes(int ppt) {
+  return static_cast<size_t>(ppt) * kCompThreads * (4 * 8 + 8 + 8 + 6 * 4 + 4);
+}
+
 __global__ void __launch_bounds__(kSeedThreads, 1)
     kpp_seed_kernel(const double* __restrict__ x64, int64_t n, int k,
-                    uint64_t seed, KinitScratch scr) {
+                    uint64_t seed, KinitScratch scr, int ppt) {
   __shared__ SeedSmem sm;
+  extern __shared__ __align__(16) unsigned char pstate_raw[];
+  const int PPT = ppt;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nblk = gridDim.x;
   // the communication warp is the CTA's last warp: the scheduler favours
@@ -329,23 +346,42 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
   const long long g0 = comm ? -1 : static_cast<long long>(blockIdx.x) * kCompThreads + tid;
   // LL regions (uint2 words): approx slots [2][nblk], exact slots [2][nblk]
   uint2* llw = reinterpret_cast<uint2*>(scr.slots);
-  double px[PPT][4], d2[PPT];
-  float inv[PPT], na0[PPT], na1[PPT], nb0[PPT], nb1[PPT];
-  uint64_t kp[PPT];
-  int lab[PPT];
+  const int P1 = PPT * kCompThreads;
+  PointState ps;
+  {
+    unsigned char* q = pstate_raw;
+    ps.x = reinterpret_cast<double*>(q);
+    q += sizeof(double) * 4 * P1;
+    ps.d2 = reinterpret_cast<double*>(q);
+    q += sizeof(double) * P1;
+    ps.kp = reinterpret_cast<uint64_t*>(q);
+    q += sizeof(uint64_t) * P1;
+    float* f = reinterpret_cast<float*>(q);
+    ps.inv = f;
+    ps.na0 = f + P1;
+    ps.na1 = f + 2 * P1;
+    ps.nb0 = f + 3 * P1;
+    ps.nb1 = f + 4 * P1;
+    ps.a = f + 5 * P1;
+    ps.lab = reinterpret_cast<int*>(f + 6 * P1);
+  }
+  const int t = comm ? 0 : tid;  // compute-thread index into the SoA state
+#define PX(j, q) ps.x[((q) * PPT + (j)) * kCompThreads + t]
+#define PS(arr, j) ps.arr[(j) * kCompThreads + t]
   unsigned chosen = 0, valid = 0;
-#pragma unroll
-  for (int j = 0; j < PPT; ++j) {
-    const long long i = g0 + j * G;
-    const bool v = !comm && i < n;
-    if (v) valid |= 1u << j;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) px[j][q] = v ? x64[q * n + i] : 0.0;
-    kp[j] = v ? scr.keys[i] : 0;
-    d2[j] = INFINITY;
-    inv[j] = 0.f;
-    lab[j] = 0;
-    na0[j] = na1[j] = nb0[j] = nb1[j] = INFINITY;
+  if (!comm) {
+#pragma unroll 1
+    for (int j = 0; j < PPT; ++j) {
+      const long long i = g0 + j * G;
+      const bool v = i < n;
+      if (v) valid |= 1u << j;
+      for (int q = 0; q < 4; ++q) PX(j, q) = v ? x64[q * n + i] : 0.0;
+      PS(kp, j) = v ? scr.keys[i] : 0;
+      PS(d2, j) = INFINITY;
+      PS(inv, j) = 0.f;
+      PS(lab, j) = 0;
+      PS(na0, j) = PS(na1, j) = PS(nb0, j) = PS(nb1, j) = PS(a, j) = INFINITY;
+    }
   }
   // slots beyond the warp's last valid point are skipped (warp-uniform)
   const unsigned wvalid = __reduce_or_sync(0xffffffffu, valid);
@@ -353,17 +389,17 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
     sm.exact_rounds = 0;
     sm.spec_hits = 0;
   }
-  auto draw = [&](int r, float (&out)[PPT]) {  // -ln(u) of round r, FP32 approximation
+  auto draw = [&](int r, float* out) {  // -ln(u) of round r, FP32 approximation
     if (r >= k) return;
     const uint64_t pre = round_prefix(seed, r);
-#pragma unroll
+#pragma unroll 1
     for (int j = 0; j < PPT; ++j) {
-      if ((wvalid >> j) & 1) out[j] = nlu_approx(mix64(pre + kp[j]));
+      if ((wvalid >> j) & 1) out[j * kCompThreads + t] = nlu_approx(mix64(pre + PS(kp, j)));
     }
   };
   if (!comm) {
-    draw(0, na0);
-    draw(1, na1);
+    draw(0, ps.na0);
+    draw(1, ps.na1);
   }
   double cf[2][4];   // centres to fold at the start of the epoch, in order
   int nf = 0, rf = 0;  // how many, and the round of the first
@@ -376,32 +412,36 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
     uint2* slot_a = llw + par * nblk * kSlotWords;
     uint2* slot_e = llw + (2 + par) * nblk * kSlotWords;
     const bool lvl1 = r > 0 && r + 1 < k;  // round r + 1 can be speculated
-    float a[PPT];
     if (!comm) {
       // ---- fold the new centres (sogmm.cpp:229-238), clocks of r, r + 1 ----
       float a1 = INFINITY, a2 = INFINITY, b1 = INFINITY, b2 = INFINITY;
       int i1 = -1, j1 = -1;
       double bd = 0.0;
-#pragma unroll
+#pragma unroll 1
       for (int j = 0; j < PPT; ++j) {
-        a[j] = INFINITY;
+        PS(a, j) = INFINITY;
         if (!((wvalid >> j) & 1)) continue;
+        double dj = PS(d2, j);
+        float ivj = PS(inv, j);
+        const double x0 = PX(j, 0), x1 = PX(j, 1), x2 = PX(j, 2), x3 = PX(j, 3);
         for (int f = 0; f < nf; ++f) {
-          const double dd = dist2(px[j][0], px[j][1], px[j][2], px[j][3], cf[f]);
-          if (dd < d2[j]) {
-            d2[j] = dd;
-            lab[j] = rf + f;
+          const double dd = dist2(x0, x1, x2, x3, cf[f]);
+          if (dd < dj) {
+            dj = dd;
+            PS(lab, j) = rf + f;
             // d2 == 0 (a chosen point or a duplicate) is ineligible (:254)
             const float fl = __double2float_rn(dd);
-            inv[j] = dd > 0.0 ? (isinf(fl) ? 1e-38f : rcp_approx(fl)) : 0.f;
+            ivj = dd > 0.0 ? (isinf(fl) ? 1e-38f : rcp_approx(fl)) : 0.f;
           }
         }
+        PS(d2, j) = dj;
+        PS(inv, j) = ivj;
         if (r >= k || !((valid >> j) & 1)) continue;
         const int ij = static_cast<int>(g0 + j * G);
-        const float aj = r == 0 ? na0[j] : (inv[j] > 0.f ? na0[j] * inv[j] : INFINITY);
-        a[j] = aj;
+        const float aj = r == 0 ? PS(na0, j) : (ivj > 0.f ? PS(na0, j) * ivj : INFINITY);
+        PS(a, j) = aj;
         if (aj < INFINITY) merge_top2(a1, i1, a2, aj, ij, INFINITY);
-        if (lvl1 && inv[j] > 0.f) merge_top2d(b1, j1, b2, bd, na1[j] * inv[j], ij, INFINITY, d2[j]);
+        if (lvl1 && ivj > 0.f) merge_top2d(b1, j1, b2, bd, PS(na1, j) * ivj, ij, INFINITY, dj);
       }
       if (r >= k) break;
 #pragma unroll
@@ -536,8 +576,8 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
         sm.thr = need_exact ? g1 * kBand : -1.f;
       }
     } else {
-      draw(r + 2, nb0);  // overlaps the exchange
-      draw(r + 3, nb1);
+      draw(r + 2, ps.nb0);  // overlaps the exchange
+      draw(r + 3, ps.nb1);
     }
     __syncthreads();
     if (sm.win[0] == -2) {
@@ -547,12 +587,12 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
         const uint64_t pre = round_prefix(seed, r);
         double bc = INFINITY;
         long long bi = -1;
-#pragma unroll
+#pragma unroll 1
         for (int j = 0; j < PPT; ++j) {
           if (!((wvalid >> j) & 1)) continue;
-          if (((valid >> j) & 1) && (r == 0 || d2[j] > 0.0) && !(a[j] > thr)) {
-            const double nl = nlu_exact(mix64(pre + kp[j]));
-            const double clk = r == 0 ? nl : nl / d2[j];
+          if (((valid >> j) & 1) && (r == 0 || PS(d2, j) > 0.0) && !(PS(a, j) > thr)) {
+            const double nl = nlu_exact(mix64(pre + PS(kp, j)));
+            const double clk = r == 0 ? nl : nl / PS(d2, j);
             const long long i = g0 + j * G;
             if (clk < INFINITY && cand_better(clk, i, bc, bi)) {
               bc = clk;
@@ -659,14 +699,14 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
       if (w0 % G == g0) chosen |= 1u << static_cast<int>(w0 / G);
       if (w1 >= 0 && w1 % G == g0) chosen |= 1u << static_cast<int>(w1 / G);
       // draws of the next epoch's two rounds
-#pragma unroll
+#pragma unroll 1
       for (int j = 0; j < PPT; ++j) {
         if (w1 >= 0) {
-          na0[j] = nb0[j];
-          na1[j] = nb1[j];
+          PS(na0, j) = PS(nb0, j);
+          PS(na1, j) = PS(nb1, j);
         } else {
-          na0[j] = na1[j];
-          na1[j] = nb0[j];
+          PS(na0, j) = PS(na1, j);
+          PS(na1, j) = PS(nb0, j);
         }
       }
     }
@@ -676,14 +716,16 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
   }
   // labels + owned counts (every point's final nearest centre)
   if (!comm) {
-#pragma unroll
+#pragma unroll 1
     for (int j = 0; j < PPT; ++j) {
       const long long i = g0 + j * G;
       if (i >= n) continue;
-      scr.labels[i] = lab[j];
-      atomicAdd(&scr.owned[lab[j]], 1);
+      scr.labels[i] = PS(lab, j);
+      atomicAdd(&scr.owned[PS(lab, j)], 1);
     }
   }
+#undef PX
+#undef PS
 }
 
 // Memory-resident variant (N beyond the register budget): state in global
@@ -1067,15 +1109,20 @@ cudaError_t launch_keys(const double* x64, int64_t n, const double* tail,
 
 cudaError_t launch_kpp_seed(const double* x64, int64_t n, int k, uint64_t seed,
                             KinitScratch scr, int sm_count, cudaStream_t s) {
-  // one CTA per SM, points register-resident while they fit
+  // one CTA per SM, per-point state resident in shared memory while it fits
   const int nblk = sm_count < kMaxSeedBlocks ? sm_count : kMaxSeedBlocks;
-  void* args[] = {(void*)&x64, (void*)&n, (void*)&k, (void*)&seed, (void*)&scr};
-  if (n <= static_cast<int64_t>(nblk) * kCompThreads * 6)
-    return cudaLaunchCooperativeKernel((void*)kpp_seed_kernel<6>, dim3(nblk), dim3(kSeedThreads),
-                                       args, 0, s);
-  if (n <= static_cast<int64_t>(nblk) * kCompThreads * kSeedPPT)
-    return cudaLaunchCooperativeKernel((void*)kpp_seed_kernel<kSeedPPT>, dim3(nblk),
-                                       dim3(kSeedThreads), args, 0, s);
+  const int64_t per_thread = (n + static_cast<int64_t>(nblk) * kCompThreads - 1) /
+                             (static_cast<int64_t>(nblk) * kCompThreads);
+  const size_t bytes = point_state_bytes(static_cast<int>(per_thread));
+  if (per_thread <= 32 && bytes <= 220 * 1024) {
+    int ppt = static_cast<int>(per_thread);
+    cudaError_t e = cudaFuncSetAttribute(kpp_seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(bytes));
+    if (e != cudaSuccess) return e;
+    void* args[] = {(void*)&x64, (void*)&n, (void*)&k, (void*)&seed, (void*)&scr, (void*)&ppt};
+    return cudaLaunchCooperativeKernel((void*)kpp_seed_kernel, dim3(nblk), dim3(kSeedThreads), args,
+                                       bytes, s);
+  }
   // memory-resident fallback: one launch per round; a thread holds up to
   // kMemPPT points (n > sm_count * 4 * 512 * kMemPPT: more CTAs)
   const int64_t cap = static_cast<int64_t>(sm_count) * 4 * kMemThreads * kMemPPT;
