@@ -248,3 +248,27 @@ def test_cpp_example_fits_blobs(gm, tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stderr
     assert "K=3" in r.stdout
+
+
+# ---- edge shapes of the fused kernels (partial tiles / sub-tiles, tiny N) ---
+@pytest.mark.parametrize("n,k,d", [(7, 1, 4), (50, 3, 4), (129, 4, 4), (1000, 17, 3),
+                                   (4097, 64, 4), (20011, 300, 4)])
+def test_small_and_ragged_fits(gm, orc, ctx, n, k, d):
+    # k separated blobs (EM well conditioned, so parameter errors measure the
+    # kernels, not EM's amplification on unstructured data), N not a multiple
+    # of the 128-point tile or the 16-point sub-tile
+    rng = np.random.default_rng(n)
+    centers = np.column_stack([rng.random((k, 3)) * 10.0, 0.2 + 0.6 * rng.random(k)])
+    lab = rng.integers(0, k, n)
+    base = centers[lab] + np.column_stack([0.05 * rng.normal(size=(n, 3)),
+                                          0.01 * rng.normal(size=n)])
+    base[:, 3] = np.clip(base[:, 3], 0.0, 1.0)
+    base = base[:, :d].copy()
+    em = gm.EmParams(40, 1e-6, 1e-6, 1)
+    r = gm.fit_k(base, k, em, ctx=ctx, want_labels=True)
+    ref = orc.fit_k(base, k, 40, 1e-6, 1e-6, 1)
+    assert np.array_equal(r.centers, ref["centers"]) and np.array_equal(r.labels, ref["labels"])
+    assert r.em_iterations == ref["em_iterations"] and r.removed_components == ref["removed"]
+    assert ll_err(r.ll_trace, ref["ll_trace"]) <= LL_TOL
+    assert_model_close(r.model.weights, r.model.means, r.model.covariances,
+                       ref["w"], ref["mu"][:, :d], ref["cov"][:, :d * (d + 1) // 2])
