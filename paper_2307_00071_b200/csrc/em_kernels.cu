@@ -1353,14 +1353,16 @@ __device__ __forceinline__ void commit_body(
 
   // keep flags -> exclusive scan (compaction preserves order, sogmm.cpp:418-429):
   // warp scans + one warp over the 32 warp totals; total kept count with a
-  // fixed-shape reduction (deterministic)
+  // fixed-shape reduction (deterministic). A thread owns `per` consecutive
+  // components (1 up to K = T, so small K spreads over all threads).
+  const int per = (k_in + T - 1) / T;
   int keep[PER];
   int cnt = 0;
   double tot = 0.0;
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
-    const int k = tid * PER + i;
-    keep[i] = (k < k_in) ? (rec.flags[k] & 1) : 0;
+    const int k = tid * per + i;
+    keep[i] = (i < per && k < k_in) ? (rec.flags[k] & 1) : 0;
     cnt += keep[i];
     if (keep[i]) tot += rec.count[k];
   }
@@ -1410,7 +1412,7 @@ __device__ __forceinline__ void commit_body(
   int j = excl;
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
-    const int k = tid * PER + i;
+    const int k = tid * per + i;
     if (keep[i]) {
       if (!(rec.flags[k] & 2)) atomicMin(&s_flag, j);
       ++j;
@@ -1432,7 +1434,7 @@ __device__ __forceinline__ void commit_body(
   j = excl;
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
-    const int k = tid * PER + i;
+    const int k = tid * per + i;
     if (!keep[i]) continue;
     const double w = rec.count[k] / total;
     dst.w[j] = w;
