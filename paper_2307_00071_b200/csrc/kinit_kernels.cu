@@ -278,6 +278,30 @@ __device__ __forceinline__ void grid_exchange(unsigned* counter, unsigned target
 // The exact resolution (round-0 key duplicates, near-ties): every point
 // inside the band gets the exact FP64 clock and a second exchange decides on
 // (clock, index), as the reference's strict-< scan does.
+#ifdef GMMB_KPP_PROF
+// phase timestamps per (CTA, epoch): clock64 in slots 0-8, globaltimer 9-10
+constexpr int kProfEpochs = 320, kProfSlots = 12;
+__device__ long long g_kpp_prof[160 * kProfEpochs * kProfSlots];
+__device__ __forceinline__ long long gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define KPROF(slot, v)                                                              \
+  do {                                                                              \
+    if (tag - 1 < kProfEpochs && blockIdx.x < 160)                                 \
+      g_kpp_prof[(blockIdx.x * kProfEpochs + (tag - 1)) * kProfSlots + (slot)] = (v); \
+  } while (0)
+#else
+#define KPROF(slot, v) \
+  do {                 \
+  } while (0)
+#endif
+#ifndef GMMB_KPP_UNROLL
+#define GMMB_KPP_UNROLL 1
+#endif
+// points per iteration of the per-point loops (independent FP64 / hash chains)
+constexpr int kPtUnroll = GMMB_KPP_UNROLL;
 constexpr int kCompWarps = kSeedWarps - 1;
 constexpr int kCompThreads = kCompWarps * 32;
 constexpr int kSlotWords = 8;  // approx: a1 i1 a2 b1 j1 b2 d2lo d2hi; exact: clock lo hi, idx, pad
@@ -290,6 +314,15 @@ struct SeedSmem {
   int wj1[kSeedWarps];
   float wb2[kSeedWarps];
   double wd2[kSeedWarps];
+  // per-warp top-2s precomputed for the next epoch (valid if no point of the
+  // warp changes its nearest centre in the fold)
+  float pa1[kSeedWarps];
+  int pi1[kSeedWarps];
+  float pa2[kSeedWarps];
+  float pb1[kSeedWarps];
+  int pj1[kSeedWarps];
+  float pb2[kSeedWarps];
+  double pd2[kSeedWarps];
   double ec[kSeedWarps];
   long long ei[kSeedWarps];
   long long gu[kSeedWarps];
@@ -315,20 +348,50 @@ __device__ __forceinline__ void merge_top2d(float& a1, int& i1, float& a2, doubl
   d = take ? e : d;
 }
 
+// warp top-2s of both levels (every lane ends with the warp's result)
+__device__ __forceinline__ void warp_top2s(float& a1, int& i1, float& a2, float& b1, int& j1,
+                                           float& b2, double& bd) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const float o1 = __shfl_xor_sync(0xffffffffu, a1, off);
+    const int oi = __shfl_xor_sync(0xffffffffu, i1, off);
+    const float o2 = __shfl_xor_sync(0xffffffffu, a2, off);
+    merge_top2(a1, i1, a2, o1, oi, o2);
+    const float p1 = __shfl_xor_sync(0xffffffffu, b1, off);
+    const int pj = __shfl_xor_sync(0xffffffffu, j1, off);
+    const float p2 = __shfl_xor_sync(0xffffffffu, b2, off);
+    const double pd = __shfl_xor_sync(0xffffffffu, bd, off);
+    merge_top2d(b1, j1, b2, bd, p1, pj, p2, pd);
+  }
+}
+
 // Per-point state lives in shared memory (SoA by compute thread) and every
 // per-point loop is rolled: the compute warps' executed code stays a few KB,
 // so the communication warp's exchange code is not evicted from the
 // instruction cache every epoch (it was, with register-resident points and
 // fully unrolled loops: ~7k-cycle exchange phases of `no_instruction` stalls).
+//
+// Clocks are precomputed off the critical path: while the communication warp
+// runs epoch e's exchange, the compute warps draw -ln(u) of the next epoch's
+// two rounds and already form their clocks and warp top-2s with the current
+// d2. A clock only depends on the point's d2, so after the next fold these
+// values are exact for every point whose nearest centre did not change (the
+// vast majority); the critical path after the exchange shrinks to the FP64
+// fold, plus a recompute from the stored clocks in the few warps where a
+// point changed. (Valid when the speculation held, so that the next epoch's
+// rounds are the ones precomputed; otherwise the epoch computes everything.)
 struct PointState {
   double* x;      // [4][ppt][kCompThreads]
   double* d2;     // [ppt][kCompThreads]
   uint64_t* kp;   // pre-multiplied keys
-  float *inv, *na0, *na1, *nb0, *nb1, *a;
+  float* inv;
+  float *e0, *e1, *e2, *e3;  // -ln(u) of rounds r, r + 1, r + 2, r + 3 (rotated pointers)
+  float *ac, *an; // level-0 clocks, this epoch / next epoch (swapped)
+  float* b;       // level-1 clocks (next epoch's after the precompute)
   int* lab;
 };
 __host__ __device__ constexpr size_t point_state_bytes(int ppt) {
-  return static_cast<size_t>(ppt) * kCompThreads * (4 * 8 + 8 + 8 + 6 * 4 + 4);
+  return static_cast<size_t>(ppt) * kCompThreads * (4 * 8 + 8 + 8 + 8 * 4 + 4);
 }
 
 __global__ void __launch_bounds__(kSeedThreads, 1)
@@ -358,16 +421,19 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
     q += sizeof(uint64_t) * P1;
     float* f = reinterpret_cast<float*>(q);
     ps.inv = f;
-    ps.na0 = f + P1;
-    ps.na1 = f + 2 * P1;
-    ps.nb0 = f + 3 * P1;
-    ps.nb1 = f + 4 * P1;
-    ps.a = f + 5 * P1;
-    ps.lab = reinterpret_cast<int*>(f + 6 * P1);
+    ps.e0 = f + 1 * P1;
+    ps.e1 = f + 2 * P1;
+    ps.e2 = f + 3 * P1;
+    ps.e3 = f + 4 * P1;
+    ps.ac = f + 5 * P1;
+    ps.an = f + 6 * P1;
+    ps.b = f + 7 * P1;
+    ps.lab = reinterpret_cast<int*>(f + 8 * P1);
   }
   const int t = comm ? 0 : tid;  // compute-thread index into the SoA state
 #define PX(j, q) ps.x[((q) * PPT + (j)) * kCompThreads + t]
 #define PS(arr, j) ps.arr[(j) * kCompThreads + t]
+#define PF(ptr, j) (ptr)[(j) * kCompThreads + t]
   unsigned chosen = 0, valid = 0;
   if (!comm) {
 #pragma unroll 1
@@ -380,7 +446,8 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
       PS(d2, j) = INFINITY;
       PS(inv, j) = 0.f;
       PS(lab, j) = 0;
-      PS(na0, j) = PS(na1, j) = PS(nb0, j) = PS(nb1, j) = PS(a, j) = INFINITY;
+      PF(ps.e0, j) = PF(ps.e1, j) = PF(ps.e2, j) = PF(ps.e3, j) = INFINITY;
+      PF(ps.ac, j) = PF(ps.an, j) = PF(ps.b, j) = INFINITY;
     }
   }
   // slots beyond the warp's last valid point are skipped (warp-uniform)
@@ -389,73 +456,113 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
     sm.exact_rounds = 0;
     sm.spec_hits = 0;
   }
-  auto draw = [&](int r, float* out) {  // -ln(u) of round r, FP32 approximation
-    if (r >= k) return;
-    const uint64_t pre = round_prefix(seed, r);
-#pragma unroll 1
-    for (int j = 0; j < PPT; ++j) {
-      if ((wvalid >> j) & 1) out[j * kCompThreads + t] = nlu_approx(mix64(pre + PS(kp, j)));
-    }
-  };
   if (!comm) {
-    draw(0, ps.na0);
-    draw(1, ps.na1);
+#pragma unroll 1
+    for (int rr = 0; rr < 2 && rr < k; ++rr) {
+      const uint64_t pre = round_prefix(seed, rr);
+#pragma unroll 1
+      for (int j = 0; j < PPT; ++j)
+        if ((wvalid >> j) & 1) PF(rr == 0 ? ps.e0 : ps.e1, j) = nlu_approx(mix64(pre + PS(kp, j)));
+    }
   }
   double cf[2][4];   // centres to fold at the start of the epoch, in order
   int nf = 0, rf = 0;  // how many, and the round of the first
   unsigned epoch = 0;  // completed counter-based grid exchanges (fallback)
   unsigned xtag = 0;   // LL tag (one per epoch)
   int r = 0;
+  bool pre_ok = false; // this epoch's clocks / warp top-2s were precomputed
   while (true) {
     const unsigned tag = ++xtag;
     const int par = tag & 1;
     uint2* slot_a = llw + par * nblk * kSlotWords;
     uint2* slot_e = llw + (2 + par) * nblk * kSlotWords;
     const bool lvl1 = r > 0 && r + 1 < k;  // round r + 1 can be speculated
+    if (tid == 0) KPROF(0, clock64());
     if (!comm) {
-      // ---- fold the new centres (sogmm.cpp:229-238), clocks of r, r + 1 ----
+      float* acur = ps.ac;
+      // ---- fold the new centres (sogmm.cpp:229-238) ----
       float a1 = INFINITY, a2 = INFINITY, b1 = INFINITY, b2 = INFINITY;
       int i1 = -1, j1 = -1;
       double bd = 0.0;
-#pragma unroll 1
-      for (int j = 0; j < PPT; ++j) {
-        PS(a, j) = INFINITY;
-        if (!((wvalid >> j) & 1)) continue;
-        double dj = PS(d2, j);
-        float ivj = PS(inv, j);
-        const double x0 = PX(j, 0), x1 = PX(j, 1), x2 = PX(j, 2), x3 = PX(j, 3);
-        for (int f = 0; f < nf; ++f) {
-          const double dd = dist2(x0, x1, x2, x3, cf[f]);
-          if (dd < dj) {
-            dj = dd;
-            PS(lab, j) = rf + f;
+      if (pre_ok && r < k) {
+        unsigned cm = 0;  // points whose nearest centre changed
+#pragma unroll kPtUnroll
+        for (int j = 0; j < PPT; ++j) {
+          if (!((wvalid >> j) & 1)) continue;
+          double dj = PS(d2, j);
+          const double x0 = PX(j, 0), x1 = PX(j, 1), x2 = PX(j, 2), x3 = PX(j, 3);
+          int lb = -1;
+          for (int f = 0; f < nf; ++f) {
+            const double dd = dist2(x0, x1, x2, x3, cf[f]);
+            if (dd < dj) {
+              dj = dd;
+              lb = rf + f;
+            }
+          }
+          if (lb >= 0) {
+            PS(d2, j) = dj;
+            PS(lab, j) = lb;
             // d2 == 0 (a chosen point or a duplicate) is ineligible (:254)
-            const float fl = __double2float_rn(dd);
-            ivj = dd > 0.0 ? (isinf(fl) ? 1e-38f : rcp_approx(fl)) : 0.f;
+            const float fl = __double2float_rn(dj);
+            PS(inv, j) = dj > 0.0 ? (isinf(fl) ? 1e-38f : rcp_approx(fl)) : 0.f;
+            cm |= 1u << j;
           }
         }
-        PS(d2, j) = dj;
-        PS(inv, j) = ivj;
-        if (r >= k || !((valid >> j) & 1)) continue;
-        const int ij = static_cast<int>(g0 + j * G);
-        const float aj = r == 0 ? PS(na0, j) : (ivj > 0.f ? PS(na0, j) * ivj : INFINITY);
-        PS(a, j) = aj;
-        if (aj < INFINITY) merge_top2(a1, i1, a2, aj, ij, INFINITY);
-        if (lvl1 && ivj > 0.f) merge_top2d(b1, j1, b2, bd, PS(na1, j) * ivj, ij, INFINITY, dj);
+        if (__any_sync(0xffffffffu, cm != 0)) {
+          // ---- recompute the changed points' clocks, the thread and warp top-2s ----
+#pragma unroll 1
+          for (int j = 0; j < PPT; ++j) {
+            if (!((valid >> j) & 1)) continue;
+            const int ij = static_cast<int>(g0 + j * G);
+            float aj, bj;
+            if ((cm >> j) & 1) {
+              const float ivj = PS(inv, j);
+              aj = ivj > 0.f ? PF(ps.e0, j) * ivj : INFINITY;
+              bj = (lvl1 && ivj > 0.f) ? PF(ps.e1, j) * ivj : INFINITY;
+              PF(acur, j) = aj;
+            } else {
+              aj = PF(acur, j);
+              bj = PF(ps.b, j);
+            }
+            if (aj < INFINITY) merge_top2(a1, i1, a2, aj, ij, INFINITY);
+            if (bj < INFINITY) merge_top2d(b1, j1, b2, bd, bj, ij, INFINITY, PS(d2, j));
+          }
+          warp_top2s(a1, i1, a2, b1, j1, b2, bd);
+        } else {
+          a1 = sm.pa1[warp]; i1 = sm.pi1[warp]; a2 = sm.pa2[warp];
+          b1 = sm.pb1[warp]; j1 = sm.pj1[warp]; b2 = sm.pb2[warp]; bd = sm.pd2[warp];
+        }
+      } else {
+        // ---- full pass: fold + clocks of r, r + 1 ----
+#pragma unroll kPtUnroll
+        for (int j = 0; j < PPT; ++j) {
+          PF(acur, j) = INFINITY;
+          if (!((wvalid >> j) & 1)) continue;
+          double dj = PS(d2, j);
+          float ivj = PS(inv, j);
+          const double x0 = PX(j, 0), x1 = PX(j, 1), x2 = PX(j, 2), x3 = PX(j, 3);
+          for (int f = 0; f < nf; ++f) {
+            const double dd = dist2(x0, x1, x2, x3, cf[f]);
+            if (dd < dj) {
+              dj = dd;
+              PS(lab, j) = rf + f;
+              const float fl = __double2float_rn(dd);
+              ivj = dd > 0.0 ? (isinf(fl) ? 1e-38f : rcp_approx(fl)) : 0.f;
+            }
+          }
+          PS(d2, j) = dj;
+          PS(inv, j) = ivj;
+          if (r >= k || !((valid >> j) & 1)) continue;
+          const int ij = static_cast<int>(g0 + j * G);
+          const float aj = r == 0 ? PF(ps.e0, j) : (ivj > 0.f ? PF(ps.e0, j) * ivj : INFINITY);
+          PF(acur, j) = aj;
+          if (aj < INFINITY) merge_top2(a1, i1, a2, aj, ij, INFINITY);
+          if (lvl1 && ivj > 0.f) merge_top2d(b1, j1, b2, bd, PF(ps.e1, j) * ivj, ij, INFINITY, dj);
+        }
+        if (r >= k) break;
+        warp_top2s(a1, i1, a2, b1, j1, b2, bd);
       }
-      if (r >= k) break;
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) {
-        const float o1 = __shfl_xor_sync(0xffffffffu, a1, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, i1, off);
-        const float o2 = __shfl_xor_sync(0xffffffffu, a2, off);
-        merge_top2(a1, i1, a2, o1, oi, o2);
-        const float p1 = __shfl_xor_sync(0xffffffffu, b1, off);
-        const int pj = __shfl_xor_sync(0xffffffffu, j1, off);
-        const float p2 = __shfl_xor_sync(0xffffffffu, b2, off);
-        const double pd = __shfl_xor_sync(0xffffffffu, bd, off);
-        merge_top2d(b1, j1, b2, bd, p1, pj, p2, pd);
-      }
+      if (tid == 0) KPROF(1, clock64());
       if (lane == 0) {
         sm.wa1[warp] = a1; sm.wi1[warp] = i1; sm.wa2[warp] = a2;
         sm.wb1[warp] = b1; sm.wj1[warp] = j1; sm.wb2[warp] = b2; sm.wd2[warp] = bd;
@@ -464,6 +571,7 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
       break;
     }
     __syncthreads();
+    if (comm && lane == 0) KPROF(2, clock64());
     if (comm) {
       // ---- CTA top-2s -> one LL slot of 8-byte (payload, tag) words ----
       const bool w = lane < kCompWarps;
@@ -491,6 +599,10 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
                          : lane == 4 ? static_cast<unsigned>(l1) : lane == 5 ? __float_as_uint(e2)
                          : lane == 6 ? static_cast<unsigned>(db) : static_cast<unsigned>(db >> 32);
         st_ll(slot_a + blockIdx.x * kSlotWords + lane, v, tag);
+      }
+      if (lane == 0) {
+        KPROF(3, clock64());
+        KPROF(9, gtime());
       }
       // ---- grid top-2s: every CTA gathers every slot (a lane's slots
       // polled concurrently), reduces in a fixed order ----
@@ -548,6 +660,10 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
         const double pd = __shfl_xor_sync(0xffffffffu, hd, off);
         merge_top2d(h1, hj, h2, hd, p1, pj, p2, pd);
       }
+      if (lane == 0) {
+        KPROF(4, clock64());
+        KPROF(10, gtime());
+      }
       // level 0: exact unless the runner-up lies within the FP32 error band
       const bool need_exact = gi >= 0 && !(g2 > g1 * kBand);
       const long long wi = need_exact ? -2 : gi;
@@ -574,12 +690,49 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
         sm.win[0] = wi;
         sm.win[1] = si;
         sm.thr = need_exact ? g1 * kBand : -1.f;
+        KPROF(5, clock64());
       }
     } else {
-      draw(r + 2, ps.nb0);  // overlaps the exchange
-      draw(r + 3, ps.nb1);
+      // ---- overlaps the exchange: draws of rounds r + 2, r + 3 and, for the
+      // case that both of this epoch's rounds are decided, their clocks and
+      // warp top-2s with the current d2 ----
+      const int r2 = r + 2;
+      const bool lv1n = r2 + 1 < k;
+      float* an = ps.an;
+      float a1 = INFINITY, a2 = INFINITY, b1 = INFINITY, b2 = INFINITY;
+      int i1 = -1, j1 = -1;
+      double bd = 0.0;
+      if (r2 < k) {
+        const uint64_t pre0 = round_prefix(seed, r2);
+        const uint64_t pre1 = round_prefix(seed, lv1n ? r2 + 1 : r2);
+#pragma unroll kPtUnroll
+        for (int j = 0; j < PPT; ++j) {
+          if (!((wvalid >> j) & 1)) continue;
+          const uint64_t kpj = PS(kp, j);
+          const float e0 = nlu_approx(mix64(pre0 + kpj));
+          const float e1 = lv1n ? nlu_approx(mix64(pre1 + kpj)) : INFINITY;
+          PF(ps.e2, j) = e0;
+          PF(ps.e3, j) = e1;
+          const float ivj = PS(inv, j);
+          const bool ok = ((valid >> j) & 1) && ivj > 0.f;
+          const float aj = ok ? e0 * ivj : INFINITY;
+          const float bj = (ok && lv1n) ? e1 * ivj : INFINITY;
+          PF(an, j) = aj;
+          PF(ps.b, j) = bj;
+          const int ij = static_cast<int>(g0 + j * G);
+          if (aj < INFINITY) merge_top2(a1, i1, a2, aj, ij, INFINITY);
+          if (bj < INFINITY) merge_top2d(b1, j1, b2, bd, bj, ij, INFINITY, PS(d2, j));
+        }
+        warp_top2s(a1, i1, a2, b1, j1, b2, bd);
+        if (lane == 0) {
+          sm.pa1[warp] = a1; sm.pi1[warp] = i1; sm.pa2[warp] = a2;
+          sm.pb1[warp] = b1; sm.pj1[warp] = j1; sm.pb2[warp] = b2; sm.pd2[warp] = bd;
+        }
+      }
+      if (tid == 0) KPROF(6, clock64());
     }
     __syncthreads();
+    if (tid == 0) KPROF(7, clock64());
     if (sm.win[0] == -2) {
       // ---- exact resolution among the points inside the band (rare) ----
       if (!comm) {
@@ -590,7 +743,7 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
 #pragma unroll 1
         for (int j = 0; j < PPT; ++j) {
           if (!((wvalid >> j) & 1)) continue;
-          if (((valid >> j) & 1) && (r == 0 || PS(d2, j) > 0.0) && !(PS(a, j) > thr)) {
+          if (((valid >> j) & 1) && (r == 0 || PS(d2, j) > 0.0) && !(PF(ps.ac, j) > thr)) {
             const double nl = nlu_exact(mix64(pre + PS(kp, j)));
             const double clk = r == 0 ? nl : nl / PS(d2, j);
             const long long i = g0 + j * G;
@@ -698,18 +851,27 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
     if (!comm) {
       if (w0 % G == g0) chosen |= 1u << static_cast<int>(w0 / G);
       if (w1 >= 0 && w1 % G == g0) chosen |= 1u << static_cast<int>(w1 / G);
-      // draws of the next epoch's two rounds
-#pragma unroll 1
-      for (int j = 0; j < PPT; ++j) {
-        if (w1 >= 0) {
-          PS(na0, j) = PS(nb0, j);
-          PS(na1, j) = PS(nb1, j);
-        } else {
-          PS(na0, j) = PS(na1, j);
-          PS(na1, j) = PS(nb0, j);
-        }
-      }
     }
+    // draws of the next epoch's two rounds (pointer rotation)
+    {
+      float* e0 = ps.e0;
+      float* e1 = ps.e1;
+      if (w1 >= 0) {  // rounds r + 2, r + 3: precomputed
+        ps.e0 = ps.e2;
+        ps.e1 = ps.e3;
+        ps.e2 = e0;
+        ps.e3 = e1;
+        float* a = ps.ac;
+        ps.ac = ps.an;
+        ps.an = a;
+      } else {        // rounds r + 1, r + 2: computed in full
+        ps.e0 = e1;
+        ps.e1 = ps.e2;
+        ps.e2 = e0;
+      }
+      pre_ok = w1 >= 0;
+    }
+    if (tid == 0) KPROF(8, clock64());
     r += nf;
     // sm.win / sm.cx are rewritten by warp 0 only after the next epoch's
     // first barrier, which every thread reaches after these reads
@@ -1168,3 +1330,9 @@ cudaError_t launch_kpp_final(const double* x64, int64_t n, int64_t offset,
 }
 
 }  // namespace gmmb
+
+#ifdef GMMB_KPP_PROF
+extern "C" int gmmb_debug_kpp_prof(long long* out, int count) {
+  return static_cast<int>(cudaMemcpyFromSymbol(out, gmmb::g_kpp_prof, sizeof(long long) * count));
+}
+#endif
