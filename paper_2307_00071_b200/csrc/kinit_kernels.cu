@@ -348,21 +348,39 @@ __device__ __forceinline__ void merge_top2d(float& a1, int& i1, float& a2, doubl
   d = take ? e : d;
 }
 
+__device__ __forceinline__ void prefetch_point(const double* x64, int64_t n, int i) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) asm volatile("prefetch.global.L1 [%0];" ::"l"(x64 + q * n + i));
+}
+
+// Warp top-2 by three redux.sync.min: clocks are non-negative floats (or
+// +inf), so their bit patterns order like the values; the best entry is the
+// (clock, index) minimum, and the runner-up is the minimum over lanes of
+// "my second" for the lane(s) holding the best entry, "my best" for the
+// others (equal to merge_top2's pairwise result).
+__device__ __forceinline__ void warp_top2(float& a1, int& i1, float& a2) {
+  const unsigned u1 = __float_as_uint(a1);
+  const unsigned m1 = __reduce_min_sync(0xffffffffu, u1);
+  const unsigned mi = __reduce_min_sync(0xffffffffu, u1 == m1 ? static_cast<unsigned>(i1) : ~0u);
+  const unsigned u2 = static_cast<unsigned>(i1) == mi ? __float_as_uint(a2) : u1;
+  a2 = __uint_as_float(__reduce_min_sync(0xffffffffu, u2));
+  a1 = __uint_as_float(m1);
+  i1 = static_cast<int>(mi);
+}
 // warp top-2s of both levels (every lane ends with the warp's result)
 __device__ __forceinline__ void warp_top2s(float& a1, int& i1, float& a2, float& b1, int& j1,
                                            float& b2, double& bd) {
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) {
-    const float o1 = __shfl_xor_sync(0xffffffffu, a1, off);
-    const int oi = __shfl_xor_sync(0xffffffffu, i1, off);
-    const float o2 = __shfl_xor_sync(0xffffffffu, a2, off);
-    merge_top2(a1, i1, a2, o1, oi, o2);
-    const float p1 = __shfl_xor_sync(0xffffffffu, b1, off);
-    const int pj = __shfl_xor_sync(0xffffffffu, j1, off);
-    const float p2 = __shfl_xor_sync(0xffffffffu, b2, off);
-    const double pd = __shfl_xor_sync(0xffffffffu, bd, off);
-    merge_top2d(b1, j1, b2, bd, p1, pj, p2, pd);
-  }
+  warp_top2(a1, i1, a2);
+  const unsigned u1 = __float_as_uint(b1);
+  const unsigned m1 = __reduce_min_sync(0xffffffffu, u1);
+  const unsigned mj = __reduce_min_sync(0xffffffffu, u1 == m1 ? static_cast<unsigned>(j1) : ~0u);
+  const bool holder = static_cast<unsigned>(j1) == mj;
+  const unsigned u2 = holder ? __float_as_uint(b2) : u1;
+  b2 = __uint_as_float(__reduce_min_sync(0xffffffffu, u2));
+  const int src = __ffs(__ballot_sync(0xffffffffu, holder)) - 1;
+  bd = __shfl_sync(0xffffffffu, bd, src);
+  b1 = __uint_as_float(m1);
+  j1 = static_cast<int>(mj);
 }
 
 // Per-point state lives in shared memory (SoA by compute thread) and every
@@ -580,18 +598,7 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
       float e1 = w ? sm.wb1[lane] : INFINITY, e2 = w ? sm.wb2[lane] : INFINITY;
       int l1 = w ? sm.wj1[lane] : -1;
       double ed = w ? sm.wd2[lane] : 0.0;
-#pragma unroll 1
-      for (int off = 16; off >= 1; off >>= 1) {
-        const float o1 = __shfl_xor_sync(0xffffffffu, c1, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, k1, off);
-        const float o2 = __shfl_xor_sync(0xffffffffu, c2, off);
-        merge_top2(c1, k1, c2, o1, oi, o2);
-        const float p1 = __shfl_xor_sync(0xffffffffu, e1, off);
-        const int pj = __shfl_xor_sync(0xffffffffu, l1, off);
-        const float p2 = __shfl_xor_sync(0xffffffffu, e2, off);
-        const double pd = __shfl_xor_sync(0xffffffffu, ed, off);
-        merge_top2d(e1, l1, e2, ed, p1, pj, p2, pd);
-      }
+      warp_top2s(c1, k1, c2, e1, l1, e2, ed);
       if (lane < kSlotWords) {
         const unsigned long long db = dbits(ed);
         const unsigned v = lane == 0 ? __float_as_uint(c1) : lane == 1 ? static_cast<unsigned>(k1)
@@ -643,27 +650,16 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
                          __uint_as_float(v[q][2]));
               merge_top2d(h1, hj, h2, hd, __uint_as_float(v[q][3]), static_cast<int>(v[q][4]),
                           __uint_as_float(v[q][5]), bitsd(v[q][6], v[q][7]));
+              // a lane's new best may be the winner: start its coordinates
+              // towards L1 now, the decision below reads them
+              if (gi == static_cast<int>(v[q][1]) && gi >= 0) prefetch_point(x64, n, gi);
+              if (hj == static_cast<int>(v[q][4]) && hj >= 0) prefetch_point(x64, n, hj);
               pend &= ~(1u << q);
             }
           }
         }
       }
-#pragma unroll 1
-      for (int off = 16; off >= 1; off >>= 1) {
-        const float o1 = __shfl_xor_sync(0xffffffffu, g1, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, gi, off);
-        const float o2 = __shfl_xor_sync(0xffffffffu, g2, off);
-        merge_top2(g1, gi, g2, o1, oi, o2);
-        const float p1 = __shfl_xor_sync(0xffffffffu, h1, off);
-        const int pj = __shfl_xor_sync(0xffffffffu, hj, off);
-        const float p2 = __shfl_xor_sync(0xffffffffu, h2, off);
-        const double pd = __shfl_xor_sync(0xffffffffu, hd, off);
-        merge_top2d(h1, hj, h2, hd, p1, pj, p2, pd);
-      }
-      if (lane == 0) {
-        KPROF(4, clock64());
-        KPROF(10, gtime());
-      }
+      warp_top2s(g1, gi, g2, h1, hj, h2, hd);
       // level 0: exact unless the runner-up lies within the FP32 error band
       const bool need_exact = gi >= 0 && !(g2 > g1 * kBand);
       const long long wi = need_exact ? -2 : gi;
