@@ -279,22 +279,26 @@ __device__ __forceinline__ void grid_exchange(unsigned* counter, unsigned target
 // inside the band gets the exact FP64 clock and a second exchange decides on
 // (clock, index), as the reference's strict-< scan does.
 #ifdef GMMB_KPP_PROF
-// phase timestamps per (CTA, epoch): clock64 in slots 0-8, globaltimer 9-10
-constexpr int kProfEpochs = 320, kProfSlots = 12;
+// phase timestamps per (CTA, epoch) in shared memory (no memory-system
+// traffic inside the loop), copied out at the end. clock64 per warp: the
+// counters of different SM sub-partitions are not comparable, and a counter
+// read is not ordered with a barrier, so only intervals within one warp
+// between barriers are meaningful (slots 0-4: compute thread 0; 5-7: the
+// communication warp)
+constexpr int kProfEpochs = 300, kProfSlots = 9;
 __device__ long long g_kpp_prof[160 * kProfEpochs * kProfSlots];
-__device__ __forceinline__ long long gtime() {
+__device__ __forceinline__ long long pclock() {
   long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
   return t;
 }
-#define KPROF(slot, v)                                                              \
-  do {                                                                              \
-    if (tag - 1 < kProfEpochs && blockIdx.x < 160)                                 \
-      g_kpp_prof[(blockIdx.x * kProfEpochs + (tag - 1)) * kProfSlots + (slot)] = (v); \
+#define KPROF(slot)                                                  \
+  do {                                                               \
+    if (tag - 1 < kProfEpochs) prof_s[tag - 1][slot] = pclock();     \
   } while (0)
 #else
-#define KPROF(slot, v) \
-  do {                 \
+#define KPROF(slot) \
+  do {              \
   } while (0)
 #endif
 #ifndef GMMB_KPP_UNROLL
@@ -302,6 +306,12 @@ __device__ __forceinline__ long long gtime() {
 #endif
 // points per iteration of the per-point loops (independent FP64 / hash chains)
 constexpr int kPtUnroll = GMMB_KPP_UNROLL;
+#ifndef GMMB_FOLD_STEP
+#define GMMB_FOLD_STEP 2
+#endif
+// points folded at once (independent FP64 chains per thread; more costs
+// registers the exchange code needs)
+constexpr int kFoldStep = GMMB_FOLD_STEP;
 constexpr int kCompWarps = kSeedWarps - 1;
 constexpr int kCompThreads = kCompWarps * 32;
 constexpr int kSlotWords = 8;  // approx: a1 i1 a2 b1 j1 b2 d2lo d2hi; exact: clock lo hi, idx, pad
@@ -412,10 +422,55 @@ __host__ __device__ constexpr size_t point_state_bytes(int ppt) {
   return static_cast<size_t>(ppt) * kCompThreads * (4 * 8 + 8 + 8 + 8 * 4 + 4);
 }
 
+
+// Fold two centres into up to P consecutive point slots j0 .. j0 + P - 1 of
+// this thread (sogmm.cpp:229-238, strict < in centre order); returns the
+// slots whose nearest centre changed, with d2 / label / 1/d2 updated.
+template <int P>
+__device__ __forceinline__ unsigned fold_pts(const double* __restrict__ x, double* __restrict__ d2,
+                                             int* __restrict__ lab, float* __restrict__ inv,
+                                             int stride, int ppt, int t, int j0, int cnt,
+                                             const double (&cf)[2][4], int rf) {
+  // branch-free (slot indices clamped to the thread's own slots, results of
+  // the slots >= cnt dropped), so the P points' chains interleave
+  double dj[P];
+  int lb[P];
+#pragma unroll
+  for (int u = 0; u < P; ++u) {
+    const int o = min(j0 + u, ppt - 1) * kCompThreads + t;
+    const double x0 = x[o], x1 = x[o + stride], x2 = x[o + 2 * stride], x3 = x[o + 3 * stride];
+    const double d = d2[o];
+    const double e0 = dist2(x0, x1, x2, x3, cf[0]);
+    const double e1 = dist2(x0, x1, x2, x3, cf[1]);
+    const bool c0 = e0 < d;
+    const double m0 = c0 ? e0 : d;
+    const bool c1 = e1 < m0;
+    dj[u] = c1 ? e1 : m0;
+    lb[u] = u >= cnt ? -1 : c1 ? rf + 1 : c0 ? rf : -1;
+  }
+  unsigned cm = 0;
+#pragma unroll
+  for (int u = 0; u < P; ++u) {
+    if (lb[u] >= 0) {
+      const int o = (j0 + u) * kCompThreads + t;
+      d2[o] = dj[u];
+      lab[o] = lb[u];
+      // d2 == 0 (a chosen point or a duplicate) is ineligible (:254)
+      const float fl = __double2float_rn(dj[u]);
+      inv[o] = dj[u] > 0.0 ? (isinf(fl) ? 1e-38f : rcp_approx(fl)) : 0.f;
+      cm |= 1u << (j0 + u);
+    }
+  }
+  return cm;
+}
+
 __global__ void __launch_bounds__(kSeedThreads, 1)
     kpp_seed_kernel(const double* __restrict__ x64, int64_t n, int k,
                     uint64_t seed, KinitScratch scr, int ppt) {
   __shared__ SeedSmem sm;
+#ifdef GMMB_KPP_PROF
+  __shared__ long long prof_s[kProfEpochs][kProfSlots];
+#endif
   extern __shared__ __align__(16) unsigned char pstate_raw[];
   const int PPT = ppt;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -495,7 +550,7 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
     uint2* slot_a = llw + par * nblk * kSlotWords;
     uint2* slot_e = llw + (2 + par) * nblk * kSlotWords;
     const bool lvl1 = r > 0 && r + 1 < k;  // round r + 1 can be speculated
-    if (tid == 0) KPROF(0, clock64());
+    if (tid == 0) KPROF(0);
     if (!comm) {
       float* acur = ps.ac;
       // ---- fold the new centres (sogmm.cpp:229-238) ----
@@ -504,28 +559,14 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
       double bd = 0.0;
       if (pre_ok && r < k) {
         unsigned cm = 0;  // points whose nearest centre changed
-#pragma unroll kPtUnroll
-        for (int j = 0; j < PPT; ++j) {
-          if (!((wvalid >> j) & 1)) continue;
-          double dj = PS(d2, j);
-          const double x0 = PX(j, 0), x1 = PX(j, 1), x2 = PX(j, 2), x3 = PX(j, 3);
-          int lb = -1;
-          for (int f = 0; f < nf; ++f) {
-            const double dd = dist2(x0, x1, x2, x3, cf[f]);
-            if (dd < dj) {
-              dj = dd;
-              lb = rf + f;
-            }
-          }
-          if (lb >= 0) {
-            PS(d2, j) = dj;
-            PS(lab, j) = lb;
-            // d2 == 0 (a chosen point or a duplicate) is ineligible (:254)
-            const float fl = __double2float_rn(dj);
-            PS(inv, j) = dj > 0.0 ? (isinf(fl) ? 1e-38f : rcp_approx(fl)) : 0.f;
-            cm |= 1u << j;
-          }
-        }
+        // (a precomputed epoch follows a hit: two centres to fold) four
+        // points per step, all loads first and the rare stores last, so that
+        // eight independent FP64 chains overlap
+        const int nw = __popc(wvalid);  // valid slots are a prefix
+#pragma unroll 1
+        for (int j0 = 0; j0 < nw; j0 += kFoldStep)
+          cm |= fold_pts<kFoldStep>(ps.x, ps.d2, ps.lab, ps.inv, P1, PPT, t, j0, nw - j0, cf, rf);
+        if (tid == 0) KPROF(1);
         if (__any_sync(0xffffffffu, cm != 0)) {
           // ---- recompute the changed points' clocks, the thread and warp top-2s ----
 #pragma unroll 1
@@ -580,7 +621,7 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
         if (r >= k) break;
         warp_top2s(a1, i1, a2, b1, j1, b2, bd);
       }
-      if (tid == 0) KPROF(1, clock64());
+      if (tid == 0) KPROF(2);
       if (lane == 0) {
         sm.wa1[warp] = a1; sm.wi1[warp] = i1; sm.wa2[warp] = a2;
         sm.wb1[warp] = b1; sm.wj1[warp] = j1; sm.wb2[warp] = b2; sm.wd2[warp] = bd;
@@ -589,7 +630,6 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
       break;
     }
     __syncthreads();
-    if (comm && lane == 0) KPROF(2, clock64());
     if (comm) {
       // ---- CTA top-2s -> one LL slot of 8-byte (payload, tag) words ----
       const bool w = lane < kCompWarps;
@@ -607,10 +647,7 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
                          : lane == 6 ? static_cast<unsigned>(db) : static_cast<unsigned>(db >> 32);
         st_ll(slot_a + blockIdx.x * kSlotWords + lane, v, tag);
       }
-      if (lane == 0) {
-        KPROF(3, clock64());
-        KPROF(9, gtime());
-      }
+      if (lane == 0) KPROF(5);
       // ---- grid top-2s: every CTA gathers every slot (a lane's slots
       // polled concurrently), reduces in a fixed order ----
       float g1 = INFINITY, g2 = INFINITY, h1 = INFINITY, h2 = INFINITY;
@@ -625,10 +662,11 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
         while (pend) {
           unsigned v[kQ][8];
           bool ok[kQ];
+          const unsigned seen = pend;
 #pragma unroll
           for (int q = 0; q < kQ; ++q) {
             ok[q] = false;
-            if ((pend >> q) & 1) {
+            if ((seen >> q) & 1) {
               const uint2* wp = slot_a + (base + lane + 32 * q) * kSlotWords;
               bool good = true;
 #pragma unroll
@@ -659,7 +697,9 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
           }
         }
       }
+      if (lane == 0) KPROF(6);
       warp_top2s(g1, gi, g2, h1, hj, h2, hd);
+      if (lane == 0) KPROF(6);
       // level 0: exact unless the runner-up lies within the FP32 error band
       const bool need_exact = gi >= 0 && !(g2 > g1 * kBand);
       const long long wi = need_exact ? -2 : gi;
@@ -686,7 +726,7 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
         sm.win[0] = wi;
         sm.win[1] = si;
         sm.thr = need_exact ? g1 * kBand : -1.f;
-        KPROF(5, clock64());
+        KPROF(7);
       }
     } else {
       // ---- overlaps the exchange: draws of rounds r + 2, r + 3 and, for the
@@ -725,10 +765,9 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
           sm.pb1[warp] = b1; sm.pj1[warp] = j1; sm.pb2[warp] = b2; sm.pd2[warp] = bd;
         }
       }
-      if (tid == 0) KPROF(6, clock64());
+      if (tid == 0) KPROF(3);
     }
     __syncthreads();
-    if (tid == 0) KPROF(7, clock64());
     if (sm.win[0] == -2) {
       // ---- exact resolution among the points inside the band (rare) ----
       if (!comm) {
@@ -844,6 +883,7 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
       cf[0][q] = sm.cx[0][q];
       cf[1][q] = sm.cx[1][q];
     }
+
     if (!comm) {
       if (w0 % G == g0) chosen |= 1u << static_cast<int>(w0 / G);
       if (w1 >= 0 && w1 % G == g0) chosen |= 1u << static_cast<int>(w1 / G);
@@ -867,11 +907,17 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
       }
       pre_ok = w1 >= 0;
     }
-    if (tid == 0) KPROF(8, clock64());
+    if (tid == 0) KPROF(4);
     r += nf;
     // sm.win / sm.cx are rewritten by warp 0 only after the next epoch's
     // first barrier, which every thread reaches after these reads
   }
+#ifdef GMMB_KPP_PROF
+  __syncthreads();
+  if (blockIdx.x < 160)
+    for (int i = tid; i < kProfEpochs * kProfSlots; i += blockDim.x)
+      g_kpp_prof[blockIdx.x * kProfEpochs * kProfSlots + i] = (&prof_s[0][0])[i];
+#endif
   // labels + owned counts (every point's final nearest centre)
   if (!comm) {
 #pragma unroll 1
