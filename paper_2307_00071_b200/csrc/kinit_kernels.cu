@@ -697,7 +697,6 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
           }
         }
       }
-      if (lane == 0) KPROF(6);
       warp_top2s(g1, gi, g2, h1, hj, h2, hd);
       if (lane == 0) KPROF(6);
       // level 0: exact unless the runner-up lies within the FP32 error band
