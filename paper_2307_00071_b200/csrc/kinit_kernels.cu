@@ -568,23 +568,23 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
           cm |= fold_pts<kFoldStep>(ps.x, ps.d2, ps.lab, ps.inv, P1, PPT, t, j0, nw - j0, cf, rf);
         if (tid == 0) KPROF(1);
         if (__any_sync(0xffffffffu, cm != 0)) {
-          // ---- recompute the changed points' clocks, the thread and warp top-2s ----
-#pragma unroll 1
-          for (int j = 0; j < PPT; ++j) {
-            if (!((valid >> j) & 1)) continue;
+          // ---- recompute the changed points' clocks (rare: stores first, so
+          // that the merge pass below is load-only and pipelines), then the
+          // thread and warp top-2s ----
+          for (unsigned cv = cm & valid; cv; cv &= cv - 1) {
+            const int j = __ffs(cv) - 1;
+            const float ivj = PS(inv, j);
+            PF(acur, j) = ivj > 0.f ? PF(ps.e0, j) * ivj : INFINITY;
+            PF(ps.b, j) = (lvl1 && ivj > 0.f) ? PF(ps.e1, j) * ivj : INFINITY;
+          }
+          const int nv = __popc(valid);  // valid slots are a prefix
+#pragma unroll 2
+          for (int j = 0; j < nv; ++j) {
             const int ij = static_cast<int>(g0 + j * G);
-            float aj, bj;
-            if ((cm >> j) & 1) {
-              const float ivj = PS(inv, j);
-              aj = ivj > 0.f ? PF(ps.e0, j) * ivj : INFINITY;
-              bj = (lvl1 && ivj > 0.f) ? PF(ps.e1, j) * ivj : INFINITY;
-              PF(acur, j) = aj;
-            } else {
-              aj = PF(acur, j);
-              bj = PF(ps.b, j);
-            }
+            const float aj = PF(acur, j), bj = PF(ps.b, j);
+            const double dj = PS(d2, j);
             if (aj < INFINITY) merge_top2(a1, i1, a2, aj, ij, INFINITY);
-            if (bj < INFINITY) merge_top2d(b1, j1, b2, bd, bj, ij, INFINITY, PS(d2, j));
+            if (bj < INFINITY) merge_top2d(b1, j1, b2, bd, bj, ij, INFINITY, dj);
           }
           warp_top2s(a1, i1, a2, b1, j1, b2, bd);
         } else {
