@@ -1296,6 +1296,12 @@ __global__ void __launch_bounds__(128) em_reduce_finalize_kernel(
 
 // ---------------------------------------------------------------------------
 // Commit (single CTA of 1024 threads): sogmm.cpp:418-453 + :488-504.
+// The kernel is a chain of dependent memory round trips, so it issues every
+// independent load first (state, ll partials, the components' keep flags,
+// counts and log-dets), scans the keep flags chunk by chunk in component
+// order (component k = chunk * T + tid, order-preserving compaction), and
+// copies the kept records with 16-byte vector accesses (coalesced: thread j
+// writes compacted component j).
 // ---------------------------------------------------------------------------
 template <int D>
 __device__ __forceinline__ void commit_body(
@@ -1303,30 +1309,47 @@ __device__ __forceinline__ void commit_body(
     const double* __restrict__ ll_part, int ncl,
     const ModelBuf& b0, const ModelBuf& b1, EmState* st, double* __restrict__ ll_trace) {
   constexpr int T = 1024;
-  constexpr int PER = kMaxK / T;  // components per thread (<= 4)
+  constexpr int CH = kMaxK / T;  // chunks of T components (<= 4)
   __shared__ int s_wcnt[32];
   __shared__ double s_wtot[32];
   __shared__ int s_woff[32];
-  __shared__ int s_knew;
-  __shared__ double s_total;
+  __shared__ int s_base[CH + 1];
+  __shared__ double s_ctot[CH];
   __shared__ int s_flag;
+  __shared__ short s_map[kMaxK];  // compacted index -> component
   static_assert(T == 1024, "one CTA of 1024 threads");
+  static_assert(kMaxK <= 32767, "short map");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (st->done) return;
-  const int k_in = mode == 0 ? st->k_cur : k_in_arg;
+  // ---- every independent load up front (one round trip) ----
+  const int done0 = st->done;
+  const int kcur0 = st->k_cur;
+  const int kcap = k_in_arg;  // rec holds at least this many records
+  int flg[CH];
+  double cntv[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int k = c * T + tid;
+    flg[c] = k < kcap ? rec.flags[k] : 0;
+    cntv[c] = k < kcap ? rec.count[k] : 0.0;
+  }
+  double llv = 0.0;
+  if (mode == 0 && warp == 0) {
+    if (ll_part) {
+      for (int c = lane; c < ncl; c += 32) llv += ll_part[c];
+    } else if (lane == 0) {
+      llv = red_ll[0];
+    }
+  }
+  if (done0) return;
+  const int k_in = mode == 0 ? kcur0 : k_in_arg;
 
   if (mode == 0) {
     // log-likelihood: the per-CTA partials of the fused E kernel in a fixed
     // order (lane-strided sums, then a fixed butterfly), or a reduced value
-    double ll = 0.0;
-    if (warp == 0) {
-      if (ll_part) {
-        for (int c = lane; c < ncl; c += 32) ll += ll_part[c];
+    double ll = llv;
+    if (warp == 0 && ll_part) {
 #pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) ll += __shfl_xor_sync(0xffffffffu, ll, off);
-      } else {
-        ll = red_ll[0];
-      }
+      for (int off = 16; off >= 1; off >>= 1) ll += __shfl_xor_sync(0xffffffffu, ll, off);
     }
     // EM bookkeeping: sogmm.cpp:490-498
     if (tid == 0) {
@@ -1351,52 +1374,64 @@ __device__ __forceinline__ void commit_body(
     if (s_flag) return;
   }
 
-  // keep flags -> exclusive scan (compaction preserves order, sogmm.cpp:418-429):
-  // warp scans + one warp over the 32 warp totals; total kept count with a
-  // fixed-shape reduction (deterministic). A thread owns `per` consecutive
-  // components (1 up to K = T, so small K spreads over all threads).
-  const int per = (k_in + T - 1) / T;
-  int keep[PER];
-  int cnt = 0;
-  double tot = 0.0;
+  // keep flags -> per-chunk exclusive scans (compaction preserves component
+  // order, sogmm.cpp:418-429); chunk totals and kept counts with fixed-shape
+  // reductions (deterministic)
+  int keep[CH], excl[CH];
+  const int nch = (k_in + T - 1) / T;
 #pragma unroll
-  for (int i = 0; i < PER; ++i) {
-    const int k = tid * per + i;
-    keep[i] = (i < per && k < k_in) ? (rec.flags[k] & 1) : 0;
-    cnt += keep[i];
-    if (keep[i]) tot += rec.count[k];
-  }
-  int incl = cnt;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, off);
-    if (lane >= off) incl += v;
-  }
-  double wt = tot;
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) wt += __shfl_xor_sync(0xffffffffu, wt, off);
-  if (lane == 31) s_wcnt[warp] = incl;
-  if (lane == 0) s_wtot[warp] = wt;
-  __syncthreads();
-  if (warp == 0) {
-    const int wc = s_wcnt[lane];
-    int wi = wc;
+  for (int c = 0; c < CH; ++c) {
+    const int k = c * T + tid;
+    keep[c] = (c < nch && k < k_in) ? (flg[c] & 1) : 0;
+    int incl = keep[c];
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, wi, off);
-      if (lane >= off) wi += v;
+      const int v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += v;
     }
-    s_woff[lane] = wi - wc;
-    double t = s_wtot[lane];
+    double wt = keep[c] ? cntv[c] : 0.0;
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
-    if (lane == 31) s_knew = wi;
-    if (lane == 0) s_total = t;
+    for (int off = 16; off >= 1; off >>= 1) wt += __shfl_xor_sync(0xffffffffu, wt, off);
+    if (c < nch) {
+      if (lane == 31) s_wcnt[warp] = incl;
+      if (lane == 0) s_wtot[warp] = wt;
+    }
+    __syncthreads();
+    if (c < nch && warp == 0) {
+      const int wc = s_wcnt[lane];
+      int wi = wc;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, wi, off);
+        if (lane >= off) wi += v;
+      }
+      s_woff[lane] = wi - wc;
+      double t = s_wtot[lane];
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+      if (lane == 31) s_base[c + 1] = wi;  // kept in this chunk
+      if (lane == 0) s_ctot[c] = t;
+    }
+    __syncthreads();
+    excl[c] = c < nch ? s_woff[warp] + incl - keep[c] : 0;
+    __syncthreads();  // s_wcnt / s_woff reused by the next chunk
+  }
+  if (tid == 0) {
+    int b = 0;
+    double tot = 0.0;
+    s_base[0] = 0;
+    for (int c = 0; c < nch; ++c) {
+      const int kc = s_base[c + 1];
+      s_base[c + 1] = b + kc;
+      b += kc;
+      tot += s_ctot[c];
+    }
+    s_ctot[0] = tot;
+    s_flag = 0x7fffffff;
   }
   __syncthreads();
-  const int excl = s_woff[warp] + incl - cnt;
-  const int k_new = s_knew;
-  const double total = s_total;
+  const int k_new = s_base[nch];
+  const double total = s_ctot[0];
   if (k_new == 0) {
     if (tid == 0) {
       st->error = 3;
@@ -1406,16 +1441,14 @@ __device__ __forceinline__ void commit_body(
     }
     return;
   }
-  // first non-SPD kept component (compacted index), sogmm.cpp:447-452
-  if (tid == 0) s_flag = 0x7fffffff;
-  __syncthreads();
-  int j = excl;
+  // first non-SPD kept component (compacted index), sogmm.cpp:447-452; the
+  // compaction map
 #pragma unroll
-  for (int i = 0; i < PER; ++i) {
-    const int k = tid * per + i;
-    if (keep[i]) {
-      if (!(rec.flags[k] & 2)) atomicMin(&s_flag, j);
-      ++j;
+  for (int c = 0; c < CH; ++c) {
+    if (keep[c]) {
+      const int j = s_base[c] + excl[c];
+      s_map[j] = static_cast<short>(c * T + tid);
+      if (!(flg[c] & 2)) atomicMin(&s_flag, j);
     }
   }
   __syncthreads();
@@ -1431,25 +1464,28 @@ __device__ __forceinline__ void commit_body(
   const int dst_sel = mode == 0 ? (st->cur ^ 1) : st->cur;
   const ModelBuf& dst = dst_sel ? b1 : b0;
   const double half_d_ln2pi = 0.5 * D * kLog2Pi;
-  j = excl;
-#pragma unroll
-  for (int i = 0; i < PER; ++i) {
-    const int k = tid * per + i;
-    if (!keep[i]) continue;
+  for (int j = tid; j < k_new; j += T) {
+    const int k = s_map[j];
     const double w = rec.count[k] / total;
     dst.w[j] = w;
+    const double2* sm2 = reinterpret_cast<const double2*>(rec.mean + k * 4);
+    double2* dm2 = reinterpret_cast<double2*>(dst.mu + j * 4);
+    dm2[0] = sm2[0];
+    dm2[1] = sm2[1];
+    const double2* sc2 = reinterpret_cast<const double2*>(rec.cov + k * 10);
+    double2* dc2 = reinterpret_cast<double2*>(dst.cov + j * 10);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) dst.mu[j * 4 + q] = rec.mean[k * 4 + q];
-#pragma unroll
-    for (int q = 0; q < 10; ++q) dst.cov[j * 10 + q] = rec.cov[k * 10 + q];
-    CompConst c;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) c.p[q] = rec.pc[k * 16 + q];
+    for (int q = 0; q < 5; ++q) dc2[q] = sc2[q];
+    const float4* sp4 = reinterpret_cast<const float4*>(rec.pc + k * 16);
+    float4* dp4 = reinterpret_cast<float4*>(&dst.cst[j]);
+    float4 v2 = sp4[2];
     const double b2 = kLog2E * (log(w) + rec.logdet[k] - half_d_ln2pi);
-    c.p[10] = static_cast<float>(b2);
-    c.p[11] = static_cast<float>(b2 - static_cast<double>(c.p[10]));
-    dst.cst[j] = c;
-    ++j;
+    v2.z = static_cast<float>(b2);                          // c.p[10]
+    v2.w = static_cast<float>(b2 - static_cast<double>(v2.z));  // c.p[11]
+    dp4[0] = sp4[0];
+    dp4[1] = sp4[1];
+    dp4[2] = v2;
+    dp4[3] = sp4[3];
   }
   __syncthreads();
   if (tid == 0) {
