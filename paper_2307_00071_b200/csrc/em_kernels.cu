@@ -1211,8 +1211,12 @@ __global__ void em_reduce_kernel(const double* __restrict__ partials,
 // Finalize one component from its reduced statistics s[NS] (centred at the
 // old mean): mean, covariance + cov_reg, FP64 Cholesky / precision factor.
 template <int D>
+// The mean, covariance and precision factor go straight into the fresh model
+// buffer (the one the commit makes current) at index k; the commit then only
+// adds weights and log-normalisers, or compacts when components are dropped.
 __device__ __forceinline__ void finalize_component(const double* s, int k, const ModelBuf& mb,
-                                                   double cov_reg, RecBuf& rec) {
+                                                   double cov_reg, RecBuf& rec,
+                                                   const ModelBuf& fresh) {
   constexpr int NP = npacked(D);
   const double cnt = s[0];
   int flags = 0;
@@ -1242,13 +1246,16 @@ __device__ __forceinline__ void finalize_component(const double* s, int k, const
     if (factor_component<D>(cov, pc, &logdet)) flags |= 2;
   }
   rec.count[k] = cnt;
+  double2* dm = reinterpret_cast<double2*>(fresh.mu + k * 4);
+  dm[0] = make_double2(mean[0], mean[1]);
+  dm[1] = make_double2(mean[2], mean[3]);
+  double2* dc = reinterpret_cast<double2*>(fresh.cov + k * 10);
 #pragma unroll
-  for (int j = 0; j < 4; ++j) rec.mean[k * 4 + j] = mean[j];
-#pragma unroll
-  for (int j = 0; j < 10; ++j) rec.cov[k * 10 + j] = cov[j];
+  for (int j = 0; j < 5; ++j) dc[j] = make_double2(cov[2 * j], cov[2 * j + 1]);
   rec.logdet[k] = logdet;
+  float4* dp = reinterpret_cast<float4*>(&fresh.cst[k]);
 #pragma unroll
-  for (int j = 0; j < 16; ++j) rec.pc[k * 16 + j] = pc[j];
+  for (int j = 0; j < 4; ++j) dp[j] = make_float4(pc[4 * j], pc[4 * j + 1], pc[4 * j + 2], pc[4 * j + 3]);
   rec.flags[k] = flags;
 }
 
@@ -1260,7 +1267,8 @@ __global__ void em_finalize_kernel(const double* __restrict__ red,
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= st->k_cur) return;
   const ModelBuf& mb = st->cur ? b1 : b0;
-  finalize_component<D>(red + static_cast<int64_t>(k) * nstats(D), k, mb, st->cov_reg, rec);
+  const ModelBuf& fresh = st->cur ? b0 : b1;
+  finalize_component<D>(red + static_cast<int64_t>(k) * nstats(D), k, mb, st->cov_reg, rec, fresh);
 }
 
 // Single-device fused second stage: one warp per component reduces the
@@ -1290,7 +1298,8 @@ __global__ void __launch_bounds__(128) em_reduce_finalize_kernel(
   }
   if (lane == 0) {
     const ModelBuf& mb = st->cur ? b1 : b0;
-    finalize_component<D>(acc, k, mb, st->cov_reg, rec);
+    const ModelBuf& fresh = st->cur ? b0 : b1;
+    finalize_component<D>(acc, k, mb, st->cov_reg, rec, fresh);
   }
 }
 
@@ -1461,31 +1470,53 @@ __device__ __forceinline__ void commit_body(
     }
     return;
   }
-  const int dst_sel = mode == 0 ? (st->cur ^ 1) : st->cur;
-  const ModelBuf& dst = dst_sel ? b1 : b0;
   const double half_d_ln2pi = 0.5 * D * kLog2Pi;
-  for (int j = tid; j < k_new; j += T) {
-    const int k = s_map[j];
-    const double w = rec.count[k] / total;
-    dst.w[j] = w;
-    const double2* sm2 = reinterpret_cast<const double2*>(rec.mean + k * 4);
-    double2* dm2 = reinterpret_cast<double2*>(dst.mu + j * 4);
-    dm2[0] = sm2[0];
-    dm2[1] = sm2[1];
-    const double2* sc2 = reinterpret_cast<const double2*>(rec.cov + k * 10);
-    double2* dc2 = reinterpret_cast<double2*>(dst.cov + j * 10);
+  int dst_sel;
+  if (mode == 0 && k_new == k_in) {
+    // nothing dropped (the common case): the finalize already wrote means,
+    // covariances and factors into the fresh buffer in place; add the
+    // weights and log-normalisers
+    dst_sel = st->cur ^ 1;
+    const ModelBuf& dst = dst_sel ? b1 : b0;
+    for (int k = tid; k < k_new; k += T) {
+      const double w = rec.count[k] / total;
+      dst.w[k] = w;
+      const double b2 = kLog2E * (log(w) + rec.logdet[k] - half_d_ln2pi);
+      const float hi = static_cast<float>(b2);
+      *reinterpret_cast<float2*>(&dst.cst[k].p[10]) =
+          make_float2(hi, static_cast<float>(b2 - static_cast<double>(hi)));
+    }
+  } else {
+    // compaction: mode 0 from the fresh buffer (written by the finalize) into
+    // the other one (the previous model, consumed by now); mode 1 from the
+    // record buffers into the current one
+    dst_sel = st->cur;
+    const ModelBuf& dst = dst_sel ? b1 : b0;
+    const ModelBuf& src_m = st->cur ? b0 : b1;
+    for (int j = tid; j < k_new; j += T) {
+      const int k = s_map[j];
+      const double w = rec.count[k] / total;
+      dst.w[j] = w;
+      const double2* sm2 = reinterpret_cast<const double2*>(mode == 0 ? src_m.mu + k * 4 : rec.mean + k * 4);
+      double2* dm2 = reinterpret_cast<double2*>(dst.mu + j * 4);
+      dm2[0] = sm2[0];
+      dm2[1] = sm2[1];
+      const double2* sc2 = reinterpret_cast<const double2*>(mode == 0 ? src_m.cov + k * 10 : rec.cov + k * 10);
+      double2* dc2 = reinterpret_cast<double2*>(dst.cov + j * 10);
 #pragma unroll
-    for (int q = 0; q < 5; ++q) dc2[q] = sc2[q];
-    const float4* sp4 = reinterpret_cast<const float4*>(rec.pc + k * 16);
-    float4* dp4 = reinterpret_cast<float4*>(&dst.cst[j]);
-    float4 v2 = sp4[2];
-    const double b2 = kLog2E * (log(w) + rec.logdet[k] - half_d_ln2pi);
-    v2.z = static_cast<float>(b2);                          // c.p[10]
-    v2.w = static_cast<float>(b2 - static_cast<double>(v2.z));  // c.p[11]
-    dp4[0] = sp4[0];
-    dp4[1] = sp4[1];
-    dp4[2] = v2;
-    dp4[3] = sp4[3];
+      for (int q = 0; q < 5; ++q) dc2[q] = sc2[q];
+      const float4* sp4 = mode == 0 ? reinterpret_cast<const float4*>(&src_m.cst[k])
+                                    : reinterpret_cast<const float4*>(rec.pc + k * 16);
+      float4* dp4 = reinterpret_cast<float4*>(&dst.cst[j]);
+      float4 v2 = sp4[2];
+      const double b2 = kLog2E * (log(w) + rec.logdet[k] - half_d_ln2pi);
+      v2.z = static_cast<float>(b2);                              // c.p[10]
+      v2.w = static_cast<float>(b2 - static_cast<double>(v2.z));  // c.p[11]
+      dp4[0] = sp4[0];
+      dp4[1] = sp4[1];
+      dp4[2] = v2;
+      dp4[3] = sp4[3];
+    }
   }
   __syncthreads();
   if (tid == 0) {
