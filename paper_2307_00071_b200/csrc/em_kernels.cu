@@ -1231,12 +1231,12 @@ __device__ __forceinline__ void finalize_component(const double* s, int k, const
   if (!(cnt < kDegenerateCount)) {
     flags |= 1;
     double delta[D];
+    const double inv = 1.0 / cnt;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      delta[j] = s[1 + j] / cnt;
+      delta[j] = s[1 + j] * inv;
       mean[j] = mb.mu[k * 4 + j] + delta[j];
     }
-    const double inv = 1.0 / cnt;
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
       const int i = packed_row(q), j = packed_col(q);
