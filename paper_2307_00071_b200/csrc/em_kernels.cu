@@ -1332,6 +1332,18 @@ __device__ __forceinline__ void commit_body(
   // ---- every independent load up front (one round trip) ----
   const int done0 = st->done;
   const int kcur0 = st->k_cur;
+  const int cur0 = st->cur;
+  int iter0 = 0, maxit0 = 0, removed0 = 0;
+  double units0 = 0.0, npts0 = 0.0, llprev0 = 0.0, tol0 = 0.0;
+  if (tid == 0) {  // the rest of the state thread 0 needs
+    iter0 = st->iter;
+    maxit0 = st->max_iters;
+    removed0 = st->removed;
+    units0 = st->units;
+    npts0 = st->npts;
+    llprev0 = st->ll_prev;
+    tol0 = st->tol;
+  }
   const int kcap = k_in_arg;  // rec holds at least this many records
   int flg[CH];
   double cntv[CH];
@@ -1362,15 +1374,15 @@ __device__ __forceinline__ void commit_body(
     }
     // EM bookkeeping: sogmm.cpp:490-498
     if (tid == 0) {
-      const int iter = st->iter;
-      st->units += st->npts * static_cast<double>(k_in);
+      const int iter = iter0;
+      st->units = units0 + npts0 * static_cast<double>(k_in);
       if (ll_trace) ll_trace[iter] = ll;
       st->ll = ll;
       st->iter = iter + 1;
       int conv = 0;
       if (iter > 0) {
-        const double rel = fabs(ll - st->ll_prev) / fmax(fabs(st->ll_prev), 1e-12);
-        if (rel < st->tol) conv = 1;
+        const double rel = fabs(ll - llprev0) / fmax(fabs(llprev0), 1e-12);
+        if (rel < tol0) conv = 1;
       }
       if (conv) {
         st->converged = 1;
@@ -1389,7 +1401,10 @@ __device__ __forceinline__ void commit_body(
   int keep[CH], excl[CH];
   const int nch = (k_in + T - 1) / T;
 #pragma unroll
+  for (int c = 0; c < CH; ++c) keep[c] = excl[c] = 0;
+#pragma unroll
   for (int c = 0; c < CH; ++c) {
+    if (c >= nch) break;  // uniform: only the chunks that hold components
     const int k = c * T + tid;
     keep[c] = (c < nch && k < k_in) ? (flg[c] & 1) : 0;
     int incl = keep[c];
@@ -1476,7 +1491,7 @@ __device__ __forceinline__ void commit_body(
     // nothing dropped (the common case): the finalize already wrote means,
     // covariances and factors into the fresh buffer in place; add the
     // weights and log-normalisers
-    dst_sel = st->cur ^ 1;
+    dst_sel = cur0 ^ 1;
     const ModelBuf& dst = dst_sel ? b1 : b0;
     for (int k = tid; k < k_new; k += T) {
       const double w = rec.count[k] / total;
@@ -1490,9 +1505,9 @@ __device__ __forceinline__ void commit_body(
     // compaction: mode 0 from the fresh buffer (written by the finalize) into
     // the other one (the previous model, consumed by now); mode 1 from the
     // record buffers into the current one
-    dst_sel = st->cur;
+    dst_sel = cur0;
     const ModelBuf& dst = dst_sel ? b1 : b0;
-    const ModelBuf& src_m = st->cur ? b0 : b1;
+    const ModelBuf& src_m = cur0 ? b0 : b1;
     for (int j = tid; j < k_new; j += T) {
       const int k = s_map[j];
       const double w = rec.count[k] / total;
@@ -1520,11 +1535,11 @@ __device__ __forceinline__ void commit_body(
   }
   __syncthreads();
   if (tid == 0) {
-    st->removed += k_in - k_new;
+    st->removed = removed0 + (k_in - k_new);
     st->k_cur = k_new;
     if (mode == 0) {
       st->cur = dst_sel;
-      if (st->iter >= st->max_iters) st->done = 1;
+      if (iter0 + 1 >= maxit0) st->done = 1;
     }
   }
 }
