@@ -306,6 +306,9 @@ __device__ __forceinline__ long long pclock() {
 #endif
 // points per iteration of the per-point loops (independent FP64 / hash chains)
 constexpr int kPtUnroll = GMMB_KPP_UNROLL;
+#ifndef GMMB_KPP_MAXDEPTH
+#define GMMB_KPP_MAXDEPTH 2  // rounds decided per grid exchange (2 or 3; 3 measured no faster)
+#endif
 #ifndef GMMB_FOLD_STEP
 #define GMMB_FOLD_STEP 2
 #endif
@@ -314,30 +317,35 @@ constexpr int kPtUnroll = GMMB_KPP_UNROLL;
 constexpr int kFoldStep = GMMB_FOLD_STEP;
 constexpr int kCompWarps = kSeedWarps - 1;
 constexpr int kCompThreads = kCompWarps * 32;
-constexpr int kSlotWords = 8;  // approx: a1 i1 a2 b1 j1 b2 d2lo d2hi; exact: clock lo hi, idx, pad
+// LL slot of a CTA per epoch (uint2 words, 4-byte payload + tag each):
+// per level l: best clock, its index, runner-up clock; levels >= 1 add the
+// best's FP64 d2 (2 words). Padded to an even count (16-byte loads).
+template <int L>
+struct SlotLayout {
+  static constexpr int kWords = 3 + 5 * (L - 1) + ((3 + 5 * (L - 1)) & 1);
+  static constexpr int base(int l) { return l == 0 ? 0 : 3 + 5 * (l - 1); }
+};
+constexpr int kSlotStride = 14;  // uint2 words reserved per CTA slot (>= kWords for L <= 3)
+constexpr int kExactWords = 4;   // exact-resolution slot: clock lo hi, idx, pad
 
+template <int L>
 struct SeedSmem {
-  float wa1[kSeedWarps];
-  int wi1[kSeedWarps];
-  float wa2[kSeedWarps];
-  float wb1[kSeedWarps];
-  int wj1[kSeedWarps];
-  float wb2[kSeedWarps];
-  double wd2[kSeedWarps];
-  // per-warp top-2s precomputed for the next epoch (valid if no point of the
-  // warp changes its nearest centre in the fold)
-  float pa1[kSeedWarps];
-  int pi1[kSeedWarps];
-  float pa2[kSeedWarps];
-  float pb1[kSeedWarps];
-  int pj1[kSeedWarps];
-  float pb2[kSeedWarps];
-  double pd2[kSeedWarps];
+  // per level, per warp: top-2 of this epoch (w*) and the precomputed ones
+  // for the next epoch (p*, valid if no point of the warp changes its
+  // nearest centre in the fold)
+  float w1[L][kSeedWarps];
+  int wi[L][kSeedWarps];
+  float w2[L][kSeedWarps];
+  double wd[L][kSeedWarps];
+  float p1[L][kSeedWarps];
+  int pi[L][kSeedWarps];
+  float p2[L][kSeedWarps];
+  double pd[L][kSeedWarps];
   double ec[kSeedWarps];
   long long ei[kSeedWarps];
   long long gu[kSeedWarps];
-  double cx[2][4];
-  long long win[2];  // round r winner; round r + 1 speculative winner (-1: rejected)
+  double cx[L][4];
+  long long win[L];  // round r + l winner (-1: not decided this epoch)
   float thr;
   int exact_rounds;
   int spec_hits;
@@ -367,32 +375,50 @@ __device__ __forceinline__ void prefetch_point(const double* x64, int64_t n, int
 // +inf), so their bit patterns order like the values; the best entry is the
 // (clock, index) minimum, and the runner-up is the minimum over lanes of
 // "my second" for the lane(s) holding the best entry, "my best" for the
-// others (equal to merge_top2's pairwise result).
-__device__ __forceinline__ void warp_top2(float& a1, int& i1, float& a2) {
+// others (equal to merge_top2's pairwise result). The payload (d2) of the
+// best entry comes from its holder.
+__device__ __forceinline__ void warp_top2d(float& a1, int& i1, float& a2, double& d) {
   const unsigned u1 = __float_as_uint(a1);
   const unsigned m1 = __reduce_min_sync(0xffffffffu, u1);
   const unsigned mi = __reduce_min_sync(0xffffffffu, u1 == m1 ? static_cast<unsigned>(i1) : ~0u);
-  const unsigned u2 = static_cast<unsigned>(i1) == mi ? __float_as_uint(a2) : u1;
+  const bool holder = static_cast<unsigned>(i1) == mi;
+  const unsigned u2 = holder ? __float_as_uint(a2) : u1;
   a2 = __uint_as_float(__reduce_min_sync(0xffffffffu, u2));
+  const int src = __ffs(__ballot_sync(0xffffffffu, holder)) - 1;
+  d = __shfl_sync(0xffffffffu, d, src);
   a1 = __uint_as_float(m1);
   i1 = static_cast<int>(mi);
 }
-// warp top-2s of both levels (every lane ends with the warp's result)
-__device__ __forceinline__ void warp_top2s(float& a1, int& i1, float& a2, float& b1, int& j1,
-                                           float& b2, double& bd) {
-  warp_top2(a1, i1, a2);
-  const unsigned u1 = __float_as_uint(b1);
-  const unsigned m1 = __reduce_min_sync(0xffffffffu, u1);
-  const unsigned mj = __reduce_min_sync(0xffffffffu, u1 == m1 ? static_cast<unsigned>(j1) : ~0u);
-  const bool holder = static_cast<unsigned>(j1) == mj;
-  const unsigned u2 = holder ? __float_as_uint(b2) : u1;
-  b2 = __uint_as_float(__reduce_min_sync(0xffffffffu, u2));
-  const int src = __ffs(__ballot_sync(0xffffffffu, holder)) - 1;
-  bd = __shfl_sync(0xffffffffu, bd, src);
-  b1 = __uint_as_float(m1);
-  j1 = static_cast<int>(mj);
+template <int L>
+__device__ __forceinline__ void warp_top2_levels(float (&v1)[L], int (&vi)[L], float (&v2)[L],
+                                                 double (&vd)[L]) {
+#pragma unroll
+  for (int l = 0; l < L; ++l) warp_top2d(v1[l], vi[l], v2[l], vd[l]);
 }
 
+// Each compute thread keeps PPT points (stride = grid compute threads) in
+// shared memory. The last warp of every CTA holds no points: it is the
+// communication warp. The rounds run L at a time, speculatively ("epochs"):
+//   compute warps: fold the centres decided in the previous epoch into d2 /
+//     labels (in centre order, strict <), then for round r + l the FP32
+//     clocks -ln(u_{r+l}) / d2, all with the same (pre-c_r) d2; a warp top-2
+//     of each level (levels >= 1 carry the best's FP64 d2) -> shared memory;
+//     barrier;
+//   comm warp: CTA top-2s -> one LL slot; every comm warp gathers every slot,
+//     reduces in a fixed order and decides: c_r is the level-0 winner (exact
+//     unless the runner-up lies within the FP32 error band, then the exact
+//     FP64 resolution below), and the level-l winner s is round r + l's
+//     centre iff every lower level was decided, its clock is out of band,
+//     and none of the centres decided before it changes its d2 (exact FP64
+//     tests): every other point's true clock can only be larger than its
+//     speculative one, d2 only shrinks. Otherwise round r + l runs in the
+//     next epoch (on cfg2 the two-level speculation holds in 99.4 % of the
+//     rounds);
+//   compute warps meanwhile draw -ln(u) of the next epoch's L rounds (and
+//     precompute their clocks, see PointState); barrier.
+// The exact resolution (round-0 key duplicates, near-ties): every point
+// inside the band gets the exact FP64 clock and a second exchange decides on
+// (clock, index), as the reference's strict-< scan does.
 // Per-point state lives in shared memory (SoA by compute thread) and every
 // per-point loop is rolled: the compute warps' executed code stays a few KB,
 // so the communication warp's exchange code is not evicted from the
@@ -401,36 +427,49 @@ __device__ __forceinline__ void warp_top2s(float& a1, int& i1, float& a2, float&
 //
 // Clocks are precomputed off the critical path: while the communication warp
 // runs epoch e's exchange, the compute warps draw -ln(u) of the next epoch's
-// two rounds and already form their clocks and warp top-2s with the current
+// L rounds and already form their clocks and warp top-2s with the current
 // d2. A clock only depends on the point's d2, so after the next fold these
 // values are exact for every point whose nearest centre did not change (the
 // vast majority); the critical path after the exchange shrinks to the FP64
 // fold, plus a recompute from the stored clocks in the few warps where a
-// point changed. (Valid when the speculation held, so that the next epoch's
-// rounds are the ones precomputed; otherwise the epoch computes everything.)
+// point changed. (Valid when every speculative round held, so that the next
+// epoch's rounds are the ones precomputed; otherwise the epoch computes
+// everything.) The draws themselves depend only on the round, so they stay
+// valid whatever the epoch decided: e[] is rotated by the number of rounds
+// decided.
+// The 4-byte arrays are addressed as element offsets from one base (one
+// register each instead of a 64-bit pointer: the kernel runs at the register
+// limit, and spills go to local memory, which the large shared-memory
+// carve-out leaves little L1 for).
+template <int L>
 struct PointState {
   double* x;      // [4][ppt][kCompThreads]
   double* d2;     // [ppt][kCompThreads]
   uint64_t* kp;   // pre-multiplied keys
-  float* inv;
-  float *e0, *e1, *e2, *e3;  // -ln(u) of rounds r, r + 1, r + 2, r + 3 (rotated pointers)
-  float *ac, *an; // level-0 clocks, this epoch / next epoch (swapped)
-  float* b;       // level-1 clocks (next epoch's after the precompute)
-  int* lab;
+  float* fb;      // base of the 4-byte arrays below (offsets in elements)
+  int inv;
+  int e[2 * L];   // -ln(u) of rounds r .. r + 2L - 1 (rotated)
+  int ac, an;     // level-0 clocks, this epoch / next epoch (swapped)
+  int cl[L - 1];  // level-1.. clocks (the next epoch's after the precompute)
+  int lab;        // int array
 };
-__host__ __device__ constexpr size_t point_state_bytes(int ppt) {
-  return static_cast<size_t>(ppt) * kCompThreads * (4 * 8 + 8 + 8 + 8 * 4 + 4);
+__host__ __device__ constexpr size_t point_state_bytes(int ppt, int L) {
+  return static_cast<size_t>(ppt) * kCompThreads * (4 * 8 + 8 + 8 + 4 * (1 + 2 * L + 2 + (L - 1)) + 4);
 }
 
-
-// Fold two centres into up to P consecutive point slots j0 .. j0 + P - 1 of
+// Fold NC centres into up to P consecutive point slots j0 .. j0 + P - 1 of
 // this thread (sogmm.cpp:229-238, strict < in centre order); returns the
 // slots whose nearest centre changed, with d2 / label / 1/d2 updated.
-template <int P>
+template <int P, int NC>
 __device__ __forceinline__ unsigned fold_pts(const double* __restrict__ x, double* __restrict__ d2,
                                              int* __restrict__ lab, float* __restrict__ inv,
                                              int stride, int ppt, int t, int j0, int cnt,
-                                             const double (&cf)[2][4], int rf) {
+                                             const double (*cfs)[4], int rf) {
+  double cf[NC][4];  // the centres, from shared memory (broadcast loads)
+#pragma unroll
+  for (int f = 0; f < NC; ++f)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) cf[f][q] = cfs[f][q];
   // branch-free (slot indices clamped to the thread's own slots, results of
   // the slots >= cnt dropped), so the P points' chains interleave
   double dj[P];
@@ -439,14 +478,17 @@ __device__ __forceinline__ unsigned fold_pts(const double* __restrict__ x, doubl
   for (int u = 0; u < P; ++u) {
     const int o = min(j0 + u, ppt - 1) * kCompThreads + t;
     const double x0 = x[o], x1 = x[o + stride], x2 = x[o + 2 * stride], x3 = x[o + 3 * stride];
-    const double d = d2[o];
-    const double e0 = dist2(x0, x1, x2, x3, cf[0]);
-    const double e1 = dist2(x0, x1, x2, x3, cf[1]);
-    const bool c0 = e0 < d;
-    const double m0 = c0 ? e0 : d;
-    const bool c1 = e1 < m0;
-    dj[u] = c1 ? e1 : m0;
-    lb[u] = u >= cnt ? -1 : c1 ? rf + 1 : c0 ? rf : -1;
+    double m = d2[o];
+    int l = -1;
+#pragma unroll
+    for (int f = 0; f < NC; ++f) {
+      const double e = dist2(x0, x1, x2, x3, cf[f]);
+      const bool c = e < m;
+      m = c ? e : m;
+      l = c ? rf + f : l;
+    }
+    dj[u] = m;
+    lb[u] = u >= cnt ? -1 : l;
   }
   unsigned cm = 0;
 #pragma unroll
@@ -464,10 +506,23 @@ __device__ __forceinline__ unsigned fold_pts(const double* __restrict__ x, doubl
   return cm;
 }
 
+// rotate the 2L draw buffers left by S (S rounds decided this epoch)
+template <int L, int S>
+__device__ __forceinline__ void rotate_draws(int (&e)[2 * L]) {
+  int t[2 * L];
+#pragma unroll
+  for (int i = 0; i < 2 * L; ++i) t[i] = e[(i + S) % (2 * L)];
+#pragma unroll
+  for (int i = 0; i < 2 * L; ++i) e[i] = t[i];
+}
+
+template <int L>
 __global__ void __launch_bounds__(kSeedThreads, 1)
     kpp_seed_kernel(const double* __restrict__ x64, int64_t n, int k,
                     uint64_t seed, KinitScratch scr, int ppt) {
-  __shared__ SeedSmem sm;
+  using SL = SlotLayout<L>;
+  static_assert(SL::kWords <= kSlotStride, "slot stride");
+  __shared__ SeedSmem<L> sm;
 #ifdef GMMB_KPP_PROF
   __shared__ long long prof_s[kProfEpochs][kProfSlots];
 #endif
@@ -483,7 +538,7 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
   // LL regions (uint2 words): approx slots [2][nblk], exact slots [2][nblk]
   uint2* llw = reinterpret_cast<uint2*>(scr.slots);
   const int P1 = PPT * kCompThreads;
-  PointState ps;
+  PointState<L> ps;
   {
     unsigned char* q = pstate_raw;
     ps.x = reinterpret_cast<double*>(q);
@@ -492,21 +547,31 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
     q += sizeof(double) * P1;
     ps.kp = reinterpret_cast<uint64_t*>(q);
     q += sizeof(uint64_t) * P1;
-    float* f = reinterpret_cast<float*>(q);
+    ps.fb = reinterpret_cast<float*>(q);
+    int f = 0;
     ps.inv = f;
-    ps.e0 = f + 1 * P1;
-    ps.e1 = f + 2 * P1;
-    ps.e2 = f + 3 * P1;
-    ps.e3 = f + 4 * P1;
-    ps.ac = f + 5 * P1;
-    ps.an = f + 6 * P1;
-    ps.b = f + 7 * P1;
-    ps.lab = reinterpret_cast<int*>(f + 8 * P1);
+    f += P1;
+#pragma unroll
+    for (int i = 0; i < 2 * L; ++i) {
+      ps.e[i] = f;
+      f += P1;
+    }
+    ps.ac = f;
+    f += P1;
+    ps.an = f;
+    f += P1;
+#pragma unroll
+    for (int l = 0; l < L - 1; ++l) {
+      ps.cl[l] = f;
+      f += P1;
+    }
+    ps.lab = f;
   }
   const int t = comm ? 0 : tid;  // compute-thread index into the SoA state
 #define PX(j, q) ps.x[((q) * PPT + (j)) * kCompThreads + t]
 #define PS(arr, j) ps.arr[(j) * kCompThreads + t]
-#define PF(ptr, j) (ptr)[(j) * kCompThreads + t]
+#define PF(off, j) ps.fb[(off) + (j) * kCompThreads + t]
+#define PL(j) reinterpret_cast<int*>(ps.fb)[ps.lab + (j) * kCompThreads + t]
   unsigned chosen = 0, valid = 0;
   if (!comm) {
 #pragma unroll 1
@@ -517,10 +582,13 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
       for (int q = 0; q < 4; ++q) PX(j, q) = v ? x64[q * n + i] : 0.0;
       PS(kp, j) = v ? scr.keys[i] : 0;
       PS(d2, j) = INFINITY;
-      PS(inv, j) = 0.f;
-      PS(lab, j) = 0;
-      PF(ps.e0, j) = PF(ps.e1, j) = PF(ps.e2, j) = PF(ps.e3, j) = INFINITY;
-      PF(ps.ac, j) = PF(ps.an, j) = PF(ps.b, j) = INFINITY;
+      PF(ps.inv, j) = 0.f;
+      PL(j) = 0;
+#pragma unroll
+      for (int e = 0; e < 2 * L; ++e) PF(ps.e[e], j) = INFINITY;
+      PF(ps.ac, j) = PF(ps.an, j) = INFINITY;
+#pragma unroll
+      for (int l = 0; l < L - 1; ++l) PF(ps.cl[l], j) = INFINITY;
     }
   }
   // slots beyond the warp's last valid point are skipped (warp-uniform)
@@ -530,15 +598,17 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
     sm.spec_hits = 0;
   }
   if (!comm) {
-#pragma unroll 1
-    for (int rr = 0; rr < 2 && rr < k; ++rr) {
+#pragma unroll
+    for (int rr = 0; rr < L; ++rr) {
+      if (rr >= k) break;
       const uint64_t pre = round_prefix(seed, rr);
 #pragma unroll 1
       for (int j = 0; j < PPT; ++j)
-        if ((wvalid >> j) & 1) PF(rr == 0 ? ps.e0 : ps.e1, j) = nlu_approx(mix64(pre + PS(kp, j)));
+        if ((wvalid >> j) & 1) PF(ps.e[rr], j) = nlu_approx(mix64(pre + PS(kp, j)));
     }
   }
-  double cf[2][4];   // centres to fold at the start of the epoch, in order
+  // the centres to fold at the start of an epoch are sm.cx[0 .. nf) (in
+  // order; rewritten by the communication warp only after the next barrier)
   int nf = 0, rf = 0;  // how many, and the round of the first
   unsigned epoch = 0;  // completed counter-based grid exchanges (fallback)
   unsigned xtag = 0;   // LL tag (one per epoch)
@@ -547,25 +617,34 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
   while (true) {
     const unsigned tag = ++xtag;
     const int par = tag & 1;
-    uint2* slot_a = llw + par * nblk * kSlotWords;
-    uint2* slot_e = llw + (2 + par) * nblk * kSlotWords;
-    const bool lvl1 = r > 0 && r + 1 < k;  // round r + 1 can be speculated
+    uint2* slot_a = llw + par * nblk * kSlotStride;
+    uint2* slot_e = llw + (2 + par) * nblk * kSlotStride;
+    bool lvl[L];  // round r + l can be speculated
+#pragma unroll
+    for (int l = 0; l < L; ++l) lvl[l] = l == 0 ? true : (r > 0 && r + l < k);
     if (tid == 0) KPROF(0);
     if (!comm) {
-      float* acur = ps.ac;
+      const int acur = ps.ac;
       // ---- fold the new centres (sogmm.cpp:229-238) ----
-      float a1 = INFINITY, a2 = INFINITY, b1 = INFINITY, b2 = INFINITY;
-      int i1 = -1, j1 = -1;
-      double bd = 0.0;
+      float v1[L], v2[L];
+      int vi[L];
+      double vd[L];
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        v1[l] = v2[l] = INFINITY;
+        vi[l] = -1;
+        vd[l] = 0.0;
+      }
       if (pre_ok && r < k) {
         unsigned cm = 0;  // points whose nearest centre changed
-        // (a precomputed epoch follows a hit: two centres to fold) four
+        // (a precomputed epoch follows a full hit: L centres to fold) a few
         // points per step, all loads first and the rare stores last, so that
-        // eight independent FP64 chains overlap
+        // their FP64 chains overlap
         const int nw = __popc(wvalid);  // valid slots are a prefix
 #pragma unroll 1
         for (int j0 = 0; j0 < nw; j0 += kFoldStep)
-          cm |= fold_pts<kFoldStep>(ps.x, ps.d2, ps.lab, ps.inv, P1, PPT, t, j0, nw - j0, cf, rf);
+          cm |= fold_pts<kFoldStep, L>(ps.x, ps.d2, reinterpret_cast<int*>(ps.fb) + ps.lab,
+                                       ps.fb + ps.inv, P1, PPT, t, j0, nw - j0, sm.cx, rf);
         if (tid == 0) KPROF(1);
         if (__any_sync(0xffffffffu, cm != 0)) {
           // ---- recompute the changed points' clocks (rare: stores first, so
@@ -573,58 +652,77 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
           // thread and warp top-2s ----
           for (unsigned cv = cm & valid; cv; cv &= cv - 1) {
             const int j = __ffs(cv) - 1;
-            const float ivj = PS(inv, j);
-            PF(acur, j) = ivj > 0.f ? PF(ps.e0, j) * ivj : INFINITY;
-            PF(ps.b, j) = (lvl1 && ivj > 0.f) ? PF(ps.e1, j) * ivj : INFINITY;
+            const float ivj = PF(ps.inv, j);
+            PF(acur, j) = ivj > 0.f ? PF(ps.e[0], j) * ivj : INFINITY;
+#pragma unroll
+            for (int l = 1; l < L; ++l)
+              PF(ps.cl[l - 1], j) = (lvl[l] && ivj > 0.f) ? PF(ps.e[l], j) * ivj : INFINITY;
           }
           const int nv = __popc(valid);  // valid slots are a prefix
 #pragma unroll 2
           for (int j = 0; j < nv; ++j) {
             const int ij = static_cast<int>(g0 + j * G);
-            const float aj = PF(acur, j), bj = PF(ps.b, j);
             const double dj = PS(d2, j);
-            if (aj < INFINITY) merge_top2(a1, i1, a2, aj, ij, INFINITY);
-            if (bj < INFINITY) merge_top2d(b1, j1, b2, bd, bj, ij, INFINITY, dj);
+            const float aj = PF(acur, j);
+            if (aj < INFINITY) merge_top2(v1[0], vi[0], v2[0], aj, ij, INFINITY);
+#pragma unroll
+            for (int l = 1; l < L; ++l) {
+              const float bj = PF(ps.cl[l - 1], j);
+              if (bj < INFINITY) merge_top2d(v1[l], vi[l], v2[l], vd[l], bj, ij, INFINITY, dj);
+            }
           }
-          warp_top2s(a1, i1, a2, b1, j1, b2, bd);
+          warp_top2_levels<L>(v1, vi, v2, vd);
         } else {
-          a1 = sm.pa1[warp]; i1 = sm.pi1[warp]; a2 = sm.pa2[warp];
-          b1 = sm.pb1[warp]; j1 = sm.pj1[warp]; b2 = sm.pb2[warp]; bd = sm.pd2[warp];
+#pragma unroll
+          for (int l = 0; l < L; ++l) {
+            v1[l] = sm.p1[l][warp];
+            vi[l] = sm.pi[l][warp];
+            v2[l] = sm.p2[l][warp];
+            vd[l] = sm.pd[l][warp];
+          }
         }
       } else {
-        // ---- full pass: fold + clocks of r, r + 1 ----
+        // ---- full pass: fold + clocks of r .. r + L - 1 ----
 #pragma unroll kPtUnroll
         for (int j = 0; j < PPT; ++j) {
           PF(acur, j) = INFINITY;
           if (!((wvalid >> j) & 1)) continue;
           double dj = PS(d2, j);
-          float ivj = PS(inv, j);
+          float ivj = PF(ps.inv, j);
           const double x0 = PX(j, 0), x1 = PX(j, 1), x2 = PX(j, 2), x3 = PX(j, 3);
           for (int f = 0; f < nf; ++f) {
-            const double dd = dist2(x0, x1, x2, x3, cf[f]);
+            const double dd = dist2(x0, x1, x2, x3, sm.cx[f]);
             if (dd < dj) {
               dj = dd;
-              PS(lab, j) = rf + f;
+              PL(j) = rf + f;
               const float fl = __double2float_rn(dd);
               ivj = dd > 0.0 ? (isinf(fl) ? 1e-38f : rcp_approx(fl)) : 0.f;
             }
           }
           PS(d2, j) = dj;
-          PS(inv, j) = ivj;
+          PF(ps.inv, j) = ivj;
           if (r >= k || !((valid >> j) & 1)) continue;
           const int ij = static_cast<int>(g0 + j * G);
-          const float aj = r == 0 ? PF(ps.e0, j) : (ivj > 0.f ? PF(ps.e0, j) * ivj : INFINITY);
+          const float aj = r == 0 ? PF(ps.e[0], j) : (ivj > 0.f ? PF(ps.e[0], j) * ivj : INFINITY);
           PF(acur, j) = aj;
-          if (aj < INFINITY) merge_top2(a1, i1, a2, aj, ij, INFINITY);
-          if (lvl1 && ivj > 0.f) merge_top2d(b1, j1, b2, bd, PF(ps.e1, j) * ivj, ij, INFINITY, dj);
+          if (aj < INFINITY) merge_top2(v1[0], vi[0], v2[0], aj, ij, INFINITY);
+#pragma unroll
+          for (int l = 1; l < L; ++l)
+            if (lvl[l] && ivj > 0.f)
+              merge_top2d(v1[l], vi[l], v2[l], vd[l], PF(ps.e[l], j) * ivj, ij, INFINITY, dj);
         }
         if (r >= k) break;
-        warp_top2s(a1, i1, a2, b1, j1, b2, bd);
+        warp_top2_levels<L>(v1, vi, v2, vd);
       }
       if (tid == 0) KPROF(2);
       if (lane == 0) {
-        sm.wa1[warp] = a1; sm.wi1[warp] = i1; sm.wa2[warp] = a2;
-        sm.wb1[warp] = b1; sm.wj1[warp] = j1; sm.wb2[warp] = b2; sm.wd2[warp] = bd;
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+          sm.w1[l][warp] = v1[l];
+          sm.wi[l][warp] = vi[l];
+          sm.w2[l][warp] = v2[l];
+          sm.wd[l][warp] = vd[l];
+        }
       }
     } else if (r >= k) {
       break;
@@ -633,44 +731,62 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
     if (comm) {
       // ---- CTA top-2s -> one LL slot of 8-byte (payload, tag) words ----
       const bool w = lane < kCompWarps;
-      float c1 = w ? sm.wa1[lane] : INFINITY, c2 = w ? sm.wa2[lane] : INFINITY;
-      int k1 = w ? sm.wi1[lane] : -1;
-      float e1 = w ? sm.wb1[lane] : INFINITY, e2 = w ? sm.wb2[lane] : INFINITY;
-      int l1 = w ? sm.wj1[lane] : -1;
-      double ed = w ? sm.wd2[lane] : 0.0;
-      warp_top2s(c1, k1, c2, e1, l1, e2, ed);
-      if (lane < kSlotWords) {
-        const unsigned long long db = dbits(ed);
-        const unsigned v = lane == 0 ? __float_as_uint(c1) : lane == 1 ? static_cast<unsigned>(k1)
-                         : lane == 2 ? __float_as_uint(c2) : lane == 3 ? __float_as_uint(e1)
-                         : lane == 4 ? static_cast<unsigned>(l1) : lane == 5 ? __float_as_uint(e2)
-                         : lane == 6 ? static_cast<unsigned>(db) : static_cast<unsigned>(db >> 32);
-        st_ll(slot_a + blockIdx.x * kSlotWords + lane, v, tag);
+      float c1[L], c2[L];
+      int ci[L];
+      double cd[L];
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        c1[l] = w ? sm.w1[l][lane] : INFINITY;
+        c2[l] = w ? sm.w2[l][lane] : INFINITY;
+        ci[l] = w ? sm.wi[l][lane] : -1;
+        cd[l] = w ? sm.wd[l][lane] : 0.0;
+      }
+      warp_top2_levels<L>(c1, ci, c2, cd);
+      if (lane < SL::kWords) {
+        unsigned v = 0u;
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+          const int b = SL::base(l);
+          v = lane == b ? __float_as_uint(c1[l]) : v;
+          v = lane == b + 1 ? static_cast<unsigned>(ci[l]) : v;
+          v = lane == b + 2 ? __float_as_uint(c2[l]) : v;
+          if (l > 0) {
+            const unsigned long long db = dbits(cd[l]);
+            v = lane == b + 3 ? static_cast<unsigned>(db) : v;
+            v = lane == b + 4 ? static_cast<unsigned>(db >> 32) : v;
+          }
+        }
+        st_ll(slot_a + blockIdx.x * kSlotStride + lane, v, tag);
       }
       if (lane == 0) KPROF(5);
       // ---- grid top-2s: every CTA gathers every slot (a lane's slots
       // polled concurrently), reduces in a fixed order ----
-      float g1 = INFINITY, g2 = INFINITY, h1 = INFINITY, h2 = INFINITY;
-      int gi = -1, hj = -1;
-      double hd = 0.0;
-      constexpr int kQ = 5;  // slots per lane per pass (one pass covers 160 CTAs)
+      float g1[L], g2[L];
+      int gi[L];
+      double gd[L];
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        g1[l] = g2[l] = INFINITY;
+        gi[l] = -1;
+        gd[l] = 0.0;
+      }
+      constexpr int kQ = L == 2 ? 5 : 3;  // slots per lane per pass (registers)
       for (int base = 0; base < nblk; base += 32 * kQ) {
         unsigned pend = 0;
 #pragma unroll
         for (int q = 0; q < kQ; ++q)
           if (base + lane + 32 * q < nblk) pend |= 1u << q;
         while (pend) {
-          unsigned v[kQ][8];
+          unsigned v[kQ][SL::kWords];
           bool ok[kQ];
-          const unsigned seen = pend;
 #pragma unroll
           for (int q = 0; q < kQ; ++q) {
             ok[q] = false;
-            if ((seen >> q) & 1) {
-              const uint2* wp = slot_a + (base + lane + 32 * q) * kSlotWords;
+            if ((pend >> q) & 1) {
+              const uint2* wp = slot_a + (base + lane + 32 * q) * kSlotStride;
               bool good = true;
 #pragma unroll
-              for (int h = 0; h < 4; ++h) {
+              for (int h = 0; h < SL::kWords / 2; ++h) {
                 unsigned t0, t1;
                 asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
                              : "=r"(v[q][2 * h]), "=r"(t0), "=r"(v[q][2 * h + 1]), "=r"(t1)
@@ -684,84 +800,123 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
 #pragma unroll
           for (int q = 0; q < kQ; ++q) {
             if (ok[q]) {
-              merge_top2(g1, gi, g2, __uint_as_float(v[q][0]), static_cast<int>(v[q][1]),
-                         __uint_as_float(v[q][2]));
-              merge_top2d(h1, hj, h2, hd, __uint_as_float(v[q][3]), static_cast<int>(v[q][4]),
-                          __uint_as_float(v[q][5]), bitsd(v[q][6], v[q][7]));
-              // a lane's new best may be the winner: start its coordinates
-              // towards L1 now, the decision below reads them
-              if (gi == static_cast<int>(v[q][1]) && gi >= 0) prefetch_point(x64, n, gi);
-              if (hj == static_cast<int>(v[q][4]) && hj >= 0) prefetch_point(x64, n, hj);
+#pragma unroll
+              for (int l = 0; l < L; ++l) {
+                const int b = SL::base(l);
+                const int cand = static_cast<int>(v[q][b + 1]);
+                if (l == 0) {
+                  merge_top2(g1[0], gi[0], g2[0], __uint_as_float(v[q][b]), cand,
+                             __uint_as_float(v[q][b + 2]));
+                } else {
+                  merge_top2d(g1[l], gi[l], g2[l], gd[l], __uint_as_float(v[q][b]), cand,
+                              __uint_as_float(v[q][b + 2]), bitsd(v[q][b + 3], v[q][b + 4]));
+                }
+                // a lane's new best may be the winner: start its coordinates
+                // towards L1 now, the decision below reads them
+                if (gi[l] == cand && cand >= 0) prefetch_point(x64, n, cand);
+              }
               pend &= ~(1u << q);
             }
           }
         }
       }
-      warp_top2s(g1, gi, g2, h1, hj, h2, hd);
+      warp_top2_levels<L>(g1, gi, g2, gd);
       if (lane == 0) KPROF(6);
       // level 0: exact unless the runner-up lies within the FP32 error band
-      const bool need_exact = gi >= 0 && !(g2 > g1 * kBand);
-      const long long wi = need_exact ? -2 : gi;
-      // level 1: out of band, and c_r leaves the speculative winner's d2 as is
-      long long si = -1;
-      double xs[4] = {0, 0, 0, 0}, xc[4] = {0, 0, 0, 0};
-      if (lvl1 && wi >= 0 && hj >= 0 && h2 > h1 * kBand) {
+      const bool need_exact = gi[0] >= 0 && !(g2[0] > g1[0] * kBand);
+      long long wsel[L];
+      wsel[0] = need_exact ? -2 : gi[0];
+      // level l: every lower level decided, out of band, and no centre
+      // decided before it changes its d2
+      bool cand_ok[L];
+      cand_ok[0] = wsel[0] >= 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          xc[q] = __ldg(x64 + q * n + wi);
-          xs[q] = __ldg(x64 + q * n + hj);
-        }
-        const double dd = dist2(xs[0], xs[1], xs[2], xs[3], xc);
-        if (!(dd < hd)) si = hj;
-      } else if (wi >= 0) {
+      for (int l = 1; l < L; ++l) cand_ok[l] = lvl[l] && gi[l] >= 0 && g2[l] > g1[l] * kBand;
+      // candidates' coordinates: lane 4l + q loads coordinate q of level l
+      // into shared memory (one round trip, no per-lane register arrays)
+      if (lane < 4 * L) {
+        const int l = lane >> 2, q = lane & 3;
+        bool ld = cand_ok[0];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) xc[q] = __ldg(x64 + q * n + wi);
+        for (int m = 1; m < L; ++m) ld = (l == m) ? (cand_ok[0] && cand_ok[m]) : ld;
+        int gl = gi[0];
+#pragma unroll
+        for (int m = 1; m < L; ++m) gl = (l == m) ? gi[m] : gl;
+        sm.cx[l][q] = ld ? __ldg(x64 + q * n + gl) : 0.0;
       }
-      if (lane < 4) {
-        sm.cx[0][lane] = xc[lane == 0 ? 0 : lane == 1 ? 1 : lane == 2 ? 2 : 3];
-        sm.cx[1][lane] = xs[lane == 0 ? 0 : lane == 1 ? 1 : lane == 2 ? 2 : 3];
+      __syncwarp();
+      bool hit = cand_ok[0];
+#pragma unroll
+      for (int l = 1; l < L; ++l) {
+        bool h = hit && cand_ok[l];
+        if (h) {
+#pragma unroll
+          for (int m = 0; m < l; ++m) {
+            const double dd = dist2(sm.cx[l][0], sm.cx[l][1], sm.cx[l][2], sm.cx[l][3], sm.cx[m]);
+            h = h && !(dd < gd[l]);
+          }
+        }
+        wsel[l] = h ? gi[l] : -1;
+        hit = h;
       }
       if (lane == 0) {
-        sm.win[0] = wi;
-        sm.win[1] = si;
-        sm.thr = need_exact ? g1 * kBand : -1.f;
+#pragma unroll
+        for (int l = 0; l < L; ++l) sm.win[l] = wsel[l];
+        sm.thr = need_exact ? g1[0] * kBand : -1.f;
         KPROF(7);
       }
     } else {
-      // ---- overlaps the exchange: draws of rounds r + 2, r + 3 and, for the
-      // case that both of this epoch's rounds are decided, their clocks and
-      // warp top-2s with the current d2 ----
-      const int r2 = r + 2;
-      const bool lv1n = r2 + 1 < k;
-      float* an = ps.an;
-      float a1 = INFINITY, a2 = INFINITY, b1 = INFINITY, b2 = INFINITY;
-      int i1 = -1, j1 = -1;
-      double bd = 0.0;
+      // ---- overlaps the exchange: draws of rounds r + L .. r + 2L - 1 and,
+      // for the case that all of this epoch's rounds are decided, their
+      // clocks and warp top-2s with the current d2 ----
+      const int r2 = r + L;
+      float v1[L], v2[L];
+      int vi[L];
+      double vd[L];
+      bool lvn[L];
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        v1[l] = v2[l] = INFINITY;
+        vi[l] = -1;
+        vd[l] = 0.0;
+        lvn[l] = r2 + l < k;
+      }
       if (r2 < k) {
-        const uint64_t pre0 = round_prefix(seed, r2);
-        const uint64_t pre1 = round_prefix(seed, lv1n ? r2 + 1 : r2);
+        uint64_t pre[L];
+#pragma unroll
+        for (int l = 0; l < L; ++l) pre[l] = round_prefix(seed, lvn[l] ? r2 + l : r2);
+        const int an = ps.an;
 #pragma unroll kPtUnroll
         for (int j = 0; j < PPT; ++j) {
           if (!((wvalid >> j) & 1)) continue;
           const uint64_t kpj = PS(kp, j);
-          const float e0 = nlu_approx(mix64(pre0 + kpj));
-          const float e1 = lv1n ? nlu_approx(mix64(pre1 + kpj)) : INFINITY;
-          PF(ps.e2, j) = e0;
-          PF(ps.e3, j) = e1;
-          const float ivj = PS(inv, j);
-          const bool ok = ((valid >> j) & 1) && ivj > 0.f;
-          const float aj = ok ? e0 * ivj : INFINITY;
-          const float bj = (ok && lv1n) ? e1 * ivj : INFINITY;
-          PF(an, j) = aj;
-          PF(ps.b, j) = bj;
+          const float ivj = PF(ps.inv, j);
+          const bool okj = ((valid >> j) & 1) && ivj > 0.f;
           const int ij = static_cast<int>(g0 + j * G);
-          if (aj < INFINITY) merge_top2(a1, i1, a2, aj, ij, INFINITY);
-          if (bj < INFINITY) merge_top2d(b1, j1, b2, bd, bj, ij, INFINITY, PS(d2, j));
+          const double dj = PS(d2, j);
+#pragma unroll
+          for (int l = 0; l < L; ++l) {
+            const float el = lvn[l] ? nlu_approx(mix64(pre[l] + kpj)) : INFINITY;
+            PF(ps.e[L + l], j) = el;
+            const float cj = (okj && lvn[l]) ? el * ivj : INFINITY;
+            if (l == 0) {
+              PF(an, j) = cj;
+              if (cj < INFINITY) merge_top2(v1[0], vi[0], v2[0], cj, ij, INFINITY);
+            } else {
+              PF(ps.cl[l - 1], j) = cj;
+              if (cj < INFINITY) merge_top2d(v1[l], vi[l], v2[l], vd[l], cj, ij, INFINITY, dj);
+            }
+          }
         }
-        warp_top2s(a1, i1, a2, b1, j1, b2, bd);
+        warp_top2_levels<L>(v1, vi, v2, vd);
         if (lane == 0) {
-          sm.pa1[warp] = a1; sm.pi1[warp] = i1; sm.pa2[warp] = a2;
-          sm.pb1[warp] = b1; sm.pj1[warp] = j1; sm.pb2[warp] = b2; sm.pd2[warp] = bd;
+#pragma unroll
+          for (int l = 0; l < L; ++l) {
+            sm.p1[l][warp] = v1[l];
+            sm.pi[l][warp] = vi[l];
+            sm.p2[l][warp] = v2[l];
+            sm.pd[l][warp] = vd[l];
+          }
         }
       }
       if (tid == 0) KPROF(3);
@@ -803,7 +958,7 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) shfl_cand(c1, j1, src, off);
         if (lane == 0) {
-          uint2* w = slot_e + blockIdx.x * kSlotWords;
+          uint2* w = slot_e + blockIdx.x * kSlotStride;
           const unsigned long long cb = dbits(c1);
           st_ll(w + 0, static_cast<unsigned>(cb), tag);
           st_ll(w + 1, static_cast<unsigned>(cb >> 32), tag);
@@ -813,8 +968,8 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
         double gc = INFINITY;
         long long gj = -1;
         for (int b = lane; b < nblk; b += 32) {
-          unsigned wv[4];
-          ld_ll_n<4>(slot_e + b * kSlotWords, tag, wv);
+          unsigned wv[kExactWords];
+          ld_ll_n<kExactWords>(slot_e + b * kSlotStride, tag, wv);
           const double c2 = bitsd(wv[0], wv[1]);
           const long long j2 = static_cast<int>(wv[2]);
           if (cand_better(c2, j2, gc, gj)) {
@@ -829,7 +984,8 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
         if (lane < 4 && wi >= 0) sm.cx[0][lane] = __ldg(x64 + lane * n + wi);
         if (lane == 0) {
           sm.win[0] = wi;
-          sm.win[1] = -1;  // no speculation across an exact round
+#pragma unroll
+          for (int l = 1; l < L; ++l) sm.win[l] = -1;  // no speculation across an exact round
         }
       }
       __syncthreads();
@@ -850,7 +1006,7 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
       if (tid == 32 * (kSeedWarps - 1)) {
         long long m = LLONG_MAX;
         for (int w = 0; w < kCompWarps; ++w) m = sm.gu[w] < m ? sm.gu[w] : m;
-        KppSlot* fs = reinterpret_cast<KppSlot*>(llw + 4 * nblk * kSlotWords);
+        KppSlot* fs = reinterpret_cast<KppSlot*>(llw + 4 * nblk * kSlotStride);
         fs[blockIdx.x].unchosen = m;
         ++epoch;
         grid_exchange(scr.counter, static_cast<unsigned>(nblk) * epoch);
@@ -860,56 +1016,48 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
           m = u2 < m ? u2 : m;
         }
         sm.win[0] = m;
-        sm.win[1] = -1;
+        for (int l = 1; l < L; ++l) sm.win[l] = -1;
 #pragma unroll
         for (int q = 0; q < 4; ++q) sm.cx[0][q] = x64[q * n + m];
       }
       __syncthreads();
     }
-    // ---- commit this epoch's centres (1 or 2) ----
-    const long long w0 = sm.win[0], w1 = sm.win[1];
+    // ---- commit this epoch's centres (1 .. L) ----
+    long long wv[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) wv[l] = sm.win[l];
+    int nd = 1;  // rounds decided: the level-0 winner and the consecutive hits
+#pragma unroll
+    for (int l = 1; l < L; ++l) nd += (nd == l && wv[l] >= 0) ? 1 : 0;
     if (blockIdx.x == 0 && tid == 0) {  // (a compute thread)
-      scr.centers[r] = w0;
-      if (w1 >= 0) {
-        scr.centers[r + 1] = w1;
-        sm.spec_hits += 1;
-      }
+#pragma unroll
+      for (int l = 0; l < L; ++l)
+        if (l < nd) scr.centers[r + l] = wv[l];
+      sm.spec_hits += nd - 1;
     }
     rf = r;
-    nf = w1 >= 0 ? 2 : 1;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      cf[0][q] = sm.cx[0][q];
-      cf[1][q] = sm.cx[1][q];
-    }
-
+    nf = nd;
     if (!comm) {
-      if (w0 % G == g0) chosen |= 1u << static_cast<int>(w0 / G);
-      if (w1 >= 0 && w1 % G == g0) chosen |= 1u << static_cast<int>(w1 / G);
+#pragma unroll
+      for (int l = 0; l < L; ++l)
+        if (l < nd && wv[l] % G == g0) chosen |= 1u << static_cast<int>(wv[l] / G);
     }
-    // draws of the next epoch's two rounds (pointer rotation)
-    {
-      float* e0 = ps.e0;
-      float* e1 = ps.e1;
-      if (w1 >= 0) {  // rounds r + 2, r + 3: precomputed
-        ps.e0 = ps.e2;
-        ps.e1 = ps.e3;
-        ps.e2 = e0;
-        ps.e3 = e1;
-        float* a = ps.ac;
-        ps.ac = ps.an;
-        ps.an = a;
-      } else {        // rounds r + 1, r + 2: computed in full
-        ps.e0 = e1;
-        ps.e1 = ps.e2;
-        ps.e2 = e0;
-      }
-      pre_ok = w1 >= 0;
+    // the draws of rounds r + nd .. move to the front (pointer rotation)
+    if (nd == L) {
+      rotate_draws<L, L>(ps.e);
+      const int a = ps.ac;
+      ps.ac = ps.an;
+      ps.an = a;
+    } else if (nd == 1) {
+      rotate_draws<L, 1>(ps.e);
+    } else {
+      rotate_draws<L, (L > 2 ? 2 : 1)>(ps.e);
     }
+    pre_ok = nd == L;
     if (tid == 0) KPROF(4);
-    r += nf;
-    // sm.win / sm.cx are rewritten by warp 0 only after the next epoch's
-    // first barrier, which every thread reaches after these reads
+    r += nd;
+    // sm.win / sm.cx are rewritten by the communication warp only after the
+    // next epoch's first barrier, which every thread reaches after these reads
   }
 #ifdef GMMB_KPP_PROF
   __syncthreads();
@@ -923,12 +1071,14 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
     for (int j = 0; j < PPT; ++j) {
       const long long i = g0 + j * G;
       if (i >= n) continue;
-      scr.labels[i] = PS(lab, j);
-      atomicAdd(&scr.owned[PS(lab, j)], 1);
+      scr.labels[i] = PL(j);
+      atomicAdd(&scr.owned[PL(j)], 1);
     }
   }
 #undef PX
 #undef PS
+#undef PF
+#undef PL
 }
 
 // Memory-resident variant (N beyond the register budget): state in global
@@ -1316,15 +1466,21 @@ cudaError_t launch_kpp_seed(const double* x64, int64_t n, int k, uint64_t seed,
   const int nblk = sm_count < kMaxSeedBlocks ? sm_count : kMaxSeedBlocks;
   const int64_t per_thread = (n + static_cast<int64_t>(nblk) * kCompThreads - 1) /
                              (static_cast<int64_t>(nblk) * kCompThreads);
-  const size_t bytes = point_state_bytes(static_cast<int>(per_thread));
-  if (per_thread <= 32 && bytes <= 220 * 1024) {
-    int ppt = static_cast<int>(per_thread);
-    cudaError_t e = cudaFuncSetAttribute(kpp_seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  // speculation depth: three rounds per exchange while the per-point state
+  // fits shared memory, else two
+  const int ppt_i = static_cast<int>(per_thread < 32 ? per_thread : 32);
+  const size_t b3 = point_state_bytes(ppt_i, 3), b2 = point_state_bytes(ppt_i, 2);
+  const size_t budget = 200 * 1024;
+  if (per_thread <= 32 && (b2 <= budget || b3 <= budget)) {
+    int ppt = ppt_i;
+    const bool deep = GMMB_KPP_MAXDEPTH >= 3 && b3 <= budget;
+    const void* fn = deep ? (const void*)kpp_seed_kernel<3> : (const void*)kpp_seed_kernel<2>;
+    const size_t bytes = deep ? b3 : b2;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(bytes));
     if (e != cudaSuccess) return e;
     void* args[] = {(void*)&x64, (void*)&n, (void*)&k, (void*)&seed, (void*)&scr, (void*)&ppt};
-    return cudaLaunchCooperativeKernel((void*)kpp_seed_kernel, dim3(nblk), dim3(kSeedThreads), args,
-                                       bytes, s);
+    return cudaLaunchCooperativeKernel(fn, dim3(nblk), dim3(kSeedThreads), args, bytes, s);
   }
   // memory-resident fallback: one launch per round; a thread holds up to
   // kMemPPT points (n > sm_count * 4 * 512 * kMemPPT: more CTAs)
