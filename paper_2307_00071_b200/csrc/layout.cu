@@ -91,29 +91,51 @@ __global__ void morton_kernel(const double* __restrict__ x64, int64_t n,
                               const double* __restrict__ part, int nparts,
                               uint64_t* __restrict__ keys,
                               int32_t* __restrict__ idx) {
+  // the bounding box from the per-CTA partials: all threads, then a fixed
+  // tree (min / max are order-independent anyway)
+  __shared__ double red[6][256];
   __shared__ double bb[6];
-  if (threadIdx.x < 6) {
-    const int j = threadIdx.x;
-    double v = j < 3 ? INFINITY : -INFINITY;
-    for (int p = 0; p < nparts; ++p) {
-      v = j < 3 ? fmin(v, part[p * 6 + j]) : fmax(v, part[p * 6 + j]);
+  {
+    double v[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    for (int p = threadIdx.x; p < nparts; p += blockDim.x) {
+#pragma unroll
+      for (int j = 0; j < 6; ++j)
+        v[j] = j < 3 ? fmin(v[j], part[p * 6 + j]) : fmax(v[j], part[p * 6 + j]);
     }
-    bb[j] = v;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) red[j][threadIdx.x] = v[j];
+    __syncthreads();
+    for (int off = blockDim.x / 2; off >= 1; off >>= 1) {
+      if (threadIdx.x < off) {
+#pragma unroll
+        for (int j = 0; j < 6; ++j)
+          red[j][threadIdx.x] = j < 3 ? fmin(red[j][threadIdx.x], red[j][threadIdx.x + off])
+                                      : fmax(red[j][threadIdx.x], red[j][threadIdx.x + off]);
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x < 6) bb[threadIdx.x] = red[threadIdx.x][0];
+    __syncthreads();
   }
-  __syncthreads();
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  uint64_t key = 0;
+  double lo[3], ex[3];
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
-    const double ext = bb[3 + j] - bb[j];
-    double t = ext > 0.0 ? (x64[j * n + i] - bb[j]) / ext : 0.0;
-    t = fmin(fmax(t, 0.0), 1.0);
-    const uint64_t q = static_cast<uint64_t>(t * 2097151.0);
-    key |= spread3(q) << j;
+    lo[j] = bb[j];
+    ex[j] = bb[3 + j] - bb[j];
   }
-  keys[i] = key;
-  idx[i] = static_cast<int32_t>(i);
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint64_t key = 0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      double t = ex[j] > 0.0 ? (x64[j * n + i] - lo[j]) / ex[j] : 0.0;
+      t = fmin(fmax(t, 0.0), 1.0);
+      const uint64_t q = static_cast<uint64_t>(t * 2097151.0);
+      key |= spread3(q) << j;
+    }
+    keys[i] = key;
+    idx[i] = static_cast<int32_t>(i);
+  }
 }
 
 // One CTA per 128-point tile: FP64 centroid, then FP32 offsets.
@@ -175,8 +197,10 @@ cudaError_t launch_layout(const double* x64, int64_t n, LayoutScratch scr,
   int nparts = sm_count * 2;
   if (nparts > kBboxParts) nparts = kBboxParts;
   bbox_kernel<<<nparts, 256, 0, s>>>(x64, n, scr.bbox_part);
-  const int grid = static_cast<int>((n + 255) / 256);
-  morton_kernel<<<grid, 256, 0, s>>>(x64, n, scr.bbox_part, nparts, scr.keys_in, scr.idx_in);
+  const int64_t need = (n + 255) / 256;
+  const int grid = static_cast<int>(need < sm_count * 4 ? need : sm_count * 4);
+  morton_kernel<<<grid > 0 ? grid : 1, 256, 0, s>>>(x64, n, scr.bbox_part, nparts, scr.keys_in,
+                                                   scr.idx_in);
   size_t bytes = scr.temp_bytes;
   cudaError_t e = cub::DeviceRadixSort::SortPairs(
       scr.temp, bytes, scr.keys_in, scr.keys_out, scr.idx_in, perm,

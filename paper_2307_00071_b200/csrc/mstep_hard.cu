@@ -36,13 +36,40 @@ __device__ __forceinline__ int64_t lower_bound(const int32_t* keys, int64_t n, i
   return lo;
 }
 
+// Block-wide FP64 sum of NV values per thread (fixed tree: deterministic).
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double (*red)[NV]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NV; ++q)
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) red[warp][q] = v[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    double s = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s += red[w][q];
+    v[q] = s;
+  }
+  __syncthreads();
+}
+
+// One CTA per component (the segment of its points in label-sorted order):
+// large clusters (the back wall of cfg2 holds tens of thousands of points)
+// spread over 256 threads with independent loads in flight.
+constexpr int kHardThreads = 256;
 template <int D>
-__global__ void __launch_bounds__(128) hard_moments_kernel(
+__global__ void __launch_bounds__(kHardThreads) hard_moments_kernel(
     const double* __restrict__ x64, int64_t n, const int32_t* __restrict__ skeys,
     const int32_t* __restrict__ sidx, int m, double cov_reg, RecBuf rec) {
   constexpr int NP = npacked(D);
-  const int lane = threadIdx.x & 31;
-  const int k = blockIdx.x * 4 + (threadIdx.x >> 5);
+  __shared__ double red1[kHardThreads / 32][D];
+  __shared__ double red2[kHardThreads / 32][NP];
+  const int k = blockIdx.x;
   if (k >= m) return;
   const int64_t b = lower_bound(skeys, n, k), e = lower_bound(skeys, n, k + 1);
   const double cnt = static_cast<double>(e - b);
@@ -50,15 +77,13 @@ __global__ void __launch_bounds__(128) hard_moments_kernel(
   double sx[D];
 #pragma unroll
   for (int j = 0; j < D; ++j) sx[j] = 0.0;
-  for (int64_t i = b + lane; i < e; i += 32) {
+#pragma unroll 4
+  for (int64_t i = b + threadIdx.x; i < e; i += kHardThreads) {
     const int64_t p = sidx[i];
 #pragma unroll
     for (int j = 0; j < D; ++j) sx[j] += x64[j * n + p];
   }
-#pragma unroll
-  for (int j = 0; j < D; ++j)
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) sx[j] += __shfl_xor_sync(0xffffffffu, sx[j], off);
+  block_sum<D>(sx, red1);
   const bool keep = !(cnt < kDegenerateCount);  // kernels.hpp:121-128
   double mean[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -67,7 +92,8 @@ __global__ void __launch_bounds__(128) hard_moments_kernel(
   double sc[NP];
 #pragma unroll
   for (int q = 0; q < NP; ++q) sc[q] = 0.0;
-  for (int64_t i = b + lane; i < e; i += 32) {
+#pragma unroll 4
+  for (int64_t i = b + threadIdx.x; i < e; i += kHardThreads) {
     const int64_t p = sidx[i];
     double d[D];
 #pragma unroll
@@ -75,11 +101,8 @@ __global__ void __launch_bounds__(128) hard_moments_kernel(
 #pragma unroll
     for (int q = 0; q < NP; ++q) sc[q] += d[packed_row(q)] * d[packed_col(q)];
   }
-#pragma unroll
-  for (int q = 0; q < NP; ++q)
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) sc[q] += __shfl_xor_sync(0xffffffffu, sc[q], off);
-  if (lane != 0) return;
+  block_sum<NP>(sc, red2);
+  if (threadIdx.x != 0) return;
   const double inv = keep ? 1.0 / cnt : 0.0;
   double cov[10];
 #pragma unroll
@@ -131,11 +154,12 @@ cudaError_t launch_hard_moments(int d, const double* x64, int64_t n, const int32
                                                   scr.idx_in, scr.idx_out, static_cast<int>(n),
                                                   0, label_bits(m), s);
   if (e != cudaSuccess) return e;
-  const int grid = (m + 3) / 4;
   if (d == 4)
-    hard_moments_kernel<4><<<grid, 128, 0, s>>>(x64, n, scr.keys_out, scr.idx_out, m, cov_reg, rec);
+    hard_moments_kernel<4><<<m, kHardThreads, 0, s>>>(x64, n, scr.keys_out, scr.idx_out, m,
+                                                      cov_reg, rec);
   else
-    hard_moments_kernel<3><<<grid, 128, 0, s>>>(x64, n, scr.keys_out, scr.idx_out, m, cov_reg, rec);
+    hard_moments_kernel<3><<<m, kHardThreads, 0, s>>>(x64, n, scr.keys_out, scr.idx_out, m,
+                                                      cov_reg, rec);
   return cudaGetLastError();
 }
 
