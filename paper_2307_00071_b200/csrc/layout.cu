@@ -89,7 +89,7 @@ __device__ __forceinline__ uint64_t spread3(uint64_t v) {  // 21 bits -> 63
 
 __global__ void morton_kernel(const double* __restrict__ x64, int64_t n,
                               const double* __restrict__ part, int nparts,
-                              uint64_t* __restrict__ keys,
+                              uint32_t* __restrict__ keys,
                               int32_t* __restrict__ idx) {
   // the bounding box from the per-CTA partials: all threads, then a fixed
   // tree (min / max are order-independent anyway)
@@ -133,7 +133,7 @@ __global__ void morton_kernel(const double* __restrict__ x64, int64_t n,
       const uint64_t q = static_cast<uint64_t>(t * 2097151.0);
       key |= spread3(q) << j;
     }
-    keys[i] = key;
+    keys[i] = static_cast<uint32_t>(key >> kMortonLoBit);  // the top 30 bits (4 radix passes)
     idx[i] = static_cast<int32_t>(i);
   }
 }
@@ -185,9 +185,9 @@ cudaError_t launch_validate(const double* x64, int64_t n, int d, int* flags,
 
 size_t layout_sort_temp_bytes(int64_t n) {
   size_t bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint64_t*)nullptr,
-                                  (uint64_t*)nullptr, (const int32_t*)nullptr,
-                                  (int32_t*)nullptr, static_cast<int>(n), kMortonLoBit, 63);
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, (const int32_t*)nullptr,
+                                  (int32_t*)nullptr, static_cast<int>(n), 0, 63 - kMortonLoBit);
   return bytes;
 }
 
@@ -199,12 +199,13 @@ cudaError_t launch_layout(const double* x64, int64_t n, LayoutScratch scr,
   bbox_kernel<<<nparts, 256, 0, s>>>(x64, n, scr.bbox_part);
   const int64_t need = (n + 255) / 256;
   const int grid = static_cast<int>(need < sm_count * 4 ? need : sm_count * 4);
-  morton_kernel<<<grid > 0 ? grid : 1, 256, 0, s>>>(x64, n, scr.bbox_part, nparts, scr.keys_in,
+  uint32_t* kin = reinterpret_cast<uint32_t*>(scr.keys_in);
+  uint32_t* kout = reinterpret_cast<uint32_t*>(scr.keys_out);
+  morton_kernel<<<grid > 0 ? grid : 1, 256, 0, s>>>(x64, n, scr.bbox_part, nparts, kin,
                                                    scr.idx_in);
   size_t bytes = scr.temp_bytes;
   cudaError_t e = cub::DeviceRadixSort::SortPairs(
-      scr.temp, bytes, scr.keys_in, scr.keys_out, scr.idx_in, perm,
-      static_cast<int>(n), kMortonLoBit, 63, s);
+      scr.temp, bytes, kin, kout, scr.idx_in, perm, static_cast<int>(n), 0, 63 - kMortonLoBit, s);
   if (e != cudaSuccess) return e;
   const int ntiles = static_cast<int>((n + kTile - 1) / kTile);
   tile_kernel<<<ntiles, kTile, 0, s>>>(x64, n, perm, xt, tc);
