@@ -30,6 +30,7 @@
 // arrival counter (scripts/micro/ll_bench.cu: 2.2 us per exchange against
 // 2.5 us for counter + fence, 3.5 us through a master CTA).
 #include <climits>
+#include <cstdlib>
 
 #include "kinit_kernels.cuh"
 
@@ -1473,7 +1474,10 @@ cudaError_t launch_kpp_seed(const double* x64, int64_t n, int k, uint64_t seed,
   const size_t budget = 200 * 1024;
   if (per_thread <= 32 && (b2 <= budget || b3 <= budget)) {
     int ppt = ppt_i;
-    const bool deep = GMMB_KPP_MAXDEPTH >= 3 && b3 <= budget;
+    // GMMB_KPP_DEPTH=3 (environment) selects the three-round epochs (tests)
+    const char* env = getenv("GMMB_KPP_DEPTH");
+    const int depth = env ? atoi(env) : GMMB_KPP_MAXDEPTH;
+    const bool deep = depth >= 3 && b3 <= budget;
     const void* fn = deep ? (const void*)kpp_seed_kernel<3> : (const void*)kpp_seed_kernel<2>;
     const size_t bytes = deep ? b3 : b2;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -272,3 +272,15 @@ def test_small_and_ragged_fits(gm, orc, ctx, n, k, d):
     assert ll_err(r.ll_trace, ref["ll_trace"]) <= LL_TOL
     assert_model_close(r.model.weights, r.model.means, r.model.covariances,
                        ref["w"], ref["mu"][:, :d], ref["cov"][:, :d * (d + 1) // 2])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k,seed", [(512, 0), (97, 5)])
+def test_kinit_depth3_exact(gm, orc, ctx, k, seed, monkeypatch):
+    """The three-rounds-per-exchange seeding variant (not the default) is bit-exact too."""
+    monkeypatch.setenv("GMMB_KPP_DEPTH", "3")
+    p = frame(gm)
+    lab, cen = gm.kinit(p, k, seed, ctx=ctx)
+    rl, rc = orc.kinit(p, k, seed)
+    assert np.array_equal(cen, rc)
+    assert np.array_equal(lab, rl)
