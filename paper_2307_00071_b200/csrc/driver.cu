@@ -379,7 +379,7 @@ void run_kinit(gmmb_ctx* c, int k, uint64_t seed) {
     ck(cudaMemsetAsync(c->kstatus.p, 0, sizeof(int) * 8, c->s), "memset");
     // LL exchange words carry round tags: start from all-zero tags
     ck(cudaMemsetAsync(c->slots.p, 0, sizeof(KppSlot) * c->slots.cap, c->s), "memset");
-    ck(launch_kpp_seed(c->x64.p, n, k, seed, ks, c->sm_count, c->s), "kpp_seed");
+    ck(launch_kpp_seed(c->x64.p, n, c->d, k, seed, ks, c->sm_count, c->s), "kpp_seed");
     ck(launch_fixup(n, k, ks, c->s), "fixup");
     c->launches += 3;  // keys, seed (persistent), fixup
     return;

@@ -1097,7 +1097,7 @@ constexpr int kMemPPT = 16;  // points per thread held as FP32 clocks in shared 
 __global__ void __launch_bounds__(kMemThreads)
     kpp_mem_round_kernel(const double* __restrict__ x64, int64_t n, int r,
                          int k, uint64_t seed, KinitScratch scr, int* ticket,
-                         long long* win_io) {
+                         long long* win_io, int d) {
   __shared__ float s_a[kMemPPT * kMemThreads];
   __shared__ double s_c[kMemThreads / 32];
   __shared__ long long s_i[kMemThreads / 32];
@@ -1111,9 +1111,8 @@ __global__ void __launch_bounds__(kMemThreads)
   const long long win = r > 0 ? win_io[0] : -1;
   double c[4] = {0, 0, 0, 0};
   if (r > 0)
-    for (int q = 0; q < 4; ++q) c[q] = x64[q * n + win];
+    for (int q = 0; q < d; ++q) c[q] = x64[q * n + win];
   const uint64_t pre = round_prefix(seed, r);
-  long long bu = LLONG_MAX;
   float amin = INFINITY;
   // phase 1: fold centre r-1, FP32 clocks
 #pragma unroll 4
@@ -1124,18 +1123,18 @@ __global__ void __launch_bounds__(kMemThreads)
       double dcur;
       if (r > 0) {
         dcur = scr.d2[i];
-        const double dd = dist2(x64[i], x64[n + i], x64[2 * n + i], x64[3 * n + i], c);
+        // 3D clouds: the fourth (zero) coordinate is not read (0 - 0 = 0)
+        const double x3 = d == 4 ? x64[3 * n + i] : 0.0;
+        const double dd = dist2(x64[i], x64[n + i], x64[2 * n + i], x3, c);
         if (dd < dcur) {
           dcur = dd;
           scr.d2[i] = dd;
           scr.labels[i] = r - 1;
         }
-        if (i == win) scr.chosen[i] = 1;
       } else {
         dcur = INFINITY;
         scr.d2[i] = INFINITY;
         scr.labels[i] = 0;
-        scr.chosen[i] = 0;
       }
       if (r < k) {
         const float na = nlu_approx(mix64(pre + scr.keys[i]));
@@ -1145,7 +1144,6 @@ __global__ void __launch_bounds__(kMemThreads)
           const float f = __double2float_rn(dcur);
           a = na * (isinf(f) ? 1e-38f : rcp_approx(f));
         }
-        if (!scr.chosen[i] && i < bu) bu = i;
       }
     }
     s_a[m * kMemThreads + tid] = a;
@@ -1177,28 +1175,18 @@ __global__ void __launch_bounds__(kMemThreads)
   }
   int bs = 0;
 #pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) {
-    shfl_cand(bc, bi, bs, off);
-    const long long u2 = __shfl_xor_sync(0xffffffffu, bu, off);
-    bu = u2 < bu ? u2 : bu;
-  }
-  if (lane == 0) { s_c[warp] = bc; s_i[warp] = bi; s_u[warp] = bu; }
+  for (int off = 16; off >= 1; off >>= 1) shfl_cand(bc, bi, bs, off);
+  if (lane == 0) { s_c[warp] = bc; s_i[warp] = bi; }
   __syncthreads();
   if (warp == 0) {
     bc = lane < NW ? s_c[lane] : INFINITY;
     bi = lane < NW ? s_i[lane] : -1;
-    bu = lane < NW ? s_u[lane] : LLONG_MAX;
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-      shfl_cand(bc, bi, bs, off);
-      const long long u2 = __shfl_xor_sync(0xffffffffu, bu, off);
-      bu = u2 < bu ? u2 : bu;
-    }
+    for (int off = 16; off >= 1; off >>= 1) shfl_cand(bc, bi, bs, off);
     if (lane == 0) {
       KppSlot& sl = scr.slots[blockIdx.x];
       sl.clock = bc;
       sl.idx = bi;
-      sl.unchosen = bu;
       __threadfence();
       s_last = (atomicAdd(ticket, 1) == static_cast<int>(gridDim.x) - 1);
     }
@@ -1208,38 +1196,54 @@ __global__ void __launch_bounds__(kMemThreads)
   // last CTA: every slot, in parallel, fixed order
   __threadfence();
   double gc = INFINITY;
-  long long gi = -1, gu = LLONG_MAX;
+  long long gi = -1;
   for (int b = tid; b < static_cast<int>(gridDim.x); b += kMemThreads) {
     const volatile KppSlot& sl = scr.slots[b];
     const double c2 = sl.clock;
-    const long long i2 = sl.idx, u2 = sl.unchosen;
+    const long long i2 = sl.idx;
     if (cand_better(c2, i2, gc, gi)) { gc = c2; gi = i2; }
-    gu = u2 < gu ? u2 : gu;
   }
 #pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) {
-    shfl_cand(gc, gi, bs, off);
-    const long long u2 = __shfl_xor_sync(0xffffffffu, gu, off);
-    gu = u2 < gu ? u2 : gu;
-  }
-  if (lane == 0) { s_c[warp] = gc; s_i[warp] = gi; s_u[warp] = gu; }
+  for (int off = 16; off >= 1; off >>= 1) shfl_cand(gc, gi, bs, off);
+  if (lane == 0) { s_c[warp] = gc; s_i[warp] = gi; }
   __syncthreads();
+  gc = tid < NW ? s_c[tid] : INFINITY;
+  gi = tid < NW ? s_i[tid] : -1;
   if (warp == 0) {
-    gc = lane < NW ? s_c[lane] : INFINITY;
-    gi = lane < NW ? s_i[lane] : -1;
-    gu = lane < NW ? s_u[lane] : LLONG_MAX;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) shfl_cand(gc, gi, bs, off);
+    if (lane == 0) s_i[0] = (gi >= 0 && gc < INFINITY) ? gi : -1;
+  }
+  __syncthreads();
+  long long w = s_i[0];
+  if (w < 0) {
+    // sogmm.cpp:276-284: no eligible point -> the lowest unchosen index. The
+    // chosen points are centres[0 .. r), so it is among 0 .. r: the lowest
+    // candidate not in that list (rare; one CTA, O(r^2 / threads))
+    long long lo = LLONG_MAX;
+    for (long long cnd = tid; cnd <= r && cnd < n; cnd += kMemThreads) {
+      bool taken = false;
+      for (int q = 0; q < r && !taken; ++q) taken = scr.centers[q] == cnd;
+      if (!taken && cnd < lo) lo = cnd;
+    }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
-      shfl_cand(gc, gi, bs, off);
-      const long long u2 = __shfl_xor_sync(0xffffffffu, gu, off);
-      gu = u2 < gu ? u2 : gu;
+      const long long u2 = __shfl_xor_sync(0xffffffffu, lo, off);
+      lo = u2 < lo ? u2 : lo;
     }
-    if (lane == 0) {
-      const long long w = (gi >= 0 && gc < INFINITY) ? gi : gu;  // :276-284 fallback
-      win_io[0] = w;
-      scr.centers[r] = w;
-      *ticket = 0;
+    if (lane == 0) s_u[warp] = lo;
+    __syncthreads();
+    if (tid == 0) {
+      for (int q = 0; q < NW; ++q) lo = s_u[q] < lo ? s_u[q] : lo;
+      s_u[0] = lo;
     }
+    __syncthreads();
+    w = s_u[0];
+  }
+  if (tid == 0) {
+    win_io[0] = w;
+    scr.centers[r] = w;
+    *ticket = 0;
   }
 }
 
@@ -1461,7 +1465,7 @@ cudaError_t launch_keys(const double* x64, int64_t n, const double* tail,
   return cudaGetLastError();
 }
 
-cudaError_t launch_kpp_seed(const double* x64, int64_t n, int k, uint64_t seed,
+cudaError_t launch_kpp_seed(const double* x64, int64_t n, int d, int k, uint64_t seed,
                             KinitScratch scr, int sm_count, cudaStream_t s) {
   // one CTA per SM, per-point state resident in shared memory while it fits
   const int nblk = sm_count < kMaxSeedBlocks ? sm_count : kMaxSeedBlocks;
@@ -1471,7 +1475,11 @@ cudaError_t launch_kpp_seed(const double* x64, int64_t n, int k, uint64_t seed,
   // fits shared memory, else two
   const int ppt_i = static_cast<int>(per_thread < 32 ? per_thread : 32);
   const size_t b3 = point_state_bytes(ppt_i, 3), b2 = point_state_bytes(ppt_i, 2);
-  const size_t budget = 200 * 1024;
+#ifdef GMMB_KPP_PROF
+  const size_t budget = 195 * 1024;  // the probes' static shared memory
+#else
+  const size_t budget = 220 * 1024;
+#endif
   if (per_thread <= 32 && (b2 <= budget || b3 <= budget)) {
     int ppt = ppt_i;
     // GMMB_KPP_DEPTH=3 (environment) selects the three-round epochs (tests)
@@ -1497,7 +1505,7 @@ cudaError_t launch_kpp_seed(const double* x64, int64_t n, int k, uint64_t seed,
   cudaError_t e = cudaMemsetAsync(scr.status, 0, sizeof(int) * 4, s);
   if (e != cudaSuccess) return e;
   for (int r = 0; r <= k; ++r) {
-    kpp_mem_round_kernel<<<grid, kMemThreads, 0, s>>>(x64, n, r, k, seed, scr, ticket, win);
+    kpp_mem_round_kernel<<<grid, kMemThreads, 0, s>>>(x64, n, r, k, seed, scr, ticket, win, d);
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;

@@ -38,7 +38,7 @@ cudaError_t launch_keys(const double* x64, int64_t n, const double* tail,
 // Persistent k-means++ seeding for one device holding all points
 // (sogmm.cpp:224-287), followed by the final centre fold that yields the
 // nearest-centre labels (:290-312) and owned counts. Cooperative launch.
-cudaError_t launch_kpp_seed(const double* x64, int64_t n, int k, uint64_t seed,
+cudaError_t launch_kpp_seed(const double* x64, int64_t n, int d, int k, uint64_t seed,
                             KinitScratch scr, int sm_count, cudaStream_t s);
 
 // Owned fix-up (sogmm.cpp:315-331), single CTA, no-op when nothing is empty.

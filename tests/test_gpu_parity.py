@@ -284,3 +284,15 @@ def test_kinit_depth3_exact(gm, orc, ctx, k, seed, monkeypatch):
     rl, rc = orc.kinit(p, k, seed)
     assert np.array_equal(cen, rc)
     assert np.array_equal(lab, rl)
+
+
+@pytest.mark.gpu
+def test_kinit_memory_variant_3d_duplicates_fallback(gm, orc, ctx):
+    """Memory-resident seeding (N > the shared-memory budget) on a 3D cloud of
+    20 distinct points repeated: after 20 rounds every d2 is 0 and the rounds
+    take the lowest unchosen index (sogmm.cpp:276-284)."""
+    base = gm.structured_scene(20, 3, 0.005)[:, :3]
+    p = np.repeat(base, 20000, axis=0)  # 400,000 points
+    lab, cen = gm.kinit(p, 32, 0, ctx=ctx)
+    rl, rc = orc.kinit(p, 32, 0)
+    assert np.array_equal(cen, rc) and np.array_equal(lab, rl)
