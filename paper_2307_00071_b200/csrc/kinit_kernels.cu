@@ -1091,8 +1091,8 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
 // (the global best is no larger than the local best), so each CTA's exact
 // (clock, index) best contains the global winner. The last CTA to finish
 // reduces every CTA's slot in parallel, in a fixed order.
-constexpr int kMemThreads = 512;
-constexpr int kMemPPT = 16;  // points per thread held as FP32 clocks in shared memory
+constexpr int kMemThreads = 256;  // 4 CTAs per SM resident: one wave
+constexpr int kMemPPT = 32;  // points per thread held as FP32 clocks in shared memory
 
 __global__ void __launch_bounds__(kMemThreads)
     kpp_mem_round_kernel(const double* __restrict__ x64, int64_t n, int r,
@@ -1111,7 +1111,8 @@ __global__ void __launch_bounds__(kMemThreads)
   const long long win = r > 0 ? win_io[0] : -1;
   double c[4] = {0, 0, 0, 0};
   if (r > 0)
-    for (int q = 0; q < d; ++q) c[q] = x64[q * n + win];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c[q] = q < d ? x64[q * n + win] : 0.0;
   const uint64_t pre = round_prefix(seed, r);
   float amin = INFINITY;
   // phase 1: fold centre r-1, FP32 clocks
@@ -1495,7 +1496,7 @@ cudaError_t launch_kpp_seed(const double* x64, int64_t n, int d, int k, uint64_t
     return cudaLaunchCooperativeKernel(fn, dim3(nblk), dim3(kSeedThreads), args, bytes, s);
   }
   // memory-resident fallback: one launch per round; a thread holds up to
-  // kMemPPT points (n > sm_count * 4 * 512 * kMemPPT: more CTAs)
+  // kMemPPT points (n > sm_count * 4 * kMemThreads * kMemPPT: more CTAs)
   const int64_t cap = static_cast<int64_t>(sm_count) * 4 * kMemThreads * kMemPPT;
   const int grid = static_cast<int>(
       n <= cap ? sm_count * 4 : (n + static_cast<int64_t>(kMemThreads) * kMemPPT - 1) /
