@@ -157,6 +157,8 @@ struct gmmb_ctx {
   DevBuf<double> kd2;
   DevBuf<int32_t> labels;
   DevBuf<unsigned char> chosen;
+  DevBuf<float4> kxf;
+  DevBuf<float> ktp, kinv;
   DevBuf<KppSlot> slots;
   DevBuf<int> owned;
   DevBuf<long long> centers;
@@ -365,9 +367,13 @@ KinitScratch kinit_scratch(gmmb_ctx* c, int k) {
   c->owned.ensure(std::max(k, 1));
   c->centers.ensure(std::max(k, 1));
   c->kstatus.ensure(8);
+  c->kxf.ensure(n);
+  c->ktp.ensure(n);
+  c->kinv.ensure(n);
   return KinitScratch{c->keys.p, c->kd2.p, c->labels.p, c->chosen.p,
                       c->slots.p, c->owned.p, c->centers.p, c->kstatus.p,
-                      reinterpret_cast<unsigned*>(c->kstatus.p + 4)};
+                      reinterpret_cast<unsigned*>(c->kstatus.p + 4), c->kxf.p, c->ktp.p,
+                      c->kinv.p};
 }
 
 void run_kinit(gmmb_ctx* c, int k, uint64_t seed) {
@@ -992,6 +998,7 @@ void gmmb_ctx_destroy(gmmb_ctx* c) {
   c->iout.release(); c->iout2.release(); c->ierr.release(); c->img.release();
   c->iflags.release(); c->in_n.release(); c->gb.release();
   c->keys.release(); c->kd2.release(); c->labels.release(); c->chosen.release();
+  c->kxf.release(); c->ktp.release(); c->kinv.release();
   c->slots.release(); c->owned.release(); c->centers.release(); c->rslots.release();
   c->ticket.release(); c->kstatus.release(); c->ll64.release();
   for (int b = 0; b < 2; ++b) {

@@ -1091,10 +1091,44 @@ __global__ void __launch_bounds__(kSeedThreads, 1)
 // (the global best is no larger than the local best), so each CTA's exact
 // (clock, index) best contains the global winner. The last CTA to finish
 // reduces every CTA's slot in parallel, in a fixed order.
+// FP32 fold prefilter (memory-resident rounds). With u = 2^-24 and M >= every
+// |coordinate| (of points and centres, which are points), the FP32 distance of
+// the rounded coordinates satisfies sqrt(dd32) <= (1 + 4u)(sqrt(dd) + 4.0001 u M)
+// (rounding of x, c, their difference and the 4-term sum; Minkowski), so a
+// point with dd32 > T(d2) >= ((1 + 4u)(sqrt(d2) + 4.0001 u M))^2 cannot have
+// dd < d2: the FP64 coordinates and d2 are only read for the few points with
+// dd32 <= T. T(inf) = inf never filters; NaN / overflowed dd32 never pass.
+__device__ __forceinline__ float fold_threshold(double d2, float M) {
+  if (!(d2 < INFINITY)) return INFINITY;
+  const double s = sqrt(d2) + 4.0001 * 0x1p-24 * static_cast<double>(M);
+  return __double2float_ru(s * s * (1.0 + 0x1p-16));
+}
+__device__ __forceinline__ float dist2f(const float4 p, const float4 c) {
+  const float e0 = p.x - c.x, e1 = p.y - c.y, e2 = p.z - c.z, e3 = p.w - c.w;
+  return fmaf(e3, e3, fmaf(e2, e2, fmaf(e1, e1, e0 * e0)));
+}
+__device__ __forceinline__ float inv_d2(double dd) {  // 1/d2 for the FP32 clocks (0: ineligible)
+  const float fl = __double2float_rn(dd);
+  return dd > 0.0 ? (isinf(fl) ? 1e-38f : rcp_approx(fl)) : 0.f;
+}
+
+// max |coordinate| over the cloud (the prefilter's M): float bits of
+// non-negative values order like the values
+__global__ void absmax_kernel(const double* __restrict__ x64, int64_t n, int d,
+                              unsigned* __restrict__ out) {
+  double m = 0.0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    for (int q = 0; q < d; ++q) m = fmax(m, fabs(x64[q * n + i]));
+  unsigned b = __float_as_uint(__double2float_ru(m));
+  b = __reduce_max_sync(0xffffffffu, b);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, b);
+}
+
 constexpr int kMemThreads = 256;  // 4 CTAs per SM resident: one wave
 constexpr int kMemPPT = 32;  // points per thread held as FP32 clocks in shared memory
 
-__global__ void __launch_bounds__(kMemThreads)
+__global__ void __launch_bounds__(kMemThreads, 4)
     kpp_mem_round_kernel(const double* __restrict__ x64, int64_t n, int r,
                          int k, uint64_t seed, KinitScratch scr, int* ticket,
                          long long* win_io, int d) {
@@ -1115,35 +1149,48 @@ __global__ void __launch_bounds__(kMemThreads)
     for (int q = 0; q < 4; ++q) c[q] = q < d ? x64[q * n + win] : 0.0;
   const uint64_t pre = round_prefix(seed, r);
   float amin = INFINITY;
-  // phase 1: fold centre r-1, FP32 clocks
+  const float Mg = __uint_as_float(scr.counter[1]);
+  const float4 c32 = make_float4(__double2float_rn(c[0]), __double2float_rn(c[1]),
+                                 __double2float_rn(c[2]), __double2float_rn(c[3]));
+  // phase 1: fold centre r-1 (FP32 prefilter, exact FP64 where it cannot
+  // exclude), FP32 clocks
 #pragma unroll 4
   for (int m = 0; m < kMemPPT; ++m) {
     const int64_t i = base + m * G;
     float a = INFINITY;
     if (i < n) {
-      double dcur;
+      float iv;
       if (r > 0) {
-        dcur = scr.d2[i];
-        // 3D clouds: the fourth (zero) coordinate is not read (0 - 0 = 0)
-        const double x3 = d == 4 ? x64[3 * n + i] : 0.0;
-        const double dd = dist2(x64[i], x64[n + i], x64[2 * n + i], x3, c);
-        if (dd < dcur) {
-          dcur = dd;
-          scr.d2[i] = dd;
-          scr.labels[i] = r - 1;
+        iv = scr.inv[i];
+        if (!(dist2f(scr.xf[i], c32) > scr.tp[i])) {
+          const double dcur = scr.d2[i];
+          // 3D clouds: the fourth (zero) coordinate is not read (0 - 0 = 0)
+          const double x3 = d == 4 ? x64[3 * n + i] : 0.0;
+          const double dd = dist2(x64[i], x64[n + i], x64[2 * n + i], x3, c);
+          if (dd < dcur) {
+            scr.d2[i] = dd;
+            scr.labels[i] = r - 1;
+            iv = inv_d2(dd);
+            scr.inv[i] = iv;
+            scr.tp[i] = fold_threshold(dd, Mg);
+          }
         }
       } else {
-        dcur = INFINITY;
+        iv = 0.f;
         scr.d2[i] = INFINITY;
         scr.labels[i] = 0;
+        scr.inv[i] = 0.f;
+        scr.tp[i] = INFINITY;
+        const double x3 = d == 4 ? x64[3 * n + i] : 0.0;
+        scr.xf[i] = make_float4(__double2float_rn(x64[i]), __double2float_rn(x64[n + i]),
+                                __double2float_rn(x64[2 * n + i]), __double2float_rn(x3));
       }
       if (r < k) {
         const float na = nlu_approx(mix64(pre + scr.keys[i]));
         if (r == 0) {
           a = na;
-        } else if (dcur > 0.0) {
-          const float f = __double2float_rn(dcur);
-          a = na * (isinf(f) ? 1e-38f : rcp_approx(f));
+        } else if (iv > 0.f) {
+          a = na * iv;
         }
       }
     }
@@ -1501,6 +1548,7 @@ cudaError_t launch_kpp_seed(const double* x64, int64_t n, int d, int k, uint64_t
   const int grid = static_cast<int>(
       n <= cap ? sm_count * 4 : (n + static_cast<int64_t>(kMemThreads) * kMemPPT - 1) /
                                     (static_cast<int64_t>(kMemThreads) * kMemPPT));
+  absmax_kernel<<<sm_count * 2, 256, 0, s>>>(x64, n, d, scr.counter + 1);
   int* ticket = scr.status;
   long long* win = reinterpret_cast<long long*>(scr.status + 2);
   cudaError_t e = cudaMemsetAsync(scr.status, 0, sizeof(int) * 4, s);

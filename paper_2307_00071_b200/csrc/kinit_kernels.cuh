@@ -23,7 +23,11 @@ struct KinitScratch {
   int* owned;         // [k]
   long long* centers; // [k]
   int* status;        // [4]
-  unsigned* counter;  // [1] grid-barrier arrival counter (zeroed per launch)
+  unsigned* counter;  // [2] grid-barrier arrival counter, max |coordinate| (zeroed per launch)
+  // memory-resident rounds: FP32 coordinates, fold-prefilter thresholds, 1/d2
+  float4* xf;         // [n]
+  float* tp;          // [n]
+  float* inv;         // [n]
 };
 
 // Keys (sogmm.cpp:210-213): key_i = hash of the 4 doubles starting at x_i in
