@@ -30,7 +30,7 @@ namespace cg = cooperative_groups;
 
 // Precision / schedule switches (defaults = production).
 #ifndef GMMB_FLUSH_SUBTILES
-#define GMMB_FLUSH_SUBTILES 2   // sub-tiles per FP32 -> FP64 promotion
+#define GMMB_FLUSH_SUBTILES 4   // 8-point groups per FP32 -> FP64 promotion
 #endif
 #ifndef GMMB_PIPE
 #define GMMB_PIPE 1             // 1: warp-specialised packed kernel when one CTA holds all K
