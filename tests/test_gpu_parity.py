@@ -296,3 +296,24 @@ def test_kinit_memory_variant_3d_duplicates_fallback(gm, orc, ctx):
     lab, cen = gm.kinit(p, 32, 0, ctx=ctx)
     rl, rc = orc.kinit(p, 32, 0)
     assert np.array_equal(cen, rc) and np.array_equal(lab, rl)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [64, 1024])
+def test_em_step_far_outliers_exact_path(gm, orc, ctx, k):
+    """Points far from every component: their unshifted density sums leave
+    [2^-64, 2^64], so the fused E kernel redoes those sub-tiles with the
+    exact max shift (both the single-CTA and the cluster kernel). (Offsets of
+    metres, not kilometres: log-densities of 1e10 are beyond FP32's
+    resolution of which component a point belongs to, a documented limit.)"""
+    base = gm.structured_scene(30000, 9, 0.005)
+    w, mu, cov = fixed_init(orc, base, k)
+    far = base[:40].copy()
+    far[:, :3] += 3.0
+    p = np.vstack([base, far])
+    ll, m1, rm = gm.em_step(p, gm.Gmm(w, mu, cov), 1e-6, ctx=ctx)
+    lg, rll = orc.e_step(p, w, mu, cov)
+    rw, rmu, rcov, rrm = orc.m_step(p, lg, 1e-6)
+    assert rm == rrm
+    assert abs(ll - rll) / abs(rll) < LL_TOL
+    assert_model_close(m1.weights, m1.means, m1.covariances, rw, rmu, rcov, tol=1e-5)
