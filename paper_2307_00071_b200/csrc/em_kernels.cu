@@ -30,7 +30,7 @@ namespace cg = cooperative_groups;
 
 // Precision / schedule switches (defaults = production).
 #ifndef GMMB_FLUSH_SUBTILES
-#define GMMB_FLUSH_SUBTILES 4   // 8-point groups per FP32 -> FP64 promotion
+#define GMMB_FLUSH_SUBTILES 2   // 8-point groups per FP32 -> FP64 promotion
 #endif
 #ifndef GMMB_PIPE
 #define GMMB_PIPE 1             // 1: warp-specialised packed kernel when one CTA holds all K
@@ -663,6 +663,22 @@ __global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
              &sm.xs_full[buf]);
     bulk_g2s(sm.tcs[buf], tc + static_cast<int64_t>(t) * 4, 4 * sizeof(double), &sm.xs_full[buf]);
   };
+  // Each CTA (cluster) takes a contiguous, balanced range of P-point
+  // sub-tiles (a round-robin over 128-point tiles leaves 16 or 17 tiles per
+  // CTA on cfg2: a 5 % tail); the first and last tiles of a range may be
+  // partial. Sub-tile g is sub-tile g % SPT of tile g / SPT.
+  constexpr int SPT = kTile / P;
+  const int64_t last_pts = n - static_cast<int64_t>(ntiles - 1) * kTile;
+  const int64_t total_sub = static_cast<int64_t>(ntiles - 1) * SPT + (last_pts + P - 1) / P;
+  const int64_t per_cl = (total_sub + ncl - 1) / ncl;
+  const int64_t g_begin = min64(static_cast<int64_t>(cid) * per_cl, total_sub);
+  const int64_t g_end = min64(g_begin + per_cl, total_sub);
+  const int t_first = static_cast<int>(g_begin / SPT);
+  const int t_last = g_end > g_begin ? static_cast<int>((g_end - 1) / SPT) : t_first - 1;
+  auto sub_range = [&](int t, int nsub, int& s0, int& s1) {
+    s0 = t == t_first ? static_cast<int>(g_begin % SPT) : 0;
+    s1 = t == t_last ? static_cast<int>((g_end - 1) % SPT) + 1 : nsub;
+  };
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int i = 0; i < kRing; ++i) {
@@ -677,7 +693,7 @@ __global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
       mbar_init(&sm.xbar[b], C * NWH);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (cid < ntiles) issue_tile(cid, 0);
+    if (t_first <= t_last) issue_tile(t_first, 0);
   }
 
   // component constants as pairs (lo = component j, hi = component T + j)
@@ -767,9 +783,10 @@ __global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
     load_consts(PP, NBASE);
     unsigned g = 0;  // global sub-tile counter
     int ti = 0;      // tile iteration
-    for (int t = cid; t < ntiles; t += ncl, ++ti) {
+    for (int t = t_first; t <= t_last; ++t, ++ti) {
       const int npts = static_cast<int>(min64(kTile, n - static_cast<int64_t>(t) * kTile));
-      const int nsub = (npts + P - 1) / P;
+      int s0, s1;
+      sub_range(t, (npts + P - 1) / P, s0, s1);
       const int tb = ti & 1;
       mbar_wait(&sm.xs_full[tb], (ti >> 1) & 1u);
       {
@@ -778,12 +795,12 @@ __global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
         for (int q = 0; q < 4; ++q) ct[q] = sm.tcs[tb][q];
         tile_nb(ct, PP, NB);
       }
-      for (int s = 0; s < nsub; ++s, ++g) {
-        if (j == 0 && s == min(kRing, nsub - 1)) {
+      for (int s = s0; s < s1; ++s, ++g) {
+        if (j == 0 && s == min(s0 + kRing, s1 - 1)) {
           // prefetch the next tile: consumers have started this tile (they
           // read sub-tile g - kRing), so they released the other buffer
-          const int tn = t + ncl;
-          if (tn < ntiles) {
+          const int tn = t + 1;
+          if (tn <= t_last) {
             if (ti >= 1) mbar_wait(&sm.xs_free[tb ^ 1], ((ti - 1) >> 1) & 1u);
             issue_tile(tn, tb ^ 1);
           }
@@ -872,9 +889,10 @@ __global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
   int xb = 0;
   unsigned g = 0;
   int ti = 0;
-  for (int t = cid; t < ntiles; t += ncl, ++ti) {
+  for (int t = t_first; t <= t_last; ++t, ++ti) {
     const int npts = static_cast<int>(min64(kTile, n - static_cast<int64_t>(t) * kTile));
-    const int nsub = (npts + P - 1) / P;
+    int s0, s1;
+    sub_range(t, (npts + P - 1) / P, s0, s1);
     const int tb = ti & 1;
     mbar_wait(&sm.xs_full[tb], (ti >> 1) & 1u);
     f2_t NMU[D];  // -(mu - c_t) as FP32 pairs
@@ -888,7 +906,7 @@ __global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
 #pragma unroll
       for (int q = 0; q < D; ++q) NMU[q] = pk(nm[0][q], nm[1][q]);
     }
-    for (int s = 0; s < nsub; ++s, ++g) {
+    for (int s = s0; s < s1; ++s, ++g) {
       const int q0 = s * P;
       const int slot = g % kRing;
       if constexpr (C > 1) {
