@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
                     int64_t n, int ntiles, ModelBuf b0, ModelBuf b1,
                     const EmState* __restrict__ st, int kpad,
                     double* __restrict__ partials, double* __restrict__ ll_part,
-                    int exact_mode) {
+                    int exact_mode, int split_sub) {
   constexpr int NP = npacked(D);
   constexpr int NS = nstats(D);
   constexpr int T = NWH * 32;  // threads per role
@@ -666,18 +666,28 @@ __global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
   // Each CTA (cluster) takes a contiguous, balanced range of P-point
   // sub-tiles (a round-robin over 128-point tiles leaves 16 or 17 tiles per
   // CTA on cfg2: a 5 % tail); the first and last tiles of a range may be
-  // partial. Sub-tile g is sub-tile g % SPT of tile g / SPT.
+  // partial. Sub-tile g is sub-tile g % SPT of tile g / SPT. With several
+  // CTAs per SM (small K) the SM averages its CTAs' imbalance, and the
+  // round-robin over whole tiles measured faster (split_sub = 0).
   constexpr int SPT = kTile / P;
   const int64_t last_pts = n - static_cast<int64_t>(ntiles - 1) * kTile;
   const int64_t total_sub = static_cast<int64_t>(ntiles - 1) * SPT + (last_pts + P - 1) / P;
-  const int64_t per_cl = (total_sub + ncl - 1) / ncl;
-  const int64_t g_begin = min64(static_cast<int64_t>(cid) * per_cl, total_sub);
-  const int64_t g_end = min64(g_begin + per_cl, total_sub);
+  // range boundaries floor(c * units / ncl): sizes differ by at most one
+  const int64_t g_begin = static_cast<int64_t>(cid) * total_sub / ncl;
+  const int64_t g_end = static_cast<int64_t>(cid + 1) * total_sub / ncl;
   const int t_first = static_cast<int>(g_begin / SPT);
   const int t_last = g_end > g_begin ? static_cast<int>((g_end - 1) / SPT) : t_first - 1;
+  // this CTA's tiles: ti-th tile, and the sub-tiles [s0, s1) it processes
+  const int ntiles_cta = split_sub ? t_last - t_first + 1
+                                   : (cid < ntiles ? (ntiles - 1 - cid) / ncl + 1 : 0);
+  auto tile_of = [&](int ti) { return split_sub ? t_first + ti : cid + ti * ncl; };
   auto sub_range = [&](int t, int nsub, int& s0, int& s1) {
-    s0 = t == t_first ? static_cast<int>(g_begin % SPT) : 0;
-    s1 = t == t_last ? static_cast<int>((g_end - 1) % SPT) + 1 : nsub;
+    s0 = 0;
+    s1 = nsub;
+    if (split_sub) {
+      if (t == t_first) s0 = static_cast<int>(g_begin % SPT);
+      if (t == t_last) s1 = static_cast<int>((g_end - 1) % SPT) + 1;
+    }
   };
   if (threadIdx.x == 0) {
 #pragma unroll
@@ -693,7 +703,7 @@ __global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
       mbar_init(&sm.xbar[b], C * NWH);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (t_first <= t_last) issue_tile(t_first, 0);
+    if (ntiles_cta > 0) issue_tile(tile_of(0), 0);
   }
 
   // component constants as pairs (lo = component j, hi = component T + j)
@@ -783,7 +793,8 @@ __global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
     load_consts(PP, NBASE);
     unsigned g = 0;  // global sub-tile counter
     int ti = 0;      // tile iteration
-    for (int t = t_first; t <= t_last; ++t, ++ti) {
+    for (; ti < ntiles_cta; ++ti) {
+      const int t = tile_of(ti);
       const int npts = static_cast<int>(min64(kTile, n - static_cast<int64_t>(t) * kTile));
       int s0, s1;
       sub_range(t, (npts + P - 1) / P, s0, s1);
@@ -799,8 +810,8 @@ __global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
         if (j == 0 && s == min(s0 + kRing, s1 - 1)) {
           // prefetch the next tile: consumers have started this tile (they
           // read sub-tile g - kRing), so they released the other buffer
-          const int tn = t + 1;
-          if (tn <= t_last) {
+          if (ti + 1 < ntiles_cta) {
+            const int tn = tile_of(ti + 1);
             if (ti >= 1) mbar_wait(&sm.xs_free[tb ^ 1], ((ti - 1) >> 1) & 1u);
             issue_tile(tn, tb ^ 1);
           }
@@ -889,7 +900,8 @@ __global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
   int xb = 0;
   unsigned g = 0;
   int ti = 0;
-  for (int t = t_first; t <= t_last; ++t, ++ti) {
+  for (; ti < ntiles_cta; ++ti) {
+    const int t = tile_of(ti);
     const int npts = static_cast<int>(min64(kTile, n - static_cast<int64_t>(t) * kTile));
     int s0, s1;
     sub_range(t, (npts + P - 1) / P, s0, s1);
@@ -1087,8 +1099,9 @@ cudaError_t launch_estep_ws(const PointsDev& pts, const ModelBuf* bufs, const Em
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = C > 1 ? 1 : 0;
+  const int split_sub = ncl * C <= sm_count ? 1 : 0;  // one CTA per SM: balance sub-tiles
   return cudaLaunchKernelEx(&cfg, kern, pts.xt, pts.tc, pts.n, pts.ntiles, bufs[0], bufs[1], st,
-                            kpad, partials, ll_part, exact_mode);
+                            kpad, partials, ll_part, exact_mode, split_sub);
 }
 
 template <int D, int NW, int C, int P, int CPT>
