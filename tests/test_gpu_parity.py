@@ -317,3 +317,16 @@ def test_em_step_far_outliers_exact_path(gm, orc, ctx, k):
     assert rm == rrm
     assert abs(ll - rll) / abs(rll) < LL_TOL
     assert_model_close(m1.weights, m1.means, m1.covariances, rw, rmu, rcov, tol=1e-5)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [1024, 2048])
+def test_em_step_3d_cluster_kernels(gm, orc, ctx, k):
+    """D = 3 with K > 512 (the cfg4 path: clusters of K / 512 CTAs), on
+    cfg4-like map coordinates."""
+    p = gm.structured_scene(120000, 5, 0.005)[:, :3] * 25 + np.array([100.0, -40.0, 0.0])
+    w, mu, cov = fixed_init(orc, p, k)
+    ll, m1, rm = gm.em_step(p, gm.Gmm(w, mu, cov), 1e-6, ctx=ctx)
+    r = orc.fit_from(p, w, mu, cov, max_iters=1, ll_rel_tol=0.0, cov_reg=1e-6)
+    assert abs(ll - r["final_ll"]) / abs(r["final_ll"]) < LL_TOL
+    assert_model_close(m1.weights, m1.means, m1.covariances, r["w"], r["mu"], r["cov"], tol=1e-5)
