@@ -330,3 +330,16 @@ def test_em_step_3d_cluster_kernels(gm, orc, ctx, k):
     r = orc.fit_from(p, w, mu, cov, max_iters=1, ll_rel_tol=0.0, cov_reg=1e-6)
     assert abs(ll - r["final_ll"]) / abs(r["final_ll"]) < LL_TOL
     assert_model_close(m1.weights, m1.means, m1.covariances, r["w"], r["mu"], r["cov"], tol=1e-5)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k,d", [(700, 4), (1500, 3)])
+def test_em_step_ragged_k_cluster_padding(gm, orc, ctx, k, d):
+    """K between the 512-component CTA sizes: the last CTA of each cluster
+    holds padding components (zero weight, excluded from the statistics)."""
+    p = gm.structured_scene(80000, 6, 0.005)[:, :d]
+    w, mu, cov = fixed_init(orc, p, k)
+    ll, m1, rm = gm.em_step(p, gm.Gmm(w, mu, cov), 1e-6, ctx=ctx)
+    r = orc.fit_from(p, w, mu, cov, max_iters=1, ll_rel_tol=0.0, cov_reg=1e-6)
+    assert abs(ll - r["final_ll"]) / abs(r["final_ll"]) < LL_TOL
+    assert_model_close(m1.weights, m1.means, m1.covariances, r["w"], r["mu"], r["cov"], tol=1e-5)
