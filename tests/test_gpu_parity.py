@@ -343,3 +343,17 @@ def test_em_step_ragged_k_cluster_padding(gm, orc, ctx, k, d):
     r = orc.fit_from(p, w, mu, cov, max_iters=1, ll_rel_tol=0.0, cov_reg=1e-6)
     assert abs(ll - r["final_ll"]) / abs(r["final_ll"]) < LL_TOL
     assert_model_close(m1.weights, m1.means, m1.covariances, r["w"], r["mu"], r["cov"], tol=1e-5)
+
+
+@pytest.mark.gpu
+def test_em_step_k4096_stats_kernel(gm, orc, ctx):
+    """K = 4096 (kMaxK) goes through estep_stats_kernel (barrier per sub-tile,
+    clusters) and a four-chunk commit."""
+    p = gm.structured_scene(60000, 8, 0.005)
+    w, mu, cov = fixed_init(orc, p, 4096)
+    ll, m1, rm = gm.em_step(p, gm.Gmm(w, mu, cov), 1e-6, ctx=ctx)
+    lg, rll = orc.e_step(p, w, mu, cov)
+    rw, rmu, rcov, rrm = orc.m_step(p, lg, 1e-6)
+    assert rm == rrm
+    assert abs(ll - rll) / abs(rll) < LL_TOL
+    assert_model_close(m1.weights, m1.means, m1.covariances, rw, rmu, rcov, tol=1e-5)
