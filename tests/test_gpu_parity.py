@@ -357,3 +357,22 @@ def test_em_step_k4096_stats_kernel(gm, orc, ctx):
     assert rm == rrm
     assert abs(ll - rll) / abs(rll) < LL_TOL
     assert_model_close(m1.weights, m1.means, m1.covariances, rw, rmu, rcov, tol=1e-5)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k,stride", [(1024, 4), (2048, 2)])
+def test_fit_large_k_end_to_end(gm, orc, ctx, k, stride):
+    """cfg5's large-K end: k-means++ + EM to tol 1e-3 through the cluster
+    kernels, on a subsampled cfg2 frame (the oracle's run time) with ~75
+    points per component. (Below ~40 points per component EM amplifies FP32
+    rounding past 1e-4 on any K: scripts/studies/large_k_precision.py.)"""
+    p = frame(gm)[::stride].copy()
+    em = gm.EmParams(100, 1e-3, 1e-6, 0)
+    res = gm.fit_k(p, k, em, ctx=ctx, want_labels=True)
+    ref = orc.fit_k(p, k, max_iters=100, ll_rel_tol=1e-3, cov_reg=1e-6, seed=0)
+    assert np.array_equal(res.centers, ref["centers"])
+    assert res.em_iterations == ref["em_iterations"]
+    assert res.removed_components == ref["removed"]
+    assert ll_err(res.ll_trace, ref["ll_trace"]) < LL_TOL
+    assert_model_close(res.model.weights, res.model.means, res.model.covariances,
+                       ref["w"], ref["mu"], ref["cov"])
