@@ -37,7 +37,7 @@ UNIT = "point*component*iter/s"
 FLOP_PER_UNIT = {4: 62.0, 3: 42.0}     # 2D^2 + 6D + 6
 NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 # DRAM traffic of one fused-E launch at cfg2 K=512 (ncu --set full capture)
-TRAFFIC_BYTES = 5.097e6  # 5,095,936 B read + 1,280 B written per launch
+TRAFFIC_BYTES = 5.095e6  # 5.095 MB read + 256 B written per launch
 TRAFFIC_SRC = "profiles/r1h_estep_ncu.txt"
 
 
