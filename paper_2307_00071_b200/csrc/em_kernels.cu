@@ -29,6 +29,9 @@
 namespace cg = cooperative_groups;
 
 // Precision / schedule switches (defaults = production).
+#ifndef GMMB_REDUCE_CTA_NCL
+#define GMMB_REDUCE_CTA_NCL 256  // above this many partials per component: a CTA per component
+#endif
 #ifndef GMMB_FLUSH_SUBTILES
 #define GMMB_FLUSH_SUBTILES 2   // 8-point groups per FP32 -> FP64 promotion
 #endif
@@ -1313,19 +1316,26 @@ __global__ void em_finalize_kernel(const double* __restrict__ red,
 // Single-device fused second stage: one warp per component reduces the
 // per-CTA partials in a fixed order (lane-strided sums, fixed butterfly) and
 // its lane 0 finalizes the component.
-template <int D>
+// WPC warps per component: one (K large) or the whole 128-thread CTA (small
+// K, where the E kernel runs many CTAs and leaves ncl ~ 1000 partials per
+// component). Lane-strided sums, a fixed butterfly, and (WPC > 1) the warps'
+// sums in warp order: deterministic.
+template <int D, int WPC>
 __global__ void __launch_bounds__(128) em_reduce_finalize_kernel(
     const double* __restrict__ partials, int ncl, int kpad, ModelBuf b0, ModelBuf b1,
     const EmState* __restrict__ st, RecBuf rec) {
   constexpr int NS = nstats(D);
+  __shared__ double red[4][NS];
   if (st->done) return;
-  const int lane = threadIdx.x & 31;
-  const int k = blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (k >= kpad || k >= st->k_cur) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int k = WPC == 1 ? blockIdx.x * 4 + w : blockIdx.x;
+  const int sub = WPC == 1 ? 0 : w;
+  if (k >= kpad || k >= st->k_cur) return;  // uniform over the CTA when WPC > 1
   double acc[NS];
 #pragma unroll
   for (int j = 0; j < NS; ++j) acc[j] = 0.0;
-  for (int c = lane; c < ncl; c += 32) {
+#pragma unroll 4
+  for (int c = sub * 32 + lane; c < ncl; c += 32 * WPC) {
     const double* src = partials + (static_cast<int64_t>(c) * kpad + k) * NS;
 #pragma unroll
     for (int j = 0; j < NS; ++j) acc[j] += src[j];
@@ -1335,11 +1345,26 @@ __global__ void __launch_bounds__(128) em_reduce_finalize_kernel(
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
   }
-  if (lane == 0) {
-    const ModelBuf& mb = st->cur ? b1 : b0;
-    const ModelBuf& fresh = st->cur ? b0 : b1;
-    finalize_component<D>(acc, k, mb, st->cov_reg, rec, fresh);
+  if constexpr (WPC > 1) {
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < NS; ++j) red[w][j] = acc[j];
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      double t = red[0][j];
+#pragma unroll
+      for (int q = 1; q < WPC; ++q) t += red[q][j];
+      acc[j] = t;
+    }
+  } else {
+    if (lane != 0) return;
   }
+  const ModelBuf& mb = st->cur ? b1 : b0;
+  const ModelBuf& fresh = st->cur ? b0 : b1;
+  finalize_component<D>(acc, k, mb, st->cov_reg, rec, fresh);
 }
 
 // ---------------------------------------------------------------------------
@@ -1828,11 +1853,19 @@ cudaError_t launch_em_reduce(int d, const double* partials,
 cudaError_t launch_em_reduce_finalize(int d, const double* partials, int ncl, int k0,
                                      const ModelBuf* bufs, const EmState* st, RecBuf rec,
                                      cudaStream_t s) {
+  // many partials per component (small K: many E CTAs): a CTA per component
+  if (ncl > GMMB_REDUCE_CTA_NCL) {
+    if (d == 4)
+      em_reduce_finalize_kernel<4, 4><<<k0, 128, 0, s>>>(partials, ncl, k0, bufs[0], bufs[1], st, rec);
+    else
+      em_reduce_finalize_kernel<3, 4><<<k0, 128, 0, s>>>(partials, ncl, k0, bufs[0], bufs[1], st, rec);
+    return cudaGetLastError();
+  }
   const int grid = (k0 + 3) / 4;
   if (d == 4)
-    em_reduce_finalize_kernel<4><<<grid, 128, 0, s>>>(partials, ncl, k0, bufs[0], bufs[1], st, rec);
+    em_reduce_finalize_kernel<4, 1><<<grid, 128, 0, s>>>(partials, ncl, k0, bufs[0], bufs[1], st, rec);
   else
-    em_reduce_finalize_kernel<3><<<grid, 128, 0, s>>>(partials, ncl, k0, bufs[0], bufs[1], st, rec);
+    em_reduce_finalize_kernel<3, 1><<<grid, 128, 0, s>>>(partials, ncl, k0, bufs[0], bufs[1], st, rec);
   return cudaGetLastError();
 }
 
