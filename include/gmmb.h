@@ -76,6 +76,19 @@ int gmmb_ctx_create(int device, gmmb_ctx** out);
 int gmmb_nccl_unique_id(void* out128);
 int gmmb_ctx_create_sharded(int device, int rank, int world,
                             const void* nccl_id128, gmmb_ctx** out);
+/* Virtual shards (no reference counterpart; the validation mode of the
+ * sharded path): `world` in-process ranks on ONE device. The
+ * caller creates one context per rank with gmmb_ctx_create_virtual and
+ * drives each from its own host thread with the same calls as NCCL ranks
+ * (e.g. gmmb_fit_k on contiguous shards); the collectives are fixed-order
+ * device reductions over the ranks' buffers instead of NCCL. A failure on
+ * one rank, or destroying one rank's context, aborts the group (its peers'
+ * pending collectives return 1). The group lives until it is released and
+ * every context of it is destroyed. */
+typedef struct gmmb_vgroup gmmb_vgroup;
+int gmmb_vgroup_create(int device, int world, gmmb_vgroup** out);
+void gmmb_vgroup_release(gmmb_vgroup* g);
+int gmmb_ctx_create_virtual(gmmb_vgroup* g, int rank, gmmb_ctx** out);
 void gmmb_ctx_destroy(gmmb_ctx* ctx);
 /* EM loop execution mode (no reference counterpart; measurement aid).
  * 0 (default): the EM loop of a fit is one CUDA graph with a conditional

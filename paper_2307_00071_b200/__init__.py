@@ -88,6 +88,9 @@ _SIGS = {
     "gmmb_ctx_create_sharded": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                ctypes.c_char_p, ctypes.POINTER(_V)]),
     "gmmb_ctx_destroy": (None, [_V]),
+    "gmmb_vgroup_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.POINTER(_V)]),
+    "gmmb_vgroup_release": (None, [_V]),
+    "gmmb_ctx_create_virtual": (ctypes.c_int, [_V, ctypes.c_int, ctypes.POINTER(_V)]),
     "gmmb_device_info": (ctypes.c_int, [_V, _I, _I, _I]),
     "gmmb_fit_k": (ctypes.c_int, [_V, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                   ctypes.POINTER(_EmParams), _D, _D, _D, _D,
@@ -286,14 +289,39 @@ class CholeskyCache:
     log_det_terms: np.ndarray  # (M,) = sum ln diag P
 
 
+class VGroup:
+    """In-process group of `world` virtual ranks on one device
+    (gmmb_vgroup): the sharded fit's validation mode, the collectives being
+    fixed-order device reductions instead of NCCL (include/gmmb.h)."""
+
+    def __init__(self, world: int, device: int = 0):
+        h = ctypes.c_void_p()
+        _check(load().gmmb_vgroup_create(device, world, ctypes.byref(h)))
+        self._h, self.world, self.device = h, world, device
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            load().gmmb_vgroup_release(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Context:
     """One CUDA device + stream + reusable device buffers (gmmb_ctx)."""
 
     def __init__(self, device: int = 0, rank: int = 0, world: int = 1,
-                 nccl_id: Optional[bytes] = None):
+                 nccl_id: Optional[bytes] = None, vgroup: Optional[VGroup] = None):
         lib = load()
         h = ctypes.c_void_p()
-        if world > 1:
+        if vgroup is not None:
+            _check(lib.gmmb_ctx_create_virtual(vgroup._h, rank, ctypes.byref(h)))
+            world, device = vgroup.world, vgroup.device
+        elif world > 1:
             if nccl_id is None or len(nccl_id) != 128:
                 raise ValueError("sharded context needs the 128-byte NCCL id")
             _check(lib.gmmb_ctx_create_sharded(device, rank, world, nccl_id, ctypes.byref(h)))
@@ -428,6 +456,73 @@ def fit_k(points, k: int, em: EmParams = EmParams(), ctx: Optional[Context] = No
                              _ptr(out[0]), _ptr(out[1]), _ptr(out[2]), _ptr(ll),
                              ctypes.byref(st), _ptr(lab, _I32), _ptr(cen, _I64)))
     return _result(out, ll, st, lab, cen)
+
+
+def shard_bounds(n: int, world: int) -> list:
+    """Contiguous shards [lo, hi) of n points over `world` ranks (the first
+    n % world ranks take one more point)."""
+    q, r = divmod(n, world)
+    out, lo = [], 0
+    for i in range(world):
+        hi = lo + q + (1 if i < r else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+def fit_k_vsharded(points, k: int, em: EmParams = EmParams(), world: int = 2,
+                   device: int = 0, want_labels: bool = False, fit_from: Optional[Gmm] = None,
+                   contexts: Optional[list] = None) -> list:
+    """The point-sharded fit run as `world` virtual ranks
+    on one device: contiguous shards, one host thread per rank calling
+    gmmb_fit_k (or gmmb_fit_from with `fit_from`) on its own context; the
+    statistics all-reduce and k-means++ exchange are fixed-order device
+    reductions. Returns the per-rank FitResults (identical models; labels
+    per shard). `contexts` (from vshard_contexts) reuses contexts."""
+    import threading
+    p, n, d = _points(points)
+    own = contexts is None
+    grp = None
+    if own:
+        grp = VGroup(world, device)
+        contexts = [Context(vgroup=grp, rank=r) for r in range(world)]
+    world = len(contexts)
+    bounds = shard_bounds(n, world)
+    res: list = [None] * world
+    err: list = [None] * world
+
+    def run(r):
+        lo, hi = bounds[r]
+        try:
+            if fit_from is not None:
+                res[r] = globals()["fit_from"](p[lo:hi], fit_from, em, ctx=contexts[r])
+            else:
+                res[r] = fit_k(p[lo:hi], k, em, ctx=contexts[r], want_labels=want_labels)
+        except BaseException as e:  # noqa: BLE001 - re-raised below
+            err[r] = e
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if own:
+        for c in contexts:
+            c.close()
+        grp.close()
+    for e in err:
+        if e is not None:
+            raise e
+    return res
+
+
+def vshard_contexts(world: int, device: int = 0) -> list:
+    """`world` virtual-rank contexts sharing one group (for repeated
+    fit_k_vsharded calls); close them with Context.close()."""
+    grp = VGroup(world, device)
+    ctxs = [Context(vgroup=grp, rank=r) for r in range(world)]
+    grp.close()  # the contexts keep the group alive
+    return ctxs
 
 
 @dataclasses.dataclass

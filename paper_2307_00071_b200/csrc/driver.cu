@@ -9,9 +9,6 @@
 // sharded) -> [per-component finalize] -> [commit]. Convergence is decided on
 // the device (commit kernel); the host reads the 64-byte state once per
 // chunk to stop enqueuing.
-#include <dlfcn.h>
-#include <nccl.h>
-
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -29,6 +26,7 @@
 #include "inference.cuh"
 #include "ingest.cuh"
 #include "gbms.cuh"
+#include "comm.cuh"
 
 using namespace gmmb;
 
@@ -44,44 +42,6 @@ struct Err {
 void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) {
     throw Err{1, std::string(what) + ": " + cudaGetErrorString(e)};
-  }
-}
-
-// ---- NCCL, loaded lazily (only sharded contexts need it) -----------------
-struct Nccl {
-  void* h = nullptr;
-  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
-  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t,
-                            ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t,
-                            ncclComm_t, cudaStream_t) = nullptr;
-  const char* (*GetErrorString)(ncclResult_t) = nullptr;
-};
-
-Nccl& nccl() {
-  static Nccl n;
-  if (!n.h) {
-    n.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!n.h) throw Err{1, std::string("cannot load libnccl.so.2: ") + dlerror()};
-    n.GetUniqueId = (decltype(n.GetUniqueId))dlsym(n.h, "ncclGetUniqueId");
-    n.CommInitRank = (decltype(n.CommInitRank))dlsym(n.h, "ncclCommInitRank");
-    n.CommDestroy = (decltype(n.CommDestroy))dlsym(n.h, "ncclCommDestroy");
-    n.AllReduce = (decltype(n.AllReduce))dlsym(n.h, "ncclAllReduce");
-    n.AllGather = (decltype(n.AllGather))dlsym(n.h, "ncclAllGather");
-    n.GetErrorString = (decltype(n.GetErrorString))dlsym(n.h, "ncclGetErrorString");
-    if (!n.GetUniqueId || !n.CommInitRank || !n.AllReduce || !n.AllGather) {
-      throw Err{1, "libnccl.so.2 lacks required symbols"};
-    }
-  }
-  return n;
-}
-
-void nck(ncclResult_t r, const char* what) {
-  if (r != ncclSuccess) {
-    throw Err{1, std::string(what) + ": " +
-                     (nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error")};
   }
 }
 
@@ -130,7 +90,7 @@ struct gmmb_ctx {
   long long launches = 0;         // kernels of this library enqueued by the current call
   // sharding
   int rank = 0, world = 1;
-  ncclComm_t comm = nullptr;
+  Comm* comm = nullptr;            // world > 1: NCCL or virtual ranks (comm.cuh)
   // resident cloud
   int64_t n = 0, offset = 0, n_global = 0;
   int d = 0;
@@ -199,6 +159,15 @@ int guarded(F&& f) {
     g_err = e.what();
     return 1;
   }
+}
+
+// guarded() for calls that may run collectives: a failure on this rank
+// aborts a virtual group so that its peers do not wait forever
+template <typename F>
+int guarded_coll(gmmb_ctx* c, F&& f) {
+  const int rc = guarded(f);
+  if (rc != 0 && c && c->comm) c->comm->abort();
+  return rc;
 }
 
 void set_device(gmmb_ctx* c) { ck(cudaSetDevice(c->device), "cudaSetDevice"); }
@@ -287,11 +256,17 @@ void raise_state_error(const EmState& h) {
   }
 }
 
+// Collectives of a sharded context (comm.cuh): NCCL or in-process virtual
+// ranks.
+void coll(gmmb_ctx* c, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  throw Err{1, std::string(what) + ": " + c->comm->last_error()};
+}
+
 void allreduce_sum(gmmb_ctx* c, double* p, int64_t count) {
   if (c->world <= 1) return;
-  nck(nccl().AllReduce(p, p, static_cast<size_t>(count), ncclFloat64, ncclSum,
-                       c->comm, c->s),
-      "ncclAllReduce");
+  coll(c, c->comm->allreduce(p, static_cast<size_t>(count), DType::kF64, RedOp::kSum, c->s),
+       "allreduce (statistics)");
 }
 
 void moments_allreduce_cb(double* p, int64_t count, void* ctx) {
@@ -349,6 +324,17 @@ void check_cloud_flags(gmmb_ctx* c) {
   int f[4];
   ck(cudaMemcpyAsync(f, c->flags.p, sizeof(f), cudaMemcpyDeviceToHost, c->s), "flags D2H");
   ck(cudaStreamSynchronize(c->s), "sync");
+  if (c->world > 1) {
+    // PointCloud4D::validate over the whole (sharded) cloud: every rank
+    // reports the same error
+    int v[2] = {(f[0] & 1) ? 1 : 0, (f[0] & 2) ? 1 : 0};
+    c->kstatus.ensure(8);
+    copy_sync(c, c->kstatus.p + 6, v, sizeof(v), cudaMemcpyHostToDevice);
+    coll(c, c->comm->allreduce(c->kstatus.p + 6, 2, DType::kI32, RedOp::kSum, c->s),
+         "allreduce (cloud flags)");
+    copy_sync(c, v, c->kstatus.p + 6, sizeof(v), cudaMemcpyDeviceToHost);
+    f[0] = (v[0] ? 1 : 0) | (v[1] ? 2 : 0);
+  }
   if (f[0] & 1) throw Err{3, "point cloud contains non-finite values"};
   if (f[0] & 2) throw Err{3, "intensity outside [0, 1]"};
 }
@@ -410,7 +396,7 @@ void run_kinit(gmmb_ctx* c, int k, uint64_t seed) {
     mine[6] = static_cast<double>(n);
     c->dense.ensure(8);
     copy_sync(c, c->dense.p, mine.data(), sizeof(double) * 8, cudaMemcpyHostToDevice);
-    nck(nccl().AllGather(c->dense.p, g, 8, ncclFloat64, c->comm, c->s), "ncclAllGather");
+    coll(c, c->comm->allgather(c->dense.p, g, 8 * sizeof(double), c->s), "allgather (shard heads)");
     std::vector<double> all(static_cast<size_t>(W) * 8);
     ck(cudaMemcpyAsync(all.data(), g, sizeof(double) * W * 8, cudaMemcpyDeviceToHost, c->s), "D2H");
     ck(cudaStreamSynchronize(c->s), "sync");
@@ -428,49 +414,33 @@ void run_kinit(gmmb_ctx* c, int k, uint64_t seed) {
     ck(launch_kpp_round(c->x64.p, n, c->offset, r, seed, all, W, ks, mine, c->ticket.p,
                         c->sm_count, c->s),
        "kpp_round");
-    nck(nccl().AllGather(mine, all, sizeof(KppRankSlot), ncclUint8, c->comm, c->s),
-        "ncclAllGather");
+    coll(c, c->comm->allgather(mine, all, sizeof(KppRankSlot), c->s), "allgather (k-means++)");
   }
   ck(launch_kpp_final(c->x64.p, n, c->offset, k, all, W, ks, c->s), "kpp_final");
-  // global owned counts; the (rare) fix-up runs on the host over ranks
+  // global owned counts; the (rare) fix-up (sogmm.cpp:315-331) runs as a
+  // host loop over the empty components, each step one device search for
+  // the donor's lowest local index and a min over ranks
+  coll(c, c->comm->allreduce(c->owned.p, k, DType::kI32, RedOp::kSum, c->s), "allreduce (owned)");
   std::vector<int> owned(k);
-  {
-    c->ll64.ensure(static_cast<size_t>(k) + 1);
-    nck(nccl().AllReduce(c->owned.p, c->owned.p, k, ncclInt32, ncclSum, c->comm, c->s),
-        "ncclAllReduce");
-    ck(cudaMemcpyAsync(owned.data(), c->owned.p, sizeof(int) * k, cudaMemcpyDeviceToHost, c->s),
-       "owned D2H");
-    ck(cudaStreamSynchronize(c->s), "sync");
-  }
-  bool any_empty = false;
-  for (int b = 0; b < k; ++b) any_empty |= owned[b] == 0;
-  if (!any_empty) return;
-  std::vector<int32_t> lab(n);
-  copy_sync(c, lab.data(), c->labels.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost);
+  copy_sync(c, owned.data(), c->owned.p, sizeof(int) * k, cudaMemcpyDeviceToHost);
+  c->ll64.ensure(2);
   for (int b = 0; b < k; ++b) {
     if (owned[b] > 0) continue;
     int donor = 0;
     for (int q = 1; q < k; ++q)
       if (owned[q] > owned[donor]) donor = q;
-    long long lo = std::numeric_limits<long long>::max();
-    for (int64_t i = 0; i < n; ++i) {
-      if (lab[i] == donor) {
-        lo = c->offset + i;
-        break;
-      }
+    ck(launch_first_label(n, c->offset, ks, donor, c->ll64.p, c->s), "first_label");
+    coll(c, c->comm->allreduce(c->ll64.p, 1, DType::kI64, RedOp::kMin, c->s), "allreduce (fix-up)");
+    long long lo = 0;
+    copy_sync(c, &lo, c->ll64.p, sizeof(lo), cudaMemcpyDeviceToHost);
+    if (lo == std::numeric_limits<long long>::max()) continue;  // donor owns nothing anywhere
+    if (lo >= c->offset && lo < c->offset + n) {
+      const int32_t v = b;
+      copy_sync(c, c->labels.p + (lo - c->offset), &v, sizeof(v), cudaMemcpyHostToDevice);
     }
-    copy_sync(c, c->ll64.p, &lo, sizeof(lo), cudaMemcpyHostToDevice);
-    nck(nccl().AllReduce(c->ll64.p, c->ll64.p, 1, ncclInt64, ncclMin, c->comm, c->s),
-        "ncclAllReduce");
-    ck(cudaMemcpyAsync(&lo, c->ll64.p, sizeof(lo), cudaMemcpyDeviceToHost, c->s), "D2H");
-    ck(cudaStreamSynchronize(c->s), "sync");
-    if (lo != std::numeric_limits<long long>::max()) {
-      if (lo >= c->offset && lo < c->offset + n) lab[lo - c->offset] = b;
-      owned[donor]--;
-      owned[b]++;
-    }
+    owned[donor]--;
+    owned[b]++;
   }
-  copy_sync(c, c->labels.p, lab.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice);
 }
 
 // ---- M step from labels / dense log_gamma -> model buffer st->cur -------
@@ -880,6 +850,45 @@ GbmsResultHost run_gbms(gmmb_ctx* c, const gmmb_gbms_params* gp, double* modes, 
   return res;
 }
 
+// Sharded entry: runs `checks` (which may throw Err), then one all-reduce of
+// [shard sizes..., error codes...] so that every rank learns the global size,
+// its offset and whether ANY rank failed; all ranks then fail together (the
+// failing rank with its own message, the others naming the first bad rank).
+template <typename F>
+void shard_exchange(gmmb_ctx* c, int64_t n, F&& checks, int64_t* off, int64_t* tot) {
+  set_device(c);
+  const int W = c->world;
+  int code = 0;
+  std::string msg;
+  try {
+    checks();
+  } catch (const Err& e) {
+    code = e.code;
+    msg = e.msg;
+  }
+  c->ll64.ensure(static_cast<size_t>(2 * W) + 1);
+  std::vector<long long> v(2 * W, 0);
+  v[c->rank] = code ? 0 : n;
+  v[W + c->rank] = code;
+  copy_sync(c, c->ll64.p, v.data(), sizeof(long long) * 2 * W, cudaMemcpyHostToDevice);
+  coll(c, c->comm->allreduce(c->ll64.p, 2 * W, DType::kI64, RedOp::kSum, c->s),
+       "allreduce (shard sizes)");
+  copy_sync(c, v.data(), c->ll64.p, sizeof(long long) * 2 * W, cudaMemcpyDeviceToHost);
+  if (code) throw Err{code, msg};
+  for (int r = 0; r < W; ++r) {
+    if (v[W + r]) {
+      throw Err{static_cast<int>(v[W + r]),
+                "sharded fit: rank " + std::to_string(r) + " rejected its input"};
+    }
+  }
+  *off = 0;
+  *tot = 0;
+  for (int r = 0; r < W; ++r) {
+    if (r < c->rank) *off += v[r];
+    *tot += v[r];
+  }
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -932,7 +941,8 @@ void gmmb_em_params_default(gmmb_em_params* p) {
   p->seed = 0;
 }
 
-static int create(int device, int rank, int world, const void* id, gmmb_ctx** out) {
+static int create(int device, int rank, int world, const void* id, VGroup* vg,
+                  gmmb_ctx** out) {
   return guarded([&] {
     if (!out) throw Err{2, "null output"};
     *out = nullptr;
@@ -953,10 +963,14 @@ static int create(int device, int rank, int world, const void* id, gmmb_ctx** ou
       ck(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking), "cudaStreamCreate");
       for (auto& e : c->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
       ck(cudaMallocHost(&c->st_host, sizeof(EmState)), "cudaMallocHost");
-      if (world > 1) {
-        ncclUniqueId uid;
-        std::memcpy(&uid, id, sizeof(uid));
-        nck(nccl().CommInitRank(&c->comm, world, uid, rank), "ncclCommInitRank");
+      if (vg) {
+        c->comm = make_virtual_comm(vg, rank);
+      } else if (world > 1) {
+        try {
+          c->comm = make_nccl_comm(id, rank, world);
+        } catch (const std::exception& e) {
+          throw Err{1, e.what()};
+        }
       }
     } catch (...) {
       gmmb_ctx_destroy(c);
@@ -966,15 +980,50 @@ static int create(int device, int rank, int world, const void* id, gmmb_ctx** ou
   });
 }
 
-int gmmb_ctx_create(int device, gmmb_ctx** out) { return create(device, 0, 1, nullptr, out); }
+int gmmb_ctx_create(int device, gmmb_ctx** out) {
+  return create(device, 0, 1, nullptr, nullptr, out);
+}
 
 int gmmb_nccl_unique_id(void* out128) {
   return guarded([&] {
     if (!out128) throw Err{2, "null output"};
-    ncclUniqueId uid;
-    nck(nccl().GetUniqueId(&uid), "ncclGetUniqueId");
-    std::memcpy(out128, &uid, sizeof(uid));
+    const char* err = nullptr;
+    if (nccl_unique_id(out128, &err) != 0) throw Err{1, std::string("ncclGetUniqueId: ") + err};
   });
+}
+
+struct gmmb_vgroup {
+  VGroup* g;
+};
+
+int gmmb_vgroup_create(int device, int world, gmmb_vgroup** out) {
+  return guarded([&] {
+    if (!out) throw Err{2, "null output"};
+    *out = nullptr;
+    int ndev = 0;
+    ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) throw Err{2, "invalid device index"};
+    if (world < 1 || world > 64) throw Err{2, "virtual world must be 1..64"};
+    try {
+      *out = new gmmb_vgroup{vgroup_create(device, world)};
+    } catch (const std::exception& e) {
+      throw Err{1, e.what()};
+    }
+  });
+}
+
+void gmmb_vgroup_release(gmmb_vgroup* g) {
+  if (!g) return;
+  vgroup_release(g->g);
+  delete g;
+}
+
+int gmmb_ctx_create_virtual(gmmb_vgroup* g, int rank, gmmb_ctx** out) {
+  if (!g || rank < 0 || rank >= vgroup_world(g->g)) {
+    g_err = "invalid virtual group / rank";
+    return 2;
+  }
+  return create(vgroup_device(g->g), rank, vgroup_world(g->g), nullptr, g->g, out);
 }
 
 int gmmb_ctx_create_sharded(int device, int rank, int world, const void* nccl_id128,
@@ -983,14 +1032,14 @@ int gmmb_ctx_create_sharded(int device, int rank, int world, const void* nccl_id
     g_err = "invalid rank/world";
     return 2;
   }
-  return create(device, rank, world, nccl_id128, out);
+  return create(device, rank, world, nccl_id128, nullptr, out);
 }
 
 void gmmb_ctx_destroy(gmmb_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->s) cudaStreamSynchronize(c->s);
-  if (c->comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
+  delete c->comm;
   c->x64.release(); c->xt.release(); c->tc.release(); c->perm.release();
   c->bbox_part.release(); c->mkeys_in.release(); c->mkeys_out.release();
   c->midx.release(); c->sort_tmp.release(); c->flags.release(); c->hidx.release();
@@ -1042,7 +1091,7 @@ int gmmb_upload(gmmb_ctx* c, const double* pts, int64_t n, int d, int64_t offset
 int gmmb_fit_k_resident(gmmb_ctx* c, int K, const gmmb_em_params* em, double* w_out,
                         double* mu_out, double* cov_out, double* ll_trace,
                         gmmb_fit_stats* stats, int32_t* labels, int64_t* centers) {
-  return guarded([&] {
+  return guarded_coll(c, [&] {
     if (!c) throw Err{2, "null context"};
     fit_k_resident(c, K, em, w_out, mu_out, cov_out, ll_trace, stats, labels, centers);
   });
@@ -1052,7 +1101,7 @@ int gmmb_fit_from_resident(gmmb_ctx* c, int m, const double* w0, const double* m
                            const double* cov0, const gmmb_em_params* em,
                            double* w_out, double* mu_out, double* cov_out,
                            double* ll_trace, gmmb_fit_stats* stats) {
-  return guarded([&] {
+  return guarded_coll(c, [&] {
     if (!c) throw Err{2, "null context"};
     fit_from_resident(c, m, w0, mu0, cov0, em, w_out, mu_out, cov_out, ll_trace, stats);
   });
@@ -1062,30 +1111,27 @@ int gmmb_fit_k(gmmb_ctx* c, const double* pts, int64_t n, int d, int K,
                const gmmb_em_params* em, double* w_out, double* mu_out,
                double* cov_out, double* ll_trace, gmmb_fit_stats* stats,
                int32_t* labels, int64_t* centers) {
-  return guarded([&] {
+  return guarded_coll(c, [&] {
     if (!c) throw Err{2, "null context"};
-    check_d(d);
-    if (n < 1) throw Err{3, "point cloud is empty"};
-    check_em(em);
-    const int64_t ng = c->world > 1 ? -1 : n;
     if (c->world > 1) {
-      // global N and this rank's offset via allreduce of the shard sizes
-      set_device(c);
-      c->ll64.ensure(static_cast<size_t>(c->world) + 1);
-      std::vector<long long> sizes(c->world, 0);
-      sizes[c->rank] = n;
-      copy_sync(c, c->ll64.p, sizes.data(), sizeof(long long) * c->world, cudaMemcpyHostToDevice);
-      nck(nccl().AllReduce(c->ll64.p, c->ll64.p, c->world, ncclInt64, ncclSum, c->comm, c->s), "allreduce");
-      ck(cudaMemcpyAsync(sizes.data(), c->ll64.p, sizeof(long long) * c->world, cudaMemcpyDeviceToHost, c->s), "D2H");
-      ck(cudaStreamSynchronize(c->s), "sync");
+      // every rank validates, then one exchange of (size, error) decides
+      // for all: a rank that failed alone must not leave its peers blocked
+      // in a later collective
       int64_t off = 0, tot = 0;
-      for (int r = 0; r < c->world; ++r) {
-        if (r < c->rank) off += sizes[r];
-        tot += sizes[r];
-      }
+      shard_exchange(c, n, [&] {
+        check_d(d);
+        if (n < 1) throw Err{3, "point cloud is empty"};
+        if (!pts) throw Err{2, "null point buffer"};
+        if (n > (int64_t{1} << 31) - 1) throw Err{2, "too many points for one device"};
+        check_em(em);
+        if (K < 1) throw Err{2, "kinit: k must satisfy 1 <= k <= N"};
+      }, &off, &tot);
       upload(c, pts, n, d, off, tot);
     } else {
-      upload(c, pts, n, d, 0, ng);
+      check_d(d);
+      if (n < 1) throw Err{3, "point cloud is empty"};
+      check_em(em);
+      upload(c, pts, n, d, 0, n);
     }
     fit_k_resident(c, K, em, w_out, mu_out, cov_out, ll_trace, stats, labels, centers);
   });
@@ -1095,10 +1141,22 @@ int gmmb_fit_from(gmmb_ctx* c, const double* pts, int64_t n, int d, int m,
                   const double* w0, const double* mu0, const double* cov0,
                   const gmmb_em_params* em, double* w_out, double* mu_out,
                   double* cov_out, double* ll_trace, gmmb_fit_stats* stats) {
-  return guarded([&] {
+  return guarded_coll(c, [&] {
     if (!c) throw Err{2, "null context"};
-    if (c->world > 1) throw Err{2, "use gmmb_upload with offsets for sharded fit_from"};
-    upload(c, pts, n, d, 0, n);
+    if (c->world > 1) {
+      int64_t off = 0, tot = 0;
+      shard_exchange(c, n, [&] {
+        check_d(d);
+        if (n < 1) throw Err{3, "point cloud is empty"};
+        if (!pts) throw Err{2, "null point buffer"};
+        if (n > (int64_t{1} << 31) - 1) throw Err{2, "too many points for one device"};
+        check_em(em);
+        if (m < 1) throw Err{2, "model has no components"};
+      }, &off, &tot);
+      upload(c, pts, n, d, off, tot);
+    } else {
+      upload(c, pts, n, d, 0, n);
+    }
     fit_from_resident(c, m, w0, mu0, cov0, em, w_out, mu_out, cov_out, ll_trace, stats);
   });
 }

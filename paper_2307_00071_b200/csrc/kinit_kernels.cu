@@ -1504,7 +1504,26 @@ __global__ void kpp_final_kernel(const double* __restrict__ x64, int64_t n,
   atomicAdd(&scr.owned[lab], 1);
 }
 
+// lowest GLOBAL index of a point labelled `donor` on this shard (LLONG_MAX
+// if none): the sharded owned fix-up's search (sogmm.cpp:323-329)
+__global__ void first_label_kernel(int64_t n, int64_t offset, const int32_t* __restrict__ labels,
+                                   int donor, long long* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n && labels[i] == donor) atomicMin(reinterpret_cast<unsigned long long*>(out),
+                                             static_cast<unsigned long long>(offset + i));
+}
+
 }  // namespace
+
+cudaError_t launch_first_label(int64_t n, int64_t offset, KinitScratch scr, int donor,
+                               long long* out, cudaStream_t s) {
+  const long long init = LLONG_MAX;
+  cudaError_t e = cudaMemcpyAsync(out, &init, sizeof(init), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  first_label_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, s>>>(n, offset, scr.labels,
+                                                                      donor, out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_keys(const double* x64, int64_t n, const double* tail,
                         uint64_t* keys, cudaStream_t s) {

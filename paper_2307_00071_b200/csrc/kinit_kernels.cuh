@@ -66,4 +66,9 @@ cudaError_t launch_kpp_final(const double* x64, int64_t n, int64_t offset,
                              int k, const KppRankSlot* prev, int world,
                              KinitScratch scr, cudaStream_t s);
 
+// sharded fix-up: *out = lowest global index i with labels[i - offset] ==
+// donor on this shard, LLONG_MAX if none
+cudaError_t launch_first_label(int64_t n, int64_t offset, KinitScratch scr, int donor,
+                               long long* out, cudaStream_t s);
+
 }  // namespace gmmb
