@@ -1,13 +1,22 @@
 #!/usr/bin/env python
 """Benchmark: EM point*component*iterations/s and ms per GMM fit (BASELINE.json).
 
-A step is one full GMM fit of the hot path on one batch of synthetic input:
-kinit (k-means++) -> initial M step -> EM to tolerance, for BASELINE cfg2
-(one 640x480 synthetic depth frame -> 307,200 4D points, K=512, seed 0,
-ll_rel_tol 1e-3, cov_reg 1e-6) on every GPU. With N > 1 GPUs (torchrun) each
-rank fits its own frame (cfg3-style replicas: frame r jittered by 2 mm, seed
-r): weak scaling, no collective on the data path; the job value is all
-ranks' units over the max-over-ranks time.
+A step is one full GMM fit of the hot path (layout -> kinit (k-means++) ->
+initial M step -> EM to tolerance) on one batch of synthetic input.
+
+--config cfg2 (default; BASELINE cfg2): one 640x480 synthetic depth frame ->
+    307,200 4D points, K=512, seed 0, ll_rel_tol 1e-3, cov_reg 1e-6. With
+    N > 1 GPUs (torchrun) each rank fits its own frame (frame r jittered by
+    2 mm, seed r: cfg3-style frame replicas, weak scaling, no collective on
+    the data path); the job value is all ranks' units over the max-over-ranks
+    time.
+--config cfg4 (BASELINE cfg4): the 4M-point 3D map (make_structured_scene x 25
+    + (100, -40, 0) m), K=2048, tol 1e-3. With N > 1 the points are sharded
+    contiguously over the ranks (one NCCL communicator; per-iteration
+    statistics all-reduce + per-round k-means++ candidate all-gather): strong
+    scaling, value = global units / max-over-ranks time. --vshard G runs the
+    same sharded path as G virtual ranks on one GPU (protocol check, not a
+    scaling number).
 
 value  = sum of units (N * K_t per E step) / device time of the fits, inputs
          resident in HBM (CUDA events inside the library around each fit;
@@ -15,7 +24,9 @@ value  = sum of units (N * K_t per E step) / device time of the fits, inputs
 e2e    = the same metric through the C ABI call with host (pinned) buffers:
          H2D of the points and D2H of the model inside the timed region.
 --impl reference times the reference algorithm on the host CPU (the FP64
-oracle port, all host threads; the reference itself cannot be built here).
+oracle port, all host threads; the reference itself cannot be built here),
+building its inputs with the oracle's restatement of the reference
+generators — it never loads libgmmb.
 """
 from __future__ import annotations
 
@@ -36,9 +47,10 @@ METRIC = "EM point*component*iters/sec and ms per GMM fit"
 UNIT = "point*component*iter/s"
 FLOP_PER_UNIT = {4: 62.0, 3: 42.0}     # 2D^2 + 6D + 6
 NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
-# DRAM traffic of one fused-E launch at cfg2 K=512 (ncu --set full capture)
-TRAFFIC_BYTES = 5.095e6  # 5.095 MB read + 256 B written per launch
-TRAFFIC_SRC = "profiles/r1h_estep_ncu.txt"
+# DRAM traffic per launch of the dominant kernel, from ncu --set full
+# captures of exactly these configurations (emitted only when the run's
+# configuration matches the capture; re-captured on every kernel change).
+TRAFFIC = {("cfg2", 512): (5.095e6, "profiles/r1h_estep_ncu.txt")}
 
 
 def parse():
@@ -47,11 +59,17 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="gmmb", choices=["gmmb", "reference"])
-    ap.add_argument("--k", type=int, default=512)
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg4"])
+    ap.add_argument("--k", type=int, default=0, help="override K (0: the config's)")
     ap.add_argument("--tol", type=float, default=1e-3)
+    ap.add_argument("--vshard", type=int, default=0,
+                    help="cfg4 on one GPU as G virtual ranks (sharded-path check)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.k == 0:
+        a.k = 512 if a.config == "cfg2" else 2048
+    return a
 
 
 def dist_env():
@@ -61,11 +79,54 @@ def dist_env():
     return rank, world, local
 
 
-def make_points(gm, rank):
-    p = gm.synthetic_frame_cloud()          # make_synthetic_frame + image_pair_to_cloud
-    if rank > 0:                            # cfg3 frame r: xyz jittered 2 mm, seed r
-        p = gm.jitter_cloud(p, 0.002, rank)
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---- inputs: `gen` is the product's host generators (GPU arm) or the
+# oracle's restatement of the reference generators (reference arm, which
+# must not load libgmmb); the two are bit-identical (tests/test_abi.py) ------
+def cfg2_points(gen, rank):
+    p = gen.synthetic_frame_cloud()             # make_synthetic_frame + image_pair_to_cloud
+    if rank > 0:                                # cfg3 frame r: xyz jittered 2 mm, seed r
+        p = gen.jitter_cloud(p, 0.002, rank)
     return p
+
+
+def cfg4_points(gen):
+    s = gen.structured_scene(4_000_000, 4, 0.005)[:, :3]
+    return s * 25.0 + np.array([100.0, -40.0, 0.0])
+
+
+def shard_bounds(n, world):
+    q, r = divmod(n, world)
+    out, lo = [], 0
+    for i in range(world):
+        hi = lo + q + (1 if i < r else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+def config_dict(args, world):
+    """Identical for both arms (the driver compares them)."""
+    if args.config == "cfg2":
+        return {"workload": "cfg2: 4D frame N=307200, K=%d, k-means++ + EM to tol %g "
+                            "(one fit per GPU per step)" % (args.k, args.tol),
+                "global_batch": world, "points_per_fit": 307200, "k": args.k,
+                "parallelism": "replicas%d" % world,
+                "l2": "flushed between steps (256 MiB write)"}
+    par = "shard%d" % world if world > 1 else ("vshard%d" % args.vshard if args.vshard else "1")
+    return {"workload": "cfg4: 3D map N=4000000, K=%d, k-means++ + EM to tol %g "
+                        "(one fit per step, points sharded over the GPUs)" % (args.k, args.tol),
+            "global_batch": 1, "points_per_fit": 4_000_000, "k": args.k, "parallelism": par,
+            "l2": "flushed between steps (256 MiB write); inputs 96 MB > L2"}
 
 
 class Clocks:
@@ -108,10 +169,7 @@ class Clocks:
         for line in open(self.path):
             parts = [x.strip() for x in line.split(",")]
             if len(parts) >= 8:
-                try:
-                    rows.append(parts)
-                except ValueError:
-                    pass
+                rows.append(parts)
         try:
             os.remove(self.path)
         except OSError:
@@ -128,60 +186,102 @@ class Clocks:
                 "samples": len(rows)}
 
 
-def cpu_fit_rate(points, k, tol, budget_s, steps=None):
-    """Times the FP64 oracle port (all host threads) on full cfg fits."""
+# ---- CPU reference (oracle port) ---------------------------------------------
+def cpu_cfg2_rate(points, k, tol, budget_s, steps=None):
+    """Full cfg2 fits with the FP64 oracle port on all host threads."""
     import oracle
     oracle.set_num_threads(0)
     threads = oracle.num_threads()
     times, units = [], []
     t_end = time.time() + budget_s
     n = len(points)
-    count = 0
     while True:
         t0 = time.perf_counter()
         r = oracle.fit_k(points, k, max_iters=100, ll_rel_tol=tol, cov_reg=1e-6, seed=0)
-        dt = time.perf_counter() - t0
-        times.append(dt)
-        units.append(float(n) * sum([k] * r["em_iterations"]) if r["removed"] == 0 else
-                     float(n) * k * r["em_iterations"])
-        count += 1
+        times.append(time.perf_counter() - t0)
+        units.append(float(n) * k * r["em_iterations"])
         if steps is not None:
-            if count >= steps:
+            if len(times) >= steps:
                 break
-        elif time.time() > t_end or count >= 3:
+        elif time.time() > t_end or len(times) >= 3:
             break
-    return sum(units) / sum(times), threads, times, units
+    sample = ("%d full cfg2 fit(s) (kinit + M + EM, %.1f s), FP64 oracle restatement, "
+              "std::thread fan-out over 4096-point blocks" % (len(times), sum(times)))
+    return sum(units) / sum(times), threads, times, sample
+
+
+CFG4_CPU_SAMPLE = 250_000
+
+
+def cfg4_cpu_init(points, k):
+    """Fixed initial model for the CPU cfg4 sample: K evenly strided points,
+    equal weights, isotropic 5 cm covariance (iteration cost is independent
+    of the model's values)."""
+    idx = np.linspace(0, len(points) - 1, k).astype(np.int64)
+    mu = points[idx].copy()
+    w = np.full(k, 1.0 / k)
+    cov = np.zeros((k, 6))
+    cov[:, [0, 2, 5]] = 0.05 ** 2
+    return w, mu, cov
+
+
+def cpu_cfg4_rate(points, k, steps):
+    """Bounded sample of cfg4 on the CPU: one streaming FP64 EM iteration
+    (E + M, sogmm.cpp:488-503 without the N x K matrix) over a contiguous
+    250,000-point slice of the map, per step."""
+    import oracle
+    oracle.set_num_threads(0)
+    threads = oracle.num_threads()
+    sub = np.ascontiguousarray(points[:CFG4_CPU_SAMPLE])
+    w, mu, cov = cfg4_cpu_init(sub, k)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        oracle.fit_from(sub, w, mu, cov, max_iters=1, ll_rel_tol=0.0, cov_reg=1e-6,
+                        streaming=True)
+        times.append(time.perf_counter() - t0)
+    units = float(len(sub)) * k * len(times)
+    sample = ("%d streaming FP64 EM iteration(s) (E + M) over a contiguous %d-point slice "
+              "of the cfg4 map, K=%d (%.1f s), oracle restatement" %
+              (len(times), len(sub), k, sum(times)))
+    return units / sum(times), threads, times, sample
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    import paper_2307_00071_b200 as gm
-    pts = make_points(gm, 0)
-    if args.warmup > 0:
-        cpu_fit_rate(pts, args.k, args.tol, 0, steps=args.warmup)
-    rate, threads, times, units = cpu_fit_rate(pts, args.k, args.tol, 0, steps=max(args.steps, 1))
+    import oracle
+    if args.config == "cfg2":
+        pts = cfg2_points(oracle, 0)
+        if args.warmup > 0:
+            cpu_cfg2_rate(pts, args.k, args.tol, 0, steps=min(args.warmup, 2))
+        rate, threads, times, sample = cpu_cfg2_rate(pts, args.k, args.tol, 0,
+                                                     steps=max(args.steps, 1))
+    else:
+        pts = cfg4_points(oracle)
+        cpu_cfg4_rate(pts, args.k, 1)
+        rate, threads, times, sample = cpu_cfg4_rate(pts, args.k, max(args.steps, 1))
     ms = 1e3 * sum(times) / len(times)
     line = {
         "metric": METRIC, "value": rate, "unit": UNIT, "impl": "reference",
         "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (make_synthetic_frame 640x480 -> 307,200 4D points)",
-        "config": {"workload": "cfg2: 4D frame, N=307200, K=%d, k-means++ + EM to tol %g" %
-                   (args.k, args.tol), "global_batch": 1, "parallelism": "cpu"},
+        "higher_is_better": True, "scaling": "weak" if args.config == "cfg2" else "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (oracle restatement of the reference generators)",
+        "config": config_dict(args, args.gpus),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": "%d full fits (kinit + M + EM), FP64 oracle restatement, "
-                                   "std::thread fan-out over 4096-point blocks" % len(times)},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def flush_l2(torch, buf):
+def flush_l2(buf):
     buf.add_(1.0)  # 256 MiB write > 126 MB L2
 
 
+# ---- GPU arm --------------------------------------------------------------------
 def main():
     args = parse()
     if args.impl == "reference":
@@ -192,112 +292,164 @@ def main():
     import paper_2307_00071_b200 as gm
 
     torch.cuda.set_device(local)
+    dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    ctx = gm.Context(local)
+    sharded = args.config == "cfg4" and world > 1
+    vshard = args.config == "cfg4" and world == 1 and args.vshard > 1
+    if sharded:
+        ids = [gm.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(ids, src=0)
+        ctx = gm.Context(local, rank, world, ids[0])
+    else:
+        ctx = gm.Context(local)
     sm, cc_major, cc_minor = ctx.device_info()
-    pts = make_points(gm, rank)
+    if args.config == "cfg2":
+        pts = cfg2_points(gm, rank)
+        em = gm.EmParams(100, args.tol, 1e-6, rank)
+        full_n = len(pts)
+    else:
+        full = cfg4_points(gm)
+        full_n = len(full)
+        em = gm.EmParams(100, args.tol, 1e-6, 0)
+        if sharded:
+            lo, hi = shard_bounds(full_n, world)[rank]
+            pts = np.ascontiguousarray(full[lo:hi])
+        else:
+            lo, hi = 0, full_n
+            pts = full
     n, d = pts.shape
-    em = gm.EmParams(100, args.tol, 1e-6, rank)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 
     def barrier():
         torch.cuda.synchronize()
         if world > 1:
-            torch.distributed.barrier()
+            dist.barrier()
         torch.cuda.synchronize()
 
+    vctx = gm.vshard_contexts(args.vshard) if vshard else None
+
+    def fit_resident():
+        if vshard:
+            rs = gm.fit_k_vsharded(pts, args.k, em, contexts=vctx)
+            r0 = rs[0]
+            r0.ms_total = max(r.ms_total for r in rs)
+            r0.ms_em = max(r.ms_em for r in rs)
+            r0.ms_estep = max(r.ms_estep for r in rs)
+            r0.launches = sum(r.launches for r in rs)
+            return r0
+        return ctx.fit_k_resident(args.k, em)
+
     # ---- value: inputs resident in HBM ------------------------------------
-    ctx.upload(pts)
+    if not vshard:
+        if sharded:
+            ctx.upload(pts, lo, full_n)
+        else:
+            ctx.upload(pts)
     res = []
     with Clocks(local) as clk:          # sampling spans warm-up + timed region
         for _ in range(max(args.warmup, 3)):
-            ctx.fit_k_resident(args.k, em)
-        flush_l2(torch, flush)
+            fit_resident()
+        flush_l2(flush)
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            flush_l2(torch, flush)
+            flush_l2(flush)
             torch.cuda.synchronize()
-            res.append(ctx.fit_k_resident(args.k, em))
+            res.append(fit_resident())
         barrier()
         wall = time.perf_counter() - t0
     clocks = clk.summary()
     dev_ms = sum(r.ms_total for r in res)
-    units = sum(r.units for r in res)
-    est_ms = sum(r.ms_estep for r in res)
+    em_ms = sum(r.ms_em for r in res)
+    units = sum(r.units for r in res)   # units count the GLOBAL N (sharded: every rank the same)
     iters = [r.em_iterations for r in res]
     if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([dev_ms, units, est_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([dev_ms, em_ms, units], dtype=torch.float64, device="cuda")
         mx = t.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        dev_ms_job, units_job = float(mx[0]), float(t[1])
+        dev_ms_job, em_ms_job = float(mx[0]), float(mx[1])
+        units_job = float(mx[2]) if sharded else float(t[2])
     else:
-        dev_ms_job, units_job = dev_ms, units
+        dev_ms_job, em_ms_job, units_job = dev_ms, em_ms, units
     value = units_job / (dev_ms_job * 1e-3)
 
     # ---- e2e: C ABI call with pinned host buffers --------------------------
     host = torch.empty((d, n), dtype=torch.float64, pin_memory=True)
     host.numpy()[:] = pts.T                      # column-major N x D
     host_pts = host.numpy().T                    # (N, D) Fortran view, pinned
-    assert not host_pts.flags["C_CONTIGUOUS"] and host_pts.flags["F_CONTIGUOUS"]
+    assert host_pts.flags["F_CONTIGUOUS"]
+
+    def fit_host():
+        if vshard:
+            return gm.fit_k_vsharded(host_pts, args.k, em, contexts=vctx)[0]
+        return gm.fit_k(host_pts, args.k, em, ctx=ctx)
+
     for _ in range(2):
-        gm.fit_k(host_pts, args.k, em, ctx=ctx)
+        fit_host()
     barrier()
     e2e_units, t_e2e = 0.0, 0.0
     for _ in range(args.steps):
-        flush_l2(torch, flush)
+        flush_l2(flush)
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t1 = time.perf_counter()
-        r = gm.fit_k(host_pts, args.k, em, ctx=ctx)
+        r = fit_host()
         torch.cuda.synchronize()
         t_e2e += time.perf_counter() - t1
         e2e_units += r.units
     if world > 1:
-        import torch.distributed as dist
         t = torch.tensor([t_e2e, e2e_units], dtype=torch.float64, device="cuda")
         mx = t.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        t_e2e, e2e_units = float(mx[0]), float(t[1])
+        t_e2e = float(mx[0])
+        e2e_units = float(mx[1]) if sharded else float(t[1])
     e2e = e2e_units / t_e2e
     kk = args.k
     d2h = 8 * (kk * (1 + d + d * (d + 1) // 2) + 100) + 96
 
     # ---- roofline of the dominant kernel (fused E step + statistics) ------
-    # The EM loop of a fit is one CUDA graph (no per-kernel events inside);
-    # the same K fits are repeated in timing mode (chunked launches, CUDA
-    # events on the library stream around every fused E kernel; identical
-    # kernels and results) to get the kernel's average launch duration.
-    ctx.upload(pts)
-    ctx.set_timing(True)
-    est_ms, est_units, est_launches = 0.0, 0.0, 0
-    for _ in range(args.steps):
-        flush_l2(torch, flush)
-        torch.cuda.synchronize()
-        rt = ctx.fit_k_resident(args.k, em)
-        est_ms += rt.ms_estep
-        est_units += rt.units
-        est_launches += rt.em_iterations
-    ctx.set_timing(False)
+    # Graph mode has no per-kernel events inside the EM loop: the same fits
+    # are repeated in timing mode (chunked launches, CUDA events on the
+    # library stream around every fused E kernel; identical kernels and
+    # results). Sharded fits always run chunked, so their pass above has them.
+    if sharded or vshard:
+        est_ms = sum(r.ms_estep for r in res)
+        est_units = float(n if sharded else -(-full_n // args.vshard)) * kk * sum(iters)
+        est_launches = sum(iters)
+    else:
+        ctx.upload(pts)
+        ctx.set_timing(True)
+        est_ms, est_units, est_launches = 0.0, 0.0, 0
+        for _ in range(args.steps):
+            flush_l2(flush)
+            torch.cuda.synchronize()
+            rt = ctx.fit_k_resident(args.k, em)
+            est_ms += rt.ms_estep
+            est_units += rt.units
+            est_launches += rt.em_iterations
+        ctx.set_timing(False)
     peak_tf, _ = ctx.ffma_peak(50.0)
     achieved_tf = FLOP_PER_UNIT[d] * est_units / (est_ms * 1e-3) / 1e12
+    tr = TRAFFIC.get((args.config, kk)) if world == 1 and not vshard else None
+    kernel = ("estep_ws_kernel (warp-specialised fused E step + sufficient statistics)"
+              if kk <= 512 else "fused E step + sufficient statistics (K > 512 path)")
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 3),
         "ms_per_step": dev_ms_job / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (make_synthetic_frame 640x480 -> 307,200 4D points; "
-                "rank r>0: 2 mm jitter, seed r)",
-        "config": {"workload": "cfg2: 4D frame N=307200, K=%d, k-means++ + EM to tol %g "
-                               "(one fit per GPU per step)" % (args.k, args.tol),
-                   "global_batch": world, "points_per_fit": n, "k": args.k,
-                   "em_iterations": iters, "parallelism": "replicas%d" % world,
-                   "l2": "flushed between steps (256 MiB write)"},
+        "higher_is_better": True, "scaling": "strong" if args.config == "cfg4" else "weak",
+        "vs_baseline": None, "dtype": "f32",
+        "data": ("synthetic (make_synthetic_frame 640x480 -> 307,200 4D points; rank r>0: "
+                 "2 mm jitter, seed r)" if args.config == "cfg2" else
+                 "synthetic (make_structured_scene 4M x 25 + (100, -40, 0) m, 3D)"),
+        "config": config_dict(args, world),
+        "em_iterations": iters,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": n * d * 8,
                 "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * t_e2e / args.steps},
         "gpu_launches": int(sum(r.launches for r in res)),
@@ -307,36 +459,40 @@ def main():
                      "em": statistics.mean(r.ms_em for r in res),
                      "estep_kernel": est_ms / args.steps,
                      "estep_us_per_launch": 1e3 * est_ms / max(est_launches, 1)},
-        "em_only_value": units / (sum(r.ms_em for r in res) * 1e-3),
-        "roofline": {"bound": "fp32", "kernel": "estep_ws_kernel (warp-specialised fused E "
-                     "step + sufficient statistics)", "achieved": achieved_tf, "peak": peak_tf,
-                     "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
+        "em_only_value": units_job / (em_ms_job * 1e-3),
+        "roofline": {"bound": "fp32", "kernel": kernel, "achieved": achieved_tf,
+                     "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
                      "flop_per_unit": FLOP_PER_UNIT[d],
                      "timing": "CUDA events around each fused E launch on the library stream, "
-                               "%d launches in a timing-mode pass of the same %d fits"
-                               % (est_launches, args.steps),
+                               "%d launches over the same %d fits" % (est_launches, args.steps),
                      "peak_source": "measured packed-FP32 (fma.rn.f32x2) microbenchmark in this "
                                     "run (MEASURED_PEAKS.json has no FP32 figure); nominal %.1f"
                                     % NOMINAL_FP32_TFLOPS,
-                     "traffic": TRAFFIC_BYTES,
-                     "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch, "
-                                     "ncu --set full (%s); algorithmic %.0f B (points 16 B each "
-                                     "+ FP64 partials)" % (TRAFFIC_SRC, 16 * n)},
+                     "traffic": tr[0] if tr else None,
+                     "traffic_note": ("dram__bytes_read.sum + dram__bytes_write.sum per launch, "
+                                      "ncu --set full of this configuration (%s); algorithmic "
+                                      "%.0f B (points 16 B each)" % (tr[1], 16 * n)) if tr else
+                                     "no ncu capture of this configuration; algorithmic "
+                                     "%.0f B per launch (points 16 B each)" % (16 * n)},
         "clocks": clocks,
         "wall_s": wall,
         "device": {"sm_count": sm, "cc": "%d.%d" % (cc_major, cc_minor)},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, threads, times, cunits = cpu_fit_rate(pts, args.k, args.tol, args.cpu_sample_s)
-        line["cpu_baseline"] = {
-            "value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": "%d full cfg2 fit(s) (kinit + M + EM, %.1f s) with the FP64 oracle "
-                      "restatement on all host threads" % (len(times), sum(times))}
+        if args.config == "cfg2":
+            rate, threads, times, sample = cpu_cfg2_rate(pts, args.k, args.tol, args.cpu_sample_s)
+        else:
+            rate, threads, times, sample = cpu_cfg4_rate(pts, args.k, 3)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                                "cpu_model": cpu_model(), "sample": sample}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if vctx:
+        for c in vctx:
+            c.close()
     ctx.close()
     if world > 1:
-        torch.distributed.destroy_process_group()
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

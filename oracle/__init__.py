@@ -91,6 +91,12 @@ def load():
             "orc_gbms": (ctypes.c_int, [D, ctypes.c_int64, ctypes.c_double, ctypes.c_int,
                                         ctypes.c_double, ctypes.c_double, I, I, I, D,
                                         ctypes.c_int]),
+            "orc_synthetic_frame_cloud": (ctypes.c_int, [ctypes.c_int, ctypes.c_int,
+                                                         ctypes.c_double, D, I64]),
+            "orc_structured_scene": (ctypes.c_int, [ctypes.c_int64, ctypes.c_uint64,
+                                                    ctypes.c_double, D]),
+            "orc_jitter_cloud": (ctypes.c_int, [D, ctypes.c_int64, ctypes.c_double,
+                                                ctypes.c_uint64]),
             "orc_score": (ctypes.c_int, [D, ctypes.c_int64, ctypes.c_int, D, D, D, D]),
             "orc_sample": (ctypes.c_int, [ctypes.c_int, D, D, D, ctypes.c_int64,
                                           ctypes.c_uint64, D]),
@@ -325,3 +331,27 @@ def gbms(points, bandwidth=0.015, max_iters=100, tol=1e-5, merge_radius=-1.0):
     _check(load().orc_gbms(_p(p), p.shape[0], bandwidth, max_iters, tol, merge_radius,
                            ctypes.byref(comp), ctypes.byref(it), ctypes.byref(s0), _p(modes), cap))
     return comp.value, it.value, s0.value, modes[:comp.value].copy()
+
+
+# ---- benchmark inputs (synthetic.cpp:9-129, ingest.cpp:27-57 restated) ----
+def synthetic_frame_cloud(width=640, height=480, depth_scale=1000.0):
+    """make_synthetic_frame + image_pair_to_cloud: (N, 4) float64."""
+    buf = np.zeros(4 * width * height)
+    n = ctypes.c_int64()
+    _check(load().orc_synthetic_frame_cloud(width, height, depth_scale, _p(buf),
+                                            ctypes.byref(n)))
+    return buf[:4 * n.value].reshape(4, n.value).T.copy()
+
+
+def structured_scene(n, seed=0, noise_sigma=0.005):
+    """make_structured_scene: (n, 4) float64."""
+    buf = np.zeros(4 * n)
+    _check(load().orc_structured_scene(n, seed, noise_sigma, _p(buf)))
+    return buf.reshape(4, n).T.copy()
+
+
+def jitter_cloud(points, sigma, seed):
+    """cfg3 frame jitter: xyz += sigma * normal_pair(seed, 13, 4i ...)."""
+    p = np.asfortranarray(np.array(points, dtype=np.float64))
+    _check(load().orc_jitter_cloud(_p(p), len(p), sigma, seed))
+    return np.ascontiguousarray(p)

@@ -1379,4 +1379,109 @@ int orc_gbms(const double* pts, int64_t n, double bandwidth, int max_iters, doub
                   sizeof(double) * 4 * std::min(g.components, modes_capacity));
   });
 }
+// ---- benchmark inputs, restated from the reference -----
+// make_synthetic_frame (synthetic.cpp:9-72) + image_pair_to_cloud
+// (ingest.cpp:27-57, row-major pixels, zero depths dropped): N x 4 col-major
+// into pts (capacity width*height rows), *n_out = N. Vec3 dot / squaredNorm
+// are ((a0 b0 + a1 b1) + a2 b2), the order Eigen's fixed-size redux yields.
+int orc_synthetic_frame_cloud(int width, int height, double depth_scale, double* pts,
+                              int64_t* n_out) {
+  return guarded([&] {
+    if (width < 1 || height < 1 || !(depth_scale > 0.0)) throw ArgError{"bad frame size"};
+    const double fx = 525.0 * width / 640.0, fy = 525.0 * width / 640.0;  // :12-13
+    const double cx = width * 0.5 - 0.5, cy = height * 0.5 - 0.5;         // :14-15
+    const size_t npx = static_cast<size_t>(width) * height;
+    std::vector<uint16_t> depth(npx), inten(npx);
+    const double scx = 0.35, scy = -0.1, scz = 2.1, sr = 0.35;             // :27-28
+    for (int v = 0; v < height; ++v) {
+      for (int u = 0; u < width; ++u) {
+        const double rx = (u - cx) / fx, ry = (v - cy) / fy;               // :33-34
+        double z = 3.0;                                                    // :38
+        const double denom = ry + 0.18;                                    // :42-46
+        if (denom > 1e-9) {
+          const double zd = 0.45 / denom;
+          if (zd > 0.4 && zd < z) z = zd;
+        }
+        const double a = (rx * rx + ry * ry) + 1.0 * 1.0;                  // :49-56
+        const double bq = -2.0 * ((rx * scx + ry * scy) + 1.0 * scz);
+        const double c = ((scx * scx + scy * scy) + scz * scz) - sr * sr;
+        const double disc = bq * bq - 4.0 * a * c;
+        if (disc > 0.0) {
+          const double t = (-bq - std::sqrt(disc)) / (2.0 * a);
+          if (t > 0.0 && t < z) z = t;
+        }
+        const double px = rx * z, py = ry * z, pz = 1.0 * z;               // :58
+        depth[static_cast<size_t>(v) * width + u] =
+            static_cast<uint16_t>(std::min(depth_scale * z, 65535.0));     // :59-61
+        double in = 0.55 + 0.25 * std::sin(7.0 * px) * std::cos(5.0 * py) +
+                    0.15 * std::sin(3.0 * pz);                             // :64-66
+        in = std::clamp(in, 0.0, 1.0);
+        inten[static_cast<size_t>(v) * width + u] =
+            static_cast<uint16_t>(std::lround(in * 255.0));                // :67-68
+      }
+    }
+    int64_t n = 0;
+    for (const uint16_t d : depth) n += d > 0;                             // ingest.cpp:33-36
+    const double inv_scale = 1.0 / depth_scale, inv_max = 1.0 / 255.0;     // :41-42
+    int64_t k = 0;
+    for (int v = 0; v < height; ++v) {
+      for (int u = 0; u < width; ++u) {
+        const uint16_t d = depth[static_cast<size_t>(v) * width + u];
+        if (d == 0) continue;
+        const double z = d * inv_scale;                                    // :48-53
+        pts[0 * n + k] = (u - cx) * z / fx;
+        pts[1 * n + k] = (v - cy) * z / fy;
+        pts[2 * n + k] = z;
+        pts[3 * n + k] = inten[static_cast<size_t>(v) * width + u] * inv_max;
+        ++k;
+      }
+    }
+    *n_out = n;
+  });
+}
+
+// make_structured_scene (synthetic.cpp:94-129): n x 4 col-major.
+int orc_structured_scene(int64_t n, uint64_t seed, double noise_sigma, double* pts) {
+  return guarded([&] {
+    for (int64_t i = 0; i < n; ++i) {
+      const auto ctr = static_cast<uint64_t>(i);
+      const double u = orc_uniform(seed, 11, ctr * 8), v = orc_uniform(seed, 11, ctr * 8 + 1);
+      double nz0, nz1, nz2, unused;
+      orc_normal_pair(seed, 12, ctr * 8 + 2, &nz0, &nz1);
+      orc_normal_pair(seed, 12, ctr * 8 + 4, &nz2, &unused);
+      double x, y, z;
+      if (i % 3 == 0) {          // ground plane z = 0
+        x = 2.0 * u - 1.0; y = 2.0 * v - 1.0; z = 0.0;
+      } else if (i % 3 == 1) {   // wall plane x = 0
+        x = 0.0; y = 2.0 * u - 1.0; z = 1.2 * v;
+      } else {                   // cylinder along z
+        const double ang = 2.0 * M_PI * u;
+        x = 0.55 + 0.3 * std::cos(ang); y = -0.35 + 0.3 * std::sin(ang); z = 1.1 * v;
+      }
+      x += noise_sigma * nz0;
+      y += noise_sigma * nz1;
+      z += noise_sigma * nz2;
+      pts[0 * n + i] = x;
+      pts[1 * n + i] = y;
+      pts[2 * n + i] = z;
+      pts[3 * n + i] =
+          std::clamp(0.5 + 0.3 * std::sin(4.0 * x) + 0.2 * std::cos(3.0 * y + z), 0.0, 1.0);
+    }
+  });
+}
+
+// cfg3 frame f (a generator new to this build): xyz of the
+// cfg2 frame jittered by sigma * normal_pair(seed = f, stream 13, 4i ...).
+int orc_jitter_cloud(double* pts, int64_t n, double sigma, uint64_t seed) {
+  return guarded([&] {
+    for (int64_t i = 0; i < n; ++i) {
+      double z0, z1, z2, z3;
+      orc_normal_pair(seed, 13, static_cast<uint64_t>(i) * 4, &z0, &z1);
+      orc_normal_pair(seed, 13, static_cast<uint64_t>(i) * 4 + 2, &z2, &z3);
+      pts[0 * n + i] += sigma * z0;
+      pts[1 * n + i] += sigma * z1;
+      pts[2 * n + i] += sigma * z2;
+    }
+  });
+}
 }  // extern "C"

@@ -142,6 +142,12 @@ int orc_gbms(const double* pts, int64_t n, double bandwidth, int max_iters, doub
              double merge_radius, int* components, int* iterations, int* seeds0,
              double* modes, int modes_capacity);
 
+/* benchmark inputs (reference synthetic.cpp / ingest.cpp restated) */
+int orc_synthetic_frame_cloud(int width, int height, double depth_scale, double* pts,
+                              int64_t* n_out);
+int orc_structured_scene(int64_t n, uint64_t seed, double noise_sigma, double* pts);
+int orc_jitter_cloud(double* pts, int64_t n, double sigma, uint64_t seed);
+
 #ifdef __cplusplus
 }
 #endif

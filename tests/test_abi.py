@@ -126,3 +126,14 @@ def test_cpp_api_builds_and_reports_device_errors(gm, tmp_path):
         assert r.returncode == 0, r.stderr
     else:
         assert r.returncode == 1 and "device error" in r.stderr
+
+
+def test_oracle_generators_match_product(gm, orc):
+    """The reference arm of bench.py builds its inputs with the oracle-side
+    restatement of synthetic.cpp / ingest.cpp (it must not load libgmmb);
+    they are bit-identical to the product's generators."""
+    a, b = orc.synthetic_frame_cloud(), gm.synthetic_frame_cloud()
+    assert a.shape == (307200, 4) and np.array_equal(a, b)
+    s = gm.structured_scene(30000, 4, 0.005)
+    assert np.array_equal(orc.structured_scene(30000, 4, 0.005), s)
+    assert np.array_equal(orc.jitter_cloud(b, 0.002, 3), gm.jitter_cloud(b, 0.002, 3))
