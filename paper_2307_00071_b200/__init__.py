@@ -402,11 +402,11 @@ class Context:
                        want_labels: bool = False) -> FitResult:
         n, d = self._n, self._d
         kk = max(1, min(k, 1 << 30))
-        out = _alloc_model(min(kk, 4096), d)
+        out = _alloc_model(kk, d)
         ll = np.zeros(max(em.max_iters, 1))
         st = _FitStats()
         lab = np.zeros(n, np.int32) if want_labels else None
-        cen = np.zeros(min(kk, 4096), np.int64) if want_labels else None
+        cen = np.zeros(kk, np.int64) if want_labels else None
         _check(load().gmmb_fit_k_resident(self._h, k, ctypes.byref(em._c()), _ptr(out[0]),
                                           _ptr(out[1]), _ptr(out[2]), _ptr(ll),
                                           ctypes.byref(st), _ptr(lab, _I32), _ptr(cen, _I64)))
@@ -558,7 +558,7 @@ def fit(points, params: GbmsParams = GbmsParams(), em: EmParams = EmParams(),
     """fit (sogmm.cpp:465-510): GBMS decides K, then k-means++ -> m_step -> EM."""
     c = _ctx(ctx)
     p, n, d = _points(points)
-    cap = 4096
+    cap = max(n, 1)   # K <= N (sogmm.cpp:477)
     out = _alloc_model(cap, d)
     ll = np.zeros(max(em.max_iters, 1))
     st = _FitStats()

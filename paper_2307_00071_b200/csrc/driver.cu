@@ -69,10 +69,10 @@ struct DevBuf {
 struct EmGraphKey {
   int k0, d, world;
   int64_t n;
-  const void* p[12];
+  const void* p[14];
   bool operator==(const EmGraphKey& o) const {
     if (k0 != o.k0 || d != o.d || n != o.n || world != o.world) return false;
-    for (int i = 0; i < 12; ++i)
+    for (int i = 0; i < 14; ++i)
       if (p[i] != o.p[i]) return false;
     return true;
   }
@@ -131,9 +131,12 @@ struct gmmb_ctx {
   DevBuf<CompConst> mcst[2];
   DevBuf<double> rcount, rmean, rcov, rlogdet;
   DevBuf<float> rpc;
-  DevBuf<int> rflags;
+  DevBuf<int> rflags, rmap;
   DevBuf<double> mpart, msums, mmeans, mcounts;
   DevBuf<double> partials, ll_part, red, ll_trace;
+  DevBuf<float> chunkf;          // chunked E step (K > 512): per-chunk sums + normalisers
+  DevBuf<int> chunki;            // ... exact-path point list + count
+  ChunkScratch chunk{};
   DevBuf<double> dense;  // log_gamma staging for m_step / e_step
   DevBuf<EmState> st;
   EmState* st_host = nullptr;  // pinned
@@ -207,7 +210,9 @@ void ensure_model(gmmb_ctx* c, int k) {
   c->rlogdet.ensure(kc);
   c->rpc.ensure(kc * 16);
   c->rflags.ensure(kc);
-  c->rec = RecBuf{c->rcount.p, c->rmean.p, c->rcov.p, c->rlogdet.p, c->rpc.p, c->rflags.p};
+  c->rmap.ensure(kc);
+  c->rec = RecBuf{c->rcount.p, c->rmean.p, c->rcov.p, c->rlogdet.p, c->rpc.p, c->rflags.p,
+                  c->rmap.p};
   c->red.ensure(kc * 16 + 1);
   c->st.ensure(1);
 }
@@ -506,6 +511,10 @@ void download_model(gmmb_ctx* c, int buf, int m, double* w, double* mu,
 }
 
 // ---- EM loop ----------------------------------------------------------
+// kernels of the fused E step + statistics per iteration (the chunked
+// K > 512 path: per-chunk sums, combine, exact list, statistics)
+int estep_launches(int k0) { return k0 > kCtaComps ? 4 : 1; }
+
 void em_iteration(gmmb_ctx* c, int k0, int it,
                   const cudaGraphConditionalHandle* cond = nullptr) {
   const int NS = nstats(c->d);
@@ -515,10 +524,10 @@ void em_iteration(gmmb_ctx* c, int k0, int it,
   const bool timed = it >= 0 && static_cast<size_t>(2 * it + 1) < c->ev_e.size();
   if (timed) ck(cudaEventRecord(c->ev_e[2 * it], c->s), "event");
   ck(launch_estep_stats(pts, c->bufs, c->st.p, k0, c->partials.p, c->ll_part.p, 0,
-                        c->sm_count, c->s, &ncl),
+                        c->sm_count, c->s, &ncl, &c->chunk),
      "estep_stats");
   if (timed) ck(cudaEventRecord(c->ev_e[2 * it + 1], c->s), "event");
-  c->launches += 4;
+  c->launches += estep_launches(k0) + 3;
   if (c->world == 1) {
     c->launches += -1;  // fused reduce + finalize
     ck(launch_em_reduce_finalize(c->d, c->partials.p, ncl, k0, c->bufs, c->st.p, c->rec, c->s),
@@ -549,10 +558,10 @@ EmGraphKey em_graph_key(gmmb_ctx* c, int k0) {
   k.d = c->d;
   k.n = c->n;
   k.world = c->world;
-  const void* ps[12] = {c->xt.p, c->tc.p, c->partials.p, c->ll_part.p, c->red.p, c->ll_trace.p,
+  const void* ps[14] = {c->xt.p, c->tc.p, c->partials.p, c->ll_part.p, c->red.p, c->ll_trace.p,
                         c->st.p, c->bufs[0].w, c->bufs[1].w, c->rec.count, c->bufs[0].cst,
-                        c->bufs[1].cst};
-  for (int i = 0; i < 12; ++i) k.p[i] = ps[i];
+                        c->bufs[1].cst, c->chunkf.p, c->chunki.p};
+  for (int i = 0; i < 14; ++i) k.p[i] = ps[i];
   return k;
 }
 
@@ -605,6 +614,15 @@ void ensure_em_buffers(gmmb_ctx* c, int k0, int max_iters) {
      "estep query");
   c->partials.ensure(static_cast<size_t>(ncl) * k0 * NS);
   c->ll_part.ensure(ncl);
+  if (k0 > kCtaComps) {  // chunked two-pass E step
+    const int64_t npad = static_cast<int64_t>(pts.ntiles) * kTile;
+    const int nch = (k0 + kCtaComps - 1) / kCtaComps;
+    c->chunkf.ensure(chunk_scratch_floats(k0, c->n));
+    c->chunki.ensure(static_cast<size_t>(npad) + 1);
+    c->chunk = ChunkScratch{c->chunkf.p,
+                            reinterpret_cast<float2*>(c->chunkf.p + static_cast<size_t>(nch) * npad),
+                            c->chunki.p, c->chunki.p + npad};
+  }
   c->red.ensure(static_cast<size_t>(k0) * NS + 1);
   c->ll_trace.ensure(std::max(max_iters, 1));
 }
@@ -622,7 +640,7 @@ EmState run_em(gmmb_ctx* c, int k0, const gmmb_em_params* em) {
   if (!c->last_timed) {
     launch_em_graph(c, k0);
     EmState h = read_state(c);
-    c->launches += 3LL * h.iter;
+    c->launches += static_cast<long long>(estep_launches(k0) + 2) * h.iter;
     return h;
   }
   int launched = 0;
@@ -681,7 +699,6 @@ void fit_k_resident(gmmb_ctx* c, int K, const gmmb_em_params* em, double* w_out,
   set_device(c);
   const int64_t ng = c->n_global;
   const int k = static_cast<int>(std::min<int64_t>(K, ng));  // sogmm.cpp:477
-  if (k > kMaxK) throw Err{2, "K > 4096 is not supported by the fused E/M kernel"};
   c->launches = 0;
   ck(cudaEventRecord(c->ev[0], c->s), "event");
   layout(c);
@@ -727,7 +744,6 @@ void fit_from_resident(gmmb_ctx* c, int m, const double* w0, const double* mu0,
   if (!c->have_cloud) throw Err{2, "no point cloud uploaded"};
   check_em(em);
   if (m < 1) throw Err{2, "model has no components"};
-  if (m > kMaxK) throw Err{2, "K > 4096 is not supported by the fused E/M kernel"};
   set_device(c);
   c->launches = 0;
   ck(cudaEventRecord(c->ev[0], c->s), "event");
@@ -1054,9 +1070,10 @@ void gmmb_ctx_destroy(gmmb_ctx* c) {
     c->mw[b].release(); c->mmu[b].release(); c->mcov[b].release(); c->mcst[b].release();
   }
   c->rcount.release(); c->rmean.release(); c->rcov.release(); c->rlogdet.release();
-  c->rpc.release(); c->rflags.release(); c->mpart.release(); c->msums.release();
+  c->rpc.release(); c->rflags.release(); c->rmap.release(); c->mpart.release(); c->msums.release();
   c->mmeans.release(); c->mcounts.release(); c->partials.release(); c->ll_part.release();
   c->red.release(); c->ll_trace.release(); c->dense.release(); c->st.release();
+  c->chunkf.release(); c->chunki.release();
   if (c->em_graph) cudaGraphExecDestroy(c->em_graph);
   if (c->st_host) cudaFreeHost(c->st_host);
   for (auto& e : c->ev)
@@ -1382,7 +1399,6 @@ int gmmb_m_step(gmmb_ctx* c, const double* pts, int64_t n, int d, const double* 
     if (!c) throw Err{2, "null context"};
     if (cov_reg < 0.0) throw Err{2, "cov_reg must be >= 0"};
     if (!log_gamma || m < 1) throw Err{2, "responsibility rows != point count"};
-    if (m > kMaxK) throw Err{2, "m > 4096 not supported"};
     upload(c, pts, n, d, 0, n);
     ensure_model(c, m);
     c->dense.ensure(static_cast<size_t>(n) * m);
@@ -1407,7 +1423,6 @@ int gmmb_em_step(gmmb_ctx* c, const double* pts, int64_t n, int d, int m, const 
     upload(c, pts, n, d, 0, n);
     layout(c);
     check_cloud_flags(c);
-    if (m > kMaxK) throw Err{2, "m > 4096 not supported"};
     ensure_model(c, m);
     upload_model(c, m, w, mu, cov);
     reset_state(c, m, &em, 0);

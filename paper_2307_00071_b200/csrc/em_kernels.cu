@@ -25,6 +25,7 @@
 
 #include "em_kernels.cuh"
 #include "factor.cuh"
+#include "f32x2.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -44,6 +45,9 @@ namespace cg = cooperative_groups;
 #ifndef GMMB_F2F_ALU
 #define GMMB_F2F_ALU 0          // 1: FP32 -> FP64 widening on the integer ALU
 #endif
+#ifndef GMMB_CHUNKED
+#define GMMB_CHUNKED 1          // 1: K > 512 through the chunked two-pass kernels
+#endif
 #ifndef GMMB_PXB
 #define GMMB_PXB 1              // 1: y = P'x - P'mu (FFMA chains); 0: y = P'(x - mu)
 #endif
@@ -52,49 +56,9 @@ namespace gmmb {
 
 namespace {
 
-__device__ __forceinline__ float ex2f(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float lg2f(float x) {
-  float y;
-  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
+using namespace dev;
 
-template <int P>
-struct Log2 {
-  static constexpr int v = P == 1 ? 0 : 1 + Log2<P / 2>::v;
-};
-template <>
-struct Log2<1> {
-  static constexpr int v = 0;
-};
 
-// Warp reduce-scatter over 32 lanes of P per-lane values (one per point).
-// On return v[0] of lane l holds the reduction for point l >> (5 - log2 P)
-// over all 32 lanes. Fixed butterfly order => deterministic.
-template <int P, bool MAX>
-__device__ __forceinline__ float warp_reduce_scatter(float (&v)[P], int lane) {
-#pragma unroll
-  for (int h = P / 2, off = 16; h >= 1; h >>= 1, off >>= 1) {
-    const bool up = (lane & off) != 0;
-#pragma unroll
-    for (int i = 0; i < h; ++i) {
-      const float send = up ? v[i] : v[i + h];
-      const float keep = up ? v[i + h] : v[i];
-      const float got = __shfl_xor_sync(0xffffffffu, send, off);
-      v[i] = MAX ? fmaxf(keep, got) : keep + got;
-    }
-  }
-#pragma unroll
-  for (int off = 16 / P; off >= 1; off >>= 1) {
-    const float got = __shfl_xor_sync(0xffffffffu, v[0], off);
-    v[0] = MAX ? fmaxf(v[0], got) : v[0] + got;
-  }
-  return v[0];
-}
 
 // ---------------------------------------------------------------------------
 // Fused E-step + sufficient statistics.
@@ -151,11 +115,6 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
-__device__ __forceinline__ float rcpf(float x) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 
 // CPT components per thread: thread tid of CTA rank r owns components
 // r * kCtaComps + c * (32 NW) + tid, c < CPT. Per 8-point sub-tile: phase A
@@ -467,78 +426,6 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW)
 //   slots suffice: a thread that writes slot s % 3 has passed the wait for
 //   s - 1, so every thread has finished reading sub-tile s - 3.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
-  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(b));
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
-  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(b));
-  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(a)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
-  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(b));
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(a),
-      "r"(parity)
-      : "memory");
-}
-
-// f32x2 register pairs (lo = component tid, hi = component T + tid)
-typedef unsigned long long f2_t;
-__device__ __forceinline__ f2_t pk(float a, float b) {
-  f2_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ float lo2(f2_t v) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-  return a;
-}
-__device__ __forceinline__ float hi2(f2_t v) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-  return b;
-}
-__device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) {
-  f2_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ f2_t add2(f2_t a, f2_t b) {
-  f2_t d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) {
-  f2_t d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ float ex2n(float x) {  // 2^-x
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(-x));
-  return y;
-}
-
-// FP32 -> FP64 widening. The XU pipe (F2F) also carries the ex2 of every
-// unit; GMMB_F2F_ALU = 1 widens on the integer ALU instead (exact for
-// normal numbers; FP32 subnormals, ~1e-38, flush to zero).
-__device__ __forceinline__ double f32_to_f64(float f) {
-#if GMMB_F2F_ALU
-  const unsigned b = __float_as_uint(f);
-  const unsigned e = b & 0x7f800000u;
-  const unsigned hi = e ? (((b >> 3) & 0x0fffffffu) + 0x38000000u) | (b & 0x80000000u) : 0u;
-  const unsigned lo = e ? (b << 29) : 0u;
-  return __hiloint2double(static_cast<int>(hi), static_cast<int>(lo));
-#else
-  return static_cast<double>(f);
-#endif
-}
 
 // ---------------------------------------------------------------------------
 // Warp-specialised fused E step (one CTA holds all K <= 512 components).
@@ -582,6 +469,7 @@ template <int NWH, int P, int C>
 struct WsSmem {
   float4 xs[2][kTile];                   // point tiles (TMA destination)
   double tcs[2][4];                      // tile centres (TMA destination)
+  float2 ls[2][kTile];                   // PRE: the tile's log2 normalisers (TMA destination)
   static constexpr int kRing = ring_slots<C>();
   float4 ering[kRing][P / 2][NWH * 32];  // e pairs: [slot][point pair][thread]
   float red[kRing][P][C * NWH];          // per-warp partial sums of every CTA of the cluster
@@ -614,30 +502,21 @@ __device__ __forceinline__ void mbar_wait_cluster(unsigned long long* b, unsigne
       : "memory");
 }
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
-                                         unsigned long long* b) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(b))
-      : "memory");
-}
 
-template <int D, int NWH, int P, int C>
+// PRE (pass B of the chunked K > 512 E step, estep_chunked.cu): the
+// per-point log2 normalisers L_n over ALL K are known (pass A), so the CTA
+// holds one 512-component chunk c = blockIdx.x % nch of them; producers
+// emit r = 2^-(Q + L_n) directly (no reduce-scatter, no per-warp partials),
+// consumers accumulate with no combine / rescale / exact path.
+template <int D, int NWH, int P, int C, bool PRE = false>
 __global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
     estep_ws_kernel(const float4* __restrict__ xt, const double* __restrict__ tc,
                     int64_t n, int ntiles, ModelBuf b0, ModelBuf b1,
                     const EmState* __restrict__ st, int kpad,
                     double* __restrict__ partials, double* __restrict__ ll_part,
-                    int exact_mode, int split_sub) {
+                    int exact_mode, int split_sub, const float2* __restrict__ lse = nullptr,
+                    int nch = 1) {
+  static_assert(!PRE || C == 1, "pre-normalised pass: one CTA per chunk");
   constexpr int NP = npacked(D);
   constexpr int NS = nstats(D);
   constexpr int T = NWH * 32;  // threads per role
@@ -662,17 +541,27 @@ __global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
     cid = blockIdx.x / C;
     ncl = gridDim.x / C;
   }
+  int chunk = 0;
+  if constexpr (PRE) {
+    chunk = blockIdx.x % nch;
+    cid = blockIdx.x / nch;
+    ncl = gridDim.x / nch;
+  }
   // component pair (rank * 2T + j, rank * 2T + T + j); j is the local index
   const int j = static_cast<int>(threadIdx.x) % T;
-  const int kb = rank * 2 * T;
+  const int kb = (PRE ? chunk : rank) * 2 * T;
   const int k_cur = st->k_cur;
   const ModelBuf& mb = st->cur ? b1 : b0;
-  constexpr unsigned kTileBytes = kTile * sizeof(float4) + 4 * sizeof(double);
+  constexpr unsigned kTileBytes =
+      kTile * sizeof(float4) + 4 * sizeof(double) + (PRE ? kTile * sizeof(float2) : 0);
   auto issue_tile = [&](int t, int buf) {  // one thread: TMA bulk copy of tile t
     mbar_expect_tx(&sm.xs_full[buf], kTileBytes);
     bulk_g2s(sm.xs[buf], xt + static_cast<int64_t>(t) * kTile, kTile * sizeof(float4),
              &sm.xs_full[buf]);
     bulk_g2s(sm.tcs[buf], tc + static_cast<int64_t>(t) * 4, 4 * sizeof(double), &sm.xs_full[buf]);
+    if constexpr (PRE)
+      bulk_g2s(sm.ls[buf], lse + static_cast<int64_t>(t) * kTile, kTile * sizeof(float2),
+               &sm.xs_full[buf]);
   };
   // Each CTA (cluster) takes a contiguous, balanced range of P-point
   // sub-tiles (a round-robin over 128-point tiles leaves 16 or 17 tiles per
@@ -765,6 +654,21 @@ __global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
 #pragma unroll
     for (int q = 0; q < D; ++q) NB[q] = pk(nbf[0][q], nbf[1][q]);
   };
+  // one point (the same FFMA tree as dens), chain started from nbase
+  auto dens1 = [&](const float4 x, const f2_t (&PP)[NP], const f2_t (&NB)[D], f2_t nbase,
+                   f2_t& Q) {
+    const f2_t X0 = pk(x.x, x.x), X1 = pk(x.y, x.y), X2 = pk(x.z, x.z);
+    const f2_t Y0 = fma2(PP[0], X0, NB[0]);
+    const f2_t Y1 = fma2(PP[2], X1, fma2(PP[1], X0, NB[1]));
+    const f2_t Y2 = fma2(PP[5], X2, fma2(PP[4], X1, fma2(PP[3], X0, NB[2])));
+    f2_t qv = fma2(Y2, Y2, fma2(Y1, Y1, fma2(Y0, Y0, nbase)));
+    if constexpr (D == 4) {
+      const f2_t X3 = pk(x.w, x.w);
+      const f2_t Y3 = fma2(PP[9], X3, fma2(PP[8], X2, fma2(PP[7], X1, fma2(PP[6], X0, NB[3]))));
+      qv = fma2(Y3, Y3, qv);
+    }
+    Q = qv;
+  };
   // Q = q - base2 = -(log2 density) of the P points at xs, both components
   auto dens = [&](const float4* xs, const f2_t (&PP)[NP], const f2_t (&NB)[D], f2_t NBASE,
                   f2_t (&Q)[P]) {
@@ -836,6 +740,27 @@ __global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
           }
         }
         f2_t E[P];
+        if constexpr (PRE) {
+          // r = 2^-(Q + L): the shift starts the FFMA chain (L.x = 0), or a
+          // far point (L.x = -Q_min, uniform) adds Q - Q_min first, then the
+          // small remainder (estep_chunked.cu)
+#pragma unroll
+          for (int p = 0; p < P; ++p) {
+            const float2 L = sm.ls[tb][s * P + p];
+            const bool far = L.x != 0.f;
+            f2_t q1[1];
+            const f2_t nb1 = far ? NBASE : add2(NBASE, pk(L.y, L.y));
+            dens1(sm.xs[tb][s * P + p], PP, NB, nb1, q1[0]);
+            E[p] = far ? add2(add2(q1[0], pk(L.x, L.x)), pk(L.y, L.y)) : q1[0];
+          }
+#pragma unroll
+          for (int p = 0; p < P; p += 2) {
+            sm.ering[slot][p / 2][j] = make_float4(ex2n(lo2(E[p])), ex2n(hi2(E[p])),
+                                                   ex2n(lo2(E[p + 1])), ex2n(hi2(E[p + 1])));
+          }
+          mbar_arrive(&sm.full[slot]);
+          continue;
+        }
         dens(&sm.xs[tb][s * P], PP, NB, NBASE, E);
         float v[P];
 #pragma unroll
@@ -937,7 +862,7 @@ __global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
       } else {
         mbar_wait(&sm.full[slot], (g / kRing) & 1u);
       }
-      float S = cta_combine<NWC, P, false>(sm.red[slot], lane);
+      float S = PRE ? 1.f : cta_combine<NWC, P, false>(sm.red[slot], lane);
       f2_t E[P];
 #pragma unroll
       for (int p = 0; p < P; p += 2) {
@@ -953,7 +878,7 @@ __global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
       }
       float M = 0.f;
       const bool valid_g = q0 + fp < npts;
-      const bool exact = __any_sync(0xffffffffu, valid_g && (exact_mode != 0 ||
+      const bool exact = !PRE && __any_sync(0xffffffffu, valid_g && (exact_mode != 0 ||
                                                              !(S >= 0x1p-64f && S <= 0x1p64f)));
       if (exact) {  // uniform over consumer warps: identical S everywhere
         f2_t PP[NP], NBASE, NB[D];
@@ -997,14 +922,26 @@ __global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
         xb ^= 1;
         ++xcount;
       }
-      if (finisher && valid_g && rank == 0) ll_acc += static_cast<double>(M + lg2f(S));
+      if constexpr (PRE) {
+        if (finisher && valid_g && chunk == 0) {
+          const float2 L = sm.ls[tb][q0 + fp];
+          ll_acc += static_cast<double>(L.x) + static_cast<double>(L.y);
+        }
+      } else {
+        if (finisher && valid_g && rank == 0) ll_acc += static_cast<double>(M + lg2f(S));
+      }
       const float scale_g = valid_g ? rcpf(S) : 0.f;
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        const float sc = __shfl_sync(0xffffffffu, scale_g, p * G);
         const float4 x = sm.xs[tb][q0 + p];
         const float xv[4] = {x.x, x.y, x.z, x.w};
-        const f2_t R = mul2(E[p], pk(sc, sc));
+        f2_t R;
+        if constexpr (PRE) {
+          R = q0 + p < npts ? E[p] : 0ull;  // padding points of a partial tile
+        } else {
+          const float sc = __shfl_sync(0xffffffffu, scale_g, p * G);
+          R = mul2(E[p], pk(sc, sc));
+        }
         f2_t DD[D], W[D];
 #pragma unroll
         for (int i = 0; i < D; ++i) {
@@ -1045,7 +982,7 @@ __global__ void __launch_bounds__(2 * NWH * 32, 8 / NWH)
     double s = 0.0;
 #pragma unroll
     for (int p = 0; p < P; ++p) s += __shfl_sync(0xffffffffu, ll_acc, p * G);
-    if (lane == 0 && rank == 0) ll_part[cid] = s * kLn2;
+    if (lane == 0 && rank == 0 && chunk == 0) ll_part[cid] = s * kLn2;
   }
   }  // consumers
   if constexpr (C > 1) {
@@ -1112,7 +1049,39 @@ cudaError_t launch_estep_ws(const PointsDev& pts, const ModelBuf* bufs, const Em
   cfg.numAttrs = C > 1 ? 1 : 0;
   const int split_sub = ncl * C <= sm_count ? 1 : 0;  // one CTA per SM: balance sub-tiles
   return cudaLaunchKernelEx(&cfg, kern, pts.xt, pts.tc, pts.n, pts.ntiles, bufs[0], bufs[1], st,
-                            kpad, partials, ll_part, exact_mode, split_sub);
+                            kpad, partials, ll_part, exact_mode, split_sub,
+                            static_cast<const float2*>(nullptr), 1);
+}
+
+// pass B of the chunked E step (K > 512): the warp-specialised kernel with
+// known normalisers, one CTA per (512-component chunk, point range), one CTA
+// per SM (groups = sm_count / nch point ranges)
+template <int D>
+cudaError_t launch_estep_ws_pre_d(const PointsDev& pts, const ModelBuf* bufs, const EmState* st,
+                                  int kpad, int nch, const float2* lse, double* partials,
+                                  double* ll_part, int sm_count, cudaStream_t s, int* ncl_out) {
+  constexpr int P = GMMB_WS_P, NWH = 8;
+  using Smem = WsSmem<NWH, P, 1>;
+  auto kern = estep_ws_kernel<D, NWH, P, 1, true>;
+  const size_t smem = ((sizeof(Smem) + 15) & ~size_t(15)) + sizeof(double2) * nstats(D) * NWH * 32;
+  static bool attr_set[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr_set[dev & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr_set[dev & 63] = true;
+  }
+  int groups = sm_count / nch;
+  if (groups < 1) groups = 1;
+  if (groups > pts.ntiles) groups = pts.ntiles;
+  *ncl_out = groups;
+  if (!partials) return cudaSuccess;
+  kern<<<nch * groups, 2 * NWH * 32, smem, s>>>(pts.xt, pts.tc, pts.n, pts.ntiles, bufs[0],
+                                                bufs[1], st, kpad, partials, ll_part, 0, 1, lse,
+                                                nch);
+  return cudaGetLastError();
 }
 
 template <int D, int NW, int C, int P, int CPT>
@@ -1611,13 +1580,186 @@ __device__ __forceinline__ void commit_body(
 // Commit kernel. Inside the EM while-graph (use_cond = 1) it also sets the
 // loop condition from the device state: the whole EM loop runs without a
 // host round trip (CUDA conditional graph node).
+// Any K (k_in > kMaxK): the same commit with the chunk loop at run time and
+// the compaction map in global memory (rec.map[k] = compacted index of a
+// kept component). Chunk totals are combined serially in chunk order, so
+// the result does not depend on the schedule.
+template <int D>
+__device__ __forceinline__ void commit_body_big(
+    int mode, const RecBuf& rec, int k_in_arg, const double* __restrict__ red_ll,
+    const double* __restrict__ ll_part, int ncl,
+    const ModelBuf& b0, const ModelBuf& b1, EmState* st, double* __restrict__ ll_trace) {
+  constexpr int T = 1024;
+  __shared__ int s_wcnt[32];
+  __shared__ double s_wtot[32];
+  __shared__ int s_woff[32];
+  __shared__ int s_base;
+  __shared__ double s_tot;
+  __shared__ int s_flag;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (st->done) return;
+  const int cur0 = st->cur;
+  const int k_in = mode == 0 ? st->k_cur : k_in_arg;
+  if (mode == 0) {  // EM bookkeeping: sogmm.cpp:490-498
+    double ll = 0.0;
+    if (warp == 0) {
+      if (ll_part) {
+        for (int c = lane; c < ncl; c += 32) ll += ll_part[c];
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) ll += __shfl_xor_sync(0xffffffffu, ll, off);
+      } else {
+        ll = red_ll[0];
+      }
+    }
+    if (tid == 0) {
+      const int iter = st->iter;
+      st->units = st->units + st->npts * static_cast<double>(k_in);
+      if (ll_trace) ll_trace[iter] = ll;
+      st->ll = ll;
+      st->iter = iter + 1;
+      int conv = 0;
+      if (iter > 0) {
+        const double rel = fabs(ll - st->ll_prev) / fmax(fabs(st->ll_prev), 1e-12);
+        if (rel < st->tol) conv = 1;
+      }
+      if (conv) {
+        st->converged = 1;
+        st->done = 1;
+      }
+      st->ll_prev = ll;
+      s_flag = conv;
+    }
+    __syncthreads();
+    if (s_flag) return;
+  }
+  if (tid == 0) {
+    s_base = 0;
+    s_tot = 0.0;
+    s_flag = 0x7fffffff;
+  }
+  __syncthreads();
+  // order-preserving compaction map + kept weight total (sogmm.cpp:418-433)
+  for (int k0 = 0; k0 < k_in; k0 += T) {
+    const int k = k0 + tid;
+    const int fl = k < k_in ? rec.flags[k] : 0;
+    const int keep = fl & 1;
+    int incl = keep;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += v;
+    }
+    double wt = keep ? rec.count[k] : 0.0;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) wt += __shfl_xor_sync(0xffffffffu, wt, off);
+    if (lane == 31) s_wcnt[warp] = incl;
+    if (lane == 0) s_wtot[warp] = wt;
+    __syncthreads();
+    if (warp == 0) {
+      const int wc = s_wcnt[lane];
+      int wi = wc;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, wi, off);
+        if (lane >= off) wi += v;
+      }
+      s_woff[lane] = wi - wc;
+      double t = s_wtot[lane];
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+      if (lane == 31) s_wcnt[0] = wi;  // kept in this chunk (read after the barrier)
+      if (lane == 0) s_wtot[0] = t;
+    }
+    __syncthreads();
+    const int base = s_base;
+    if (keep) {
+      const int j = base + s_woff[warp] + incl - keep;
+      rec.map[k] = j;
+      if (!(fl & 2)) atomicMin(&s_flag, j);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      s_base = base + s_wcnt[0];
+      s_tot += s_wtot[0];
+    }
+    __syncthreads();
+  }
+  const int k_new = s_base;
+  const double total = s_tot;
+  if (k_new == 0) {
+    if (tid == 0) {
+      st->error = 3;
+      st->error_kind = 2;
+      st->error_index = 0;
+      st->done = 1;
+    }
+    return;
+  }
+  if (s_flag != 0x7fffffff) {
+    if (tid == 0) {
+      st->error = 3;
+      st->error_kind = 1;
+      st->error_index = s_flag;
+      st->done = 1;
+    }
+    return;
+  }
+  const double half_d_ln2pi = 0.5 * D * kLog2Pi;
+  int dst_sel;
+  if (mode == 0 && k_new == k_in) {
+    dst_sel = cur0 ^ 1;
+    const ModelBuf& dst = dst_sel ? b1 : b0;
+    for (int k = tid; k < k_new; k += T) {
+      const double w = rec.count[k] / total;
+      dst.w[k] = w;
+      const double b2 = kLog2E * (log(w) + rec.logdet[k] - half_d_ln2pi);
+      const float hi = static_cast<float>(b2);
+      *reinterpret_cast<float2*>(&dst.cst[k].p[10]) =
+          make_float2(hi, static_cast<float>(b2 - static_cast<double>(hi)));
+    }
+  } else {
+    dst_sel = cur0;
+    const ModelBuf& dst = dst_sel ? b1 : b0;
+    const ModelBuf& src_m = cur0 ? b0 : b1;
+    for (int k = tid; k < k_in; k += T) {
+      if (!(rec.flags[k] & 1)) continue;
+      const int j = rec.map[k];
+      const double w = rec.count[k] / total;
+      dst.w[j] = w;
+      const double* sm = mode == 0 ? src_m.mu + k * 4 : rec.mean + k * 4;
+      for (int q = 0; q < 4; ++q) dst.mu[j * 4 + q] = sm[q];
+      const double* sc = mode == 0 ? src_m.cov + k * 10 : rec.cov + k * 10;
+      for (int q = 0; q < 10; ++q) dst.cov[j * 10 + q] = sc[q];
+      const float* sp = mode == 0 ? src_m.cst[k].p : rec.pc + k * 16;
+      float v[16];
+      for (int q = 0; q < 16; ++q) v[q] = sp[q];
+      const double b2 = kLog2E * (log(w) + rec.logdet[k] - half_d_ln2pi);
+      v[10] = static_cast<float>(b2);
+      v[11] = static_cast<float>(b2 - static_cast<double>(v[10]));
+      for (int q = 0; q < 16; ++q) dst.cst[j].p[q] = v[q];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    st->removed = st->removed + (k_in - k_new);
+    st->k_cur = k_new;
+    if (mode == 0) {
+      st->cur = dst_sel;
+      if (st->iter >= st->max_iters) st->done = 1;
+    }
+  }
+}
+
 template <int D>
 __global__ void __launch_bounds__(1024) commit_kernel(
     int mode, RecBuf rec, int k_in_arg, const double* __restrict__ red_ll,
     const double* __restrict__ ll_part, int ncl,
     ModelBuf b0, ModelBuf b1, EmState* st, double* __restrict__ ll_trace,
     cudaGraphConditionalHandle cond, int use_cond) {
-  commit_body<D>(mode, rec, k_in_arg, red_ll, ll_part, ncl, b0, b1, st, ll_trace);
+  if (k_in_arg > kMaxK)
+    commit_body_big<D>(mode, rec, k_in_arg, red_ll, ll_part, ncl, b0, b1, st, ll_trace);
+  else
+    commit_body<D>(mode, rec, k_in_arg, red_ll, ll_part, ncl, b0, b1, st, ll_trace);
   if (use_cond) {
     __syncthreads();
     if (threadIdx.x == 0) cudaGraphSetConditional(cond, st->done ? 0u : 1u);
@@ -1825,10 +1967,26 @@ cudaError_t launch_factor_dump(int d, const ModelBuf* bufs, const EmState* st,
 // ---------------------------------------------------------------------------
 // launch helpers
 // ---------------------------------------------------------------------------
+cudaError_t launch_estep_ws_pre(const PointsDev& pts, const ModelBuf* bufs, const EmState* st,
+                                int kpad, int nch, const float2* lse, double* partials,
+                                double* ll_part, int sm_count, cudaStream_t s, int* ncl_out) {
+  if (pts.d == 4)
+    return launch_estep_ws_pre_d<4>(pts, bufs, st, kpad, nch, lse, partials, ll_part, sm_count,
+                                    s, ncl_out);
+  return launch_estep_ws_pre_d<3>(pts, bufs, st, kpad, nch, lse, partials, ll_part, sm_count, s,
+                                  ncl_out);
+}
+
 cudaError_t launch_estep_stats(const PointsDev& pts, const ModelBuf* bufs,
                                const EmState* st, int k0, double* partials,
                                double* ll_part, int exact_mode,
-                               int sm_count, cudaStream_t s, int* ncl_out) {
+                               int sm_count, cudaStream_t s, int* ncl_out,
+                               const ChunkScratch* chunk) {
+  if (GMMB_CHUNKED && k0 > kCtaComps) {
+    if (partials && !chunk) return cudaErrorInvalidValue;
+    return launch_estep_chunked(pts, bufs, st, k0, partials, ll_part, exact_mode, sm_count, s,
+                                ncl_out, chunk);
+  }
   if (pts.d == 4)
     return launch_estep_d<4>(pts, bufs, st, k0, partials, ll_part, exact_mode,
                              sm_count, s, ncl_out);

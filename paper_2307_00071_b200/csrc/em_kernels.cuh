@@ -20,6 +20,7 @@ struct RecBuf {
   double* logdet;   // [kcap]      sum ln diag P
   float* pc;        // [kcap][16]  scaled precision factor
   int* flags;       // [kcap]      bit0 keep, bit1 SPD ok
+  int* map;         // [kcap]      compacted index (commit, K > kMaxK)
 };
 
 struct PointsDev {
@@ -31,6 +32,29 @@ struct PointsDev {
   int ntiles;
 };
 
+// Scratch of the chunked two-pass E step (K > 512, estep_chunked.cu):
+// part[nch][npad] per-chunk per-point sums, lse[npad] per-point log2
+// normalisers as (shift, remainder) pairs (shift = 0 except for points that
+// needed the exact max-shifted log-sum-exp), xlist[npad] + *xcount those
+// points (npad = ntiles * kTile, nch = ceil(K / 512)).
+struct ChunkScratch {
+  float* part;
+  float2* lse;
+  int* xlist;
+  int* xcount;
+};
+size_t chunk_scratch_floats(int k0, int64_t n);  // part + lse
+cudaError_t launch_estep_chunked(const PointsDev& pts, const ModelBuf* bufs, const EmState* st,
+                                 int k0, double* partials, double* ll_part, int exact_mode,
+                                 int sm_count, cudaStream_t s, int* ncl_out,
+                                 const ChunkScratch* scr);
+
+// Pass B of the chunked E step on the warp-specialised kernel (normalisers
+// known): grid nch x (sm_count / nch); *ncl_out = point ranges.
+cudaError_t launch_estep_ws_pre(const PointsDev& pts, const ModelBuf* bufs, const EmState* st,
+                                int kpad, int nch, const float2* lse, double* partials,
+                                double* ll_part, int sm_count, cudaStream_t s, int* ncl_out);
+
 // Fused E-step + sufficient statistics (one EM iteration's data pass).
 // Writes per-cluster FP64 partial statistics [ncl][kpad][nstats(D)] and
 // per-cluster log-likelihood partials (natural log) [ncl]. exact_mode = 1
@@ -38,9 +62,12 @@ struct PointsDev {
 cudaError_t launch_estep_stats(const PointsDev& pts, const ModelBuf* bufs,
                                const EmState* st, int k0, double* partials,
                                double* ll_part, int exact_mode,
-                               int sm_count, cudaStream_t s, int* ncl_out);
+                               int sm_count, cudaStream_t s, int* ncl_out,
+                               const ChunkScratch* chunk = nullptr);
 
-// (partials == nullptr: only report the cluster count *ncl_out.)
+// (partials == nullptr: only report the cluster count *ncl_out.) K > 512
+// runs the chunked two-pass kernels (chunk scratch required) unless
+// GMMB_CHUNKED=0 at build time (the cluster kernels, K <= 4096).
 
 // FP64 L, P, logdet of buffer st->cur (cholesky_cache API), 33 doubles/comp.
 cudaError_t launch_factor_dump(int d, const ModelBuf* bufs, const EmState* st,

@@ -1,18 +1,24 @@
 """Per-region stall attribution from an ncu source page (SASS).
 
-usage: python scripts/ncu_source.py <rep> [chunk]
+usage: python scripts/ncu_source.py <rep> [chunk] [kernel regex]
 Prints chunks of consecutive SASS instructions holding >1% of stall samples,
 with their top stall reasons and opcodes.
 """
 import csv, io, subprocess, sys
 rep = sys.argv[1]
 chunk = int(sys.argv[2]) if len(sys.argv) > 2 else 64
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+kf = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+out = subprocess.run(["ncu", "-i", rep, *kf, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 i = next(k for k, r in enumerate(rows) if r and r[0] == "Address")
 h = rows[i]
-data = [dict(zip(h, r)) for r in rows[i + 1:] if len(r) == len(h)]
+data = []
+for r in rows[i + 1:]:
+    if r and r[0] == "Address":
+        break  # next kernel's section
+    if len(r) == len(h):
+        data.append(dict(zip(h, r)))
 sc = [k for k in h if k.startswith("stall_")]
 S = "Warp Stall Sampling (All Samples)"
 tot = sum(int(d[S] or 0) for d in data) or 1

@@ -376,3 +376,19 @@ def test_fit_large_k_end_to_end(gm, orc, ctx, k, stride):
     assert ll_err(res.ll_trace, ref["ll_trace"]) < LL_TOL
     assert_model_close(res.model.weights, res.model.means, res.model.covariances,
                        ref["w"], ref["mu"], ref["cov"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [4608, 5000])
+def test_em_step_above_4096_chunked(gm, orc, ctx, k):
+    """K > 4096 (the reference accepts any 1 <= k <= N, sogmm.cpp:200-202):
+    the chunked two-pass E step (9-10 chunks of 512) and the run-time-chunked
+    commit (compaction map in global memory)."""
+    p = gm.structured_scene(60000, 8, 0.005)
+    w, mu, cov = fixed_init(orc, p, k)
+    ll, m1, rm = gm.em_step(p, gm.Gmm(w, mu, cov), 1e-6, ctx=ctx)
+    lg, rll = orc.e_step(p, w, mu, cov)
+    rw, rmu, rcov, rrm = orc.m_step(p, lg, 1e-6)
+    assert rm == rrm
+    assert abs(ll - rll) / abs(rll) < LL_TOL
+    assert_model_close(m1.weights, m1.means, m1.covariances, rw, rmu, rcov, tol=1e-5)
