@@ -135,7 +135,10 @@ int gmmb_fit_from_resident(gmmb_ctx* ctx, int m, const double* w0,
                            double* mu_out, double* cov_out, double* ll_trace,
                            gmmb_fit_stats* stats);
 
-/* ---- single steps (teacher forcing / API parity) -----------------------*/
+/* ---- single steps (teacher forcing / API parity) -----------------------
+ * These calls stage their own input in the context's buffers: afterwards
+ * the context holds no resident cloud (gmmb_fit_*_resident return 2 until
+ * the next gmmb_upload / gmmb_fit_k / gmmb_ingest_images). */
 /* kinit (sogmm.hpp:52, sogmm.cpp:197-337): labels[N] = column of the 0 in
  * each row of the one-hot log_gamma; centers[k] = k-means++ seed indices. */
 int gmmb_kinit(gmmb_ctx* ctx, const double* pts, int64_t n, int d, int k,

@@ -1184,6 +1184,7 @@ int gmmb_kinit(gmmb_ctx* c, const double* pts, int64_t n, int d, int k, uint64_t
     if (!c) throw Err{2, "null context"};
     if (c->world > 1) throw Err{2, "gmmb_kinit is single-device; use gmmb_fit_k"};
     upload(c, pts, n, d, 0, n);
+    c->have_cloud = false;  // single-step input: not a resident cloud for *_resident fits
     validate(c);
     check_cloud_flags(c);
     if (k < 1 || k > n) throw Err{2, "kinit: k must satisfy 1 <= k <= N"};  // sogmm.cpp:200
@@ -1205,6 +1206,7 @@ int gmmb_e_step(gmmb_ctx* c, const double* pts, int64_t n, int d, int m, const d
   return guarded([&] {
     if (!c) throw Err{2, "null context"};
     upload(c, pts, n, d, 0, n);
+    c->have_cloud = false;  // single-step input: not a resident cloud for *_resident fits
     validate(c);
     check_cloud_flags(c);
     if (m < 1 || !w || !mu || !cov) throw Err{2, "model has no components"};
@@ -1285,6 +1287,7 @@ int gmmb_gbms(gmmb_ctx* c, const double* pts, int64_t n, int d, const gmmb_gbms_
   return guarded([&] {
     if (!c) throw Err{2, "null context"};
     upload(c, pts, n, d, 0, n);
+    c->have_cloud = false;  // single-step input: not a resident cloud for *_resident fits
     validate(c);
     check_cloud_flags(c);  // cloud.validate() (sogmm.cpp:36)
     const GbmsResultHost r = run_gbms(c, gp, modes, modes_capacity);
@@ -1319,6 +1322,7 @@ int gmmb_score(gmmb_ctx* c, const double* pts, int64_t n, int d, int m, const do
     if (n < 1) throw Err{2, "empty cloud"};  // inference.cpp:143
     validate_model(m, d, w, mu, cov);
     upload(c, pts, n, d, 0, n);
+    c->have_cloud = false;  // single-step input: not a resident cloud for *_resident fits
     validate(c);
     check_cloud_flags(c);
     const int bad = upload_factors(c, m, d, w, mu, cov, false);
@@ -1400,6 +1404,7 @@ int gmmb_m_step(gmmb_ctx* c, const double* pts, int64_t n, int d, const double* 
     if (cov_reg < 0.0) throw Err{2, "cov_reg must be >= 0"};
     if (!log_gamma || m < 1) throw Err{2, "responsibility rows != point count"};
     upload(c, pts, n, d, 0, n);
+    c->have_cloud = false;  // single-step input: not a resident cloud for *_resident fits
     ensure_model(c, m);
     c->dense.ensure(static_cast<size_t>(n) * m);
     ck(cudaMemcpyAsync(c->dense.p, log_gamma, sizeof(double) * n * m, cudaMemcpyHostToDevice, c->s), "H2D");
@@ -1421,6 +1426,7 @@ int gmmb_em_step(gmmb_ctx* c, const double* pts, int64_t n, int d, int m, const 
     if (!c) throw Err{2, "null context"};
     gmmb_em_params em{1, 0.0, cov_reg, 0};
     upload(c, pts, n, d, 0, n);
+    c->have_cloud = false;  // single-step input: not a resident cloud for *_resident fits
     layout(c);
     check_cloud_flags(c);
     ensure_model(c, m);
@@ -1449,6 +1455,7 @@ int gmmb_cholesky_cache(gmmb_ctx* c, int d, int m, const double* covs, double* l
     // the device and read back the FP64 factors through a dedicated pass
     set_device(c);
     c->d = d;
+    c->have_cloud = false;  // the resident cloud's D no longer holds
     ensure_model(c, m);
     std::vector<double> w(m, 1.0 / m), mu(static_cast<size_t>(m) * d, 0.0);
     upload_model(c, m, w.data(), mu.data(), covs);

@@ -90,13 +90,18 @@ __global__ void seed_centroid_kernel(const double* __restrict__ norm,
   weights[s] = 1.0;
 }
 
-__device__ __forceinline__ uint64_t cell_key(const double* x, double bw) {
-  uint64_t key = 0;
-  for (int d = 0; d < 4; ++d) {
-    const int64_t c = static_cast<int64_t>(floor(x[d] / bw));
-    key = (key << 16) | (static_cast<uint64_t>(c) & 0xffff);
-  }
+// Grid cell key: a 64-bit hash of the four integer cell coordinates (no
+// range limit, so any bandwidth works). Different cells that collide only
+// share a sorted run; every visit re-checks the exact distance.
+__device__ __forceinline__ uint64_t cell_hash(const int64_t (&c)[4]) {
+  uint64_t key = 0x243f6a8885a308d3ULL;
+  for (int d = 0; d < 4; ++d) key = mix64(key ^ static_cast<uint64_t>(c[d]));
   return key;
+}
+__device__ __forceinline__ uint64_t cell_key(const double* x, double cell) {
+  int64_t c[4];
+  for (int d = 0; d < 4; ++d) c[d] = static_cast<int64_t>(floor(x[d] / cell));
+  return cell_hash(c);
 }
 
 __global__ void grid_keys_kernel(const double* __restrict__ seeds, int S, double bw,
@@ -117,26 +122,27 @@ __device__ __forceinline__ int lower_bound_u64(const uint64_t* k, int n, uint64_
   return lo;
 }
 
-// visit every seed j within radius r of q through the cell grid (cell = bw)
+// visit every seed j within radius r <= cell of q through the cell grid
+// (the 3^4 cells around q's own); a hash collision that puts another cell's
+// seeds in a visited run is filtered by the distance check (two of the 81
+// neighbour cells sharing one 64-bit hash, which would visit a run twice,
+// has probability ~2^-52)
 template <typename V>
-__device__ __forceinline__ void for_each_near(const double* q, double r, double bw,
+__device__ __forceinline__ void for_each_near(const double* q, double r, double cell,
                                               const double* __restrict__ seeds,
                                               const uint64_t* __restrict__ gk,
                                               const int32_t* __restrict__ gi, int S, V&& visit) {
   int64_t c[4];
-  for (int d = 0; d < 4; ++d) c[d] = static_cast<int64_t>(floor(q[d] / bw));
+  for (int d = 0; d < 4; ++d) c[d] = static_cast<int64_t>(floor(q[d] / cell));
   const double r2 = r * r;
   for (int nb = 0; nb < 81; ++nb) {
     int t = nb;
-    uint64_t key = 0;
-    bool ok = true;
+    int64_t cc[4];
     for (int d = 0; d < 4; ++d) {
-      const int64_t cd = c[d] + (t % 3) - 1;
+      cc[d] = c[d] + (t % 3) - 1;
       t /= 3;
-      ok = ok && cd >= 0 && cd <= 0xffff;
-      key = (key << 16) | (static_cast<uint64_t>(cd) & 0xffff);
     }
-    if (!ok) continue;
+    const uint64_t key = cell_hash(cc);
     for (int p = lower_bound_u64(gk, S, key); p < S && gk[p] == key; ++p) {
       const int j = gi[p];
       const double* x = seeds + j * 4;
@@ -340,15 +346,17 @@ cudaError_t gbms_run(const double* x64, int64_t n, GbmsParamsDev prm, GbmsScratc
     }
     if (shift < prm.tol) break;
   }
-  // single-linkage merge (sogmm.cpp:148-168)
-  grid_keys_kernel<<<blocks(S), 256, 0, s>>>(g.seeds, S, prm.bandwidth, g.k0, g.i0);
+  // single-linkage merge (sogmm.cpp:148-168): cells at least as wide as the
+  // merge radius, so the 3^4 neighbourhood covers every link
+  const double mcell = fmax(prm.bandwidth, prm.merge_radius);
+  grid_keys_kernel<<<blocks(S), 256, 0, s>>>(g.seeds, S, mcell, g.k0, g.i0);
   bytes = g.temp_bytes;
   GB_CK(cub::DeviceRadixSort::SortPairs(g.temp, bytes, g.k0, g.k1, g.i0, g.i1, S, 0, 64, s));
   int32_t* label = g.i2;
   iota_kernel32<<<blocks(S), 256, 0, s>>>(label, S);
   for (int pass = 0; pass < S + 1; ++pass) {
     GB_CK(cudaMemsetAsync(g.flag, 0, sizeof(int), s));
-    link_kernel<<<blocks(S), 256, 0, s>>>(g.seeds, S, prm.merge_radius, prm.bandwidth, g.k1, g.i1,
+    link_kernel<<<blocks(S), 256, 0, s>>>(g.seeds, S, prm.merge_radius, mcell, g.k1, g.i1,
                                           label, g.flag);
     int changed = 0;
     GB_CK(cudaMemcpyAsync(&changed, g.flag, sizeof(int), cudaMemcpyDeviceToHost, s));

@@ -294,8 +294,18 @@ int gmmb_load_model_json(const char* path, int capacity, double* w, double* mu, 
           jc->arr[b].arr.size() != 10)
         throw IoErr{1, std::string("bad row size in ") + path};
       vw[b] = jw->arr[b].num;
-      for (int d = 0; d < 4; ++d) vmu[b * 4 + d] = jm->arr[b].arr[d].num;
-      for (int k = 0; k < 10; ++k) vc[b * 10 + k] = jc->arr[b].arr[k].num;
+      // every element must be a number (the reference's get<double>() raises
+      // GmmFormatError on anything else, gmm_io.cpp)
+      for (int d = 0; d < 4; ++d) {
+        if (jm->arr[b].arr[d].kind != Json::Num)
+          throw IoErr{1, std::string("malformed model data in ") + path};
+        vmu[b * 4 + d] = jm->arr[b].arr[d].num;
+      }
+      for (int k = 0; k < 10; ++k) {
+        if (jc->arr[b].arr[k].kind != Json::Num)
+          throw IoErr{1, std::string("malformed model data in ") + path};
+        vc[b * 10 + k] = jc->arr[b].arr[k].num;
+      }
     }
     finalize_loaded(vw, vmu, vc);
     if (m_out) *m_out = static_cast<int>(m);

@@ -6,6 +6,8 @@ component and iteration counts must match exactly, modes within 1e-9."""
 import numpy as np
 import pytest
 
+from parity import LL_TOL, assert_model_close
+
 
 def test_oracle_gbms_invariants(gm, orc):
     # two well separated blobs -> two modes near the blob centres
@@ -47,3 +49,55 @@ def test_fit_with_gbms(gm, orc, ctx):
     assert abs(r.final_log_likelihood - ref["final_ll"]) <= 1e-5 * abs(ref["final_ll"])
     with pytest.raises(ValueError, match="bandwidth"):
         gm.fit(p, gm.GbmsParams(bandwidth=0.0), ctx=ctx)
+
+
+@pytest.mark.gpu
+def test_gbms_merge_radius_above_bandwidth(gm, orc, ctx):
+    """merge_radius > bandwidth: the merge grid's cells are as wide as the
+    merge radius (sogmm.cpp:148-168 links every pair within it)."""
+    p = gm.synthetic_frame_cloud()
+    comp, it, modes = gm.gbms(p, gm.GbmsParams(bandwidth=0.03, merge_radius=0.05), ctx=ctx)
+    rc, rit, _, rmodes = orc.gbms(p, 0.03, merge_radius=0.05)
+    assert (comp, it) == (rc, rit)
+    assert np.max(np.abs(modes - rmodes) / np.maximum(np.abs(rmodes), 1.0)) < 1e-9
+
+
+@pytest.mark.gpu
+def test_gbms_tiny_bandwidth_cells_beyond_16_bits(gm, orc, ctx):
+    """bandwidth < 1/65535: cell coordinates beyond 16 bits (hashed keys)."""
+    rng = np.random.default_rng(3)
+    p = np.column_stack([rng.random((3000, 3)) * 1e-3, rng.random(3000)])
+    p[:1500, :3] += 1.0   # two far clusters: normalised bandwidth 1e-5 of the range
+    comp, it, modes = gm.gbms(p, gm.GbmsParams(bandwidth=1e-5), ctx=ctx)
+    rc, rit, _, rmodes = orc.gbms(p, 1e-5)
+    assert (comp, it) == (rc, rit)
+    assert np.all(np.isfinite(modes))
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_fit_default_bandwidth_above_4096_components(gm, orc, ctx):
+    """fit(cloud, 0.015) on the cfg2 frame: GBMS finds 5,844 components, so
+    K > 4096 (sogmm.cpp:475-477 accepts any K <= N). GBMS count vs the
+    oracle, k-means++ centres bit-exact, one EM step (E + M) from the
+    oracle's initial model within the BASELINE bars, and fit() == fit_k(K)
+    bitwise."""
+    p = gm.synthetic_frame_cloud()
+    em = gm.EmParams(100, 1e-3, 1e-6, 0)
+    r = gm.fit(p, gm.GbmsParams(bandwidth=0.015), em, ctx=ctx)
+    rc, _, _, _ = orc.gbms(p, 0.015)
+    assert r.gbms_components == rc == r.k_init and rc > 4096
+    rk = gm.fit_k(p, rc, em, ctx=ctx)
+    assert np.array_equal(rk.ll_trace, r.ll_trace)
+    assert np.array_equal(rk.model.covariances, r.model.covariances)
+    lab, cen = gm.kinit(p, rc, 0, ctx=ctx)
+    rl, rcen = orc.kinit(p, rc, 0)
+    assert np.array_equal(cen, rcen) and np.array_equal(lab, rl)
+    w, mu, cov, _ = orc.m_step_labels(p, rl, rc, 1e-6)
+    one = gm.fit_from(p, gm.Gmm(w, mu, cov), gm.EmParams(1, 0.0, 1e-6), ctx=ctx)
+    ref = orc.fit_from(p, w, mu, cov, max_iters=1, ll_rel_tol=0.0, cov_reg=1e-6, streaming=True)
+    assert abs(one.final_log_likelihood - ref["final_ll"]) / abs(ref["final_ll"]) < LL_TOL
+    # the first step from the hard-assignment model (~53 points per
+    # component): the BASELINE bar (1.8e-5 measured)
+    assert_model_close(one.model.weights, one.model.means, one.model.covariances,
+                       ref["w"], ref["mu"], ref["cov"])

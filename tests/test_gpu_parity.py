@@ -392,3 +392,18 @@ def test_em_step_above_4096_chunked(gm, orc, ctx, k):
     assert rm == rrm
     assert abs(ll - rll) / abs(rll) < LL_TOL
     assert_model_close(m1.weights, m1.means, m1.covariances, rw, rmu, rcov, tol=1e-5)
+
+
+@pytest.mark.gpu
+def test_single_step_calls_invalidate_resident_cloud(gm, orc, ctx):
+    """e_step / kinit / ... stage their own input: a later *_resident fit
+    must not silently fit that input (or the old cloud with another D)."""
+    p = frame(gm)[::8].copy()
+    ctx.upload(p)
+    ctx.fit_k_resident(16, gm.EmParams(3, 0.0, 1e-6, 0))
+    w, mu, cov = fixed_init(orc, p[:, :3].copy(), 4)
+    gm.e_step(p[:, :3].copy(), gm.Gmm(w, mu, cov), ctx=ctx)
+    with pytest.raises(ValueError, match="no point cloud"):
+        ctx.fit_k_resident(16, gm.EmParams(3, 0.0, 1e-6, 0))
+    ctx.upload(p)
+    assert ctx.fit_k_resident(16, gm.EmParams(3, 0.0, 1e-6, 0)).em_iterations == 3

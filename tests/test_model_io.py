@@ -76,3 +76,20 @@ def test_load_errors(gm, tmp_path):
     (tmp_path / "x.json").write_text('{"weights": [1.0], "means": [[0,0,0]]}')
     with pytest.raises(gm.GmmFormatError):
         gm.load_gmm(str(tmp_path / "x.json"), json=True)
+
+
+def test_json_rejects_non_numeric_elements(gm, tmp_path):
+    """A string or nested array inside a mean / covariance row is a format
+    error (the reference's get<double>() raises GmmFormatError), not 0.0."""
+    import json
+    md = model(gm, 3, 1)
+    p = str(tmp_path / "m.json")
+    gm.save_gmm(md, p, json=True)
+    doc = json.load(open(p))
+    for field, bad in (("means", "x"), ("covariances_packed", [1.0])):
+        d = json.loads(json.dumps(doc))
+        d[field][1][2] = bad
+        q = str(tmp_path / f"bad_{field}.json")
+        json.dump(d, open(q, "w"))
+        with pytest.raises(gm.IoError, match="malformed"):
+            gm.load_gmm(q, json=True)
