@@ -1125,6 +1125,9 @@ __global__ void absmax_kernel(const double* __restrict__ x64, int64_t n, int d,
   if ((threadIdx.x & 31) == 0) atomicMax(out, b);
 }
 
+#ifndef GMMB_KPP_PERSIST
+#define GMMB_KPP_PERSIST 1  // memory-resident rounds in one persistent cooperative kernel
+#endif
 constexpr int kMemThreads = 256;  // 4 CTAs per SM resident: one wave
 constexpr int kMemPPT = 32;  // points per thread held as FP32 clocks in shared memory
 
@@ -1292,6 +1295,247 @@ __global__ void __launch_bounds__(kMemThreads, 4)
     win_io[0] = w;
     scr.centers[r] = w;
     *ticket = 0;
+  }
+}
+
+// Persistent memory-resident rounds (one cooperative wave of 4 CTAs per SM,
+// N up to 4 x sm_count x 256 x kMemPPT points): the per-round kernel's
+// arithmetic (FP32 fold prefilter, FP32 clocks kept in shared memory, exact
+// FP64 clocks inside each CTA's band) with the kernel boundary replaced by
+// a grid exchange: every CTA publishes its (clock, index) best in a slot
+// (double-buffered by round parity), arrives on a monotonic counter, and
+// once all have arrived reduces every slot itself in a fixed order, so all
+// CTAs agree on the winner without a second barrier. The FP32 coordinates
+// are SoA (12 bytes per 3D point) and the prefilter threshold is derived
+// from the stored 1/d2 (no threshold array): per point and round 24 bytes
+// (3D) of streaming reads instead of 32.
+//
+// Threshold from inv = rcp.approx(fp32(d2)), in round-to-nearest FP32:
+// 1/inv recovers d2 within 2^-21 (the FP32 rounding of d2 plus two
+// approximate reciprocals), so with u = 2^-24, a = 4.0001 u M
+//   T = d2' (1 + 2^-15) + 2.02 a sqrt(d2') + 1.01 a^2  >=  (sqrt(d2) + a)^2 (1 + 2^-16)
+// = fold_threshold(d2): the 2^-16 margin on the leading term and the 1 %
+// margins on the small ones cover every rounding error (~2^-20), so a
+// point is never filtered wrongly. inv = 0 means d2 = 0 (a chosen centre:
+// nothing folds), except in round 1 where every d2 is still +inf (no
+// filter); inv at the 1e-38 floor (d2 beyond FP32) disables the filter.
+__device__ __forceinline__ float fold_threshold_inv(float inv, float M) {
+  if (!(inv > 1e-38f)) return inv == 0.f ? -1.f : INFINITY;
+  const float d2p = rcp_approx(inv);
+  float rs;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(d2p));
+  const float a = 4.0001f * 0x1p-24f * M;
+  return fmaf(d2p, 1.0f + 0x1p-15f, fmaf(2.02f * a, d2p * rs, 1.01f * a * a));
+}
+
+// round-0 state of the persistent rounds: d2 = +inf, label 0, 1/d2 = 0, SoA
+// FP32 coordinates
+template <int D>
+__global__ void kpp_memp_init_kernel(const double* __restrict__ x64, int64_t n, KinitScratch scr) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float* xs = reinterpret_cast<float*>(scr.xf);
+  scr.d2[i] = INFINITY;
+  scr.labels[i] = 0;
+  scr.inv[i] = 0.f;
+#pragma unroll
+  for (int q = 0; q < D; ++q) xs[q * n + i] = __double2float_rn(x64[q * n + i]);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kMemThreads, 4)
+    kpp_memp_kernel(const double* __restrict__ x64, int64_t n, int k, uint64_t seed,
+                    KinitScratch scr, unsigned long long* arrive) {
+  __shared__ float s_a[kMemPPT * kMemThreads];
+  __shared__ double s_c[kMemThreads / 32];
+  __shared__ long long s_i[kMemThreads / 32];
+  __shared__ long long s_u[kMemThreads / 32];
+  __shared__ float s_f[kMemThreads / 32];
+  __shared__ long long s_w;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kMemThreads / 32;
+  const int nblk = gridDim.x;
+  // n < 2^31 on one device (upload): 32-bit point indices
+  const int ni = static_cast<int>(n);
+  const int G = nblk * kMemThreads;
+  const int base = blockIdx.x * kMemThreads + tid;
+  const int mcount = base < ni ? (ni - 1 - base) / G + 1 : 0;  // this thread's points
+  // SoA FP32 coordinates, written by kpp_memp_init_kernel before this
+  // launch (read-only here, like the keys): non-coherent loads
+  const float* __restrict__ xq[D];
+#pragma unroll
+  for (int q = 0; q < D; ++q) xq[q] = reinterpret_cast<const float*>(scr.xf) + q * n;
+  const double* __restrict__ x0 = x64;
+  const double* __restrict__ x1 = x64 + n;
+  const double* __restrict__ x2 = x64 + 2 * n;
+  const double* __restrict__ x3p = x64 + 3 * n;
+  const uint64_t* __restrict__ keys = scr.keys;
+  float* __restrict__ inv = scr.inv;
+  double* __restrict__ d2 = scr.d2;
+  int32_t* __restrict__ labels = scr.labels;
+  const float Mg = __uint_as_float(scr.counter[1]);
+  double c[4] = {0, 0, 0, 0};
+  float c32[4] = {0, 0, 0, 0};
+  constexpr int U = 4;  // points whose loads are issued together
+  for (int r = 0; r <= k; ++r) {
+    const uint64_t pre = round_prefix(seed, r);
+    float amin = INFINITY;
+    // phase 1: fold centre r-1 (FP32 prefilter, exact FP64 where it cannot
+    // exclude), FP32 clocks; U points' loads in flight at a time
+    for (int m0 = 0; m0 < mcount; m0 += U) {
+      float xv[U][D], ivv[U];
+      uint64_t kv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = base + (m0 + u) * G;
+        if (m0 + u < mcount) {
+#pragma unroll
+          for (int q = 0; q < D; ++q) xv[u][q] = __ldg(xq[q] + i);
+          ivv[u] = r > 0 ? inv[i] : 0.f;
+          kv[u] = r < k ? __ldg(keys + i) : 0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int m = m0 + u;
+        if (m >= mcount) break;
+        const int i = base + m * G;
+        float a = INFINITY;
+        float iv = ivv[u];
+        if (r > 0) {
+          float dd32 = 0.f;
+#pragma unroll
+          for (int q = 0; q < D; ++q) {
+            const float e = xv[u][q] - c32[q];
+            dd32 = fmaf(e, e, dd32);
+          }
+          if (r == 1 || !(dd32 > fold_threshold_inv(iv, Mg))) {
+            const double dcur = r == 1 ? INFINITY : d2[i];
+            const double dd = dist2(x0[i], x1[i], x2[i], D == 4 ? x3p[i] : 0.0, c);
+            if (dd < dcur) {
+              d2[i] = dd;
+              labels[i] = r - 1;
+              iv = inv_d2(dd);
+              inv[i] = iv;
+            }
+          }
+        }
+        if (r < k) {
+          const float na = nlu_approx(mix64(pre + kv[u]));
+          a = r == 0 ? na : (iv > 0.f ? na * iv : INFINITY);
+        }
+        s_a[m * kMemThreads + tid] = a;
+        amin = fminf(amin, a);
+      }
+    }
+    if (r == k) break;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) amin = fminf(amin, __shfl_xor_sync(0xffffffffu, amin, off));
+    if (lane == 0) s_f[warp] = amin;
+    __syncthreads();
+    float cmin = INFINITY;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) cmin = fminf(cmin, s_f[w]);
+    const float thr = cmin * kBand;
+    // phase 2: exact FP64 clocks inside the CTA's band (sogmm.cpp:240-275)
+    double bc = INFINITY;
+    long long bi = -1;
+    if (cmin < INFINITY) {
+      for (int m = 0; m < mcount; ++m) {
+        const int i = base + m * G;
+        if (!(s_a[m * kMemThreads + tid] <= thr)) continue;
+        const double nl = nlu_exact(mix64(pre + keys[i]));
+        const double clk = r == 0 ? nl : nl / d2[i];
+        if (clk < INFINITY && cand_better(clk, i, bc, bi)) {
+          bc = clk;
+          bi = i;
+        }
+      }
+    }
+    int bs = 0;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) shfl_cand(bc, bi, bs, off);
+    if (lane == 0) {
+      s_c[warp] = bc;
+      s_i[warp] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 0; w < NW; ++w)
+        if (cand_better(s_c[w], s_i[w], bc, bi)) {
+          bc = s_c[w];
+          bi = s_i[w];
+        }
+      KppSlot& sl = scr.slots[(r & 1) * nblk + blockIdx.x];
+      sl.clock = bc;
+      sl.idx = bi;
+      __threadfence();
+      atomicAdd(arrive, 1ULL);
+      const unsigned long long target = static_cast<unsigned long long>(nblk) * (r + 1);
+      while (*reinterpret_cast<volatile unsigned long long*>(arrive) < target) {
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    // every CTA: all slots of round r, fixed order
+    double gc = INFINITY;
+    long long gi = -1;
+    for (int b = tid; b < nblk; b += kMemThreads) {
+      const KppSlot* sl = scr.slots + (r & 1) * nblk + b;
+      const double c2 = __ldcg(&sl->clock);
+      const long long i2 = __ldcg(&sl->idx);
+      if (cand_better(c2, i2, gc, gi)) {
+        gc = c2;
+        gi = i2;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) shfl_cand(gc, gi, bs, off);
+    if (lane == 0) {
+      s_c[warp] = gc;
+      s_i[warp] = gi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 0; w < NW; ++w)
+        if (cand_better(s_c[w], s_i[w], gc, gi)) {
+          gc = s_c[w];
+          gi = s_i[w];
+        }
+      s_w = (gi >= 0 && gc < INFINITY) ? gi : -1;
+    }
+    __syncthreads();
+    long long w = s_w;
+    if (w < 0) {
+      // sogmm.cpp:276-284: the lowest unchosen index, among 0 .. r (the
+      // chosen are centres[0 .. r), written by CTA 0 in earlier rounds)
+      long long lo = LLONG_MAX;
+      for (long long cnd = tid; cnd <= r && cnd < n; cnd += kMemThreads) {
+        bool taken = false;
+        for (int q = 0; q < r && !taken; ++q) taken = __ldcg(scr.centers + q) == cnd;
+        if (!taken && cnd < lo) lo = cnd;
+      }
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) {
+        const long long u2 = __shfl_xor_sync(0xffffffffu, lo, off);
+        lo = u2 < lo ? u2 : lo;
+      }
+      if (lane == 0) s_u[warp] = lo;
+      __syncthreads();
+      if (tid == 0) {
+        for (int q = 0; q < NW; ++q) lo = s_u[q] < lo ? s_u[q] : lo;
+        s_w = lo;
+      }
+      __syncthreads();
+      w = s_w;
+    }
+    if (blockIdx.x == 0 && tid == 0) scr.centers[r] = w;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      c[q] = q < D ? x64[q * n + w] : 0.0;
+      c32[q] = __double2float_rn(c[q]);
+    }
+    __syncthreads();  // s_w / s_c reused next round
   }
 }
 
@@ -1568,6 +1812,34 @@ cudaError_t launch_kpp_seed(const double* x64, int64_t n, int d, int k, uint64_t
       n <= cap ? sm_count * 4 : (n + static_cast<int64_t>(kMemThreads) * kMemPPT - 1) /
                                     (static_cast<int64_t>(kMemThreads) * kMemPPT));
   absmax_kernel<<<sm_count * 2, 256, 0, s>>>(x64, n, d, scr.counter + 1);
+#if GMMB_KPP_PERSIST
+  {
+    // persistent cooperative wave when every point fits kMemPPT per thread
+    const void* fn = d == 4 ? (const void*)kpp_memp_kernel<4> : (const void*)kpp_memp_kernel<3>;
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kMemThreads, 0);
+    if (e != cudaSuccess) return e;
+    const int64_t need = (n + static_cast<int64_t>(kMemThreads) * kMemPPT - 1) /
+                         (static_cast<int64_t>(kMemThreads) * kMemPPT);
+    const int64_t wave = static_cast<int64_t>(sm_count) * per_sm;
+    if (need <= wave) {
+      int nblk = static_cast<int>(wave);  // all co-resident CTAs (fewer points each)
+      unsigned long long* arrive = reinterpret_cast<unsigned long long*>(scr.status + 6);
+      e = cudaMemsetAsync(arrive, 0, sizeof(unsigned long long), s);
+      if (e != cudaSuccess) return e;
+      if (d == 4)
+        kpp_memp_init_kernel<4><<<static_cast<int>((n + 255) / 256), 256, 0, s>>>(x64, n, scr);
+      else
+        kpp_memp_init_kernel<3><<<static_cast<int>((n + 255) / 256), 256, 0, s>>>(x64, n, scr);
+      void* args[] = {(void*)&x64, (void*)&n, (void*)&k, (void*)&seed, (void*)&scr,
+                      (void*)&arrive};
+      e = cudaLaunchCooperativeKernel(fn, dim3(nblk), dim3(kMemThreads), args, 0, s);
+      if (e != cudaSuccess) return e;
+      owned_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, s>>>(n, scr.labels, scr.owned);
+      return cudaGetLastError();
+    }
+  }
+#endif
   int* ticket = scr.status;
   long long* win = reinterpret_cast<long long*>(scr.status + 2);
   cudaError_t e = cudaMemsetAsync(scr.status, 0, sizeof(int) * 4, s);
