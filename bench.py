@@ -59,7 +59,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="gmmb", choices=["gmmb", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg4"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--frames", type=int, default=64, help="cfg3: frames per step")
     ap.add_argument("--k", type=int, default=0, help="override K (0: the config's)")
     ap.add_argument("--tol", type=float, default=1e-3)
     ap.add_argument("--vshard", type=int, default=0,
@@ -68,7 +69,7 @@ def parse():
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
     a = ap.parse_args()
     if a.k == 0:
-        a.k = 512 if a.config == "cfg2" else 2048
+        a.k = {"cfg2": 512, "cfg3": 256, "cfg4": 2048}[a.config]
     return a
 
 
@@ -116,6 +117,12 @@ def shard_bounds(n, world):
 
 def config_dict(args, world):
     """Identical for both arms (the driver compares them)."""
+    if args.config == "cfg3":
+        return {"workload": "cfg3: batch of %d 4D frames (N=307200 each, 2 mm jitter, seed f), "
+                            "K=%d each, k-means++ + EM to tol %g, frames sharded over the GPUs "
+                            "(f mod N)" % (args.frames, args.k, args.tol),
+                "global_batch": args.frames, "points_per_fit": 307200, "k": args.k,
+                "parallelism": "frames%d" % world}
     if args.config == "cfg2":
         return {"workload": "cfg2: 4D frame N=307200, K=%d, k-means++ + EM to tol %g "
                             "(one fit per GPU per step)" % (args.k, args.tol),
@@ -247,12 +254,35 @@ def cpu_cfg4_rate(points, k, steps):
     return units / sum(times), threads, times, sample
 
 
+def cpu_cfg3_rate(gen, k, tol, steps):
+    """cfg3 on the CPU: the reference's serial loop of fits over the frames,
+    a bounded sample of it per step (frame s of the batch, seed s)."""
+    import oracle
+    oracle.set_num_threads(0)
+    threads = oracle.num_threads()
+    base = gen.synthetic_frame_cloud()
+    times, units = [], []
+    for f in range(steps):
+        p = gen.jitter_cloud(base, 0.002, f) if f > 0 else base
+        t0 = time.perf_counter()
+        r = oracle.fit_k(p, k, max_iters=100, ll_rel_tol=tol, cov_reg=1e-6, seed=f)
+        times.append(time.perf_counter() - t0)
+        units.append(float(len(p)) * k * r["em_iterations"])
+    sample = ("%d frame fit(s) of the cfg3 batch (frames 0..%d, K=%d, kinit + M + EM, %.1f s), "
+              "FP64 oracle restatement" % (len(times), len(times) - 1, k, sum(times)))
+    return sum(units) / sum(times), threads, times, sample
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
     import oracle
-    if args.config == "cfg2":
+    if args.config == "cfg3":
+        cpu_cfg3_rate(oracle, args.k, args.tol, 1)
+        rate, threads, times, sample = cpu_cfg3_rate(oracle, args.k, args.tol,
+                                                     max(args.steps, 1))
+    elif args.config == "cfg2":
         pts = cfg2_points(oracle, 0)
         if args.warmup > 0:
             cpu_cfg2_rate(pts, args.k, args.tol, 0, steps=min(args.warmup, 2))
@@ -296,6 +326,9 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.config == "cfg3":
+        run_cfg3(args, gm, torch, dist, rank, world, local)
+        return
     sharded = args.config == "cfg4" and world > 1
     vshard = args.config == "cfg4" and world == 1 and args.vshard > 1
     if sharded:
@@ -490,6 +523,140 @@ def main():
     if vctx:
         for c in vctx:
             c.close()
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_cfg3(args, gm, torch, dist, rank, world, local):
+    """cfg3: a step fits the whole batch of frames; frame f (2 mm jitter,
+    seed f) runs on rank f mod N through gmmb_fit_k_batch (the next frame's
+    copy overlaps the current fit). value: frames resident in HBM, the batch
+    call bracketed by CUDA events on the launching side (includes every
+    per-frame host round trip); e2e: the same call with pinned host frames."""
+    ctx = gm.Context(local)
+    sm, cc_major, cc_minor = ctx.device_info()
+    base = gm.synthetic_frame_cloud()
+    mine = [f for f in range(args.frames) if f % world == rank]
+    host = []
+    for f in mine:
+        p = gm.jitter_cloud(base, 0.002, f) if f > 0 else base
+        t = torch.empty((4, len(p)), dtype=torch.float64, pin_memory=True)
+        t.numpy()[:] = p.T
+        host.append(t)
+    dev = [t.cuda() for t in host]
+    host_views = [t.numpy().T for t in host]          # (N, 4) Fortran views, pinned
+    em = gm.EmParams(100, args.tol, 1e-6, 0)
+    seeds = mine
+    n = len(base)
+
+    def run_batch(frames_dev):
+        # device pointers: call the C ABI directly (the Python wrapper takes host arrays)
+        import ctypes
+        F = len(frames_dev)
+        ptrs = (ctypes.POINTER(ctypes.c_double) * F)(
+            *[ctypes.cast(ctypes.c_void_p(t.data_ptr()), ctypes.POINTER(ctypes.c_double))
+              for t in frames_dev])
+        ns = np.full(F, n, dtype=np.int64)
+        sd = np.array(seeds, dtype=np.uint64)
+        st = (gm._FitStats * F)()
+        gm._check(gm.load().gmmb_fit_k_batch(
+            ctx.handle, F, ptrs, ns.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), 4, args.k,
+            ctypes.byref(em._c()), sd.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+            None, None, None, st))
+        return [st[f] for f in range(F)]
+
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    res, ms = [], 0.0
+    with Clocks(local) as clk:
+        for _ in range(max(args.warmup, 3) if args.warmup > 0 else 3):
+            run_batch(dev)
+        barrier()
+        steps = args.steps
+        for _ in range(steps):
+            flush.add_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            res.append(run_batch(dev))
+            e1.record()
+            torch.cuda.synchronize()
+            ms += e0.elapsed_time(e1)
+        barrier()
+    clocks = clk.summary()
+    units = sum(s.units for r in res for s in r)
+    dev_ms = sum(s.ms_total for r in res for s in r)
+    launches = sum(s.launches for r in res for s in r)
+    est_ms = 0.0
+    # e2e: pinned host frames through the same call
+    t_e2e, e2e_units = 0.0, 0.0
+    for _ in range(max(1, steps // 2)):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t1 = time.perf_counter()
+        rr = gm.fit_k_batch(host_views, args.k, em, seeds=seeds, ctx=ctx)
+        torch.cuda.synchronize()
+        t_e2e += time.perf_counter() - t1
+        e2e_units += sum(r.units for r in rr)
+    e2e_steps = max(1, steps // 2)
+    # roofline: the fused E kernel per launch in timing mode on one frame
+    ctx.upload(host_views[0])
+    ctx.set_timing(True)
+    tf = [ctx.fit_k_resident(args.k, gm.EmParams(100, args.tol, 1e-6, seeds[0])) for _ in range(3)]
+    ctx.set_timing(False)
+    est_ms = sum(r.ms_estep for r in tf)
+    est_units = sum(r.units for r in tf)
+    est_launches = sum(r.em_iterations for r in tf)
+    if world > 1:
+        t = torch.tensor([ms, units, t_e2e, e2e_units, dev_ms], dtype=torch.float64, device="cuda")
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        ms_job, units_job, t_e2e_job, e2e_units_job = float(mx[0]), float(t[1]), float(mx[2]), float(t[3])
+    else:
+        ms_job, units_job, t_e2e_job, e2e_units_job = ms, units, t_e2e, e2e_units
+    peak_tf, _ = ctx.ffma_peak(50.0)
+    achieved_tf = FLOP_PER_UNIT[4] * est_units / (est_ms * 1e-3) / 1e12
+    line = {
+        "metric": METRIC, "value": units_job / (ms_job * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_job / steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (make_synthetic_frame 640x480 -> 307,200 4D points; frame f: 2 mm "
+                "jitter, seed f)",
+        "config": config_dict(args, world),
+        "frames_per_s": args.frames * steps / (ms_job * 1e-3),
+        "e2e": {"value": e2e_units_job / t_e2e_job, "unit": UNIT,
+                "h2d_bytes_per_step": len(mine) * n * 4 * 8,
+                "d2h_bytes_per_step": len(mine) * 8 * args.k * 15,
+                "ms_per_step": 1e3 * t_e2e_job / e2e_steps,
+                "frames_per_s": args.frames * e2e_steps / t_e2e_job},
+        "gpu_launches": int(launches),
+        "device_ms_per_step_sum_of_fits": dev_ms / steps,
+        "roofline": {"bound": "fp32", "kernel": "estep_ws_kernel (fused E step + statistics, K=%d)"
+                     % args.k, "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": achieved_tf / peak_tf, "flop_per_unit": FLOP_PER_UNIT[4],
+                     "timing": "CUDA events around each fused E launch, %d launches (3 fits of "
+                               "frame %d in timing mode)" % (est_launches, seeds[0]),
+                     "peak_source": "measured packed-FP32 microbenchmark in this run",
+                     "traffic": None,
+                     "traffic_note": "no ncu capture of this configuration; algorithmic %.0f B "
+                                     "per launch" % (16 * n)},
+        "clocks": clocks,
+        "device": {"sm_count": sm, "cc": "%d.%d" % (cc_major, cc_minor)},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, threads, times, sample = cpu_cfg3_rate(gm, args.k, args.tol, 2)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                                "cpu_model": cpu_model(), "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:
         dist.destroy_process_group()

@@ -113,6 +113,18 @@ int gmmb_fit_k(gmmb_ctx* ctx, const double* pts, int64_t n, int d, int K,
                double* cov_out, double* ll_trace, gmmb_fit_stats* stats,
                int32_t* labels, int64_t* centers);
 
+/* A batch of independent frames (BASELINE cfg3), the reference's serial
+ * loop of fit calls (gmmscape_cli.cpp:208-227) on one device: frame f is
+ * fitted exactly as gmmb_fit_k(pts[f], n[f], d, K, em with seed seeds[f])
+ * (seeds nullable: em->seed for all), while frame f+1's points are copied to
+ * the device on a second stream (pinned host frames overlap fully; frames
+ * already in device memory are accepted too). Outputs
+ * per frame at f*K (w), f*K*d (mu), f*K*d(d+1)/2 (cov); stats[f]. Sharded
+ * contexts: shard the frames over the ranks instead (returns 2). */
+int gmmb_fit_k_batch(gmmb_ctx* ctx, int frames, const double* const* pts, const int64_t* n,
+                     int d, int K, const gmmb_em_params* em, const uint64_t* seeds,
+                     double* w_out, double* mu_out, double* cov_out, gmmb_fit_stats* stats);
+
 /* EM loop of fit (sogmm.cpp:484-509) from a caller-supplied initial model
  * (the "fixed init" configuration). */
 int gmmb_fit_from(gmmb_ctx* ctx, const double* pts, int64_t n, int d, int m,

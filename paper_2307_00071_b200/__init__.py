@@ -95,6 +95,10 @@ _SIGS = {
     "gmmb_fit_k": (ctypes.c_int, [_V, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                   ctypes.POINTER(_EmParams), _D, _D, _D, _D,
                                   ctypes.POINTER(_FitStats), _I32, _I64]),
+    "gmmb_fit_k_batch": (ctypes.c_int, [_V, ctypes.c_int, ctypes.POINTER(_D), _I64, ctypes.c_int,
+                                        ctypes.c_int, ctypes.POINTER(_EmParams),
+                                        ctypes.POINTER(ctypes.c_uint64), _D, _D, _D,
+                                        ctypes.POINTER(_FitStats)]),
     "gmmb_fit_from": (ctypes.c_int, [_V, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                      _D, _D, _D, ctypes.POINTER(_EmParams), _D, _D, _D, _D,
                                      ctypes.POINTER(_FitStats)]),
@@ -523,6 +527,46 @@ def vshard_contexts(world: int, device: int = 0) -> list:
     ctxs = [Context(vgroup=grp, rank=r) for r in range(world)]
     grp.close()  # the contexts keep the group alive
     return ctxs
+
+
+def fit_k_batch(frames, k: int, em: EmParams = EmParams(), seeds=None,
+                ctx: Optional[Context] = None) -> list:
+    """A batch of independent frames (BASELINE cfg3), each fitted exactly as
+    fit_k(frame, k, em with seed seeds[f]); frame f+1 is copied to the device
+    while frame f fits (pinned host frames overlap fully). Frames must share
+    D; each needs k <= its N."""
+    c = _ctx(ctx)
+    ps = [_points(f) for f in frames]
+    F = len(ps)
+    if F == 0:
+        raise ValueError("empty frame batch")
+    d = ps[0][2]
+    if any(q[2] != d for q in ps):
+        raise ValueError("frames must share the dimension")
+    kk = max(1, int(k))
+    np_ = d * (d + 1) // 2
+    w = np.zeros((F, kk))
+    mu = np.zeros((F, kk, d))
+    cov = np.zeros((F, kk, np_))
+    stats = (_FitStats * F)()
+    ptrs = (_D * F)(*[_ptr(q[0]) for q in ps])
+    ns = np.array([q[1] for q in ps], dtype=np.int64)
+    sd = None if seeds is None else np.ascontiguousarray(seeds, dtype=np.uint64)
+    _check(load().gmmb_fit_k_batch(c.handle, F, ptrs, _ptr(ns, _I64), d, kk,
+                                   ctypes.byref(em._c()),
+                                   None if sd is None else sd.ctypes.data_as(
+                                       ctypes.POINTER(ctypes.c_uint64)),
+                                   _ptr(w), _ptr(mu), _ptr(cov), stats))
+    out = []
+    for f in range(F):
+        st = stats[f]
+        m = st.k_out
+        model = Gmm(w[f, :m].copy(), mu[f, :m].copy(), cov[f, :m].copy())
+        out.append(FitResult(model, st.em_iterations, st.final_log_likelihood,
+                             st.removed_components, st.k_init, bool(st.converged),
+                             np.zeros(0), st.units, st.ms_layout, st.ms_kinit, st.ms_mstep0,
+                             st.ms_em, st.ms_total, st.ms_estep, st.launches))
+    return out
 
 
 @dataclasses.dataclass

@@ -85,6 +85,8 @@ struct gmmb_ctx {
   int sm_count = 148;
   int cc_major = 0, cc_minor = 0;
   cudaStream_t s = nullptr;
+  cudaStream_t s_copy = nullptr;  // batch fits: next frame's H2D alongside this frame's fit
+  cudaEvent_t ev_copy = nullptr;
   cudaEvent_t ev[8] = {};
   std::vector<cudaEvent_t> ev_e;  // [2*i], [2*i+1] bracket the E kernel of iteration i
   long long launches = 0;         // kernels of this library enqueued by the current call
@@ -96,6 +98,7 @@ struct gmmb_ctx {
   int d = 0;
   bool have_cloud = false;
   DevBuf<double> x64;
+  DevBuf<double> x64_next;        // batch fits: the prefetched next frame
   DevBuf<float4> xt;
   DevBuf<double> tc;
   DevBuf<int32_t> perm;
@@ -772,6 +775,63 @@ void fit_from_resident(gmmb_ctx* c, int m, const double* w0, const double* mu0,
 }
 
 
+// ---- frame batches (cfg3): the reference's serial loop of fit calls ----
+// (gmmscape_cli.cpp:208-227) with frame f+1's host-to-device copy on a copy
+// stream while frame f fits (pinned host frames overlap fully).
+void fit_batch(gmmb_ctx* c, int F, const double* const* pts, const int64_t* ns, int d, int K,
+               const gmmb_em_params* em, const uint64_t* seeds, double* w_out, double* mu_out,
+               double* cov_out, gmmb_fit_stats* stats) {
+  if (F < 1) throw Err{2, "empty frame batch"};
+  if (!pts || !ns) throw Err{2, "null frame list"};
+  if (c->world > 1) throw Err{2, "frame batches run per device (shard the frames, not the points)"};
+  check_d(d);
+  check_em(em);
+  if (K < 1) throw Err{2, "kinit: k must satisfy 1 <= k <= N"};
+  for (int f = 0; f < F; ++f) {
+    if (!pts[f]) throw Err{2, "null point buffer"};
+    if (ns[f] < 1) throw Err{3, "point cloud is empty"};
+    if (ns[f] > (int64_t{1} << 31) - 1) throw Err{2, "too many points for one device"};
+  }
+  set_device(c);
+  if (!c->s_copy) {
+    ck(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming), "cudaEventCreate");
+  }
+  const int np = d * (d + 1) / 2;
+  auto prefetch = [&](int f) {  // frame f -> x64_next on the copy stream
+    const int64_t n = ns[f];
+    c->x64_next.ensure(static_cast<size_t>(n) * 4 + 4);
+    // host (ideally pinned) or device-resident frames (unified addressing)
+    ck(cudaMemcpyAsync(c->x64_next.p, pts[f], sizeof(double) * n * d, cudaMemcpyDefault,
+                       c->s_copy),
+       "points H2D");
+    if (d == 3)
+      ck(cudaMemsetAsync(c->x64_next.p + 3 * n, 0, sizeof(double) * n, c->s_copy), "memset");
+    ck(cudaEventRecord(c->ev_copy, c->s_copy), "event");
+  };
+  prefetch(0);
+  for (int f = 0; f < F; ++f) {
+    // frame f becomes the resident cloud (buffer swap, ordered after its copy)
+    ck(cudaStreamWaitEvent(c->s, c->ev_copy, 0), "cudaStreamWaitEvent");
+    std::swap(c->x64.p, c->x64_next.p);
+    std::swap(c->x64.cap, c->x64_next.cap);
+    c->n = ns[f];
+    c->d = d;
+    c->offset = 0;
+    c->n_global = ns[f];
+    c->have_cloud = true;
+    // the previous frame (now in x64_next) is finished: its fit synchronised
+    if (f + 1 < F) prefetch(f + 1);
+    gmmb_em_params ef = *em;
+    ef.seed = seeds ? seeds[f] : em->seed;
+    const size_t kk = static_cast<size_t>(K);
+    fit_k_resident(c, K, &ef, w_out ? w_out + f * kk : nullptr,
+                   mu_out ? mu_out + f * kk * d : nullptr,
+                   cov_out ? cov_out + f * kk * np : nullptr, nullptr,
+                   stats ? stats + f : nullptr, nullptr, nullptr);
+  }
+}
+
 // ---- inference helpers ----------------------------------------------------
 // gmm.cpp:8-31 Gmm4::validate (host part: sizes, finiteness, weights); the
 // SPD check runs on the device (factors kernel).
@@ -1056,7 +1116,7 @@ void gmmb_ctx_destroy(gmmb_ctx* c) {
   cudaSetDevice(c->device);
   if (c->s) cudaStreamSynchronize(c->s);
   delete c->comm;
-  c->x64.release(); c->xt.release(); c->tc.release(); c->perm.release();
+  c->x64.release(); c->x64_next.release(); c->xt.release(); c->tc.release(); c->perm.release();
   c->bbox_part.release(); c->mkeys_in.release(); c->mkeys_out.release();
   c->midx.release(); c->sort_tmp.release(); c->flags.release(); c->hidx.release();
   c->iw.release(); c->imu.release(); c->icov.release(); c->ifac.release(); c->ilow.release();
@@ -1080,6 +1140,8 @@ void gmmb_ctx_destroy(gmmb_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (auto& e : c->ev_e) cudaEventDestroy(e);
   if (c->s) cudaStreamDestroy(c->s);
+  if (c->s_copy) cudaStreamDestroy(c->s_copy);
+  if (c->ev_copy) cudaEventDestroy(c->ev_copy);
   delete c;
 }
 
@@ -1151,6 +1213,15 @@ int gmmb_fit_k(gmmb_ctx* c, const double* pts, int64_t n, int d, int K,
       upload(c, pts, n, d, 0, n);
     }
     fit_k_resident(c, K, em, w_out, mu_out, cov_out, ll_trace, stats, labels, centers);
+  });
+}
+
+int gmmb_fit_k_batch(gmmb_ctx* c, int frames, const double* const* pts, const int64_t* n, int d,
+                     int K, const gmmb_em_params* em, const uint64_t* seeds, double* w_out,
+                     double* mu_out, double* cov_out, gmmb_fit_stats* stats) {
+  return guarded([&] {
+    if (!c) throw Err{2, "null context"};
+    fit_batch(c, frames, pts, n, d, K, em, seeds, w_out, mu_out, cov_out, stats);
   });
 }
 

@@ -407,3 +407,26 @@ def test_single_step_calls_invalidate_resident_cloud(gm, orc, ctx):
         ctx.fit_k_resident(16, gm.EmParams(3, 0.0, 1e-6, 0))
     ctx.upload(p)
     assert ctx.fit_k_resident(16, gm.EmParams(3, 0.0, 1e-6, 0)).em_iterations == 3
+
+
+@pytest.mark.gpu
+def test_cfg3_frame_batch_matches_single_fits_and_oracle(gm, orc, ctx):
+    """BASELINE cfg3 batch: frames f (2 mm jitter, seed f), K=256, seed f,
+    through gmmb_fit_k_batch (the next frame's copy overlaps this frame's
+    fit): every frame bit-identical to its own fit_k, and frame 2 against
+    the oracle."""
+    base = frame(gm)[::2].copy()
+    frames = [gm.jitter_cloud(base, 0.002, f) for f in range(4)]
+    em = gm.EmParams(100, 1e-3, 1e-6, 0)
+    batch = gm.fit_k_batch(frames, 256, em, seeds=list(range(4)), ctx=ctx)
+    for f, (p, r) in enumerate(zip(frames, batch)):
+        one = gm.fit_k(p, 256, gm.EmParams(100, 1e-3, 1e-6, f), ctx=ctx)
+        assert r.em_iterations == one.em_iterations
+        assert r.final_log_likelihood == one.final_log_likelihood
+        assert np.array_equal(r.model.covariances, one.model.covariances)
+    ref = orc.fit_k(frames[2], 256, max_iters=100, ll_rel_tol=1e-3, cov_reg=1e-6, seed=2)
+    r = batch[2]
+    assert r.em_iterations == ref["em_iterations"]
+    assert abs(r.final_log_likelihood - ref["final_ll"]) / abs(ref["final_ll"]) < LL_TOL
+    assert_model_close(r.model.weights, r.model.means, r.model.covariances,
+                       ref["w"], ref["mu"], ref["cov"])
