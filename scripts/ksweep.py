@@ -9,6 +9,7 @@ import argparse, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_2307_00071_b200 as gm
+from bench import Clocks
 
 FLOP = {4: 62.0, 3: 42.0}
 ap = argparse.ArgumentParser()
@@ -24,10 +25,11 @@ def run(name, pts, k, em):
     ctx.upload(pts)
     ctx.set_timing(False)
     ctx.fit_k_resident(k, em)                      # warm-up (graph build)
-    gr = [ctx.fit_k_resident(k, em) for _ in range(args.reps)]
-    ctx.set_timing(True)
-    tr = [ctx.fit_k_resident(k, em) for _ in range(args.reps)]
-    ctx.set_timing(False)
+    with Clocks(0) as clk:                         # nvidia-smi clocks during the timed fits
+        gr = [ctx.fit_k_resident(k, em) for _ in range(args.reps)]
+        ctx.set_timing(True)
+        tr = [ctx.fit_k_resident(k, em) for _ in range(args.reps)]
+        ctx.set_timing(False)
     d = pts.shape[1]
     r = gr[-1]
     est = sum(t.ms_estep for t in tr)
@@ -41,7 +43,7 @@ def run(name, pts, k, em):
         "ms_em": round(r.ms_em, 3), "estep_us_per_iter": round(1e3 * est / it, 1),
         "units_per_s": units / (sum(g.ms_total for g in gr) * 1e-3) * len(gr) / len(tr),
         "estep_tflops": round(ach, 2), "roofline_frac": round(ach / peak, 3),
-        "peak_tflops": round(peak, 1)}), flush=True)
+        "peak_tflops": round(peak, 1), "clocks": clk.summary()}), flush=True)
 
 
 frame = gm.synthetic_frame_cloud()
