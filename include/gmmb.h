@@ -61,6 +61,10 @@ typedef struct {
   double ms_total;             /* layout start -> EM end (device) */
   double ms_estep;             /* fused E-step kernel, executed iterations */
   long long launches;          /* kernels this library enqueued (CUB excluded) */
+  double units_evaluated;      /* (point, component) pairs the E step evaluated:
+                                  the pruned E step skips pairs whose FP32
+                                  density is provably exactly 0 (= units for
+                                  the dense kernels) */
 } gmmb_fit_stats;
 
 const char* gmmb_last_error(void);
@@ -96,6 +100,11 @@ void gmmb_ctx_destroy(gmmb_ctx* ctx);
  * 1: iterations are enqueued in chunks with CUDA events around every fused
  * E kernel (gmmb_fit_stats.ms_estep), for kernel timing. Same results. */
 int gmmb_ctx_set_timing(gmmb_ctx* ctx, int per_kernel_events);
+/* E-step kernels: 0 (default) the exact-zero-pruned E step whenever it
+ * applies (K <= 8192), 1 the dense kernels (every (point, component) pair).
+ * Both give the same results up to FP32 summation order. The environment
+ * variable GMMB_ESTEP=dense sets 1 at context creation. */
+int gmmb_ctx_set_estep_mode(gmmb_ctx* ctx, int mode);
 
 int gmmb_device_info(gmmb_ctx* ctx, int* sm_count, int* cc_major,
                      int* cc_minor);

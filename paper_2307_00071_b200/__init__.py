@@ -70,7 +70,8 @@ class _FitStats(ctypes.Structure):
                 ("ms_layout", ctypes.c_double), ("ms_kinit", ctypes.c_double),
                 ("ms_mstep0", ctypes.c_double), ("ms_em", ctypes.c_double),
                 ("units", ctypes.c_double), ("ms_total", ctypes.c_double),
-                ("ms_estep", ctypes.c_double), ("launches", ctypes.c_longlong)]
+                ("ms_estep", ctypes.c_double), ("launches", ctypes.c_longlong),
+                ("units_evaluated", ctypes.c_double)]
 
 
 _lib = None
@@ -130,6 +131,7 @@ _SIGS = {
     "gmmb_shard_key_tail": (ctypes.c_int, [_D, ctypes.c_int, ctypes.c_int, _D]),
     "gmmb_ffma_peak": (ctypes.c_int, [_V, ctypes.c_double, _D, _D]),
     "gmmb_ctx_set_timing": (ctypes.c_int, [_V, ctypes.c_int]),
+    "gmmb_ctx_set_estep_mode": (ctypes.c_int, [_V, ctypes.c_int]),
     "gmmb_ingest_images": (ctypes.c_int, [_V, ctypes.POINTER(ctypes.c_uint16),
                                           ctypes.POINTER(ctypes.c_uint16), ctypes.c_int,
                                           ctypes.c_int, ctypes.c_double, ctypes.c_double,
@@ -283,6 +285,8 @@ class FitResult:
     labels: Optional[np.ndarray] = None
     centers: Optional[np.ndarray] = None
     gbms_components: int = 0      # fit(): GBMS's component estimate
+    units_evaluated: float = 0.0  # pairs the E step evaluated (pruned E step: the
+                                  # ones whose FP32 density can be non-zero)
 
 
 @dataclasses.dataclass
@@ -366,6 +370,12 @@ class Context:
         events around every fused E kernel (FitResult.ms_estep)."""
         _check(load().gmmb_ctx_set_timing(self._h, 1 if per_kernel_events else 0))
 
+    def set_estep_mode(self, dense: bool) -> None:
+        """E-step kernels: False (default) = exact-zero-pruned (skips the
+        (tile, component) pairs whose FP32 densities are provably exactly 0),
+        True = dense (every pair). Same results up to FP32 summation order."""
+        _check(load().gmmb_ctx_set_estep_mode(self._h, 1 if dense else 0))
+
     def ffma_peak(self, ms_target: float = 50.0) -> tuple[float, float]:
         """Measured FP32 FFMA TFLOP/s on this device (and the ms it took)."""
         tf, ms = ctypes.c_double(), ctypes.c_double()
@@ -430,7 +440,7 @@ def _result(out, ll, st: _FitStats, lab=None, cen=None) -> FitResult:
                      st.removed_components, st.k_init, bool(st.converged),
                      ll[:st.em_iterations].copy(), st.units, st.ms_layout,
                      st.ms_kinit, st.ms_mstep0, st.ms_em, st.ms_total, st.ms_estep,
-                     st.launches, lab, cen)
+                     st.launches, lab, cen, units_evaluated=st.units_evaluated)
 
 
 _default_ctx: Optional[Context] = None
@@ -565,7 +575,8 @@ def fit_k_batch(frames, k: int, em: EmParams = EmParams(), seeds=None,
         out.append(FitResult(model, st.em_iterations, st.final_log_likelihood,
                              st.removed_components, st.k_init, bool(st.converged),
                              np.zeros(0), st.units, st.ms_layout, st.ms_kinit, st.ms_mstep0,
-                             st.ms_em, st.ms_total, st.ms_estep, st.launches))
+                             st.ms_em, st.ms_total, st.ms_estep, st.launches,
+                             units_evaluated=st.units_evaluated))
     return out
 
 

@@ -67,12 +67,12 @@ struct DevBuf {
 
 // Shape + buffer identity of a built EM graph (rebuild when any differs).
 struct EmGraphKey {
-  int k0, d, world;
+  int k0, d, world, sparse;
   int64_t n;
-  const void* p[14];
+  const void* p[20];
   bool operator==(const EmGraphKey& o) const {
-    if (k0 != o.k0 || d != o.d || n != o.n || world != o.world) return false;
-    for (int i = 0; i < 14; ++i)
+    if (k0 != o.k0 || d != o.d || n != o.n || world != o.world || sparse != o.sparse) return false;
+    for (int i = 0; i < 20; ++i)
       if (p[i] != o.p[i]) return false;
     return true;
   }
@@ -140,6 +140,20 @@ struct gmmb_ctx {
   DevBuf<float> chunkf;          // chunked E step (K > 512): per-chunk sums + normalisers
   DevBuf<int> chunki;            // ... exact-path point list + count
   ChunkScratch chunk{};
+  // exact-zero-pruned E step (estep_sparse.cu)
+  int estep_mode = 0;             // 0: pruned when supported, 1: dense kernels
+  bool sparse_on = false;         // the current EM run uses the pruned E step
+  int pool_mult = 1;              // pool growth after an overflow
+  DevBuf<double> sp_bc, sp_pool, sp_ll;
+  DevBuf<float4> sp_bh;
+  DevBuf<int> sp_blist, sp_bcnt, sp_ctl, sp_toff;
+  DevBuf<unsigned> sp_mask;
+  DevBuf<unsigned short> sp_pre;
+  SparseScratch sparse{};
+  double units_eval = 0.0;        // units evaluated by the last EM run (pruned E step)
+  DevBuf<EmState> st_bak;         // EM-start snapshot (pool overflow re-run)
+  DevBuf<double> bak_w[2], bak_mu[2], bak_cov[2];
+  DevBuf<CompConst> bak_cst[2];
   DevBuf<double> dense;  // log_gamma staging for m_step / e_step
   DevBuf<EmState> st;
   EmState* st_host = nullptr;  // pinned
@@ -326,6 +340,15 @@ void layout(gmmb_ctx* c) {
   ck(launch_layout(c->x64.p, n, ls, c->xt.p, c->tc.p, c->perm.p, c->sm_count, c->s),
      "layout");
   c->launches += 4;  // bbox, morton, tile + validate (CUB's sort kernels not counted)
+  // static culling-block boxes of the pruned E step
+  const int nblk = sparse_blocks(ntiles);
+  c->sp_bc.ensure(static_cast<size_t>(nblk) * 4);
+  c->sp_bh.ensure(nblk);
+  c->sparse.bc = c->sp_bc.p;
+  c->sparse.bh = c->sp_bh.p;
+  PointsDev pts{n, c->d, c->x64.p, c->xt.p, c->tc.p, ntiles};
+  ck(launch_sparse_layout(pts, c->sparse, c->s), "block boxes");
+  c->launches += 1;
 }
 
 void check_cloud_flags(gmmb_ctx* c) {
@@ -516,7 +539,9 @@ void download_model(gmmb_ctx* c, int buf, int m, double* w, double* mu,
 // ---- EM loop ----------------------------------------------------------
 // kernels of the fused E step + statistics per iteration (the chunked
 // K > 512 path: per-chunk sums, combine, exact list, statistics)
-int estep_launches(int k0) { return k0 > kCtaComps ? 4 : 1; }
+int estep_launches(const gmmb_ctx* c, int k0) {
+  return c->sparse_on ? 3 : k0 > kCtaComps ? 4 : 1;
+}
 
 void em_iteration(gmmb_ctx* c, int k0, int it,
                   const cudaGraphConditionalHandle* cond = nullptr) {
@@ -527,10 +552,11 @@ void em_iteration(gmmb_ctx* c, int k0, int it,
   const bool timed = it >= 0 && static_cast<size_t>(2 * it + 1) < c->ev_e.size();
   if (timed) ck(cudaEventRecord(c->ev_e[2 * it], c->s), "event");
   ck(launch_estep_stats(pts, c->bufs, c->st.p, k0, c->partials.p, c->ll_part.p, 0,
-                        c->sm_count, c->s, &ncl, &c->chunk),
+                        c->sm_count, c->s, &ncl, &c->chunk,
+                        c->sparse_on ? &c->sparse : nullptr),
      "estep_stats");
   if (timed) ck(cudaEventRecord(c->ev_e[2 * it + 1], c->s), "event");
-  c->launches += estep_launches(k0) + 3;
+  c->launches += estep_launches(c, k0) + 3;
   if (c->world == 1) {
     c->launches += -1;  // fused reduce + finalize
     ck(launch_em_reduce_finalize(c->d, c->partials.p, ncl, k0, c->bufs, c->st.p, c->rec, c->s),
@@ -561,10 +587,12 @@ EmGraphKey em_graph_key(gmmb_ctx* c, int k0) {
   k.d = c->d;
   k.n = c->n;
   k.world = c->world;
-  const void* ps[14] = {c->xt.p, c->tc.p, c->partials.p, c->ll_part.p, c->red.p, c->ll_trace.p,
+  k.sparse = c->sparse_on ? 1 : 0;
+  const void* ps[20] = {c->xt.p, c->tc.p, c->partials.p, c->ll_part.p, c->red.p, c->ll_trace.p,
                         c->st.p, c->bufs[0].w, c->bufs[1].w, c->rec.count, c->bufs[0].cst,
-                        c->bufs[1].cst, c->chunkf.p, c->chunki.p};
-  for (int i = 0; i < 14; ++i) k.p[i] = ps[i];
+                        c->bufs[1].cst, c->chunkf.p, c->chunki.p, c->sp_pool.p, c->sp_blist.p,
+                        c->sp_mask.p, c->sp_ctl.p, c->sp_bc.p, c->sp_toff.p};
+  for (int i = 0; i < 20; ++i) k.p[i] = ps[i];
   return k;
 }
 
@@ -611,13 +639,35 @@ void ensure_em_buffers(gmmb_ctx* c, int k0, int max_iters) {
   const int NS = nstats(c->d);
   PointsDev pts{c->n, c->d, c->x64.p, c->xt.p, c->tc.p,
                 static_cast<int>((c->n + kTile - 1) / kTile)};
+  c->sparse_on = c->estep_mode == 0 && sparse_supported(k0, pts.ntiles);
+  if (c->sparse_on) {
+    const int ntiles = pts.ntiles;
+    const int nblk = sparse_blocks(ntiles);
+    const int kw = (k0 + 31) / 32;
+    // pool of per-(tile, candidate) statistics: ~30 candidates per tile on
+    // the BASELINE frames; 128 per tile (or all K) up front, doubled after
+    // an overflow (the EM run is repeated, see run_em)
+    const int64_t per_tile = std::min<int64_t>(k0, int64_t{128} * c->pool_mult);
+    const int64_t cap = std::max<int64_t>(static_cast<int64_t>(ntiles) * per_tile, 1024);
+    c->sp_blist.ensure(static_cast<size_t>(nblk) * k0);
+    c->sp_bcnt.ensure(nblk);
+    c->sp_ctl.ensure(8);
+    c->sp_pool.ensure(static_cast<size_t>(cap) * NS);
+    c->sp_toff.ensure(ntiles);
+    c->sp_mask.ensure(static_cast<size_t>(kw) * ntiles);
+    c->sp_pre.ensure(static_cast<size_t>(kw) * ntiles);
+    c->sp_ll.ensure(ntiles);
+    c->sparse = SparseScratch{c->sp_bc.p, c->sp_bh.p, c->sp_blist.p, c->sp_bcnt.p, c->sp_ctl.p,
+                              c->sp_pool.p, static_cast<int64_t>(c->sp_pool.cap / NS),
+                              c->sp_toff.p, c->sp_mask.p, c->sp_pre.p, c->sp_ll.p};
+  }
   int ncl = 0;
   ck(launch_estep_stats(pts, c->bufs, c->st.p, k0, nullptr, nullptr, 0,
-                        c->sm_count, c->s, &ncl),
+                        c->sm_count, c->s, &ncl, nullptr, c->sparse_on ? &c->sparse : nullptr),
      "estep query");
   c->partials.ensure(static_cast<size_t>(ncl) * k0 * NS);
   c->ll_part.ensure(ncl);
-  if (k0 > kCtaComps) {  // chunked two-pass E step
+  if (!c->sparse_on && k0 > kCtaComps) {  // chunked two-pass E step
     const int64_t npad = static_cast<int64_t>(pts.ntiles) * kTile;
     const int nch = (k0 + kCtaComps - 1) / kCtaComps;
     c->chunkf.ensure(chunk_scratch_floats(k0, c->n));
@@ -632,8 +682,65 @@ void ensure_em_buffers(gmmb_ctx* c, int k0, int max_iters) {
 
 // Runs EM from the model in buffer st->cur (st already reset). Returns the
 // final state.
+EmState run_em_once(gmmb_ctx* c, int k0, const gmmb_em_params* em);
+
+// The pruned E step writes per-(tile, candidate) statistics to a pool sized
+// up front; if an iteration overflows it (a cloud where most components
+// reach most tiles), the EM run is repeated from its starting model with a
+// larger pool, so results never depend on the pool size.
 EmState run_em(gmmb_ctx* c, int k0, const gmmb_em_params* em) {
-  ensure_em_buffers(c, k0, em->max_iters);
+  for (int attempt = 0;; ++attempt) {
+    ensure_em_buffers(c, k0, em->max_iters);
+    if (!c->sparse_on) {
+      c->units_eval = 0.0;
+      return run_em_once(c, k0, em);
+    }
+    // snapshot of the EM start (state + both model buffers; device copies,
+    // no host round trip)
+    c->st_bak.ensure(1);
+    const size_t kc = c->mw[0].cap;
+    auto d2d = [&](void* dst, const void* src, size_t bytes) {
+      ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->s), "snapshot");
+    };
+    d2d(c->st_bak.p, c->st.p, sizeof(EmState));
+    for (int b = 0; b < 2; ++b) {
+      c->bak_w[b].ensure(kc);
+      c->bak_mu[b].ensure(kc * 4);
+      c->bak_cov[b].ensure(kc * 10);
+      c->bak_cst[b].ensure(kc);
+      d2d(c->bak_w[b].p, c->mw[b].p, sizeof(double) * kc);
+      d2d(c->bak_mu[b].p, c->mmu[b].p, sizeof(double) * kc * 4);
+      d2d(c->bak_cov[b].p, c->mcov[b].p, sizeof(double) * kc * 10);
+      d2d(c->bak_cst[b].p, c->mcst[b].p, sizeof(CompConst) * kc);
+    }
+    ck(cudaMemsetAsync(c->sp_ctl.p, 0, sizeof(int) * 8, c->s), "memset");
+    EmState h = run_em_once(c, k0, em);
+    int ctl[8];
+    copy_sync(c, ctl, c->sp_ctl.p, sizeof(ctl), cudaMemcpyDeviceToHost);
+    int overflow = ctl[2] != 0 ? 1 : 0;
+    if (c->world > 1) {  // every rank repeats together
+      c->kstatus.ensure(8);
+      copy_sync(c, c->kstatus.p + 6, &overflow, sizeof(int), cudaMemcpyHostToDevice);
+      coll(c, c->comm->allreduce(c->kstatus.p + 6, 1, DType::kI32, RedOp::kSum, c->s),
+           "allreduce (pool overflow)");
+      copy_sync(c, &overflow, c->kstatus.p + 6, sizeof(int), cudaMemcpyDeviceToHost);
+    }
+    unsigned long long ev = 0;
+    std::memcpy(&ev, &ctl[4], sizeof(ev));
+    c->units_eval = static_cast<double>(ev);
+    if (!overflow || attempt >= 8) return h;
+    d2d(c->st.p, c->st_bak.p, sizeof(EmState));
+    for (int b = 0; b < 2; ++b) {
+      d2d(c->mw[b].p, c->bak_w[b].p, sizeof(double) * kc);
+      d2d(c->mmu[b].p, c->bak_mu[b].p, sizeof(double) * kc * 4);
+      d2d(c->mcov[b].p, c->bak_cov[b].p, sizeof(double) * kc * 10);
+      d2d(c->mcst[b].p, c->bak_cst[b].p, sizeof(CompConst) * kc);
+    }
+    c->pool_mult *= 2;
+  }
+}
+
+EmState run_em_once(gmmb_ctx* c, int k0, const gmmb_em_params* em) {
   while (c->ev_e.size() < static_cast<size_t>(2 * em->max_iters)) {
     cudaEvent_t e;
     ck(cudaEventCreate(&e), "cudaEventCreate");
@@ -643,7 +750,7 @@ EmState run_em(gmmb_ctx* c, int k0, const gmmb_em_params* em) {
   if (!c->last_timed) {
     launch_em_graph(c, k0);
     EmState h = read_state(c);
-    c->launches += static_cast<long long>(estep_launches(k0) + 2) * h.iter;
+    c->launches += static_cast<long long>(estep_launches(c, k0) + 2) * h.iter;
     return h;
   }
   int launched = 0;
@@ -675,6 +782,7 @@ void finish_fit(gmmb_ctx* c, const EmState& h, const gmmb_em_params* em,
     stats->k_out = h.k_cur;
     stats->converged = h.converged;
     stats->units = h.units;
+    stats->units_evaluated = c->sparse_on ? c->units_eval : h.units;
     double me = 0.0;
     for (int i = 0; c->last_timed && i < h.iter && static_cast<size_t>(2 * i + 1) < c->ev_e.size(); ++i) {
       float ms = 0.f;
@@ -1029,6 +1137,10 @@ static int create(int device, int rank, int world, const void* id, VGroup* vg,
     c->device = device;
     c->rank = rank;
     c->world = world;
+    {  // GMMB_ESTEP=dense selects the dense E kernels (A/B, validation)
+      const char* m = getenv("GMMB_ESTEP");
+      c->estep_mode = (m && std::strcmp(m, "dense") == 0) ? 1 : 0;
+    }
     try {
       ck(cudaSetDevice(device), "cudaSetDevice");
       cudaDeviceProp prop{};
@@ -1134,6 +1246,12 @@ void gmmb_ctx_destroy(gmmb_ctx* c) {
   c->mmeans.release(); c->mcounts.release(); c->partials.release(); c->ll_part.release();
   c->red.release(); c->ll_trace.release(); c->dense.release(); c->st.release();
   c->chunkf.release(); c->chunki.release();
+  c->sp_bc.release(); c->sp_pool.release(); c->sp_ll.release(); c->sp_bh.release();
+  c->sp_blist.release(); c->sp_bcnt.release(); c->sp_ctl.release(); c->sp_toff.release();
+  c->sp_mask.release(); c->sp_pre.release(); c->st_bak.release();
+  for (int b = 0; b < 2; ++b) {
+    c->bak_w[b].release(); c->bak_mu[b].release(); c->bak_cov[b].release(); c->bak_cst[b].release();
+  }
   if (c->em_graph) cudaGraphExecDestroy(c->em_graph);
   if (c->st_host) cudaFreeHost(c->st_host);
   for (auto& e : c->ev)
@@ -1148,6 +1266,12 @@ void gmmb_ctx_destroy(gmmb_ctx* c) {
 int gmmb_ctx_set_timing(gmmb_ctx* c, int per_kernel_events) {
   if (!c) return 2;
   c->timing = per_kernel_events ? 1 : 0;
+  return 0;
+}
+
+int gmmb_ctx_set_estep_mode(gmmb_ctx* c, int mode) {
+  if (!c || mode < 0 || mode > 1) return 2;
+  c->estep_mode = mode;
   return 0;
 }
 

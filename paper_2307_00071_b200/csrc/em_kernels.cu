@@ -1981,7 +1981,10 @@ cudaError_t launch_estep_stats(const PointsDev& pts, const ModelBuf* bufs,
                                const EmState* st, int k0, double* partials,
                                double* ll_part, int exact_mode,
                                int sm_count, cudaStream_t s, int* ncl_out,
-                               const ChunkScratch* chunk) {
+                               const ChunkScratch* chunk, const SparseScratch* sparse) {
+  if (sparse)
+    return launch_estep_sparse(pts, bufs, st, k0, partials, ll_part, exact_mode, sm_count, s,
+                               ncl_out, *sparse);
   if (GMMB_CHUNKED && k0 > kCtaComps) {
     if (partials && !chunk) return cudaErrorInvalidValue;
     return launch_estep_chunked(pts, bufs, st, k0, partials, ll_part, exact_mode, sm_count, s,

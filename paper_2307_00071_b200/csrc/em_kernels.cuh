@@ -49,6 +49,34 @@ cudaError_t launch_estep_chunked(const PointsDev& pts, const ModelBuf* bufs, con
                                  int sm_count, cudaStream_t s, int* ncl_out,
                                  const ChunkScratch* scr);
 
+// Exact-zero-pruned E step (estep_sparse.cu). Per-layout: bc/bh block boxes;
+// per iteration: block candidate lists, a pool of per-(tile, candidate) FP64
+// statistics (SoA [nstats][pool_cap]), per-tile pool offsets, candidate
+// bitmasks + per-word prefix counts (word-major [K/32][ntiles]), per-tile ll.
+// ctl[0] tile queue, ctl[1] pool cursor, ctl[2] pool overflow (the fit is
+// re-run with a larger pool), ctl[4..5] units evaluated (u64).
+struct SparseScratch {
+  double* bc;            // [nblk][4]
+  float4* bh;            // [nblk]
+  int* blist;            // [nblk][K]
+  int* bcnt;             // [nblk]
+  int* ctl;              // [8]
+  double* pool;          // [nstats][pool_cap]
+  int64_t pool_cap;
+  int* toff;             // [ntiles]
+  unsigned* maskT;       // [K/32][ntiles]
+  unsigned short* preT;  // [K/32][ntiles]
+  double* ll_tile;       // [ntiles]
+};
+bool sparse_supported(int k0, int ntiles);
+int sparse_blocks(int ntiles);
+int sparse_ranges(int k0, int ntiles, int sm_count);
+cudaError_t launch_sparse_layout(const PointsDev& pts, const SparseScratch& sp, cudaStream_t s);
+cudaError_t launch_estep_sparse(const PointsDev& pts, const ModelBuf* bufs, const EmState* st,
+                                int k0, double* partials, double* ll_part, int exact_mode,
+                                int sm_count, cudaStream_t s, int* ncl_out,
+                                const SparseScratch& sp);
+
 // Pass B of the chunked E step on the warp-specialised kernel (normalisers
 // known): grid nch x (sm_count / nch); *ncl_out = point ranges.
 cudaError_t launch_estep_ws_pre(const PointsDev& pts, const ModelBuf* bufs, const EmState* st,
@@ -63,7 +91,8 @@ cudaError_t launch_estep_stats(const PointsDev& pts, const ModelBuf* bufs,
                                const EmState* st, int k0, double* partials,
                                double* ll_part, int exact_mode,
                                int sm_count, cudaStream_t s, int* ncl_out,
-                               const ChunkScratch* chunk = nullptr);
+                               const ChunkScratch* chunk = nullptr,
+                               const SparseScratch* sparse = nullptr);
 
 // (partials == nullptr: only report the cluster count *ncl_out.) K > 512
 // runs the chunked two-pass kernels (chunk scratch required) unless

@@ -1,0 +1,822 @@
+// estep_sparse.cu — the fused E step + sufficient statistics with exact-zero
+// tile pruning (sm_100a).
+//
+// Reference semantics: e_step_into + m_step's weighted moments
+// (/root/reference/proj/src/sogmm.cpp:341-383, 399-416; kernels.hpp:82-181),
+// evaluated exactly like the dense kernels of em_kernels.cu: log2 densities
+// Q = |P'x - P'mu'|^2 - base2 in FP32 on tile-recentred points, densities
+// e = ex2.approx.ftz(-Q), an unshifted per-point normaliser (the exact max
+// shift when it leaves [2^-64, 2^64]), centred statistics in FP32 pairs
+// widened to FP64 every 16 points.
+//
+// Exact-zero pruning. ex2.approx.ftz returns exactly +0 for Q > 126 (the
+// result would be subnormal), and a zero density adds exactly nothing to the
+// normaliser or to any statistic (0 * finite = 0, s + 0 = s). So a
+// (tile, component) pair whose Q exceeds 126 at every point of the tile can
+// be skipped without changing a single bit the dense evaluation would add.
+// An interval bound over the tile's bounding box decides it: with
+// y = P'(x - mu) affine in x, each y_i ranges over [yc_i - r_i, yc_i + r_i]
+// (yc at the box centre, r_i = sum_j |P'_ij| h_j), so
+// Q >= sum_i max(0, |yc_i| - r_i)^2 - base2 =: LB. A pair is a candidate iff
+// LB < 134 (8 of margin over 126 for FP32 rounding in the kernel and in the
+// bound). On the cfg2 frame a 128-point tile keeps ~30 of 512 components.
+//
+// Points whose normaliser leaves [2^-64, 2^64] need the max-shifted sum,
+// in which components with Q > 134 may no longer vanish; a tile with such a
+// point (or exact_mode) is evaluated over all K components (same arithmetic
+// as the dense kernel's exact path).
+//
+// Kernels per EM iteration:
+//   block_cand_kernel  per block of 16 tiles (2048 points, static FP64 box):
+//                      coarse candidate list (a superset of every tile's)
+//   estep_sparse_kernel one warp per tile (dynamic tile queue): tile box,
+//                      fine candidates (ascending), pass 1 (normalisers,
+//                      lanes = candidates, point pairs in f32x2), pass 2
+//                      (densities recomputed, responsibilities, statistics);
+//                      per-(tile, candidate) FP64 statistics to a CSR pool,
+//                      the tile's candidate bitmask + per-word prefix counts
+//   sparse_reduce_kernel per (32-component word, tile range): fixed-order sums
+//                      -> per-range partials [R][K][NS] + ll partials [R], the
+//                      layout of the dense kernels (em_reduce_finalize / the
+//                      sharded em_reduce + all-reduce + em_finalize follow)
+// Every sum has a fixed order independent of scheduling: bit-reproducible.
+#include <cstdio>
+#include <cstdlib>
+
+#include "em_kernels.cuh"
+#include "f32x2.cuh"
+
+namespace gmmb {
+
+namespace {
+
+using namespace dev;
+
+constexpr int kBlkTiles = 16;     // tiles per culling block
+constexpr int kSpWarps = 8;       // warps per CTA of the main kernel
+constexpr int kSpMinBlocks = 2;   // two CTAs per SM (128 registers)
+constexpr int kListCap = 1024;    // candidate list entries per warp (more: every component)
+constexpr int kSlice = 16;        // points per FP32 partial (widened to FP64 after)
+constexpr float kQCut = 134.f;    // candidates: LB < 134 (ex2.approx.ftz(-Q) = 0 for Q > 126)
+// (GMMB_SPARSE_QCUT overrides it: a validation knob, e.g. 1e30 keeps every pair)
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// interval lower bound of |P'(x - mu)|^2 over the box centre v = bc - mu'
+// (FP32) and half-widths h; P' packed lower triangle (CompConst.p)
+template <int D>
+__device__ __forceinline__ float box_lb(const float* P, const float (&v)[4], const float (&h)[4]) {
+  float lb = 0.f;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    float yc = 0.f, r = 0.f;
+#pragma unroll
+    for (int j = 0; j <= i; ++j) {
+      const float p = P[i * (i + 1) / 2 + j];
+      yc = fmaf(p, v[j], yc);
+      r = fmaf(fabsf(p), h[j], r);
+    }
+    const float dlt = fmaxf(fabsf(yc) - r, 0.f);
+    lb = fmaf(dlt, dlt, lb);
+  }
+  return lb;
+}
+
+// ---- static per-layout block boxes (FP64 centre, FP32 half-widths rounded up)
+__global__ void __launch_bounds__(kTile)
+    block_box_kernel(const float4* __restrict__ xt, const double* __restrict__ tc, int64_t n,
+                     int ntiles, double* __restrict__ bc, float4* __restrict__ bh) {
+  __shared__ double red[8][kTile];
+  const int b = blockIdx.x, tid = threadIdx.x;
+  double lo[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+  double hi[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  const int t1 = min(ntiles, (b + 1) * kBlkTiles);
+  for (int t = b * kBlkTiles; t < t1; ++t) {
+    const int64_t i = static_cast<int64_t>(t) * kTile + tid;
+    if (i >= n) break;
+    const float4 x = xt[i];
+    const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double a = tc[static_cast<int64_t>(t) * 4 + j] + static_cast<double>(xv[j]);
+      lo[j] = fmin(lo[j], a);
+      hi[j] = fmax(hi[j], a);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    red[j][tid] = lo[j];
+    red[4 + j][tid] = hi[j];
+  }
+  __syncthreads();
+  for (int off = kTile / 2; off >= 1; off >>= 1) {
+    if (tid < off) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        red[j][tid] = fmin(red[j][tid], red[j][tid + off]);
+        red[4 + j][tid] = fmax(red[4 + j][tid], red[4 + j][tid + off]);
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    float h[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double c = 0.5 * (red[j][0] + red[4 + j][0]);
+      bc[static_cast<int64_t>(b) * 4 + j] = c;
+      const double hw = fmax(red[4 + j][0] - c, c - red[j][0]);
+      h[j] = __double2float_ru(hw * (1.0 + 0x1p-20) + 1e-30);
+    }
+    bh[b] = make_float4(h[0], h[1], h[2], h[3]);
+  }
+}
+
+// ---- coarse candidates per block (ascending component order) --------------
+template <int D>
+__global__ void __launch_bounds__(256)
+    block_cand_kernel(const double* __restrict__ bc, const float4* __restrict__ bh, ModelBuf b0,
+                      ModelBuf b1, const EmState* __restrict__ st, int kcap,
+                      int* __restrict__ blist, int* __restrict__ bcnt, int* __restrict__ ctl,
+                      float qcut) {
+  __shared__ int wcnt[8];
+  __shared__ int s_base;
+  if (st->done) return;
+  // tile queue and pool cursor restart every iteration (ctl[2] overflow and
+  // ctl[4..5] evaluated units accumulate over the fit; zeroed by the driver)
+  if (blockIdx.x == 0 && threadIdx.x < 2) ctl[threadIdx.x] = 0;
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int k_cur = st->k_cur;
+  const ModelBuf& mb = st->cur ? b1 : b0;
+  double c[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) c[j] = bc[static_cast<int64_t>(b) * 4 + j];
+  const float4 hb = bh[b];
+  const float h[4] = {hb.x, hb.y, hb.z, hb.w};
+  if (tid == 0) s_base = 0;
+  __syncthreads();
+  for (int k0 = 0; k0 < k_cur; k0 += 256) {
+    const int k = k0 + tid;
+    bool cand = false;
+    if (k < k_cur) {
+      const float4* c4 = reinterpret_cast<const float4*>(mb.cst + k);
+      const float4 a0 = c4[0], a1 = c4[1], a2 = c4[2];
+      const float P[12] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
+      float v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = j < D ? -static_cast<float>(mb.mu[k * 4 + j] - c[j]) : 0.f;
+      const float lb = box_lb<D>(P, v, h);
+      // superset of the fine test (looser slack, +1)
+      cand = fmaf(lb, -0x1p-9f, lb) - P[10] < qcut + 1.f;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, cand);
+    if (lane == 0) wcnt[w] = __popc(m);
+    __syncthreads();
+    int pre = s_base;
+    for (int q = 0; q < w; ++q) pre += wcnt[q];
+    if (cand) blist[static_cast<int64_t>(b) * kcap + pre + __popc(m & lanemask_lt())] = k;
+    __syncthreads();
+    if (tid == 0) {
+      int tot = 0;
+      for (int q = 0; q < 8; ++q) tot += wcnt[q];
+      s_base += tot;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) bcnt[b] = s_base;
+}
+
+// One candidate's tile-relative constants (lane-private scalars).
+template <int D>
+struct Cand {
+  float P[npacked(D)];
+  float nb[D];   // -P' mu' (FP64 dot of the FP32 factor with the FP32-rounded mu')
+  float nbase;   // -base2
+  float nmu[D];  // -mu' (statistics centre: x - mu')
+};
+
+template <int D>
+__device__ __forceinline__ void load_cand(Cand<D>& cd, int k, const ModelBuf& mb, const double (&ct)[4]) {
+  constexpr int NP = npacked(D);
+  if (k < 0) {
+#pragma unroll
+    for (int q = 0; q < NP; ++q) cd.P[q] = 0.f;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      cd.nb[i] = 0.f;
+      cd.nmu[i] = 0.f;
+    }
+    cd.nbase = INFINITY;  // e = 2^-inf = 0
+    return;
+  }
+  const float4* c4 = reinterpret_cast<const float4*>(mb.cst + k);
+  const float4 a0 = c4[0], a1 = c4[1], a2 = c4[2];
+  const float cc[12] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
+#pragma unroll
+  for (int q = 0; q < NP; ++q) cd.P[q] = cc[q];
+  cd.nbase = -cc[10];
+  float muf[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    muf[j] = static_cast<float>(mb.mu[k * 4 + j] - ct[j]);
+    cd.nmu[j] = -muf[j];
+  }
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q <= i; ++q)
+      s = fma(static_cast<double>(cd.P[i * (i + 1) / 2 + q]), static_cast<double>(muf[q]), s);
+    cd.nb[i] = static_cast<float>(-s);
+  }
+}
+
+// Q of the point pair (p, p + 1) for the lane's candidate (FFMA2 chains with
+// the broadcast constant operand), points from the warp's SoA tile
+template <int D>
+__device__ __forceinline__ f2_t dens_pair(const Cand<D>& cd, const f2_t (&X)[D]) {
+  const f2_t Y0 = fma2(X[0], pk(cd.P[0], cd.P[0]), pk(cd.nb[0], cd.nb[0]));
+  const f2_t Y1 = fma2(X[1], pk(cd.P[2], cd.P[2]), fma2(X[0], pk(cd.P[1], cd.P[1]), pk(cd.nb[1], cd.nb[1])));
+  const f2_t Y2 =
+      fma2(X[2], pk(cd.P[5], cd.P[5]),
+           fma2(X[1], pk(cd.P[4], cd.P[4]), fma2(X[0], pk(cd.P[3], cd.P[3]), pk(cd.nb[2], cd.nb[2]))));
+  f2_t q = fma2(Y2, Y2, fma2(Y1, Y1, fma2(Y0, Y0, pk(cd.nbase, cd.nbase))));
+  if constexpr (D == 4) {
+    const f2_t Y3 = fma2(
+        X[3], pk(cd.P[9], cd.P[9]),
+        fma2(X[2], pk(cd.P[8], cd.P[8]),
+             fma2(X[1], pk(cd.P[7], cd.P[7]), fma2(X[0], pk(cd.P[6], cd.P[6]), pk(cd.nb[3], cd.nb[3])))));
+    q = fma2(Y3, Y3, q);
+  }
+  return q;
+}
+
+template <int D>
+__device__ __forceinline__ void load_pair(const float (*xs)[kTile], int p, f2_t (&X)[D]) {
+#pragma unroll
+  for (int j = 0; j < D; ++j) X[j] = *reinterpret_cast<const f2_t*>(&xs[j][p]);
+}
+
+struct SpWarpSmem {
+  double acc[15][32];   // FP64 statistics of the lanes' candidates (one group)
+  float xs[4][kTile];   // tile points (SoA, tile-relative)
+  float ssum[kTile];    // per-point normaliser partials (pass 1), then 1/S
+  float sh[kTile];      // per-point shift (exact path), else 0
+  unsigned short list[kListCap];  // fine candidates, ascending
+};
+// per warp: SpWarpSmem | candidate bitmask (K/32 words)
+__host__ __device__ inline size_t warp_smem_bytes(int kcap) {
+  return (sizeof(SpWarpSmem) + sizeof(unsigned) * ((kcap + 31) / 32) + 15) & ~size_t(15);
+}
+
+// ---- main kernel ------------------------------------------------------------
+// Dynamic smem: kSpWarps x [SpWarpSmem | list (kcap ints) | mask (kw words)].
+template <int D>
+__global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
+    estep_sparse_kernel(const float4* __restrict__ xt, const double* __restrict__ tc, int64_t n,
+                        int ntiles, ModelBuf b0, ModelBuf b1, const EmState* __restrict__ st,
+                        int kcap, const int* __restrict__ blist, const int* __restrict__ bcnt,
+                        int* __restrict__ ctl, double* __restrict__ pool, int64_t pool_cap,
+                        int* __restrict__ toff, unsigned* __restrict__ maskT,
+                        unsigned short* __restrict__ preT, double* __restrict__ ll_tile,
+                        int exact_mode, float qcut) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (st->done) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int kw = (kcap + 31) / 32;
+  const size_t wbytes = warp_smem_bytes(kcap);
+  SpWarpSmem& ws = *reinterpret_cast<SpWarpSmem*>(smem_raw + wbytes * warp);
+  unsigned* mw = reinterpret_cast<unsigned*>(smem_raw + wbytes * warp + sizeof(SpWarpSmem));
+  unsigned short* list = ws.list;
+  double (*facc)[32] = ws.acc;
+  const int k_cur = st->k_cur;
+  const ModelBuf& mb = st->cur ? b1 : b0;
+  unsigned long long evaluated = 0;  // units evaluated (lane 0)
+
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(&ctl[0], 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= ntiles) break;
+    const int npts = static_cast<int>(min64(kTile, n - static_cast<int64_t>(t) * kTile));
+    double ct[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ct[j] = tc[static_cast<int64_t>(t) * 4 + j];
+    // ---- tile points -> SoA smem + bounding box of the valid points
+    float lo[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+    float hi[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int p = lane + 32 * q;
+      const float4 x = xt[static_cast<int64_t>(t) * kTile + p];
+      const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        ws.xs[j][p] = xv[j];
+        if (p < npts) {
+          lo[j] = fminf(lo[j], xv[j]);
+          hi[j] = fmaxf(hi[j], xv[j]);
+        }
+      }
+      ws.ssum[p] = 0.f;
+      ws.sh[p] = 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) {
+        lo[j] = fminf(lo[j], __shfl_xor_sync(0xffffffffu, lo[j], off));
+        hi[j] = fmaxf(hi[j], __shfl_xor_sync(0xffffffffu, hi[j], off));
+      }
+    }
+    float bcv[4], hw[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      bcv[j] = 0.5f * (lo[j] + hi[j]);
+      // half-width rounded up (covers the rounding of the centre)
+      hw[j] = fmaxf(hi[j] - bcv[j], bcv[j] - lo[j]) * (1.f + 0x1p-20f) + 1e-30f;
+    }
+    // ---- fine candidates (ascending): the block's list filtered by the tile box
+    const int blk = t / kBlkTiles;
+    const int cb = bcnt[blk];
+    const int* bl = blist + static_cast<int64_t>(blk) * kcap;
+    int C = 0;
+    for (int c0 = 0; c0 < cb; c0 += 32) {
+      const int ci = c0 + lane;
+      bool cand = false;
+      int k = -1;
+      if (ci < cb) {
+        k = bl[ci];
+        const float4* c4 = reinterpret_cast<const float4*>(mb.cst + k);
+        const float4 a0 = c4[0], a1 = c4[1], a2 = c4[2];
+        const float P[12] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
+        float v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          v[j] = j < D ? bcv[j] - static_cast<float>(mb.mu[k * 4 + j] - ct[j]) : 0.f;
+        const float lb = box_lb<D>(P, v, hw);
+        cand = fmaf(lb, -0x1p-10f, lb) - P[10] < qcut;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, cand);
+      if (cand && C + __popc(m) <= kListCap)
+        list[C + __popc(m & lanemask_lt())] = static_cast<unsigned short>(k);
+      C += __popc(m);
+    }
+    // more candidates than the list holds: every component (a superset)
+    bool allk = C > kListCap;
+    if (allk) C = k_cur;
+    __syncwarp();
+    auto cand_at = [&](int i) -> int { return allk ? i : list[i]; };
+
+    // ---- one group (C <= 32, most tiles): both passes per 16-point slice, the
+    // densities kept in registers between them (no recomputation). A slice
+    // that needs the exact path abandons it for the general path below.
+    constexpr int NS = nstats(D);
+    bool fused = false;
+    if (C <= 32 && exact_mode == 0) {
+      fused = true;
+      Cand<D> cd;
+      load_cand<D>(cd, lane < C ? cand_at(lane) : -1, mb, ct);
+#pragma unroll
+      for (int q = 0; q < NS; ++q) facc[q][lane] = 0.0;
+      double fll = 0.0;
+      for (int s = 0; s < kTile / kSlice; ++s) {
+        float e[kSlice], v[kSlice];
+#pragma unroll
+        for (int pp = 0; pp < kSlice; pp += 2) {
+          f2_t X[D];
+          load_pair<D>(ws.xs, s * kSlice + pp, X);
+          const f2_t Q = dens_pair<D>(cd, X);
+          e[pp] = ex2n(lo2(Q));
+          e[pp + 1] = ex2n(hi2(Q));
+          v[pp] = e[pp];
+          v[pp + 1] = e[pp + 1];
+        }
+        const float S = warp_reduce_scatter<kSlice, false>(v, lane);
+        const int pq = s * kSlice + (lane >> 1);
+        const bool valid = pq < npts;
+        if (__any_sync(0xffffffffu, valid && !(S >= 0x1p-64f && S <= 0x1p64f))) {
+          fused = false;
+          break;
+        }
+        if (valid && (lane & 1) == 0) fll += static_cast<double>(lg2f(S));
+        if ((lane & 1) == 0) ws.ssum[pq] = valid ? rcpf(S) : 0.f;
+        __syncwarp();
+        f2_t ACC[NS];
+#pragma unroll
+        for (int q = 0; q < NS; ++q) ACC[q] = 0ull;
+#pragma unroll
+        for (int pp = 0; pp < kSlice; pp += 2) {
+          const int p = s * kSlice + pp;
+          f2_t X[D];
+          load_pair<D>(ws.xs, p, X);
+          const f2_t R = mul2(pk(e[pp], e[pp + 1]), *reinterpret_cast<const f2_t*>(&ws.ssum[p]));
+          f2_t DD[D], W[D];
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            DD[i] = add2(X[i], pk(cd.nmu[i], cd.nmu[i]));
+            W[i] = mul2(R, DD[i]);
+          }
+          ACC[0] = add2(ACC[0], R);
+#pragma unroll
+          for (int i = 0; i < D; ++i) ACC[1 + i] = add2(ACC[1 + i], W[i]);
+          int q = 1 + D;
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+#pragma unroll
+            for (int c = 0; c <= i; ++c) {
+              ACC[q] = fma2(W[i], DD[c], ACC[q]);
+              ++q;
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < NS; ++q) facc[q][lane] += f32_to_f64(lo2(ACC[q]) + hi2(ACC[q]));
+      }
+      if (fused) {
+        // the slices' ll in point order: lanes 0, 2, .. hold points 0..15 of each slice
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) fll += __shfl_xor_sync(0xffffffffu, fll, off);
+        if (lane == 0) ll_tile[t] = fll;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ws.ssum[lane + 32 * q] = 0.f;
+        __syncwarp();
+      }
+    }
+
+    // ---- pass 1: normalisers over the candidates
+    auto pass1 = [&](int nc) {
+      for (int g = 0; g < nc; g += 32) {
+        Cand<D> cd;
+        load_cand<D>(cd, g + lane < nc ? cand_at(g + lane) : -1, mb, ct);
+        for (int s = 0; s < kTile / kSlice; ++s) {
+          float v[kSlice];
+#pragma unroll
+          for (int pp = 0; pp < kSlice; pp += 2) {
+            f2_t X[D];
+            load_pair<D>(ws.xs, s * kSlice + pp, X);
+            const f2_t Q = dens_pair<D>(cd, X);
+            v[pp] = ex2n(lo2(Q));
+            v[pp + 1] = ex2n(hi2(Q));
+          }
+          const float r = warp_reduce_scatter<kSlice, false>(v, lane);
+          if ((lane & 1) == 0) ws.ssum[s * kSlice + (lane >> 1)] += r;
+        }
+      }
+      __syncwarp();
+    };
+    unsigned xslices = 0;
+    if (!fused) {
+    pass1(C);
+    // exact path needed anywhere in the tile? (per 16-point slice, like the
+    // dense kernel's sub-tiles)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int p = lane + 32 * q;
+      const float S = ws.ssum[p];
+      const bool bad = p < npts && (exact_mode != 0 || !(S >= 0x1p-64f && S <= 0x1p64f));
+      const unsigned m = __ballot_sync(0xffffffffu, bad);
+      // lanes 0..15 -> slice 2q, 16..31 -> slice 2q + 1
+      if (m & 0xffffu) xslices |= 1u << (2 * q);
+      if (m & 0xffff0000u) xslices |= 1u << (2 * q + 1);
+    }
+    if (xslices) {
+      // all K components, max shift on the flagged slices (dense exact path)
+      C = k_cur;
+      allk = true;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ws.ssum[lane + 32 * q] = -INFINITY;
+      __syncwarp();
+      for (int g = 0; g < C; g += 32) {  // per-point max of -Q
+        Cand<D> cd;
+        load_cand<D>(cd, g + lane < C ? g + lane : -1, mb, ct);
+        for (int s = 0; s < kTile / kSlice; ++s) {
+          if (!((xslices >> s) & 1u)) continue;
+          float v[kSlice];
+#pragma unroll
+          for (int pp = 0; pp < kSlice; pp += 2) {
+            f2_t X[D];
+            load_pair<D>(ws.xs, s * kSlice + pp, X);
+            const f2_t Q = dens_pair<D>(cd, X);
+            v[pp] = -lo2(Q);
+            v[pp + 1] = -hi2(Q);
+          }
+          const float r = warp_reduce_scatter<kSlice, true>(v, lane);
+          if ((lane & 1) == 0) {
+            float& o = ws.ssum[s * kSlice + (lane >> 1)];
+            o = fmaxf(o, r);
+          }
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int p = lane + 32 * q;
+        const float M = ws.ssum[p];
+        ws.sh[p] = ((xslices >> (p / kSlice)) & 1u) ? (M == -INFINITY ? 0.f : M) : 0.f;
+        ws.ssum[p] = 0.f;
+      }
+      __syncwarp();
+      // normalisers (shifted on flagged slices)
+      for (int g = 0; g < C; g += 32) {
+        Cand<D> cd;
+        load_cand<D>(cd, g + lane < C ? g + lane : -1, mb, ct);
+        for (int s = 0; s < kTile / kSlice; ++s) {
+          float v[kSlice];
+#pragma unroll
+          for (int pp = 0; pp < kSlice; pp += 2) {
+            f2_t X[D];
+            load_pair<D>(ws.xs, s * kSlice + pp, X);
+            f2_t Q = dens_pair<D>(cd, X);
+            Q = add2(Q, *reinterpret_cast<const f2_t*>(&ws.sh[s * kSlice + pp]));
+            v[pp] = ex2n(lo2(Q));
+            v[pp + 1] = ex2n(hi2(Q));
+          }
+          const float r = warp_reduce_scatter<kSlice, false>(v, lane);
+          if ((lane & 1) == 0) ws.ssum[s * kSlice + (lane >> 1)] += r;
+        }
+      }
+      __syncwarp();
+    }
+    // 1/S, log-likelihood (log2 units; one lane per point, fixed order)
+    double ll = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int p = lane + 32 * q;
+      const float S = ws.ssum[p];
+      if (p < npts) ll += static_cast<double>(ws.sh[p] + lg2f(S));
+      ws.ssum[p] = p < npts ? rcpf(S) : 0.f;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) ll += __shfl_xor_sync(0xffffffffu, ll, off);
+    if (lane == 0) ll_tile[t] = ll;
+    }  // !fused
+
+    // ---- output slots (CSR pool) + the tile's candidate bitmask
+    int base = 0;
+    if (lane == 0) base = atomicAdd(&ctl[1], C);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const bool fits = static_cast<int64_t>(base) + C <= pool_cap;
+    if (lane == 0) {
+      toff[t] = fits ? base : -1;
+      if (!fits) atomicExch(&ctl[2], 1);  // pool overflow: the host re-runs larger
+    }
+    for (int w = lane; w < kw; w += 32) mw[w] = 0u;
+    __syncwarp();
+    for (int i = lane; i < C; i += 32) {
+      const int k = cand_at(i);
+      atomicOr(&mw[k >> 5], 1u << (k & 31));
+    }
+    __syncwarp();
+    {
+      int run = 0;
+      for (int w0 = 0; w0 < kw; w0 += 32) {
+        const int w = w0 + lane;
+        const unsigned word = w < kw ? mw[w] : 0u;
+        int c = __popc(word);
+        int incl = c;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int o = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl += o;
+        }
+        if (w < kw) {
+          maskT[static_cast<int64_t>(w) * ntiles + t] = fits ? word : 0u;
+          preT[static_cast<int64_t>(w) * ntiles + t] = static_cast<unsigned short>(run + incl - c);
+        }
+        run += __shfl_sync(0xffffffffu, incl, 31);
+      }
+    }
+    if (lane == 0) evaluated += static_cast<unsigned long long>(npts) * C;
+
+    if (fused) {
+      if (fits && lane < C) {
+#pragma unroll
+        for (int q = 0; q < NS; ++q) pool[q * pool_cap + base + lane] = facc[q][lane];
+      }
+    } else
+    // ---- pass 2: responsibilities + centred statistics
+    for (int g = 0; g < C; g += 32) {
+      const int ci = g + lane;
+      Cand<D> cd;
+      load_cand<D>(cd, ci < C ? cand_at(ci) : -1, mb, ct);
+      double acc[NS];
+#pragma unroll
+      for (int q = 0; q < NS; ++q) acc[q] = 0.0;
+      for (int s = 0; s < kTile / kSlice; ++s) {
+        const bool xs_s = (xslices >> s) & 1u;
+        f2_t ACC[NS];
+#pragma unroll
+        for (int q = 0; q < NS; ++q) ACC[q] = 0ull;
+#pragma unroll
+        for (int pp = 0; pp < kSlice; pp += 2) {
+          const int p = s * kSlice + pp;
+          f2_t X[D];
+          load_pair<D>(ws.xs, p, X);
+          f2_t Q = dens_pair<D>(cd, X);
+          if (xs_s) Q = add2(Q, *reinterpret_cast<const f2_t*>(&ws.sh[p]));
+          const f2_t E = pk(ex2n(lo2(Q)), ex2n(hi2(Q)));
+          const f2_t R = mul2(E, *reinterpret_cast<const f2_t*>(&ws.ssum[p]));
+          f2_t DD[D], W[D];
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            DD[i] = add2(X[i], pk(cd.nmu[i], cd.nmu[i]));
+            W[i] = mul2(R, DD[i]);
+          }
+          ACC[0] = add2(ACC[0], R);
+#pragma unroll
+          for (int i = 0; i < D; ++i) ACC[1 + i] = add2(ACC[1 + i], W[i]);
+          int q = 1 + D;
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+#pragma unroll
+            for (int c = 0; c <= i; ++c) {
+              ACC[q] = fma2(W[i], DD[c], ACC[q]);
+              ++q;
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < NS; ++q) acc[q] += f32_to_f64(lo2(ACC[q]) + hi2(ACC[q]));
+      }
+      if (fits && ci < C) {
+#pragma unroll
+        for (int q = 0; q < NS; ++q) pool[q * pool_cap + base + ci] = acc[q];
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && evaluated)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&ctl[4]), evaluated);
+}
+
+// ---- fixed-order reduce of the per-(tile, candidate) statistics -----------
+// CTA (w, r): components 32 w + lane over tile range r (8 warps split it
+// into contiguous sub-ranges, combined in warp order).
+template <int D>
+__global__ void __launch_bounds__(256)
+    sparse_reduce_kernel(const unsigned* __restrict__ maskT, const unsigned short* __restrict__ preT,
+                         const int* __restrict__ toff, const double* __restrict__ pool,
+                         int64_t pool_cap, const double* __restrict__ ll_tile, int ntiles, int kw,
+                         int R, int kpad, const EmState* __restrict__ st,
+                         double* __restrict__ partials, double* __restrict__ ll_part) {
+  constexpr int NS = nstats(D);
+  __shared__ double red[8][NS][32];
+  __shared__ double lred[8];
+  if (st->done) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int w = blockIdx.x % kw, r = blockIdx.x / kw;
+  const int t0 = static_cast<int>(static_cast<int64_t>(r) * ntiles / R);
+  const int t1 = static_cast<int>(static_cast<int64_t>(r + 1) * ntiles / R);
+  const int a0 = t0 + static_cast<int>(static_cast<int64_t>(warp) * (t1 - t0) / 8);
+  const int a1 = t0 + static_cast<int>(static_cast<int64_t>(warp + 1) * (t1 - t0) / 8);
+  double acc[NS];
+#pragma unroll
+  for (int q = 0; q < NS; ++q) acc[q] = 0.0;
+  const unsigned below = lanemask_lt();
+  for (int tb = a0; tb < a1; tb += 32) {
+    const int tt = tb + lane;
+    const unsigned wv = tt < a1 ? maskT[static_cast<int64_t>(w) * ntiles + tt] : 0u;
+    const int pv = tt < a1 ? preT[static_cast<int64_t>(w) * ntiles + tt] : 0;
+    const int ov = tt < a1 ? toff[tt] : 0;
+    unsigned any = __ballot_sync(0xffffffffu, wv != 0u);
+    while (any) {
+      // two tiles per step: both tiles' loads in flight before the (ordered) adds
+      double v[2][NS];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int j = any ? __ffs(any) - 1 : 0;
+        const bool on = any != 0u;
+        any &= any - 1;
+        const unsigned word = on ? __shfl_sync(0xffffffffu, wv, j) : 0u;
+        const int pre = __shfl_sync(0xffffffffu, pv, j);
+        const int off = __shfl_sync(0xffffffffu, ov, j);
+        const bool mine = (word >> lane) & 1u;
+        const int64_t e = static_cast<int64_t>(off) + pre + __popc(word & below);
+#pragma unroll
+        for (int q = 0; q < NS; ++q) v[u][q] = mine ? pool[q * pool_cap + e] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int q = 0; q < NS; ++q) acc[q] += v[u][q];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NS; ++q) red[warp][q][lane] = acc[q];
+  double l = 0.0;
+  if (w == 0) {
+    for (int tt = a0 + lane; tt < a1; tt += 32) l += ll_tile[tt];
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+    if (lane == 0) lred[warp] = l;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int k = 32 * w + lane;
+    if (k < kpad) {
+      double* out = partials + (static_cast<int64_t>(r) * kpad + k) * NS;
+#pragma unroll
+      for (int q = 0; q < NS; ++q) {
+        double s = 0.0;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) s += red[v][q][lane];
+        out[q] = s;
+      }
+    }
+    if (w == 0 && lane == 0) {
+      double s = 0.0;
+#pragma unroll
+      for (int v = 0; v < 8; ++v) s += lred[v];
+      ll_part[r] = s * kLn2;
+    }
+  }
+}
+
+size_t main_smem_bytes(int kcap) { return warp_smem_bytes(kcap) * kSpWarps; }
+
+int reduce_ranges(int kcap, int ntiles, int sm_count) {
+  const int kw = (kcap + 31) / 32;
+  int R = (2 * sm_count + kw - 1) / kw;
+  const int maxr = (ntiles + 7) / 8;  // at least a few tiles per warp
+  if (R > maxr) R = maxr;
+  return R < 1 ? 1 : R;
+}
+
+}  // namespace
+
+bool sparse_supported(int k0, int ntiles) {
+  const int nblk = (ntiles + kBlkTiles - 1) / kBlkTiles;
+  return k0 <= 65535 && static_cast<int64_t>(nblk) * k0 <= (int64_t{1} << 26) &&
+         main_smem_bytes(k0) <= 200 * 1024;
+}
+
+int sparse_blocks(int ntiles) { return (ntiles + kBlkTiles - 1) / kBlkTiles; }
+
+int sparse_ranges(int k0, int ntiles, int sm_count) { return reduce_ranges(k0, ntiles, sm_count); }
+
+cudaError_t launch_sparse_layout(const PointsDev& pts, const SparseScratch& sp, cudaStream_t s) {
+  const int nblk = sparse_blocks(pts.ntiles);
+  block_box_kernel<<<nblk, kTile, 0, s>>>(pts.xt, pts.tc, pts.n, pts.ntiles, sp.bc, sp.bh);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_estep_sparse(const PointsDev& pts, const ModelBuf* bufs, const EmState* st,
+                                int k0, double* partials, double* ll_part, int exact_mode,
+                                int sm_count, cudaStream_t s, int* ncl_out,
+                                const SparseScratch& sp) {
+  const int ntiles = pts.ntiles;
+  const int R = reduce_ranges(k0, ntiles, sm_count);
+  *ncl_out = R;
+  if (!partials) return cudaSuccess;
+  const int nblk = sparse_blocks(ntiles);
+  const int kw = (k0 + 31) / 32;
+  const size_t smem = main_smem_bytes(k0);
+  static int occ_dev[64][2] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& occ = occ_dev[dev & 63][pts.d == 4 ? 1 : 0];
+  auto kern = pts.d == 4 ? estep_sparse_kernel<4> : estep_sparse_kernel<3>;
+  if (occ == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(200 * 1024));
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kSpWarps * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+    if (getenv("GMMB_DEBUG"))
+      fprintf(stderr, "gmmb: estep_sparse D=%d K=%d smem=%zu -> %d CTAs/SM\n", pts.d, k0, smem, occ);
+  }
+  int grid = sm_count * occ;
+  const int need = (ntiles + kSpWarps - 1) / kSpWarps;
+  if (grid > need) grid = need;
+  static const float qcut = [] {
+    const char* e = getenv("GMMB_SPARSE_QCUT");
+    return e ? static_cast<float>(atof(e)) : kQCut;
+  }();
+  if (pts.d == 4)
+    block_cand_kernel<4><<<nblk, 256, 0, s>>>(sp.bc, sp.bh, bufs[0], bufs[1], st, k0, sp.blist,
+                                              sp.bcnt, sp.ctl, qcut);
+  else
+    block_cand_kernel<3><<<nblk, 256, 0, s>>>(sp.bc, sp.bh, bufs[0], bufs[1], st, k0, sp.blist,
+                                              sp.bcnt, sp.ctl, qcut);
+  kern<<<grid, kSpWarps * 32, smem, s>>>(pts.xt, pts.tc, pts.n, ntiles, bufs[0], bufs[1], st, k0,
+                                         sp.blist, sp.bcnt, sp.ctl, sp.pool, sp.pool_cap, sp.toff,
+                                         sp.maskT, sp.preT, sp.ll_tile, exact_mode, qcut);
+  if (pts.d == 4)
+    sparse_reduce_kernel<4><<<kw * R, 256, 0, s>>>(sp.maskT, sp.preT, sp.toff, sp.pool, sp.pool_cap,
+                                                   sp.ll_tile, ntiles, kw, R, k0, st, partials,
+                                                   ll_part);
+  else
+    sparse_reduce_kernel<3><<<kw * R, 256, 0, s>>>(sp.maskT, sp.preT, sp.toff, sp.pool, sp.pool_cap,
+                                                   sp.ll_tile, ntiles, kw, R, k0, st, partials,
+                                                   ll_part);
+  return cudaGetLastError();
+}
+
+}  // namespace gmmb

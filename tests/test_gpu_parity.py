@@ -316,7 +316,13 @@ def test_em_step_far_outliers_exact_path(gm, orc, ctx, k):
     rw, rmu, rcov, rrm = orc.m_step(p, lg, 1e-6)
     assert rm == rrm
     assert abs(ll - rll) / abs(rll) < LL_TOL
-    assert_model_close(m1.weights, m1.means, m1.covariances, rw, rmu, rcov, tol=1e-5)
+    # 3e-5 (a single step; the fit-level bar is 1e-4): the 40 far points
+    # dominate the scatter of the components that absorb them (|d| ~ 3 m
+    # against ~5 cm), which magnifies FP32 rounding of their r d d^T terms
+    # ~300x; the dense and the pruned kernels both sit at that floor
+    # (scripts/outlier_err.py: 5e-6 and 1.1e-5 for K = 64, 6e-6 for both at
+    # K = 1024; the pruned kernel with every pair kept gives the same 1.1e-5)
+    assert_model_close(m1.weights, m1.means, m1.covariances, rw, rmu, rcov, tol=3e-5)
 
 
 @pytest.mark.gpu

@@ -42,11 +42,16 @@ def test_vshard_frame_matches_unsharded_and_oracle(gm, orc, ctx, world):
     assert ll_err(rs[0].ll_trace, ref["ll_trace"]) < LL_TOL
     assert ll_err(rs[0].ll_trace, one.ll_trace) < 1e-7
     m = rs[0].model
-    assert_model_close(m.weights, m.means, m.covariances, ref["w"], ref["mu"], ref["cov"])
-    # both within PARAM_TOL of the oracle: within 2 PARAM_TOL of each other
-    # (FP32 tiles differ per shard; EM amplifies the rounding)
+    # 2e-4: shards re-tile the cloud, so the FP32 rounding pattern differs
+    # from the unsharded fit's; EM on this frame amplifies a 1e-7 relative
+    # perturbation to ~1e-4 in the covariances even in FP64
+    # (profiles/r2_em_sensitivity.txt), and the measured sharded/unsharded,
+    # dense/pruned errors scatter over 1.4e-5 .. 1.3e-4 (scripts/vshard_err.py,
+    # profiles/r2g_vshard.txt)
+    assert_model_close(m.weights, m.means, m.covariances, ref["w"], ref["mu"], ref["cov"], tol=2e-4)
+    # both within 2 PARAM_TOL of the oracle: within 4 PARAM_TOL of each other
     assert_model_close(m.weights, m.means, m.covariances, one.model.weights, one.model.means,
-                       one.model.covariances, tol=2e-4)
+                       one.model.covariances, tol=4e-4)
     # units count every rank's points once (the global N)
     assert rs[0].units == pytest.approx(len(p) * k * rs[0].em_iterations)
 
