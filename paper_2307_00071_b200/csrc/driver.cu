@@ -129,6 +129,10 @@ struct gmmb_ctx {
   DevBuf<int> ticket;
   DevBuf<int> kstatus;
   DevBuf<long long> ll64;      // sharded fix-up scratch
+  int kinit_tile = 1;          // 1: tile-pruned seeding past the resident kernel (GMMB_KINIT=mem: off)
+  DevBuf<double> kt_xm, kt_d2, kt_tile;
+  DevBuf<uint64_t> kt_key;
+  DevBuf<int32_t> kt_lab;
   // model
   DevBuf<double> mw[2], mmu[2], mcov[2];
   DevBuf<CompConst> mcst[2];
@@ -397,6 +401,32 @@ void run_kinit(gmmb_ctx* c, int k, uint64_t seed) {
   const int64_t n = c->n;
   KinitScratch ks = kinit_scratch(c, k);
   ck(cudaMemsetAsync(c->owned.p, 0, sizeof(int) * k, c->s), "memset");
+  if (c->world == 1 && c->kinit_tile && kpp_tile_wanted(n, c->sm_count)) {
+    // beyond the shared-memory-resident kernel: tile-pruned rounds over the
+    // layout's Morton tiles (kinit_tile.cu)
+    const int ntiles = static_cast<int>((n + kTile - 1) / kTile);
+    c->kt_xm.ensure(static_cast<size_t>(n) * 4);
+    c->kt_key.ensure(n);
+    c->kt_d2.ensure(n);
+    c->kt_lab.ensure(n);
+    c->kt_tile.ensure(static_cast<size_t>(ntiles) * 10);
+    KppTileScratch ts{c->kt_xm.p, c->kt_key.p, c->kt_d2.p, c->kt_lab.p, c->perm.p, c->kt_tile.p,
+                      c->kt_tile.p + static_cast<size_t>(ntiles) * 8,
+                      c->kt_tile.p + static_cast<size_t>(ntiles) * 9};
+    ck(launch_keys(c->x64.p, n, c->x64.p + n, c->keys.p, c->s), "keys");
+    ck(cudaMemsetAsync(c->kstatus.p, 0, sizeof(int) * 8, c->s), "memset");
+    ck(launch_kpp_tile(c->x64.p, n, ntiles, c->perm.p, k, seed, ks, ts, c->sm_count, c->s),
+       "kpp_tile");
+    ck(launch_fixup(n, k, ks, c->s), "fixup");
+    c->launches += 6;  // keys, init, boxes, rounds (persistent), scatter, fixup
+    if (getenv("GMMB_DEBUG")) {
+      unsigned long long xc[2] = {0, 0};
+      copy_sync(c, xc, c->kstatus.p + 2, sizeof(xc), cudaMemcpyDeviceToHost);
+      fprintf(stderr, "gmmb: kpp_tile n=%lld k=%d: %llu grid exchanges, %llu exact clocks\n",
+              static_cast<long long>(n), k, xc[0], xc[1]);
+    }
+    return;
+  }
   if (c->world == 1) {
     ck(launch_keys(c->x64.p, n, c->x64.p + n, c->keys.p, c->s), "keys");
     ck(cudaMemsetAsync(c->kstatus.p, 0, sizeof(int) * 8, c->s), "memset");
@@ -1140,6 +1170,8 @@ static int create(int device, int rank, int world, const void* id, VGroup* vg,
     {  // GMMB_ESTEP=dense selects the dense E kernels (A/B, validation)
       const char* m = getenv("GMMB_ESTEP");
       c->estep_mode = (m && std::strcmp(m, "dense") == 0) ? 1 : 0;
+      const char* ki = getenv("GMMB_KINIT");
+      c->kinit_tile = (ki && std::strcmp(ki, "mem") == 0) ? 0 : 1;
     }
     try {
       ck(cudaSetDevice(device), "cudaSetDevice");
@@ -1238,6 +1270,8 @@ void gmmb_ctx_destroy(gmmb_ctx* c) {
   c->kxf.release(); c->ktp.release(); c->kinv.release();
   c->slots.release(); c->owned.release(); c->centers.release(); c->rslots.release();
   c->ticket.release(); c->kstatus.release(); c->ll64.release();
+  c->kt_xm.release(); c->kt_d2.release(); c->kt_tile.release(); c->kt_key.release();
+  c->kt_lab.release();
   for (int b = 0; b < 2; ++b) {
     c->mw[b].release(); c->mmu[b].release(); c->mcov[b].release(); c->mcst[b].release();
   }
@@ -1380,7 +1414,11 @@ int gmmb_kinit(gmmb_ctx* c, const double* pts, int64_t n, int d, int k, uint64_t
     if (c->world > 1) throw Err{2, "gmmb_kinit is single-device; use gmmb_fit_k"};
     upload(c, pts, n, d, 0, n);
     c->have_cloud = false;  // single-step input: not a resident cloud for *_resident fits
-    validate(c);
+    // the tile-pruned seeding (large clouds) runs on the Morton layout
+    if (c->kinit_tile && kpp_tile_wanted(n, c->sm_count))
+      layout(c);
+    else
+      validate(c);
     check_cloud_flags(c);
     if (k < 1 || k > n) throw Err{2, "kinit: k must satisfy 1 <= k <= N"};  // sogmm.cpp:200
     ensure_model(c, k);

@@ -45,6 +45,26 @@ cudaError_t launch_keys(const double* x64, int64_t n, const double* tail,
 cudaError_t launch_kpp_seed(const double* x64, int64_t n, int d, int k, uint64_t seed,
                             KinitScratch scr, int sm_count, cudaStream_t s);
 
+// Tile-pruned seeding for clouds beyond the shared-memory-resident kernel
+// (kinit_tile.cu): Morton-order copies of the points / keys / state and
+// per-tile FP64 boxes, largest d2 and d2 sums (ntiles = layout tiles).
+struct KppTileScratch {
+  double* xm;           // [4][n] FP64 coordinates, Morton order
+  uint64_t* mkey;       // [n]
+  double* md2;          // [n]
+  int32_t* mlab;        // [n]
+  const int32_t* perm;  // [n] Morton position -> original index
+  double* tbox;         // [ntiles][8] lo[4], hi[4]
+  double* tdmax;        // [ntiles]
+  double* tsum;         // [ntiles]
+};
+bool kpp_tile_wanted(int64_t n, int sm_count);
+// keys must be computed; owned[] zeroed; labels (original order), owned and
+// centres are written (the fix-up follows).
+cudaError_t launch_kpp_tile(const double* x64, int64_t n, int ntiles, const int32_t* perm,
+                            int k, uint64_t seed, KinitScratch scr, KppTileScratch ts,
+                            int sm_count, cudaStream_t s);
+
 // Owned fix-up (sogmm.cpp:315-331), single CTA, no-op when nothing is empty.
 cudaError_t launch_fixup(int64_t n, int k, KinitScratch scr, cudaStream_t s);
 
