@@ -150,7 +150,8 @@ struct gmmb_ctx {
   int pool_mult = 1;              // pool growth after an overflow
   DevBuf<double> sp_bc, sp_pool, sp_ll;
   DevBuf<float4> sp_bh;
-  DevBuf<int> sp_blist, sp_bcnt, sp_ctl, sp_toff;
+  DevBuf<int> sp_blist, sp_bcnt, sp_ctl, sp_toff, sp_heavy;
+  DevBuf<unsigned> sp_done;
   DevBuf<unsigned> sp_mask;
   DevBuf<unsigned short> sp_pre;
   SparseScratch sparse{};
@@ -672,23 +673,32 @@ void ensure_em_buffers(gmmb_ctx* c, int k0, int max_iters) {
   c->sparse_on = c->estep_mode == 0 && sparse_supported(k0, pts.ntiles);
   if (c->sparse_on) {
     const int ntiles = pts.ntiles;
+    const int nitems = sparse_items(ntiles);
     const int nblk = sparse_blocks(ntiles);
     const int kw = (k0 + 31) / 32;
-    // pool of per-(tile, candidate) statistics: ~30 candidates per tile on
-    // the BASELINE frames; 128 per tile (or all K) up front, doubled after
-    // an overflow (the EM run is repeated, see run_em)
-    const int64_t per_tile = std::min<int64_t>(k0, int64_t{128} * c->pool_mult);
-    const int64_t cap = std::max<int64_t>(static_cast<int64_t>(ntiles) * per_tile, 1024);
+    // pool of per-(item, candidate) statistics: ~20-45 candidates per 32-point
+    // item on the BASELINE clouds; 32 + K/64 per item (or all K) up front,
+    // doubled after an overflow (the EM run is repeated, see run_em)
+    const int64_t per_item = std::min<int64_t>(k0, (32 + k0 / 64) * int64_t{c->pool_mult});
+    const int64_t cap = std::max<int64_t>(static_cast<int64_t>(nitems) * per_item, 1024);
     c->sp_blist.ensure(static_cast<size_t>(nblk) * k0);
     c->sp_bcnt.ensure(nblk);
-    c->sp_ctl.ensure(8);
-    c->sp_pool.ensure(static_cast<size_t>(cap) * NS);
-    c->sp_toff.ensure(ntiles);
-    c->sp_mask.ensure(static_cast<size_t>(kw) * ntiles);
-    c->sp_pre.ensure(static_cast<size_t>(kw) * ntiles);
-    c->sp_ll.ensure(ntiles);
+    c->sp_ctl.ensure(16);
+    c->sp_heavy.ensure(static_cast<size_t>(2) * nitems);
+    if (c->sp_done.cap < static_cast<size_t>(nitems)) {
+      c->sp_done.ensure(nitems);  // epoch stamps: zero once per allocation
+      ck(cudaMemsetAsync(c->sp_done.p, 0, sizeof(unsigned) * c->sp_done.cap, c->s), "memset");
+      ck(cudaMemsetAsync(c->sp_ctl.p, 0, sizeof(int) * 16, c->s), "memset");
+    }
+    const int NSP = (NS + 1) & ~1;  // pool entry stride (estep_sparse.cu)
+    c->sp_pool.ensure(static_cast<size_t>(cap) * NSP);
+    c->sp_toff.ensure(nitems);
+    c->sp_mask.ensure(static_cast<size_t>(kw) * nitems);
+    c->sp_pre.ensure(static_cast<size_t>(kw) * nitems);
+    c->sp_ll.ensure(nitems);
     c->sparse = SparseScratch{c->sp_bc.p, c->sp_bh.p, c->sp_blist.p, c->sp_bcnt.p, c->sp_ctl.p,
-                              c->sp_pool.p, static_cast<int64_t>(c->sp_pool.cap / NS),
+                              c->sp_heavy.p, c->sp_done.p,
+                              c->sp_pool.p, static_cast<int64_t>(c->sp_pool.cap / NSP),
                               c->sp_toff.p, c->sp_mask.p, c->sp_pre.p, c->sp_ll.p};
   }
   int ncl = 0;
@@ -743,6 +753,8 @@ EmState run_em(gmmb_ctx* c, int k0, const gmmb_em_params* em) {
       d2d(c->bak_cov[b].p, c->mcov[b].p, sizeof(double) * kc * 10);
       d2d(c->bak_cst[b].p, c->mcst[b].p, sizeof(CompConst) * kc);
     }
+    // per-fit counters (queues, pool cursor, overflow, evaluated units, heavy
+    // lists); ctl[8] (the item epoch) keeps counting
     ck(cudaMemsetAsync(c->sp_ctl.p, 0, sizeof(int) * 8, c->s), "memset");
     EmState h = run_em_once(c, k0, em);
     int ctl[8];
@@ -1283,6 +1295,7 @@ void gmmb_ctx_destroy(gmmb_ctx* c) {
   c->sp_bc.release(); c->sp_pool.release(); c->sp_ll.release(); c->sp_bh.release();
   c->sp_blist.release(); c->sp_bcnt.release(); c->sp_ctl.release(); c->sp_toff.release();
   c->sp_mask.release(); c->sp_pre.release(); c->st_bak.release();
+  c->sp_heavy.release(); c->sp_done.release();
   for (int b = 0; b < 2; ++b) {
     c->bak_w[b].release(); c->bak_mu[b].release(); c->bak_cov[b].release(); c->bak_cst[b].release();
   }

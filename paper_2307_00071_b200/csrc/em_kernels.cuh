@@ -60,16 +60,19 @@ struct SparseScratch {
   float4* bh;            // [nblk]
   int* blist;            // [nblk][K]
   int* bcnt;             // [nblk]
-  int* ctl;              // [8]
+  int* ctl;              // [16]
+  int* heavy;            // [2][nitems] heavy-item lists (iteration parity)
+  unsigned* done;        // [nitems] epoch stamps of items taken from a heavy list
   double* pool;          // [nstats][pool_cap]
   int64_t pool_cap;
-  int* toff;             // [ntiles]
-  unsigned* maskT;       // [K/32][ntiles]
-  unsigned short* preT;  // [K/32][ntiles]
-  double* ll_tile;       // [ntiles]
+  int* toff;             // [nitems]
+  unsigned* maskT;       // [K/32][nitems]
+  unsigned short* preT;  // [K/32][nitems]
+  double* ll_tile;       // [nitems]
 };
 bool sparse_supported(int k0, int ntiles);
 int sparse_blocks(int ntiles);
+int sparse_items(int ntiles);  // work items (32-point quarter tiles)
 int sparse_ranges(int k0, int ntiles, int sm_count);
 cudaError_t launch_sparse_layout(const PointsDev& pts, const SparseScratch& sp, cudaStream_t s);
 cudaError_t launch_estep_sparse(const PointsDev& pts, const ModelBuf* bufs, const EmState* st,

@@ -52,13 +52,22 @@ namespace {
 
 using namespace dev;
 
+#ifdef GMMB_SP_PROF
+__device__ unsigned long long g_sp_prof[4 * 262144];  // per tile: t0, t1, (sm, C), flags
+#endif
 constexpr int kBlkTiles = 16;     // tiles per culling block
+constexpr int kItem = 32;         // points per item (one per lane); a work unit is U = 1, 2
+constexpr int kItemsPerTile = kTile / kItem;  // or 4 consecutive items of one layout tile
 constexpr int kSpWarps = 8;       // warps per CTA of the main kernel
 constexpr int kSpMinBlocks = 2;   // two CTAs per SM (128 registers)
 constexpr int kListCap = 1024;    // candidate list entries per warp (more: every component)
 constexpr int kSlice = 16;        // points per FP32 partial (widened to FP64 after)
 constexpr float kQCut = 134.f;    // candidates: LB < 134 (ex2.approx.ftz(-Q) = 0 for Q > 126)
 // (GMMB_SPARSE_QCUT overrides it: a validation knob, e.g. 1e30 keeps every pair)
+
+// pool entries: the nstats(D) FP64 statistics of one (item, candidate),
+// padded to an even count (16-byte loads in the reduce)
+__host__ __device__ constexpr int pool_stride(int d) { return (nstats(d) + 1) & ~1; }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -84,6 +93,25 @@ __device__ __forceinline__ float box_lb(const float* P, const float (&v)[4], con
     lb = fmaf(dlt, dlt, lb);
   }
   return lb;
+}
+
+// interval upper bound of |P'(x - mu)|^2 over the same box
+template <int D>
+__device__ __forceinline__ float box_ub(const float* P, const float (&v)[4], const float (&h)[4]) {
+  float ub = 0.f;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    float yc = 0.f, r = 0.f;
+#pragma unroll
+    for (int j = 0; j <= i; ++j) {
+      const float p = P[i * (i + 1) / 2 + j];
+      yc = fmaf(p, v[j], yc);
+      r = fmaf(fabsf(p), h[j], r);
+    }
+    const float dlt = fabsf(yc) + r;
+    ub = fmaf(dlt, dlt, ub);
+  }
+  return ub;
 }
 
 // ---- static per-layout block boxes (FP64 centre, FP32 half-widths rounded up)
@@ -146,9 +174,17 @@ __global__ void __launch_bounds__(256)
   __shared__ int wcnt[8];
   __shared__ int s_base;
   if (st->done) return;
-  // tile queue and pool cursor restart every iteration (ctl[2] overflow and
-  // ctl[4..5] evaluated units accumulate over the fit; zeroed by the driver)
-  if (blockIdx.x == 0 && threadIdx.x < 2) ctl[threadIdx.x] = 0;
+  // item queues and pool cursor restart every iteration (ctl[2] overflow and
+  // ctl[4..5] evaluated units accumulate over the fit; zeroed by the driver);
+  // the heavy list this iteration appends to (parity of iter + 1) restarts;
+  // ctl[8] is the item epoch (never reset)
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl[0] = 0;
+    ctl[1] = 0;
+    ctl[3] = 0;
+    ctl[6 + ((st->iter + 1) & 1)] = 0;
+    ctl[8] += 1;
+  }
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int k_cur = st->k_cur;
   const ModelBuf& mb = st->cur ? b1 : b0;
@@ -263,7 +299,7 @@ __device__ __forceinline__ void load_pair(const float (*xs)[kTile], int p, f2_t 
 
 struct SpWarpSmem {
   double acc[15][32];   // FP64 statistics of the lanes' candidates (one group)
-  float xs[4][kTile];   // tile points (SoA, tile-relative)
+  float xs[4][kTile];   // the unit's points (SoA, tile-relative)
   float ssum[kTile];    // per-point normaliser partials (pass 1), then 1/S
   float sh[kTile];      // per-point shift (exact path), else 0
   unsigned short list[kListCap];  // fine candidates, ascending
@@ -278,13 +314,15 @@ __host__ __device__ inline size_t warp_smem_bytes(int kcap) {
 template <int D>
 __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
     estep_sparse_kernel(const float4* __restrict__ xt, const double* __restrict__ tc, int64_t n,
-                        int ntiles, ModelBuf b0, ModelBuf b1, const EmState* __restrict__ st,
+                        int nitems, ModelBuf b0, ModelBuf b1, const EmState* __restrict__ st,
                         int kcap, const int* __restrict__ blist, const int* __restrict__ bcnt,
                         int* __restrict__ ctl, double* __restrict__ pool, int64_t pool_cap,
                         int* __restrict__ toff, unsigned* __restrict__ maskT,
                         unsigned short* __restrict__ preT, double* __restrict__ ll_tile,
-                        int exact_mode, float qcut) {
+                        int* __restrict__ heavy, unsigned* __restrict__ done,
+                        int exact_mode, float qcut, int U) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int kNSP = pool_stride(D);
   if (st->done) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int kw = (kcap + 31) / 32;
@@ -297,22 +335,49 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
   const ModelBuf& mb = st->cur ? b1 : b0;
   unsigned long long evaluated = 0;  // units evaluated (lane 0)
 
+  // Work order: first the items that were heavy in the previous iteration
+  // (more than 48 candidates; longest first is the classic fix for a tail),
+  // then every item in index order, skipping those already done this epoch.
+  // The order changes no result: an item's output depends only on the item.
+  const int par = st->iter & 1;
+  const int nheavy = ctl[6 + par];
+  const int* hl_cur = heavy + static_cast<int64_t>(par) * nitems;
+  int* hl_next = heavy + static_cast<int64_t>(par ^ 1) * nitems;
+  const unsigned epoch = static_cast<unsigned>(ctl[8]);
   for (;;) {
-    int t = 0;
-    if (lane == 0) t = atomicAdd(&ctl[0], 1);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    if (t >= ntiles) break;
-    const int npts = static_cast<int>(min64(kTile, n - static_cast<int64_t>(t) * kTile));
+    // work item it = 32 consecutive points (quarter qi of layout tile t)
+    int it = 0;
+    if (lane == 0) {
+      const int h = nheavy > 0 ? atomicAdd(&ctl[3], 1) : nheavy;
+      if (h < nheavy) {
+        it = hl_cur[h];
+        done[it] = epoch;
+      } else {
+        do {
+          it = atomicAdd(&ctl[0], 1);
+        } while (it < nitems && done[it] == epoch);
+      }
+    }
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= nitems) break;
+    // unit it: points [it U 32, (it + 1) U 32) of the sorted cloud, one tile
+    const int64_t p0 = static_cast<int64_t>(it) * U * kItem;
+    const int t = static_cast<int>(p0 / kTile);
+    const int nsl = 2 * U;  // 16-point slices
+#ifdef GMMB_SP_PROF
+    unsigned long long prof_t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof_t0));
+#endif
+    const int npts = static_cast<int>(min64(U * kItem, n - p0));  // may be <= 0 (padding)
     double ct[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) ct[j] = tc[static_cast<int64_t>(t) * 4 + j];
     // ---- tile points -> SoA smem + bounding box of the valid points
     float lo[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
     float hi[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < U; ++q) {
       const int p = lane + 32 * q;
-      const float4 x = xt[static_cast<int64_t>(t) * kTile + p];
+      const float4 x = xt[p0 + p];  // (the padding of the last tile is zero)
       const float xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -342,7 +407,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
     }
     // ---- fine candidates (ascending): the block's list filtered by the tile box
     const int blk = t / kBlkTiles;
-    const int cb = bcnt[blk];
+    const int cb = npts > 0 ? bcnt[blk] : 0;
     const int* bl = blist + static_cast<int64_t>(blk) * kcap;
     int C = 0;
     for (int c0 = 0; c0 < cb; c0 += 32) {
@@ -384,7 +449,8 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
 #pragma unroll
       for (int q = 0; q < NS; ++q) facc[q][lane] = 0.0;
       double fll = 0.0;
-      for (int s = 0; s < kTile / kSlice; ++s) {
+      #pragma unroll 1
+        for (int s = 0; s < nsl; ++s) {
         float e[kSlice], v[kSlice];
 #pragma unroll
         for (int pp = 0; pp < kSlice; pp += 2) {
@@ -441,10 +507,9 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
         // the slices' ll in point order: lanes 0, 2, .. hold points 0..15 of each slice
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) fll += __shfl_xor_sync(0xffffffffu, fll, off);
-        if (lane == 0) ll_tile[t] = fll;
+        if (lane == 0) ll_tile[it] = fll;
       } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) ws.ssum[lane + 32 * q] = 0.f;
+        for (int q = 0; q < U; ++q) ws.ssum[lane + 32 * q] = 0.f;
         __syncwarp();
       }
     }
@@ -454,7 +519,8 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
       for (int g = 0; g < nc; g += 32) {
         Cand<D> cd;
         load_cand<D>(cd, g + lane < nc ? cand_at(g + lane) : -1, mb, ct);
-        for (int s = 0; s < kTile / kSlice; ++s) {
+        #pragma unroll 1
+        for (int s = 0; s < nsl; ++s) {
           float v[kSlice];
 #pragma unroll
           for (int pp = 0; pp < kSlice; pp += 2) {
@@ -473,29 +539,71 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
     unsigned xslices = 0;
     if (!fused) {
     pass1(C);
-    // exact path needed anywhere in the tile? (per 16-point slice, like the
+    // exact path needed anywhere in the item? (per 16-point slice, like the
     // dense kernel's sub-tiles)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < U; ++q) {
       const int p = lane + 32 * q;
       const float S = ws.ssum[p];
       const bool bad = p < npts && (exact_mode != 0 || !(S >= 0x1p-64f && S <= 0x1p64f));
       const unsigned m = __ballot_sync(0xffffffffu, bad);
       // lanes 0..15 -> slice 2q, 16..31 -> slice 2q + 1
       if (m & 0xffffu) xslices |= 1u << (2 * q);
-      if (m & 0xffff0000u) xslices |= 1u << (2 * q + 1);
+      if (m & 0xffff0000u) xslices |= 2u << (2 * q);
     }
     if (xslices) {
-      // all K components, max shift on the flagged slices (dense exact path)
-      C = k_cur;
-      allk = true;
+      // Max shift on the flagged slices (the dense kernel's exact path). The
+      // components that can matter: with UB_min the smallest upper bound of
+      // Q over the tile box among ALL components, every point's minimum Q is
+      // <= UB_min, so a component whose lower bound is >= max(UB_min, 0) + 134
+      // has density 0 both shifted (Q - min Q >= 134) and unshifted.
+      float ubmin = INFINITY;
+      for (int k = lane; k < k_cur; k += 32) {
+        const float4* c4 = reinterpret_cast<const float4*>(mb.cst + k);
+        const float4 a0 = c4[0], a1 = c4[1], a2 = c4[2];
+        const float P[12] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
+        float v[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) ws.ssum[lane + 32 * q] = -INFINITY;
+        for (int j = 0; j < 4; ++j)
+          v[j] = j < D ? bcv[j] - static_cast<float>(mb.mu[k * 4 + j] - ct[j]) : 0.f;
+        ubmin = fminf(ubmin, box_ub<D>(P, v, hw) * (1.f + 0x1p-10f) - P[10]);
+      }
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1)
+        ubmin = fminf(ubmin, __shfl_xor_sync(0xffffffffu, ubmin, off));
+      const float xcut = fmaxf(ubmin, 0.f) + qcut;
+      C = 0;
+      allk = false;
+      for (int k0 = 0; k0 < k_cur; k0 += 32) {
+        const int k = k0 + lane;
+        bool cand = false;
+        if (k < k_cur) {
+          const float4* c4 = reinterpret_cast<const float4*>(mb.cst + k);
+          const float4 a0 = c4[0], a1 = c4[1], a2 = c4[2];
+          const float P[12] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
+          float v[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            v[j] = j < D ? bcv[j] - static_cast<float>(mb.mu[k * 4 + j] - ct[j]) : 0.f;
+          const float lb = box_lb<D>(P, v, hw);
+          cand = !(fmaf(lb, -0x1p-10f, lb) - P[10] >= xcut);  // NaN / inf bounds: keep
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, cand);
+        if (cand && C + __popc(m) <= kListCap)
+          list[C + __popc(m & lanemask_lt())] = static_cast<unsigned short>(k);
+        C += __popc(m);
+      }
+      if (C > kListCap) {
+        C = k_cur;
+        allk = true;
+      }
+      __syncwarp();
+      for (int q = 0; q < U; ++q) ws.ssum[lane + 32 * q] = -INFINITY;
       __syncwarp();
       for (int g = 0; g < C; g += 32) {  // per-point max of -Q
         Cand<D> cd;
-        load_cand<D>(cd, g + lane < C ? g + lane : -1, mb, ct);
-        for (int s = 0; s < kTile / kSlice; ++s) {
+        load_cand<D>(cd, g + lane < C ? cand_at(g + lane) : -1, mb, ct);
+        #pragma unroll 1
+        for (int s = 0; s < nsl; ++s) {
           if (!((xslices >> s) & 1u)) continue;
           float v[kSlice];
 #pragma unroll
@@ -514,8 +622,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
         }
       }
       __syncwarp();
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < U; ++q) {
         const int p = lane + 32 * q;
         const float M = ws.ssum[p];
         ws.sh[p] = ((xslices >> (p / kSlice)) & 1u) ? (M == -INFINITY ? 0.f : M) : 0.f;
@@ -525,8 +632,9 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
       // normalisers (shifted on flagged slices)
       for (int g = 0; g < C; g += 32) {
         Cand<D> cd;
-        load_cand<D>(cd, g + lane < C ? g + lane : -1, mb, ct);
-        for (int s = 0; s < kTile / kSlice; ++s) {
+        load_cand<D>(cd, g + lane < C ? cand_at(g + lane) : -1, mb, ct);
+        #pragma unroll 1
+        for (int s = 0; s < nsl; ++s) {
           float v[kSlice];
 #pragma unroll
           for (int pp = 0; pp < kSlice; pp += 2) {
@@ -545,8 +653,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
     }
     // 1/S, log-likelihood (log2 units; one lane per point, fixed order)
     double ll = 0.0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < U; ++q) {
       const int p = lane + 32 * q;
       const float S = ws.ssum[p];
       if (p < npts) ll += static_cast<double>(ws.sh[p] + lg2f(S));
@@ -554,7 +661,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
     }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) ll += __shfl_xor_sync(0xffffffffu, ll, off);
-    if (lane == 0) ll_tile[t] = ll;
+    if (lane == 0) ll_tile[it] = ll;
     }  // !fused
 
     // ---- output slots (CSR pool) + the tile's candidate bitmask
@@ -563,7 +670,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
     base = __shfl_sync(0xffffffffu, base, 0);
     const bool fits = static_cast<int64_t>(base) + C <= pool_cap;
     if (lane == 0) {
-      toff[t] = fits ? base : -1;
+      toff[it] = fits ? base : -1;
       if (!fits) atomicExch(&ctl[2], 1);  // pool overflow: the host re-runs larger
     }
     for (int w = lane; w < kw; w += 32) mw[w] = 0u;
@@ -586,18 +693,22 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
           if (lane >= off) incl += o;
         }
         if (w < kw) {
-          maskT[static_cast<int64_t>(w) * ntiles + t] = fits ? word : 0u;
-          preT[static_cast<int64_t>(w) * ntiles + t] = static_cast<unsigned short>(run + incl - c);
+          maskT[static_cast<int64_t>(w) * nitems + it] = fits ? word : 0u;
+          preT[static_cast<int64_t>(w) * nitems + it] = static_cast<unsigned short>(run + incl - c);
         }
         run += __shfl_sync(0xffffffffu, incl, 31);
       }
     }
-    if (lane == 0) evaluated += static_cast<unsigned long long>(npts) * C;
+    if (lane == 0 && npts > 0) evaluated += static_cast<unsigned long long>(npts) * C;
+    if (lane == 0 && C > 48) hl_next[atomicAdd(&ctl[6 + (par ^ 1)], 1)] = it;
+#ifdef GMMB_SP_PROF
+    const int prof_c = C, prof_f = fused ? 1 : 0, prof_x = xslices ? 1 : 0;
+#endif
 
     if (fused) {
       if (fits && lane < C) {
 #pragma unroll
-        for (int q = 0; q < NS; ++q) pool[q * pool_cap + base + lane] = facc[q][lane];
+        for (int q = 0; q < NS; ++q) pool[(base + lane) * kNSP + q] = facc[q][lane];
       }
     } else
     // ---- pass 2: responsibilities + centred statistics
@@ -608,7 +719,8 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
       double acc[NS];
 #pragma unroll
       for (int q = 0; q < NS; ++q) acc[q] = 0.0;
-      for (int s = 0; s < kTile / kSlice; ++s) {
+      #pragma unroll 1
+        for (int s = 0; s < nsl; ++s) {
         const bool xs_s = (xslices >> s) & 1u;
         f2_t ACC[NS];
 #pragma unroll
@@ -646,10 +758,22 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
       }
       if (fits && ci < C) {
 #pragma unroll
-        for (int q = 0; q < NS; ++q) pool[q * pool_cap + base + ci] = acc[q];
+        for (int q = 0; q < NS; ++q) pool[(base + ci) * kNSP + q] = acc[q];
       }
     }
     __syncwarp();
+#ifdef GMMB_SP_PROF
+    if (lane == 0) {
+      unsigned long long prof_t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof_t1));
+      unsigned smid;
+      asm("mov.u32 %0, %%smid;" : "=r"(smid));
+      g_sp_prof[it * 4 + 0] = prof_t0;
+      g_sp_prof[it * 4 + 1] = prof_t1;
+      g_sp_prof[it * 4 + 2] = (static_cast<unsigned long long>(smid) << 32) | static_cast<unsigned>(prof_c);
+      g_sp_prof[it * 4 + 3] = prof_f | (prof_x << 1);
+    }
+#endif
   }
   if (lane == 0 && evaluated)
     atomicAdd(reinterpret_cast<unsigned long long*>(&ctl[4]), evaluated);
@@ -666,6 +790,7 @@ __global__ void __launch_bounds__(256)
                          int R, int kpad, const EmState* __restrict__ st,
                          double* __restrict__ partials, double* __restrict__ ll_part) {
   constexpr int NS = nstats(D);
+  constexpr int kNSP = pool_stride(D);
   __shared__ double red[8][NS][32];
   __shared__ double lred[8];
   if (st->done) return;
@@ -698,8 +823,13 @@ __global__ void __launch_bounds__(256)
         const int off = __shfl_sync(0xffffffffu, ov, j);
         const bool mine = (word >> lane) & 1u;
         const int64_t e = static_cast<int64_t>(off) + pre + __popc(word & below);
+        const double2* src = reinterpret_cast<const double2*>(pool + e * kNSP);
 #pragma unroll
-        for (int q = 0; q < NS; ++q) v[u][q] = mine ? pool[q * pool_cap + e] : 0.0;
+        for (int q = 0; q < kNSP / 2; ++q) {
+          const double2 x = mine ? __ldcg(src + q) : make_double2(0.0, 0.0);
+          v[u][2 * q] = x.x;
+          if (2 * q + 1 < NS) v[u][2 * q + 1] = x.y;
+        }
       }
 #pragma unroll
       for (int u = 0; u < 2; ++u)
@@ -740,10 +870,14 @@ __global__ void __launch_bounds__(256)
 
 size_t main_smem_bytes(int kcap) { return warp_smem_bytes(kcap) * kSpWarps; }
 
-int reduce_ranges(int kcap, int ntiles, int sm_count) {
+int reduce_ranges(int kcap, int nunits, int sm_count) {
+  // enough CTAs to fill the device, and at most ~512 units per CTA (64 per
+  // warp: the scan over units is a chain of dependent loads)
   const int kw = (kcap + 31) / 32;
   int R = (2 * sm_count + kw - 1) / kw;
-  const int maxr = (ntiles + 7) / 8;  // at least a few tiles per warp
+  const int r2 = (nunits + 511) / 512;
+  if (R < r2) R = r2;
+  const int maxr = (nunits + 63) / 64;  // at least 8 units per warp
   if (R > maxr) R = maxr;
   return R < 1 ? 1 : R;
 }
@@ -758,7 +892,22 @@ bool sparse_supported(int k0, int ntiles) {
 
 int sparse_blocks(int ntiles) { return (ntiles + kBlkTiles - 1) / kBlkTiles; }
 
-int sparse_ranges(int k0, int ntiles, int sm_count) { return reduce_ranges(k0, ntiles, sm_count); }
+int sparse_items(int ntiles) { return ntiles * kItemsPerTile; }
+
+// points per work unit: one item (32 points) while the cloud has few tiles per
+// warp (balance, tight boxes), whole tiles when there are plenty (4x fewer
+// per-unit statistics records to write and reduce)
+int sparse_unit_items(int ntiles, int sm_count) {
+  const int warps = sm_count * kSpWarps * kSpMinBlocks;
+  const int nitems = sparse_items(ntiles);
+  if (nitems >= 64 * warps) return 4;
+  if (nitems >= 32 * warps) return 2;
+  return 1;
+}
+
+int sparse_ranges(int k0, int ntiles, int sm_count) {
+  return reduce_ranges(k0, sparse_items(ntiles) / sparse_unit_items(ntiles, sm_count), sm_count);
+}
 
 cudaError_t launch_sparse_layout(const PointsDev& pts, const SparseScratch& sp, cudaStream_t s) {
   const int nblk = sparse_blocks(pts.ntiles);
@@ -771,7 +920,9 @@ cudaError_t launch_estep_sparse(const PointsDev& pts, const ModelBuf* bufs, cons
                                 int sm_count, cudaStream_t s, int* ncl_out,
                                 const SparseScratch& sp) {
   const int ntiles = pts.ntiles;
-  const int R = reduce_ranges(k0, ntiles, sm_count);
+  const int U = sparse_unit_items(ntiles, sm_count);
+  const int nitems = sparse_items(ntiles) / U;  // work units
+  const int R = reduce_ranges(k0, nitems, sm_count);
   *ncl_out = R;
   if (!partials) return cudaSuccess;
   const int nblk = sparse_blocks(ntiles);
@@ -793,7 +944,7 @@ cudaError_t launch_estep_sparse(const PointsDev& pts, const ModelBuf* bufs, cons
       fprintf(stderr, "gmmb: estep_sparse D=%d K=%d smem=%zu -> %d CTAs/SM\n", pts.d, k0, smem, occ);
   }
   int grid = sm_count * occ;
-  const int need = (ntiles + kSpWarps - 1) / kSpWarps;
+  const int need = (nitems + kSpWarps - 1) / kSpWarps;
   if (grid > need) grid = need;
   static const float qcut = [] {
     const char* e = getenv("GMMB_SPARSE_QCUT");
@@ -805,18 +956,25 @@ cudaError_t launch_estep_sparse(const PointsDev& pts, const ModelBuf* bufs, cons
   else
     block_cand_kernel<3><<<nblk, 256, 0, s>>>(sp.bc, sp.bh, bufs[0], bufs[1], st, k0, sp.blist,
                                               sp.bcnt, sp.ctl, qcut);
-  kern<<<grid, kSpWarps * 32, smem, s>>>(pts.xt, pts.tc, pts.n, ntiles, bufs[0], bufs[1], st, k0,
+  kern<<<grid, kSpWarps * 32, smem, s>>>(pts.xt, pts.tc, pts.n, nitems, bufs[0], bufs[1], st, k0,
                                          sp.blist, sp.bcnt, sp.ctl, sp.pool, sp.pool_cap, sp.toff,
-                                         sp.maskT, sp.preT, sp.ll_tile, exact_mode, qcut);
+                                         sp.maskT, sp.preT, sp.ll_tile, sp.heavy, sp.done,
+                                         exact_mode, qcut, U);
   if (pts.d == 4)
     sparse_reduce_kernel<4><<<kw * R, 256, 0, s>>>(sp.maskT, sp.preT, sp.toff, sp.pool, sp.pool_cap,
-                                                   sp.ll_tile, ntiles, kw, R, k0, st, partials,
+                                                   sp.ll_tile, nitems, kw, R, k0, st, partials,
                                                    ll_part);
   else
     sparse_reduce_kernel<3><<<kw * R, 256, 0, s>>>(sp.maskT, sp.preT, sp.toff, sp.pool, sp.pool_cap,
-                                                   sp.ll_tile, ntiles, kw, R, k0, st, partials,
+                                                   sp.ll_tile, nitems, kw, R, k0, st, partials,
                                                    ll_part);
   return cudaGetLastError();
 }
 
 }  // namespace gmmb
+
+#ifdef GMMB_SP_PROF
+extern "C" int gmmb_debug_sp_prof(unsigned long long* out, int count) {
+  return static_cast<int>(cudaMemcpyFromSymbol(out, gmmb::g_sp_prof, sizeof(unsigned long long) * count));
+}
+#endif
