@@ -31,7 +31,9 @@
 // One cooperative persistent launch: a CTA per SM owns a contiguous range of
 // tiles; rounds end with a grid exchange of per-CTA (clock, index, sum d2)
 // slots (arrival counter + fence), reduced by every CTA in the same order.
+#include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "kinit_kernels.cuh"
 
@@ -75,6 +77,52 @@ __device__ __forceinline__ void ld_ll6(const uint2* p, unsigned tag, unsigned (&
       ok = ok && t0 == tag && t1 == tag;
     }
   } while (!ok);
+}
+
+
+// Every slot of the exchange (4 LL words: clock, index, FP32 sum of d2):
+// lane l owns slots l, l + 32, ... (up to 5); each attempt issues the
+// 16-byte loads of all its not-yet-seen slots back to back and checks every
+// tag (one L2 round trip per attempt, not one per slot).
+constexpr int kPollSlots = 5;  // nblk <= 160 (one CTA per SM)
+__device__ __forceinline__ void poll_slots(const uint2* base, unsigned tag, int nblk, int lane,
+                                           double& gc, long long& gi, double& gs) {
+  unsigned v[kPollSlots][4];
+  unsigned pending = 0;
+#pragma unroll
+  for (int q = 0; q < kPollSlots; ++q)
+    if (lane + 32 * q < nblk) pending |= 1u << q;
+  while (pending) {
+#pragma unroll
+    for (int q = 0; q < kPollSlots; ++q) {
+      if (!((pending >> q) & 1u)) continue;
+      const uint2* p = base + (lane + 32 * q) * 8;
+      bool ok = true;
+#pragma unroll
+      for (int i = 0; i < 4; i += 2) {
+        unsigned t0, t1;
+        asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v[q][i]), "=r"(t0), "=r"(v[q][i + 1]), "=r"(t1)
+                     : "l"(p + i)
+                     : "memory");
+        ok = ok && t0 == tag && t1 == tag;
+      }
+      if (ok) pending &= ~(1u << q);
+    }
+    if (pending) __nanosleep(32);  // ease the pressure on the slot lines
+  }
+#pragma unroll
+  for (int q = 0; q < kPollSlots; ++q) {
+    if (lane + 32 * q >= nblk) continue;
+    const double c2 = __longlong_as_double(
+        static_cast<long long>((static_cast<unsigned long long>(v[q][1]) << 32) | v[q][0]));
+    const long long i2 = static_cast<long long>(static_cast<int>(v[q][2]));
+    gs += static_cast<double>(__uint_as_float(v[q][3]));
+    if (better(c2, i2, gc, gi)) {
+      gc = c2;
+      gi = i2;
+    }
+  }
 }
 
 __device__ __forceinline__ double dist2_t(const double (&x)[4], const double (&c)[4]) {
@@ -352,29 +400,17 @@ __global__ void __launch_bounds__(kTileKppThreads, 1)
         const double csum = __shfl_sync(0xffffffffu, cta_sum, 0);
         bc = __shfl_sync(0xffffffffu, bc, 0);
         bi = __shfl_sync(0xffffffffu, bi, 0);
-        if (lane < 6) {
-          const unsigned long long w[3] = {static_cast<unsigned long long>(__double_as_longlong(bc)),
-                                           static_cast<unsigned long long>(bi),
-                                           static_cast<unsigned long long>(__double_as_longlong(csum))};
-          const unsigned long long v = w[lane >> 1];
-          st_ll_t(base + blockIdx.x * 8 + lane, (lane & 1) ? static_cast<unsigned>(v >> 32)
-                                                         : static_cast<unsigned>(v), tag);
+        if (lane < 4) {  // slot: clock (2 words), index, sum of d2 (FP32)
+          const unsigned long long cb = static_cast<unsigned long long>(__double_as_longlong(bc));
+          const unsigned w = lane == 0 ? static_cast<unsigned>(cb)
+                           : lane == 1 ? static_cast<unsigned>(cb >> 32)
+                           : lane == 2 ? static_cast<unsigned>(static_cast<int>(bi))
+                                       : __float_as_uint(static_cast<float>(csum));
+          st_ll_t(base + blockIdx.x * 8 + lane, w, tag);
         }
         double gc = INFINITY, gs = 0.0;
         long long gi = -1;
-        for (int b = lane; b < nblk; b += 32) {
-          unsigned v[6];
-          ld_ll6(base + b * 8, tag, v);
-          const double c2 = __longlong_as_double(static_cast<long long>(
-              (static_cast<unsigned long long>(v[1]) << 32) | v[0]));
-          const long long i2 = static_cast<long long>((static_cast<unsigned long long>(v[3]) << 32) | v[2]);
-          gs += __longlong_as_double(static_cast<long long>(
-              (static_cast<unsigned long long>(v[5]) << 32) | v[4]));
-          if (better(c2, i2, gc, gi)) {
-            gc = c2;
-            gi = i2;
-          }
-        }
+        poll_slots(base, tag, nblk, lane, gc, gi, gs);
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) {
           const double c2 = __shfl_xor_sync(0xffffffffu, gc, off);
@@ -439,6 +475,444 @@ __global__ void __launch_bounds__(kTileKppThreads, 1)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Warp-specialised variant: warp 0 runs the grid exchange of round r while
+// warps 1..31 already draw round r + 1 for every point and keep its
+// candidates (speculative: thresholds from the tiles' largest d2 BEFORE
+// centre r is folded, which can only be larger than after, and tau from the
+// last known sum of d2), so the draws hide behind the exchange. After the
+// exchange the compute warps fold centre r and evaluate only the kept
+// candidates; the exact-winner test (best clock < tau) is unchanged.
+// Rounds 0 and 1, and a round whose test fails, are drawn synchronously.
+// ---------------------------------------------------------------------------
+#ifdef GMMB_KPP_TPROF
+// per exchange (first 4096) and CTA: publish time, all-slots-seen time, and
+// the compute warps' draw-done time (ns, globaltimer)
+__device__ unsigned long long g_tprof[6][4096][160];  // + round start, fold end, nfold
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+constexpr int kWsCompute = kTileKppThreads - 32;  // compute threads (warps 1..31)
+constexpr int kWsCWarps = kWsCompute / 32;
+constexpr int kCandCap = 1024;                    // kept candidates per CTA and round
+constexpr double kSpecAlpha = 16.0;
+
+// Dynamic shared memory of the warp-specialised kernel, for mt tiles per CTA:
+// tile state | thresholds | fold list | kept candidates | as many of the
+// CTA's keys as fit (the rest stay in global memory). Keeping the keys
+// on-chip takes the per-round stream of draws off L2, where it would slow
+// the grid exchange it runs beside.
+struct WsLayout {
+  TileSmem* tsm;
+  unsigned* thr;
+  int* fold;
+  int* cand_j;
+  double* cand_nl;   // -ln u (FP64, as the reference)
+  uint64_t* keys;
+};
+__host__ __device__ inline size_t ws_fixed_bytes(int mt) {
+  return (sizeof(TileSmem) * mt + sizeof(unsigned) * mt + sizeof(int) * mt + 15) / 16 * 16 +
+         (sizeof(int) + sizeof(double)) * kCandCap;
+}
+__device__ inline WsLayout ws_layout(unsigned char* base, int mt) {
+  WsLayout l;
+  l.tsm = reinterpret_cast<TileSmem*>(base);
+  l.thr = reinterpret_cast<unsigned*>(l.tsm + mt);
+  l.fold = reinterpret_cast<int*>(l.thr + mt);
+  unsigned char* q = base + (sizeof(TileSmem) * mt + sizeof(unsigned) * mt + sizeof(int) * mt + 15) / 16 * 16;
+  l.cand_nl = reinterpret_cast<double*>(q);
+  l.cand_j = reinterpret_cast<int*>(l.cand_nl + kCandCap);
+  l.keys = reinterpret_cast<uint64_t*>(base + ws_fixed_bytes(mt));
+  return l;
+}
+
+__device__ __forceinline__ void bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(kTileKppThreads, 1)
+    kpp_tile_ws_kernel(const double* __restrict__ x64, int64_t n, int ntiles, int k, uint64_t seed,
+                       KppTileScratch ts, KinitScratch scr, int mt, int kcache) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const WsLayout sm = ws_layout(smem_raw, mt);
+  __shared__ double s_bc[kWsCWarps];
+  __shared__ long long s_bi[kWsCWarps];
+  __shared__ double s_delta[kWsCWarps];
+  __shared__ double s_cta_sum, s_tau, s_gsum;
+  __shared__ long long s_win;
+  __shared__ int s_nfold, s_ncand, s_cover;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nblk = gridDim.x;
+  // CTA b owns tiles b, b + nblk, b + 2 nblk, ...: a new centre's
+  // neighbourhood (consecutive Morton tiles) is folded by many CTAs, not one
+  const int b0 = blockIdx.x;
+  const int nt = ntiles > b0 ? (ntiles - 1 - b0) / nblk + 1 : 0;
+  auto gtile = [&](int q) { return b0 + q * nblk; };
+  for (int q = tid; q < nt; q += kTileKppThreads) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sm.tsm[q].box[j] = ts.tbox[static_cast<int64_t>(gtile(q)) * 8 + j];
+    sm.tsm[q].dmax = INFINITY;
+    sm.tsm[q].sum = 0.0;
+  }
+  if (tid == 0) {
+    s_nfold = 0;
+    s_ncand = 0;
+    s_cover = 0;
+    s_cta_sum = 0.0;
+  }
+  // CTA point j: offset j % 128 of tile j / 128 (the last tile may be short)
+  auto gidx = [&](int j) -> int64_t {
+    return static_cast<int64_t>(gtile(j >> 7)) * kTile + (j & (kTile - 1));
+  };
+  const int np = nt * kTile;
+  const int ncache = np < kcache ? np : kcache;
+  for (int j = tid; j < ncache; j += kTileKppThreads) {
+    const int64_t i = gidx(j);
+    sm.keys[j] = i < n ? ts.mkey[i] : 0ull;
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ======================= communication warp =======================
+    unsigned xchg = 0;
+    for (int r = 0; r < k;) {
+      bar_sync(2, kTileKppThreads);  // the compute warps' bests of this attempt
+      double bc = INFINITY;
+      long long bi = -1;
+      if (lane < kWsCWarps) {
+        bc = s_bc[lane];
+        bi = s_bi[lane];
+      }
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) {
+        const double c2 = __shfl_xor_sync(0xffffffffu, bc, off);
+        const long long i2 = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (better(c2, i2, bc, bi)) {
+          bc = c2;
+          bi = i2;
+        }
+      }
+      const double tau = s_tau;
+      const double csum = s_cta_sum;
+      const unsigned tag = xchg + 1u;
+#ifdef GMMB_KPP_TPROF
+      if (lane == 0 && xchg < 4096 && blockIdx.x < 160) g_tprof[0][xchg][blockIdx.x] = gtime();
+#endif
+      uint2* base = reinterpret_cast<uint2*>(scr.slots) + static_cast<size_t>(xchg & 1) * nblk * 8;
+      if (lane < 4) {  // slot: clock (2 words), index, sum of d2 (FP32)
+        const unsigned long long cb = static_cast<unsigned long long>(__double_as_longlong(bc));
+        const unsigned w = lane == 0 ? static_cast<unsigned>(cb)
+                         : lane == 1 ? static_cast<unsigned>(cb >> 32)
+                         : lane == 2 ? static_cast<unsigned>(static_cast<int>(bi))
+                                     : __float_as_uint(static_cast<float>(csum));
+        st_ll_t(base + blockIdx.x * 8 + lane, w, tag);
+      }
+      double gc = INFINITY, gs = 0.0;
+      long long gi = -1;
+      poll_slots(base, tag, nblk, lane, gc, gi, gs);
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) {
+        const double c2 = __shfl_xor_sync(0xffffffffu, gc, off);
+        const long long i2 = __shfl_xor_sync(0xffffffffu, gi, off);
+        gs += __shfl_xor_sync(0xffffffffu, gs, off);
+        if (better(c2, i2, gc, gi)) {
+          gc = c2;
+          gi = i2;
+        }
+      }
+#ifdef GMMB_KPP_TPROF
+      if (lane == 0 && xchg < 4096 && blockIdx.x < 160) g_tprof[1][xchg][blockIdx.x] = gtime();
+#endif
+      ++xchg;
+      long long win = -1;
+      if (gi >= 0 && gc < tau * (1.0 - 1e-12)) {
+        win = gi;
+      } else if (tau == INFINITY) {
+        // sogmm.cpp:276-284: no point with d2 > 0: the lowest unchosen
+        // index among 0 .. r (CTA 0 fenced its centre stores)
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        long long lo = LLONG_MAX;
+        for (long long cnd = lane; cnd <= r && cnd < n; cnd += 32) {
+          bool taken = false;
+          for (int q = 0; q < r && !taken; ++q) taken = __ldcg(scr.centers + q) == cnd;
+          if (!taken && cnd < lo) lo = cnd;
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+          const long long u2 = __shfl_xor_sync(0xffffffffu, lo, off);
+          lo = u2 < lo ? u2 : lo;
+        }
+        win = lo;
+      }
+      if (lane == 0) {
+        s_win = win;  // -1: repeat the round with a larger tau
+        s_gsum = gs;
+        if (win >= 0 && blockIdx.x == 0) {
+          scr.centers[r] = win;
+          __threadfence();
+          if (r == k - 1) *reinterpret_cast<unsigned long long*>(scr.status + 2) = xchg;
+        }
+      }
+      __syncwarp();
+      bar_arrive(3, kTileKppThreads);
+      if (win >= 0) ++r;
+    }
+    return;
+  }
+
+  // ========================= compute warps =========================
+  const int ct = tid - 32, cw = warp - 1;
+  const uint64_t* __restrict__ kp = ts.mkey;
+  double c[4] = {0, 0, 0, 0};
+  double gsum = INFINITY;   // last known global sum of d2
+  double cta_sum = 0.0;     // (ct == 0)
+  bool spec = false;        // candidates of this round were kept during the last exchange
+  double tau_kept = 0.0;    // the tau they were drawn with
+  // best (clock, index) of this thread over the candidates it evaluates
+  double bc;
+  long long bi;
+  auto eval = [&](int j, uint64_t bits, int r) {
+    const int64_t i = gidx(j);
+    const double nl = nlu_exact_t(bits);
+    double clk = nl;
+    if (r > 0) {
+      const double d2 = ts.md2[i];
+      if (!(d2 > 0.0)) return;
+      clk = nl / d2;
+    }
+    const long long oi = ts.perm[i];
+    if (better(clk, oi, bc, bi)) {
+      bc = clk;
+      bi = oi;
+    }
+  };
+  // a kept candidate of round r >= 2: its -ln u was computed while drawing
+  auto eval_nl = [&](int j, double nl) {
+    const int64_t i = gidx(j);
+    const double d2 = ts.md2[i];
+    if (!(d2 > 0.0)) return;
+    const double clk = nl / d2;
+    const long long oi = ts.perm[i];
+    if (better(clk, oi, bc, bi)) {
+      bc = clk;
+      bi = oi;
+    }
+  };
+  // per-tile thresholds on the draw's top 32 bits for (tau, r)
+  auto thresholds = [&](double tau, int r) {
+    for (int q = ct; q < nt; q += kWsCompute) {
+      const double dmax = r == 0 ? 1.0 : sm.tsm[q].dmax;
+      unsigned th = 0xffffffffu;
+      if (dmax > 0.0) {
+        const double e = exp(-tau * dmax) * (1.0 - 1e-12);
+        th = e > 0.0 ? static_cast<unsigned>(fmin(e * 4294967296.0, 4294967295.0)) : 0u;
+      }
+      sm.thr[q] = th;
+    }
+    bar_sync(1, kWsCompute);
+  };
+  // draw round r for every point: KEEP = 0 evaluates the candidates, 1 keeps them
+  // draw round r for every point. keep = false (rounds drawn after their
+  // exchange: 0, 1, 2, repeats): candidates are evaluated on the spot.
+  // keep = true (the next round, behind the exchange): a warp per tile, the
+  // tile's threshold uniform, four points per lane; the rare candidates are
+  // only appended to the kept list (draw bits), their -ln u comes after.
+  auto draw = [&](int r, bool keep) {
+    const uint64_t pre = round_prefix_t(seed, r);
+    if (keep) {
+      for (int q = cw; q < nt; q += kWsCWarps) {
+        const unsigned th = sm.thr[q];
+        const int jb = q * kTile;
+        uint64_t kv[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int jj = jb + lane + 32 * h;
+          kv[h] = jj < ncache ? sm.keys[jj] : 0ull;
+        }
+        if (jb + kTile > ncache) {  // keys beyond the on-chip cache
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const int jj = jb + lane + 32 * h;
+            const int64_t ii = gidx(jj);
+            if (jj >= ncache && ii < n) kv[h] = __ldg(kp + ii);
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const uint64_t bits = mix64(pre + kv[h]);
+          if (static_cast<unsigned>(bits >> 32) >= th) {
+            const int jj = jb + lane + 32 * h;
+            if (gidx(jj) < n) {
+              const int slot = atomicAdd(&s_ncand, 1);
+              if (slot < kCandCap) {
+                sm.cand_j[slot] = jj;
+                sm.cand_nl[slot] = __longlong_as_double(static_cast<long long>(bits));
+              } else {
+                s_cover = 1;
+              }
+            }
+          }
+        }
+      }
+      bar_sync(1, kWsCompute);
+      const int nc = s_ncand < kCandCap ? s_ncand : kCandCap;
+      for (int q = ct; q < nc; q += kWsCompute)
+        sm.cand_nl[q] = nlu_exact_t(static_cast<uint64_t>(__double_as_longlong(sm.cand_nl[q])));
+      return;
+    }
+    for (int j = ct; j < np; j += kWsCompute) {
+      const int64_t ii = gidx(j);
+      if (ii >= n) continue;
+      const uint64_t bits = mix64(pre + (j < ncache ? sm.keys[j] : __ldg(kp + ii)));
+      if (static_cast<unsigned>(bits >> 32) >= sm.thr[j >> 7]) eval(j, bits, r);
+    }
+  };
+  auto publish_best = [&](double tau) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      const double c2 = __shfl_xor_sync(0xffffffffu, bc, off);
+      const long long i2 = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (better(c2, i2, bc, bi)) {
+        bc = c2;
+        bi = i2;
+      }
+    }
+    if (lane == 0) {
+      s_bc[cw] = bc;
+      s_bi[cw] = bi;
+    }
+    if (ct == 0) {
+      s_tau = tau;
+      s_cta_sum = cta_sum;
+    }
+    bar_arrive(2, kTileKppThreads);
+  };
+
+  for (int r = 0; r <= k; ++r) {
+#ifdef GMMB_KPP_TPROF
+    if (ct == 0 && r < 4096 && blockIdx.x < 160) g_tprof[3][r][blockIdx.x] = gtime();
+#endif
+    // ---- fold centre r - 1: box tests by threads, listed tiles by warps
+    if (r > 0) {
+      for (int q = ct; q < nt; q += kWsCompute) {
+        const TileSmem& tt = sm.tsm[q];
+        double lb = 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double g = fmax(fmax(tt.box[j] - c[j], c[j] - tt.box[4 + j]), 0.0);
+          lb = fma(g, g, lb);
+        }
+        if (!(lb * (1.0 - 1e-12) >= tt.dmax)) sm.fold[atomicAdd(&s_nfold, 1)] = q;
+      }
+      bar_sync(1, kWsCompute);
+      const int nf = s_nfold;
+      double delta = 0.0;
+      for (int f = cw; f < nf; f += kWsCWarps) {
+        const int q = sm.fold[f];
+        TileSmem& tt = sm.tsm[q];
+        const int64_t ib = static_cast<int64_t>(gtile(q)) * kTile;
+        double mx = 0.0, smv = 0.0;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int64_t i = ib + lane + 32 * h;
+          if (i < n) {
+            double x[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) x[j] = ts.xm[j * n + i];
+            const double dd = dist2_t(x, c);
+            double d2 = ts.md2[i];
+            if (dd < d2) {
+              d2 = dd;
+              ts.md2[i] = dd;
+              ts.mlab[i] = r - 1;
+            }
+            mx = fmax(mx, d2);
+            smv += d2;
+          }
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+          mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+          smv += __shfl_xor_sync(0xffffffffu, smv, off);
+        }
+        if (lane == 0) {
+          tt.dmax = mx;
+          delta += smv - tt.sum;
+          tt.sum = smv;
+        }
+      }
+      if (lane == 0) s_delta[cw] = delta;
+      bar_sync(1, kWsCompute);
+      if (ct == 0) {
+        for (int w = 0; w < kWsCWarps; ++w) cta_sum += s_delta[w];
+#ifdef GMMB_KPP_TPROF
+        if (r < 4096 && blockIdx.x < 160) {
+          g_tprof[4][r][blockIdx.x] = gtime();
+          g_tprof[5][r][blockIdx.x] = s_nfold;
+        }
+#endif
+        s_nfold = 0;
+      }
+    }
+    if (r == k) break;
+    // ---- round r: evaluate the kept candidates, or draw now
+    double tau = r == 0 ? kTauAlpha / static_cast<double>(n)
+                        : (isfinite(gsum) && gsum > 0.0 ? kTauAlpha / gsum : INFINITY);
+    bool first = true;
+    bool spec_next = false;
+    double tau_next = 0.0;
+    for (;;) {
+      bc = INFINITY;
+      bi = -1;
+      if (first && spec) {
+        tau = tau_kept;  // the kept candidates were drawn with it
+        const int nc = s_ncand;
+        for (int q = ct; q < nc; q += kWsCompute) eval_nl(sm.cand_j[q], sm.cand_nl[q]);
+      } else {
+        thresholds(tau, r);
+        draw(r, false);
+      }
+      publish_best(tau);
+      // ---- meanwhile: keep round r + 1's candidates (first attempt only)
+      bool kept = false;
+      if (first && r + 1 < k && r >= 1 && isfinite(gsum) && gsum > 0.0) {
+        bar_sync(1, kWsCompute);  // kept list consumed; s_tau published
+        if (ct == 0) {
+          s_ncand = 0;
+          s_cover = 0;
+        }
+        tau_next = kSpecAlpha / gsum;
+        thresholds(tau_next, r + 1);  // (its barrier orders the reset before the draws)
+        draw(r + 1, true);
+        kept = true;
+#ifdef GMMB_KPP_TPROF
+        bar_sync(1, kWsCompute);
+        if (ct == 0 && r < 4096 && blockIdx.x < 160) g_tprof[2][r][blockIdx.x] = gtime();
+#endif
+      }
+      bar_sync(3, kTileKppThreads);  // the exchange result (and every kept candidate)
+      const long long win = s_win;
+      gsum = s_gsum;
+      if (kept) spec_next = s_cover == 0;
+      if (win >= 0) {
+        spec = spec_next;
+        tau_kept = tau_next;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[j] = x64[j * n + win];
+        break;
+      }
+      first = false;
+      tau = tau * 64.0 > 1e300 ? INFINITY : tau * 64.0;
+    }
+  }
+}
 }  // namespace
 
 bool kpp_tile_wanted(int64_t n, int sm_count) {
@@ -462,22 +936,46 @@ cudaError_t launch_kpp_tile(const double* x64, int64_t n, int ntiles, const int3
   if (e != cudaSuccess) return e;
   int nblk = sm_count;  // one CTA per SM
   if (nblk > ntiles) nblk = ntiles;
-  if ((ntiles + nblk - 1) / nblk > kMaxCtaTiles) return cudaErrorInvalidValue;
-  const size_t smem = sizeof(TileSmem) * kMaxCtaTiles + sizeof(unsigned) * kMaxCtaTiles;
-  e = cudaFuncSetAttribute(kpp_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(smem));
+  if ((ntiles + nblk - 1) / nblk > kMaxCtaTiles || nblk > 32 * kPollSlots) return cudaErrorInvalidValue;
+  // GMMB_KPP_TILE=sync: the single-role kernel (every round drawn after its exchange)
+  static const bool ws = [] {
+    const char* v = getenv("GMMB_KPP_TILE");
+    return !(v && v[0] == 's');
+  }();
+  const void* fn = ws ? (const void*)kpp_tile_ws_kernel : (const void*)kpp_tile_kernel;
+  int mt = (ntiles + nblk - 1) / nblk;
+  int max_smem = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t statics = 2048;  // the kernels' static shared words
+  int kcache = 0;
+  size_t smem = sizeof(TileSmem) * kMaxCtaTiles + sizeof(unsigned) * kMaxCtaTiles;
+  if (ws) {
+    const size_t fixed = ws_fixed_bytes(mt);
+    const size_t avail = static_cast<size_t>(max_smem) > fixed + statics ? max_smem - fixed - statics : 0;
+    kcache = static_cast<int>(std::min<size_t>(avail / sizeof(uint64_t), static_cast<size_t>(mt) * kTile));
+    smem = fixed + sizeof(uint64_t) * kcache;
+  }
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kpp_tile_kernel, kTileKppThreads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kTileKppThreads, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorLaunchOutOfResources;
+  void* args_ws[] = {(void*)&x64, (void*)&n, (void*)&ntiles, (void*)&k, (void*)&seed,
+                     (void*)&ts, (void*)&scr, (void*)&mt, (void*)&kcache};
   void* args[] = {(void*)&x64, (void*)&n, (void*)&ntiles, (void*)&k, (void*)&seed,
                   (void*)&ts, (void*)&scr, (void*)&arrive};
-  e = cudaLaunchCooperativeKernel((const void*)kpp_tile_kernel, dim3(nblk), dim3(kTileKppThreads),
-                                  args, smem, s);
+  e = cudaLaunchCooperativeKernel(fn, dim3(nblk), dim3(kTileKppThreads), ws ? args_ws : args, smem, s);
   if (e != cudaSuccess) return e;
   kpp_tile_scatter_kernel<<<grid, 256, 0, s>>>(n, perm, ts.mlab, scr.labels, scr.owned);
   return cudaGetLastError();
 }
 
 }  // namespace gmmb
+
+#ifdef GMMB_KPP_TPROF
+extern "C" int gmmb_debug_kpp_tprof(unsigned long long* out) {
+  return static_cast<int>(cudaMemcpyFromSymbol(out, gmmb::g_tprof, sizeof(gmmb::g_tprof)));
+}
+#endif
