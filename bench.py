@@ -48,9 +48,9 @@ UNIT = "point*component*iter/s"
 FLOP_PER_UNIT = {4: 62.0, 3: 42.0}     # 2D^2 + 6D + 6
 NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 # DRAM traffic per launch of the dominant kernel, from ncu --set full
-# captures of exactly these configurations (emitted only when the run's
-# configuration matches the capture; re-captured on every kernel change).
-TRAFFIC = {("cfg2", 512): (5.095e6, "profiles/r1h_estep_ncu.txt")}
+# captures of exactly these configurations and kernels (emitted only when the
+# run matches the capture; re-captured on every kernel change).
+TRAFFIC = {}
 
 
 def parse():
@@ -450,26 +450,47 @@ def main():
     # are repeated in timing mode (chunked launches, CUDA events on the
     # library stream around every fused E kernel; identical kernels and
     # results). Sharded fits always run chunked, so their pass above has them.
-    if sharded or vshard:
-        est_ms = sum(r.ms_estep for r in res)
-        est_units = float(n if sharded else -(-full_n // args.vshard)) * kk * sum(iters)
-        est_launches = sum(iters)
-    else:
-        ctx.upload(pts)
+    # The E step evaluates only the (point, component) pairs whose FP32
+    # density can be non-zero (exact-zero pruning, estep_sparse.cu): the
+    # roofline is taken on the pairs it evaluated (units_evaluated); the
+    # dense-equivalent rate and the dense kernels' own fraction (same fits,
+    # GMMB dense mode) are reported beside it.
+    def timed_estep(dense):
+        ctx.set_estep_mode(dense)
         ctx.set_timing(True)
-        est_ms, est_units, est_launches = 0.0, 0.0, 0
-        for _ in range(args.steps):
+        ms, units_, ev, launches = 0.0, 0.0, 0.0, 0
+        for _ in range(args.steps if not dense else max(2, args.steps // 4)):
             flush_l2(flush)
             torch.cuda.synchronize()
             rt = ctx.fit_k_resident(args.k, em)
-            est_ms += rt.ms_estep
-            est_units += rt.units
-            est_launches += rt.em_iterations
+            ms += rt.ms_estep
+            units_ += rt.units
+            ev += rt.units_evaluated
+            launches += rt.em_iterations
         ctx.set_timing(False)
+        ctx.set_estep_mode(False)
+        return ms, units_, ev, launches
+
+    dense_cmp = None
+    if sharded or vshard:
+        est_ms = sum(r.ms_estep for r in res)
+        est_units = float(n if sharded else -(-full_n // args.vshard)) * kk * sum(iters)
+        est_eval = sum(r.units_evaluated for r in res) * (est_units / max(units, 1.0))
+        est_launches = sum(iters)
+    else:
+        ctx.upload(pts)
+        est_ms, est_units, est_eval, est_launches = timed_estep(False)
+        d_ms, d_units, _, d_launches = timed_estep(True)
+        dense_cmp = (d_ms, d_units, d_launches)
     peak_tf, _ = ctx.ffma_peak(50.0)
-    achieved_tf = FLOP_PER_UNIT[d] * est_units / (est_ms * 1e-3) / 1e12
-    tr = TRAFFIC.get((args.config, kk)) if world == 1 and not vshard else None
-    kernel = ("estep_ws_kernel (warp-specialised fused E step + sufficient statistics)"
+    pruned = est_eval < est_units
+    achieved_tf = FLOP_PER_UNIT[d] * est_eval / (est_ms * 1e-3) / 1e12
+    dense_equiv_tf = FLOP_PER_UNIT[d] * est_units / (est_ms * 1e-3) / 1e12
+    tr = (TRAFFIC.get((args.config, kk, "sparse" if pruned else "dense"))
+          if world == 1 and not vshard else None)
+    kernel = ("E step = block_cand_kernel + estep_sparse_kernel (exact-zero-pruned fused E "
+              "step + sufficient statistics) + sparse_reduce_kernel" if pruned else
+              "estep_ws_kernel (warp-specialised fused E step + sufficient statistics)"
               if kk <= 512 else "fused E step + sufficient statistics (K > 512 path)")
 
     line = {
@@ -496,8 +517,20 @@ def main():
         "roofline": {"bound": "fp32", "kernel": kernel, "achieved": achieved_tf,
                      "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
                      "flop_per_unit": FLOP_PER_UNIT[d],
-                     "timing": "CUDA events around each fused E launch on the library stream, "
-                               "%d launches over the same %d fits" % (est_launches, args.steps),
+                     "units_evaluated_fraction": est_eval / max(est_units, 1.0),
+                     "achieved_note": ("FLOP of the (point, component) pairs the pruned E step "
+                                       "evaluated (the skipped pairs have FP32 density exactly 0) "
+                                       "over the E-step time" if pruned else
+                                       "FLOP of every (point, component) pair over the E time"),
+                     "dense_equivalent_tflops": dense_equiv_tf,
+                     "dense_kernels": ({"us_per_iteration": 1e3 * dense_cmp[0] / max(dense_cmp[2], 1),
+                                        "tflops": FLOP_PER_UNIT[d] * dense_cmp[1]
+                                        / (dense_cmp[0] * 1e-3) / 1e12,
+                                        "frac": FLOP_PER_UNIT[d] * dense_cmp[1]
+                                        / (dense_cmp[0] * 1e-3) / 1e12 / peak_tf}
+                                       if dense_cmp else None),
+                     "timing": "CUDA events around each E step (all its kernels) on the library "
+                               "stream, %d iterations over %d fits" % (est_launches, args.steps),
                      "peak_source": "measured packed-FP32 (fma.rn.f32x2) microbenchmark in this "
                                     "run (MEASURED_PEAKS.json has no FP32 figure); nominal %.1f"
                                     % NOMINAL_FP32_TFLOPS,
@@ -613,6 +646,7 @@ def run_cfg3(args, gm, torch, dist, rank, world, local):
     ctx.set_timing(False)
     est_ms = sum(r.ms_estep for r in tf)
     est_units = sum(r.units for r in tf)
+    est_eval = sum(r.units_evaluated for r in tf)
     est_launches = sum(r.em_iterations for r in tf)
     if world > 1:
         t = torch.tensor([ms, units, t_e2e, e2e_units, dev_ms], dtype=torch.float64, device="cuda")
@@ -623,7 +657,8 @@ def run_cfg3(args, gm, torch, dist, rank, world, local):
     else:
         ms_job, units_job, t_e2e_job, e2e_units_job = ms, units, t_e2e, e2e_units
     peak_tf, _ = ctx.ffma_peak(50.0)
-    achieved_tf = FLOP_PER_UNIT[4] * est_units / (est_ms * 1e-3) / 1e12
+    achieved_tf = FLOP_PER_UNIT[4] * est_eval / (est_ms * 1e-3) / 1e12
+    pruned = est_eval < est_units
     line = {
         "metric": METRIC, "value": units_job / (ms_job * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_job / steps,
@@ -639,10 +674,14 @@ def run_cfg3(args, gm, torch, dist, rank, world, local):
                 "frames_per_s": args.frames * e2e_steps / t_e2e_job},
         "gpu_launches": int(launches),
         "device_ms_per_step_sum_of_fits": dev_ms / steps,
-        "roofline": {"bound": "fp32", "kernel": "estep_ws_kernel (fused E step + statistics, K=%d)"
-                     % args.k, "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                     "frac": achieved_tf / peak_tf, "flop_per_unit": FLOP_PER_UNIT[4],
-                     "timing": "CUDA events around each fused E launch, %d launches (3 fits of "
+        "roofline": {"bound": "fp32", "kernel": ("pruned E step (block_cand + estep_sparse + "
+                     "sparse_reduce), K=%d" if pruned else "estep_ws_kernel (fused E step + "
+                     "statistics, K=%d)") % args.k, "achieved": achieved_tf, "peak": peak_tf,
+                     "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
+                     "flop_per_unit": FLOP_PER_UNIT[4],
+                     "units_evaluated_fraction": est_eval / max(est_units, 1.0),
+                     "dense_equivalent_tflops": FLOP_PER_UNIT[4] * est_units / (est_ms * 1e-3) / 1e12,
+                     "timing": "CUDA events around each E step, %d iterations (3 fits of "
                                "frame %d in timing mode)" % (est_launches, seeds[0]),
                      "peak_source": "measured packed-FP32 microbenchmark in this run",
                      "traffic": None,

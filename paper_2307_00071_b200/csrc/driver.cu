@@ -149,7 +149,7 @@ struct gmmb_ctx {
   bool sparse_on = false;         // the current EM run uses the pruned E step
   int pool_mult = 1;              // pool growth after an overflow
   DevBuf<double> sp_bc, sp_pool, sp_ll;
-  DevBuf<float4> sp_bh;
+  DevBuf<float4> sp_bh, sp_brec;
   DevBuf<int> sp_blist, sp_bcnt, sp_ctl, sp_toff, sp_heavy;
   DevBuf<unsigned> sp_done;
   DevBuf<unsigned> sp_mask;
@@ -402,7 +402,7 @@ void run_kinit(gmmb_ctx* c, int k, uint64_t seed) {
   const int64_t n = c->n;
   KinitScratch ks = kinit_scratch(c, k);
   ck(cudaMemsetAsync(c->owned.p, 0, sizeof(int) * k, c->s), "memset");
-  if (c->world == 1 && c->kinit_tile && kpp_tile_wanted(n, c->sm_count)) {
+  if (c->world == 1 && c->kinit_tile && (c->kinit_tile == 2 || kpp_tile_wanted(n, c->sm_count))) {
     // beyond the shared-memory-resident kernel: tile-pruned rounds over the
     // layout's Morton tiles (kinit_tile.cu)
     const int ntiles = static_cast<int>((n + kTile - 1) / kTile);
@@ -680,8 +680,10 @@ void ensure_em_buffers(gmmb_ctx* c, int k0, int max_iters) {
     // item on the BASELINE clouds; 32 + K/64 per item (or all K) up front,
     // doubled after an overflow (the EM run is repeated, see run_em)
     const int64_t per_item = std::min<int64_t>(k0, (32 + k0 / 64) * int64_t{c->pool_mult});
-    const int64_t cap = std::max<int64_t>(static_cast<int64_t>(nitems) * per_item, 1024);
+    // fixed slots per unit + a quarter more for units with more candidates
+    const int64_t cap = std::max<int64_t>(static_cast<int64_t>(nitems) * per_item * 5 / 4, 1024);
     c->sp_blist.ensure(static_cast<size_t>(nblk) * k0);
+    c->sp_brec.ensure(static_cast<size_t>(nblk) * k0 * 4);
     c->sp_bcnt.ensure(nblk);
     c->sp_ctl.ensure(16);
     c->sp_heavy.ensure(static_cast<size_t>(2) * nitems);
@@ -696,7 +698,8 @@ void ensure_em_buffers(gmmb_ctx* c, int k0, int max_iters) {
     c->sp_mask.ensure(static_cast<size_t>(kw) * nitems);
     c->sp_pre.ensure(static_cast<size_t>(kw) * nitems);
     c->sp_ll.ensure(nitems);
-    c->sparse = SparseScratch{c->sp_bc.p, c->sp_bh.p, c->sp_blist.p, c->sp_bcnt.p, c->sp_ctl.p,
+    c->sparse = SparseScratch{c->sp_bc.p, c->sp_bh.p, c->sp_blist.p, c->sp_brec.p,
+                              static_cast<int>(per_item), c->sp_bcnt.p, c->sp_ctl.p,
                               c->sp_heavy.p, c->sp_done.p,
                               c->sp_pool.p, static_cast<int64_t>(c->sp_pool.cap / NSP),
                               c->sp_toff.p, c->sp_mask.p, c->sp_pre.p, c->sp_ll.p};
@@ -1183,7 +1186,9 @@ static int create(int device, int rank, int world, const void* id, VGroup* vg,
       const char* m = getenv("GMMB_ESTEP");
       c->estep_mode = (m && std::strcmp(m, "dense") == 0) ? 1 : 0;
       const char* ki = getenv("GMMB_KINIT");
-      c->kinit_tile = (ki && std::strcmp(ki, "mem") == 0) ? 0 : 1;
+      // GMMB_KINIT=mem: memory-resident rounds past the shared-memory kernel;
+      // =tile: the tile-pruned kernel at any size (A/B)
+      c->kinit_tile = (ki && std::strcmp(ki, "mem") == 0) ? 0 : (ki && std::strcmp(ki, "tile") == 0) ? 2 : 1;
     }
     try {
       ck(cudaSetDevice(device), "cudaSetDevice");
@@ -1295,7 +1300,7 @@ void gmmb_ctx_destroy(gmmb_ctx* c) {
   c->sp_bc.release(); c->sp_pool.release(); c->sp_ll.release(); c->sp_bh.release();
   c->sp_blist.release(); c->sp_bcnt.release(); c->sp_ctl.release(); c->sp_toff.release();
   c->sp_mask.release(); c->sp_pre.release(); c->st_bak.release();
-  c->sp_heavy.release(); c->sp_done.release();
+  c->sp_heavy.release(); c->sp_done.release(); c->sp_brec.release();
   for (int b = 0; b < 2; ++b) {
     c->bak_w[b].release(); c->bak_mu[b].release(); c->bak_cov[b].release(); c->bak_cst[b].release();
   }
@@ -1428,7 +1433,7 @@ int gmmb_kinit(gmmb_ctx* c, const double* pts, int64_t n, int d, int k, uint64_t
     upload(c, pts, n, d, 0, n);
     c->have_cloud = false;  // single-step input: not a resident cloud for *_resident fits
     // the tile-pruned seeding (large clouds) runs on the Morton layout
-    if (c->kinit_tile && kpp_tile_wanted(n, c->sm_count))
+    if (c->kinit_tile && (c->kinit_tile == 2 || kpp_tile_wanted(n, c->sm_count)))
       layout(c);
     else
       validate(c);

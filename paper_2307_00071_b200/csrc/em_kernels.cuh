@@ -59,6 +59,8 @@ struct SparseScratch {
   double* bc;            // [nblk][4]
   float4* bh;            // [nblk]
   int* blist;            // [nblk][K]
+  float4* brec;          // [nblk][K][4] candidate bound records (factor, base2, mean - block centre)
+  int item_cap;          // pool entries reserved per 32-point item (overflow region after)
   int* bcnt;             // [nblk]
   int* ctl;              // [16]
   int* heavy;            // [2][nitems] heavy-item lists (iteration parity)

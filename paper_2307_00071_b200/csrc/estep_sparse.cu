@@ -53,9 +53,14 @@ namespace {
 using namespace dev;
 
 #ifdef GMMB_SP_PROF
-__device__ unsigned long long g_sp_prof[4 * 262144];  // per tile: t0, t1, (sm, C), flags
+__device__ unsigned long long g_sp_prof[4 * 262144];  // per unit: t0, t1, (sm, C), flags
+__device__ unsigned g_sp_ph[6 * 262144];             // per unit: phase durations (cycles)
+#define SP_PH(i) unsigned long long ph##i = clock64()
+#else
+#define SP_PH(i)
 #endif
 constexpr int kBlkTiles = 16;     // tiles per culling block
+constexpr int kRedStep = 4;       // units whose statistics the reduce loads together
 constexpr int kItem = 32;         // points per item (one per lane); a work unit is U = 1, 2
 constexpr int kItemsPerTile = kTile / kItem;  // or 4 consecutive items of one layout tile
 constexpr int kSpWarps = 8;       // warps per CTA of the main kernel
@@ -169,8 +174,8 @@ template <int D>
 __global__ void __launch_bounds__(256)
     block_cand_kernel(const double* __restrict__ bc, const float4* __restrict__ bh, ModelBuf b0,
                       ModelBuf b1, const EmState* __restrict__ st, int kcap,
-                      int* __restrict__ blist, int* __restrict__ bcnt, int* __restrict__ ctl,
-                      float qcut) {
+                      int* __restrict__ blist, float4* __restrict__ brec, int* __restrict__ bcnt,
+                      int* __restrict__ ctl, float qcut) {
   __shared__ int wcnt[8];
   __shared__ int s_base;
   if (st->done) return;
@@ -198,11 +203,14 @@ __global__ void __launch_bounds__(256)
   for (int k0 = 0; k0 < k_cur; k0 += 256) {
     const int k = k0 + tid;
     bool cand = false;
+    float4 a0, a1, a2;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
     if (k < k_cur) {
       const float4* c4 = reinterpret_cast<const float4*>(mb.cst + k);
-      const float4 a0 = c4[0], a1 = c4[1], a2 = c4[2];
+      a0 = c4[0];
+      a1 = c4[1];
+      a2 = c4[2];
       const float P[12] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
-      float v[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) v[j] = j < D ? -static_cast<float>(mb.mu[k * 4 + j] - c[j]) : 0.f;
       const float lb = box_lb<D>(P, v, h);
@@ -214,7 +222,17 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     int pre = s_base;
     for (int q = 0; q < w; ++q) pre += wcnt[q];
-    if (cand) blist[static_cast<int64_t>(b) * kcap + pre + __popc(m & lanemask_lt())] = k;
+    if (cand) {
+      // the candidate's id + bound record (factor, base2, mean relative to the
+      // block centre in FP32): the units' filters read these contiguously
+      const int64_t pos = static_cast<int64_t>(b) * kcap + pre + __popc(m & lanemask_lt());
+      blist[pos] = k;
+      float4* rec = brec + pos * 4;
+      rec[0] = a0;
+      rec[1] = a1;
+      rec[2] = a2;
+      rec[3] = make_float4(-v[0], -v[1], -v[2], -v[3]);
+    }
     __syncthreads();
     if (tid == 0) {
       int tot = 0;
@@ -315,7 +333,8 @@ template <int D>
 __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
     estep_sparse_kernel(const float4* __restrict__ xt, const double* __restrict__ tc, int64_t n,
                         int nitems, ModelBuf b0, ModelBuf b1, const EmState* __restrict__ st,
-                        int kcap, const int* __restrict__ blist, const int* __restrict__ bcnt,
+                        int kcap, const int* __restrict__ blist, const float4* __restrict__ brec,
+                        const int* __restrict__ bcnt, const double* __restrict__ bcen, int ucap,
                         int* __restrict__ ctl, double* __restrict__ pool, int64_t pool_cap,
                         int* __restrict__ toff, unsigned* __restrict__ maskT,
                         unsigned short* __restrict__ preT, double* __restrict__ ll_tile,
@@ -368,6 +387,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
     unsigned long long prof_t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof_t0));
 #endif
+    SP_PH(0);
     const int npts = static_cast<int>(min64(U * kItem, n - p0));  // may be <= 0 (padding)
     double ct[4];
 #pragma unroll
@@ -405,10 +425,18 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
       // half-width rounded up (covers the rounding of the centre)
       hw[j] = fmaxf(hi[j] - bcv[j], bcv[j] - lo[j]) * (1.f + 0x1p-20f) + 1e-30f;
     }
+    SP_PH(1);
     // ---- fine candidates (ascending): the block's list filtered by the tile box
     const int blk = t / kBlkTiles;
     const int cb = npts > 0 ? bcnt[blk] : 0;
     const int* bl = blist + static_cast<int64_t>(blk) * kcap;
+    const float4* br = brec + static_cast<int64_t>(blk) * kcap * 4;
+    // box centre relative to the block centre (the records' frame); the
+    // FP32 rounding of the two frames (~1e-7 of the block extent) is far
+    // inside the 8-unit margin of the cut
+    float bcb[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bcb[j] = bcv[j] + static_cast<float>(ct[j] - bcen[blk * 4 + j]);
     int C = 0;
     for (int c0 = 0; c0 < cb; c0 += 32) {
       const int ci = c0 + lane;
@@ -416,13 +444,14 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
       int k = -1;
       if (ci < cb) {
         k = bl[ci];
-        const float4* c4 = reinterpret_cast<const float4*>(mb.cst + k);
-        const float4 a0 = c4[0], a1 = c4[1], a2 = c4[2];
+        const float4* rec = br + static_cast<int64_t>(ci) * 4;
+        const float4 a0 = rec[0], a1 = rec[1], a2 = rec[2], mr = rec[3];
         const float P[12] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
+        const float mu_b[4] = {mr.x, mr.y, mr.z, mr.w};
         float v[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          v[j] = j < D ? bcv[j] - static_cast<float>(mb.mu[k * 4 + j] - ct[j]) : 0.f;
+        for (int j = 0; j < 4; ++j) v[j] = j < D ? bcb[j] - mu_b[j] : 0.f;
+        // slack: 2^-10 relative + the frames' rounding (hw already rounds up)
         const float lb = box_lb<D>(P, v, hw);
         cand = fmaf(lb, -0x1p-10f, lb) - P[10] < qcut;
       }
@@ -436,6 +465,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
     if (allk) C = k_cur;
     __syncwarp();
     auto cand_at = [&](int i) -> int { return allk ? i : list[i]; };
+    SP_PH(2);
 
     // ---- one group (C <= 32, most tiles): both passes per 16-point slice, the
     // densities kept in registers between them (no recomputation). A slice
@@ -664,13 +694,19 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
     if (lane == 0) ll_tile[it] = ll;
     }  // !fused
 
+    SP_PH(3);
     // ---- output slots (CSR pool) + the tile's candidate bitmask
-    int base = 0;
-    if (lane == 0) base = atomicAdd(&ctl[1], C);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    const bool fits = static_cast<int64_t>(base) + C <= pool_cap;
+    // fixed slots of ucap entries per unit; more candidates: the overflow
+    // region after them (cursor ctl[1])
+    int64_t base = static_cast<int64_t>(it) * ucap;
+    if (C > ucap) {
+      int o = 0;
+      if (lane == 0) o = atomicAdd(&ctl[1], C);
+      base = static_cast<int64_t>(nitems) * ucap + __shfl_sync(0xffffffffu, o, 0);
+    }
+    const bool fits = base + C <= pool_cap;
     if (lane == 0) {
-      toff[it] = fits ? base : -1;
+      toff[it] = fits ? static_cast<int>(base) : -1;
       if (!fits) atomicExch(&ctl[2], 1);  // pool overflow: the host re-runs larger
     }
     for (int w = lane; w < kw; w += 32) mw[w] = 0u;
@@ -704,6 +740,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
 #ifdef GMMB_SP_PROF
     const int prof_c = C, prof_f = fused ? 1 : 0, prof_x = xslices ? 1 : 0;
 #endif
+    SP_PH(4);
 
     if (fused) {
       if (fits && lane < C) {
@@ -763,6 +800,14 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
     }
     __syncwarp();
 #ifdef GMMB_SP_PROF
+    SP_PH(5);
+    if (lane == 0) {
+      g_sp_ph[it * 6 + 0] = static_cast<unsigned>(ph1 - ph0);
+      g_sp_ph[it * 6 + 1] = static_cast<unsigned>(ph2 - ph1);
+      g_sp_ph[it * 6 + 2] = static_cast<unsigned>(ph3 - ph2);
+      g_sp_ph[it * 6 + 3] = static_cast<unsigned>(ph4 - ph3);
+      g_sp_ph[it * 6 + 4] = static_cast<unsigned>(ph5 - ph4);
+    }
     if (lane == 0) {
       unsigned long long prof_t1;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof_t1));
@@ -811,10 +856,10 @@ __global__ void __launch_bounds__(256)
     const int ov = tt < a1 ? toff[tt] : 0;
     unsigned any = __ballot_sync(0xffffffffu, wv != 0u);
     while (any) {
-      // two tiles per step: both tiles' loads in flight before the (ordered) adds
-      double v[2][NS];
+      // kRedStep units per step: their loads in flight before the (ordered) adds
+      double v[kRedStep][NS];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < kRedStep; ++u) {
         const int j = any ? __ffs(any) - 1 : 0;
         const bool on = any != 0u;
         any &= any - 1;
@@ -832,7 +877,7 @@ __global__ void __launch_bounds__(256)
         }
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+      for (int u = 0; u < kRedStep; ++u)
 #pragma unroll
         for (int q = 0; q < NS; ++q) acc[q] += v[u][q];
     }
@@ -952,12 +997,14 @@ cudaError_t launch_estep_sparse(const PointsDev& pts, const ModelBuf* bufs, cons
   }();
   if (pts.d == 4)
     block_cand_kernel<4><<<nblk, 256, 0, s>>>(sp.bc, sp.bh, bufs[0], bufs[1], st, k0, sp.blist,
-                                              sp.bcnt, sp.ctl, qcut);
+                                              sp.brec, sp.bcnt, sp.ctl, qcut);
   else
     block_cand_kernel<3><<<nblk, 256, 0, s>>>(sp.bc, sp.bh, bufs[0], bufs[1], st, k0, sp.blist,
-                                              sp.bcnt, sp.ctl, qcut);
+                                              sp.brec, sp.bcnt, sp.ctl, qcut);
+  const int ucap = sp.item_cap * U;
   kern<<<grid, kSpWarps * 32, smem, s>>>(pts.xt, pts.tc, pts.n, nitems, bufs[0], bufs[1], st, k0,
-                                         sp.blist, sp.bcnt, sp.ctl, sp.pool, sp.pool_cap, sp.toff,
+                                         sp.blist, sp.brec, sp.bcnt, sp.bc, ucap, sp.ctl, sp.pool,
+                                         sp.pool_cap, sp.toff,
                                          sp.maskT, sp.preT, sp.ll_tile, sp.heavy, sp.done,
                                          exact_mode, qcut, U);
   if (pts.d == 4)
@@ -976,5 +1023,8 @@ cudaError_t launch_estep_sparse(const PointsDev& pts, const ModelBuf* bufs, cons
 #ifdef GMMB_SP_PROF
 extern "C" int gmmb_debug_sp_prof(unsigned long long* out, int count) {
   return static_cast<int>(cudaMemcpyFromSymbol(out, gmmb::g_sp_prof, sizeof(unsigned long long) * count));
+}
+extern "C" int gmmb_debug_sp_ph(unsigned* out, int count) {
+  return static_cast<int>(cudaMemcpyFromSymbol(out, gmmb::g_sp_ph, sizeof(unsigned) * count));
 }
 #endif

@@ -6,10 +6,10 @@ TAG=${1:-r2}
 OUT=${2:-gpurun_out}
 mkdir -p "$OUT"
 CS=/usr/local/cuda/bin/compute-sanitizer
-for tool in memcheck racecheck synccheck; do
+for tool in ${TOOLS:-memcheck racecheck synccheck}; do
   log="$OUT/${TAG}_sanitize_${tool}.txt"
   : > "$log"
-  for c in ws cluster kinit_mem vshard batch aux; do
+  for c in ${CASES:-ws dense cluster kinit_mem vshard batch aux}; do
     echo "=== $tool / $c" >> "$log"
     timeout 900 $CS --tool $tool --print-limit 20 --error-exitcode 9 \
       python scripts/sanitize_cases.py $c >> "$log" 2>&1

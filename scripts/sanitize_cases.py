@@ -30,8 +30,19 @@ def case_ws():
         ctx.close()
 
 
+def case_dense():
+    """the dense E kernels (warp-specialised K <= 512, chunked K > 512)."""
+    pts = blobs(4, 12, 300, 1)
+    ctx = gm.Context(0)
+    ctx.set_estep_mode(True)
+    r = gm.fit_k(pts, 24, gm.EmParams(4, 1e-4, 1e-6, 0), ctx=ctx)
+    r2 = gm.fit_k(pts, 600 if len(pts) >= 600 else 100, gm.EmParams(2, 0.0, 1e-6, 0), ctx=ctx)
+    print("dense", r.em_iterations, r2.em_iterations)
+    ctx.close()
+
+
 def case_cluster():
-    """K > 512: chunked two-pass E step (pass A normalisers + PRE pass B)."""
+    """K > 512 through the pruned E step (block candidate lists, items)."""
     pts = blobs(4, 40, 200, 2)
     r = gm.fit_k(pts, 600, gm.EmParams(3, 0.0, 1e-6, 0))
     print("k600", r.k_init, r.em_iterations, r.final_log_likelihood)
@@ -41,8 +52,8 @@ def case_cluster():
 
 
 def case_kinit_mem():
-    """memory-resident kinit (persistent cooperative rounds) past the
-    shared-memory budget."""
+    """k-means++ past the shared-memory budget (tile-pruned warp-specialised
+    kernel; GMMB_KINIT=mem selects the memory-resident rounds)."""
     rng = np.random.default_rng(4)
     pts = rng.uniform(0.0, 1.0, size=(400_000, 3))
     lab, cen = gm.kinit(pts, 5, seed=1)
@@ -52,7 +63,7 @@ def case_kinit_mem():
 def case_vshard():
     """sharded driver (virtual ranks: comm layer, sharded kinit rounds, fix-up)."""
     pts = blobs(4, 8, 250, 5)
-    r = gm.fit_k_vsharded(pts, 16, gm.EmParams(4, 0.0, 1e-6, 0), world=2)
+    r = gm.fit_k_vsharded(pts, 16, gm.EmParams(4, 0.0, 1e-6, 0), world=2)[0]
     print("vshard", r.k_init, r.em_iterations, r.final_log_likelihood)
 
 
@@ -85,7 +96,7 @@ def case_aux():
     print("aux ok")
 
 
-CASES = {"ws": case_ws, "cluster": case_cluster, "kinit_mem": case_kinit_mem,
+CASES = {"ws": case_ws, "dense": case_dense, "cluster": case_cluster, "kinit_mem": case_kinit_mem,
          "vshard": case_vshard, "batch": case_batch, "aux": case_aux}
 
 if __name__ == "__main__":

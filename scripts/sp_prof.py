@@ -34,3 +34,14 @@ starts = np.array([t0[sm == s].min() - base for s in np.unique(sm)])
 print(f"per-SM first start {starts.max()/1e3:.1f} us max; last end min {ends.min()/1e3:.1f} p50 {np.median(ends)/1e3:.1f} max {ends.max()/1e3:.1f} us")
 # warp-time accounting: sum of tile durations / (span * warps)
 print(f"busy warp-time fraction {dur.sum() / (span * 148 * 16):.2f} (16 warps/SM)")
+
+ph = (ctypes.c_uint * (6 * nt))()
+gm.load().gmmb_debug_sp_ph(ph, 6 * nt)
+b = np.frombuffer(ph, dtype=np.uint32).reshape(nt, 6).astype(np.float64)[:, :5]
+names = ["load+box", "candidates", "passes", "slots+mask", "pass2/out"]
+tot = b.sum(1)
+print("phase cycles per unit (mean): " + ", ".join(f"{n} {b[:, i].mean():.0f}" for i, n in enumerate(names)) + f"; total {tot.mean():.0f}")
+for lo, hi in [(0, 32), (32, 64), (64, 100000)]:
+    m = (C > lo) & (C <= hi)
+    if m.any():
+        print(f"  C in ({lo},{hi}]: " + ", ".join(f"{n} {b[m, i].mean():.0f}" for i, n in enumerate(names)))
