@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdio>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -679,9 +680,18 @@ void ensure_em_buffers(gmmb_ctx* c, int k0, int max_iters) {
     // pool of per-(item, candidate) statistics: ~20-45 candidates per 32-point
     // item on the BASELINE clouds; 32 + K/64 per item (or all K) up front,
     // doubled after an overflow (the EM run is repeated, see run_em)
-    const int64_t per_item = std::min<int64_t>(k0, (32 + k0 / 64) * int64_t{c->pool_mult});
-    // fixed slots per unit + a quarter more for units with more candidates
-    const int64_t cap = std::max<int64_t>(static_cast<int64_t>(nitems) * per_item * 5 / 4, 1024);
+    // (GMMB_SPARSE_ITEM_CAP: the initial per-item reservation, a test knob
+    // that exercises the overflow region and the re-run)
+    static const int64_t cap0 = [] {
+      const char* e = getenv("GMMB_SPARSE_ITEM_CAP");
+      return e ? std::max<int64_t>(1, atoll(e)) : int64_t{0};
+    }();
+    const int64_t per_item =
+        std::min<int64_t>(k0, (cap0 ? cap0 : 32 + k0 / 64) * int64_t{c->pool_mult});
+    // fixed slots per unit + as many again for units with more candidates
+    // (K >= 1024 has many units above the reservation; an overflow costs a
+    // repeated EM run)
+    const int64_t cap = std::max<int64_t>(static_cast<int64_t>(nitems) * per_item * 2, 1024);
     c->sp_blist.ensure(static_cast<size_t>(nblk) * k0);
     c->sp_brec.ensure(static_cast<size_t>(nblk) * k0 * 4);
     c->sp_bcnt.ensure(nblk);
@@ -1685,9 +1695,9 @@ int gmmb_em_step(gmmb_ctx* c, const double* pts, int64_t n, int d, int m, const 
     reset_state(c, m, &em, 0);
     ck(launch_prep(c->d, c->bufs, c->st.p, m, c->s), "prep");
     raise_state_error(read_state(c));
-    ensure_em_buffers(c, m, 1);
-    em_iteration(c, m, -1);
-    EmState h = read_state(c);
+    // one iteration through run_em: per-run counters and the pruned E step's
+    // pool-overflow re-run live there
+    EmState h = run_em(c, m, &em);
     raise_state_error(h);
     if (ll_out) *ll_out = h.ll;
     download_model(c, h.cur, h.k_cur, w_out, mu_out, cov_out);
