@@ -30,6 +30,25 @@ def case_ws():
         ctx.close()
 
 
+def case_ws_t():
+    """as ws, plain launches only (no CUDA graph)."""
+    pts = blobs(4, 12, 300, 1)
+    ctx = gm.Context(0)
+    ctx.set_timing(True)
+    r = gm.fit_k(pts, 24, gm.EmParams(6, 1e-4, 1e-6, 0), ctx=ctx)
+    print("ws_t", r.k_init, r.em_iterations, r.final_log_likelihood)
+    ctx.close()
+
+
+def case_ws_g():
+    """as ws, the EM loop as one CUDA graph only."""
+    pts = blobs(4, 12, 300, 1)
+    ctx = gm.Context(0)
+    r = gm.fit_k(pts, 24, gm.EmParams(6, 1e-4, 1e-6, 0), ctx=ctx)
+    print("ws_g", r.k_init, r.em_iterations, r.final_log_likelihood)
+    ctx.close()
+
+
 def case_dense():
     """the dense E kernels (warp-specialised K <= 512, chunked K > 512)."""
     pts = blobs(4, 12, 300, 1)
@@ -96,7 +115,7 @@ def case_aux():
     print("aux ok")
 
 
-CASES = {"ws": case_ws, "dense": case_dense, "cluster": case_cluster, "kinit_mem": case_kinit_mem,
+CASES = {"ws": case_ws, "ws_t": case_ws_t, "ws_g": case_ws_g, "dense": case_dense, "cluster": case_cluster, "kinit_mem": case_kinit_mem,
          "vshard": case_vshard, "batch": case_batch, "aux": case_aux}
 
 if __name__ == "__main__":
