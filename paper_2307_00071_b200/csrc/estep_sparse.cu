@@ -943,6 +943,12 @@ int sparse_items(int ntiles) { return ntiles * kItemsPerTile; }
 // warp (balance, tight boxes), whole tiles when there are plenty (4x fewer
 // per-unit statistics records to write and reduce)
 int sparse_unit_items(int ntiles, int sm_count) {
+  static const int forced = [] {  // GMMB_SPARSE_U=1|2|4 (experiments)
+    const char* e = getenv("GMMB_SPARSE_U");
+    const int u = e ? atoi(e) : 0;
+    return (u == 1 || u == 2 || u == 4) ? u : 0;
+  }();
+  if (forced) return forced;
   const int warps = sm_count * kSpWarps * kSpMinBlocks;
   const int nitems = sparse_items(ntiles);
   if (nitems >= 64 * warps) return 4;
