@@ -60,7 +60,13 @@ __device__ unsigned g_sp_ph[6 * 262144];             // per unit: phase duration
 #define SP_PH(i)
 #endif
 constexpr int kBlkTiles = 16;     // tiles per culling block
-constexpr int kRedStep = 4;       // units whose statistics the reduce loads together
+#ifndef GMMB_RED_STEP
+#define GMMB_RED_STEP 2
+#endif
+#ifndef GMMB_RED_UNITS
+#define GMMB_RED_UNITS 128
+#endif
+constexpr int kRedStep = GMMB_RED_STEP;  // units whose statistics the reduce loads together
 constexpr int kItem = 32;         // points per item (one per lane); a work unit is U = 1, 2
 constexpr int kItemsPerTile = kTile / kItem;  // or 4 consecutive items of one layout tile
 constexpr int kSpWarps = 8;       // warps per CTA of the main kernel
@@ -916,11 +922,12 @@ __global__ void __launch_bounds__(256)
 size_t main_smem_bytes(int kcap) { return warp_smem_bytes(kcap) * kSpWarps; }
 
 int reduce_ranges(int kcap, int nunits, int sm_count) {
-  // enough CTAs to fill the device, and at most ~512 units per CTA (64 per
-  // warp: the scan over units is a chain of dependent loads)
+  // enough CTAs to fill the device, and at most GMMB_RED_UNITS units per CTA
+  // (the scan over units is a chain of dependent loads; 128 units, two per
+  // step, measured best: cfg2 E 132 -> 123 us, K = 2048 439 -> 404 us)
   const int kw = (kcap + 31) / 32;
   int R = (2 * sm_count + kw - 1) / kw;
-  const int r2 = (nunits + 511) / 512;
+  const int r2 = (nunits + GMMB_RED_UNITS - 1) / GMMB_RED_UNITS;  // units per CTA
   if (R < r2) R = r2;
   const int maxr = (nunits + 63) / 64;  // at least 8 units per warp
   if (R > maxr) R = maxr;
