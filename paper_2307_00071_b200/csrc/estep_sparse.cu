@@ -717,11 +717,17 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
     }
     for (int w = lane; w < kw; w += 32) mw[w] = 0u;
     __syncwarp();
-    for (int i = lane; i < C; i += 32) {
-      const int k = cand_at(i);
-      atomicOr(&mw[k >> 5], 1u << (k & 31));
+    // the candidates' bits, grouped per word in registers (no shared atomics:
+    // ascending candidates share words, which would serialise them)
+    for (int i0 = 0; i0 < C; i0 += 32) {
+      const int i = i0 + lane;
+      const int k = i < C ? cand_at(i) : -1;
+      const int wk = k >= 0 ? (k >> 5) : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, wk);
+      const unsigned bits = __reduce_or_sync(peers, k >= 0 ? 1u << (k & 31) : 0u);
+      if (k >= 0 && (peers & lanemask_lt()) == 0) mw[wk] |= bits;  // one writer per word
+      __syncwarp();
     }
-    __syncwarp();
     {
       int run = 0;
       for (int w0 = 0; w0 < kw; w0 += 32) {
