@@ -13,7 +13,7 @@ initial M step -> EM to tolerance) on one batch of synthetic input.
 --config cfg4 (BASELINE cfg4): the 4M-point 3D map (make_structured_scene x 25
     + (100, -40, 0) m), K=2048, tol 1e-3. With N > 1 the points are sharded
     contiguously over the ranks (one NCCL communicator; per-iteration
-    statistics all-reduce + per-round k-means++ candidate all-gather): strong
+    statistics all-reduce; k-means++ seeds the all-gathered cloud): strong
     scaling, value = global units / max-over-ranks time. --vshard G runs the
     same sharded path as G virtual ranks on one GPU (protocol check, not a
     scaling number).

@@ -131,6 +131,8 @@ struct gmmb_ctx {
   DevBuf<int> kstatus;
   DevBuf<long long> ll64;      // sharded fix-up scratch
   int kinit_tile = 1;          // 1: tile-pruned seeding past the resident kernel (GMMB_KINIT=mem: off)
+  int kinit_gather = 1;        // sharded: gather the cloud and seed it whole (GMMB_KINIT_SHARDED=rounds: 0)
+  DevBuf<double> kgather;
   DevBuf<double> kt_xm, kt_d2, kt_tile;
   DevBuf<uint64_t> kt_key;
   DevBuf<int32_t> kt_lab;
@@ -439,8 +441,77 @@ void run_kinit(gmmb_ctx* c, int k, uint64_t seed) {
     c->launches += 3;  // keys, seed (persistent), fixup
     return;
   }
-  // Sharded k-means++: local candidate per round -> allgather -> every rank
-  // picks the same global (clock, index) winner. Keys hash x[i..i+3] of the
+  if (c->world > 1 && c->kinit_gather) {
+    // Sharded clouds: k-means++ is K strictly sequential rounds, so a
+    // per-round collective (the path below) costs K network round trips
+    // (cfg4: 2048). Instead every rank gathers the whole cloud once (one
+    // all-gather, 128 MB for cfg4 over NVLink), seeds it exactly like one
+    // device would (identical centres and labels on every rank, no
+    // collective per round) and keeps the labels of its own shard.
+    const int W = c->world;
+    const int64_t N = c->n_global;
+    c->ll64.ensure(static_cast<size_t>(2 * W) + 2);
+    long long ext[2] = {static_cast<long long>(c->offset), static_cast<long long>(n)};
+    long long* dext = c->ll64.p + 2 * W;
+    copy_sync(c, dext, ext, sizeof(ext), cudaMemcpyHostToDevice);
+    coll(c, c->comm->allgather(dext, c->ll64.p, sizeof(ext), c->s), "allgather (shard extents)");
+    std::vector<long long> all(static_cast<size_t>(2 * W));
+    copy_sync(c, all.data(), c->ll64.p, sizeof(long long) * 2 * W, cudaMemcpyDeviceToHost);
+    long long max_n = 0, tot = 0;
+    for (int r = 0; r < W; ++r) {
+      max_n = std::max(max_n, all[2 * r + 1]);
+      tot += all[2 * r + 1];
+    }
+    if (tot != N) throw Err{2, "bad shard layout"};
+    c->dense.ensure(static_cast<size_t>(4) * max_n);
+    c->kgather.ensure(static_cast<size_t>(4) * max_n * W);
+    for (int j = 0; j < 4; ++j)
+      ck(cudaMemcpyAsync(c->dense.p + j * max_n, c->x64.p + j * n, sizeof(double) * n,
+                         cudaMemcpyDeviceToDevice, c->s), "D2D");
+    coll(c, c->comm->allgather(c->dense.p, c->kgather.p, sizeof(double) * 4 * max_n, c->s),
+         "allgather (cloud)");
+    c->x64_next.ensure(static_cast<size_t>(N) * 4 + 4);
+    for (int r = 0; r < W; ++r)
+      for (int j = 0; j < 4; ++j)
+        ck(cudaMemcpyAsync(c->x64_next.p + j * N + all[2 * r],
+                           c->kgather.p + (static_cast<size_t>(r) * 4 + j) * max_n,
+                           sizeof(double) * all[2 * r + 1], cudaMemcpyDeviceToDevice, c->s),
+           "D2D");
+    // the whole cloud as a one-device context (layout + seeding), then back
+    const int64_t off = c->offset, ng = c->n_global;
+    std::swap(c->x64.p, c->x64_next.p);
+    std::swap(c->x64.cap, c->x64_next.cap);
+    c->n = N;
+    c->offset = 0;
+    c->world = 1;
+    try {
+      layout(c);
+      run_kinit(c, k, seed);
+    } catch (...) {
+      std::swap(c->x64.p, c->x64_next.p);
+      std::swap(c->x64.cap, c->x64_next.cap);
+      c->n = n;
+      c->offset = off;
+      c->world = W;
+      throw;
+    }
+    std::swap(c->x64.p, c->x64_next.p);
+    std::swap(c->x64.cap, c->x64_next.cap);
+    c->n = n;
+    c->offset = off;
+    c->n_global = ng;
+    c->world = W;
+    // this shard's labels to the front (through scratch: the ranges overlap)
+    c->hidx.ensure(static_cast<size_t>(n));
+    ck(cudaMemcpyAsync(c->hidx.p, c->labels.p + off, sizeof(int32_t) * n,
+                       cudaMemcpyDeviceToDevice, c->s), "D2D");
+    ck(cudaMemcpyAsync(c->labels.p, c->hidx.p, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice,
+                       c->s), "D2D");
+    layout(c);  // the shard's own layout for its E steps
+    return;
+  }
+  // Sharded k-means++ (GMMB_KINIT_SHARDED=rounds): local candidate per round
+  // -> allgather -> every rank picks the same global (clock, index) winner. Keys hash x[i..i+3] of the
   // GLOBAL column-major buffer, so the last 3 local keys need the 3 doubles
   // that follow this shard's x column: the next shards' first x values, or
   // the global y column (rank 0's first y values) for the last shard.
@@ -1195,6 +1266,8 @@ static int create(int device, int rank, int world, const void* id, VGroup* vg,
     {  // GMMB_ESTEP=dense selects the dense E kernels (A/B, validation)
       const char* m = getenv("GMMB_ESTEP");
       c->estep_mode = (m && std::strcmp(m, "dense") == 0) ? 1 : 0;
+      const char* ks = getenv("GMMB_KINIT_SHARDED");
+      c->kinit_gather = (ks && std::strcmp(ks, "rounds") == 0) ? 0 : 1;
       const char* ki = getenv("GMMB_KINIT");
       // GMMB_KINIT=mem: memory-resident rounds past the shared-memory kernel;
       // =tile: the tile-pruned kernel at any size (A/B)
@@ -1298,7 +1371,7 @@ void gmmb_ctx_destroy(gmmb_ctx* c) {
   c->slots.release(); c->owned.release(); c->centers.release(); c->rslots.release();
   c->ticket.release(); c->kstatus.release(); c->ll64.release();
   c->kt_xm.release(); c->kt_d2.release(); c->kt_tile.release(); c->kt_key.release();
-  c->kt_lab.release();
+  c->kt_lab.release(); c->kgather.release();
   for (int b = 0; b < 2; ++b) {
     c->mw[b].release(); c->mmu[b].release(); c->mcov[b].release(); c->mcst[b].release();
   }

@@ -139,3 +139,17 @@ def test_vshard_repeated_fits_reuse_contexts(gm):
     _same_model(a + b)                                # deterministic bits
     for c in ctxs:
         c.close()
+
+
+def test_vshard_gathered_seeding_equals_per_round_exchange(gm, monkeypatch):
+    """Sharded k-means++ two ways: the default gathers the cloud once and
+    seeds it whole on every rank; GMMB_KINIT_SHARDED=rounds keeps the shards
+    and exchanges one candidate per round. Same centres and labels."""
+    p = gm.structured_scene(60000, 5, 0.005)
+    em = gm.EmParams(2, 0.0, 1e-6, 3)
+    a = gm.fit_k_vsharded(p, 96, em, world=3, want_labels=True)
+    monkeypatch.setenv("GMMB_KINIT_SHARDED", "rounds")
+    b = gm.fit_k_vsharded(p, 96, em, world=3, want_labels=True)
+    assert np.array_equal(a[0].centers, b[0].centers)
+    for x, y in zip(a, b):
+        assert np.array_equal(x.labels, y.labels)
