@@ -767,18 +767,19 @@ void ensure_em_buffers(gmmb_ctx* c, int k0, int max_iters) {
     c->sp_brec.ensure(static_cast<size_t>(nblk) * k0 * 4);
     c->sp_bcnt.ensure(nblk);
     c->sp_ctl.ensure(16);
-    c->sp_heavy.ensure(static_cast<size_t>(2) * nitems);
-    if (c->sp_done.cap < static_cast<size_t>(nitems)) {
-      c->sp_done.ensure(nitems);  // epoch stamps: zero once per allocation
+    c->sp_heavy.ensure(static_cast<size_t>(2) * kSparseMaxSplit * nitems);
+    if (c->sp_done.cap < static_cast<size_t>(2) * nitems) {
+      c->sp_done.ensure(static_cast<size_t>(2) * nitems);  // epoch stamps: zero once per allocation
       ck(cudaMemsetAsync(c->sp_done.p, 0, sizeof(unsigned) * c->sp_done.cap, c->s), "memset");
       ck(cudaMemsetAsync(c->sp_ctl.p, 0, sizeof(int) * 16, c->s), "memset");
     }
+
     const int NSP = (NS + 1) & ~1;  // pool entry stride (estep_sparse.cu)
     c->sp_pool.ensure(static_cast<size_t>(cap) * NSP);
-    c->sp_toff.ensure(nitems);
+    c->sp_toff.ensure(static_cast<size_t>(1 + kSparseMaxSplit) * nitems);
     c->sp_mask.ensure(static_cast<size_t>(kw) * nitems);
     c->sp_pre.ensure(static_cast<size_t>(kw) * nitems);
-    c->sp_ll.ensure(nitems);
+    c->sp_ll.ensure(static_cast<size_t>(1 + kSparseMaxSplit) * nitems);
     c->sparse = SparseScratch{c->sp_bc.p, c->sp_bh.p, c->sp_blist.p, c->sp_brec.p,
                               static_cast<int>(per_item), c->sp_bcnt.p, c->sp_ctl.p,
                               c->sp_heavy.p, c->sp_done.p,
@@ -838,12 +839,18 @@ EmState run_em(gmmb_ctx* c, int k0, const gmmb_em_params* em) {
       d2d(c->bak_cst[b].p, c->mcst[b].p, sizeof(CompConst) * kc);
     }
     // per-fit counters (queues, pool cursor, overflow, evaluated units, heavy
-    // lists); ctl[8] (the item epoch) keeps counting
+    // counts); ctl[8] (the unit epoch) keeps counting
     ck(cudaMemsetAsync(c->sp_ctl.p, 0, sizeof(int) * 8, c->s), "memset");
+    ck(cudaMemsetAsync(c->sp_ctl.p + 9, 0, sizeof(int) * 7, c->s), "memset");
     EmState h = run_em_once(c, k0, em);
-    int ctl[8];
+    int ctl[16];
     copy_sync(c, ctl, c->sp_ctl.p, sizeof(ctl), cudaMemcpyDeviceToHost);
     int overflow = ctl[2] != 0 ? 1 : 0;
+    if (getenv("GMMB_DEBUG"))
+      fprintf(stderr,
+              "gmmb: sparse run: iters %d pool cursor %d overflow %d heavy split tasks %d/%d "
+              "whole %d/%d epoch %d tasks %d combines %d\n",
+              h.iter, ctl[1], ctl[2], ctl[6], ctl[7], ctl[9], ctl[10], ctl[8], ctl[12], ctl[13]);
     if (c->world > 1) {  // every rank repeats together
       c->kstatus.ensure(8);
       copy_sync(c, c->kstatus.p + 6, &overflow, sizeof(int), cudaMemcpyHostToDevice);

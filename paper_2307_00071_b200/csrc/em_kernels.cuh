@@ -63,15 +63,16 @@ struct SparseScratch {
   int item_cap;          // pool entries reserved per 32-point item (overflow region after)
   int* bcnt;             // [nblk]
   int* ctl;              // [16]
-  int* heavy;            // [2][nitems] heavy-item lists (iteration parity)
-  unsigned* done;        // [nitems] epoch stamps of items taken from a heavy list
-  double* pool;          // [nstats][pool_cap]
+  int* heavy;            // [2][kSparseMaxSplit * nunits] heavy-unit task lists (iteration parity)
+  unsigned* done;        // [2][nunits] epoch stamps of units queued as heavy (iteration parity)
+  double* pool;          // [pool_cap][stride] per-(unit, candidate) statistics
   int64_t pool_cap;
-  int* toff;             // [nitems]
-  unsigned* maskT;       // [K/32][nitems]
-  unsigned short* preT;  // [K/32][nitems]
-  double* ll_tile;       // [nitems]
+  int* toff;             // [nunits] pool base (-S: split) + [nunits][kSparseMaxSplit] sub-unit bases
+  unsigned* maskT;       // [K/32][nunits]
+  unsigned short* preT;  // [K/32][nunits]
+  double* ll_tile;       // [nunits] + [nunits][kSparseMaxSplit] (split units)
 };
+constexpr int kSparseMaxSplit = 8;  // sub-units per heavy unit (estep_sparse.cu)
 bool sparse_supported(int k0, int ntiles);
 int sparse_blocks(int ntiles);
 int sparse_items(int ntiles);  // work items (32-point quarter tiles)

@@ -40,6 +40,7 @@
 //                      layout of the dense kernels (em_reduce_finalize / the
 //                      sharded em_reduce + all-reduce + em_finalize follow)
 // Every sum has a fixed order independent of scheduling: bit-reproducible.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -59,6 +60,9 @@ __device__ unsigned g_sp_ph[6 * 262144];             // per unit: phase duration
 #else
 #define SP_PH(i)
 #endif
+constexpr int kSpEvCalls = 256;
+cudaEvent_t g_sp_ev[kSpEvCalls][4] = {};
+int g_sp_nev = 0;
 constexpr int kBlkTiles = 16;     // tiles per culling block
 #ifndef GMMB_RED_STEP
 #define GMMB_RED_STEP 2
@@ -76,9 +80,23 @@ constexpr int kSlice = 16;        // points per FP32 partial (widened to FP64 af
 constexpr float kQCut = 134.f;    // candidates: LB < 134 (ex2.approx.ftz(-Q) = 0 for Q > 126)
 // (GMMB_SPARSE_QCUT overrides it: a validation knob, e.g. 1e30 keeps every pair)
 
-// pool entries: the nstats(D) FP64 statistics of one (item, candidate),
-// padded to an even count (16-byte loads in the reduce)
+// pool entries: the nstats(D) FP64 statistics of one (unit, candidate),
+// padded to an even count (16-byte loads in the reduce). (FP32 entries halve
+// the bytes but measured slower: the reduce is latency-bound, and the
+// conversions lengthen its dependent chain: cfg4 E reduce 373 -> 480 us.)
 __host__ __device__ constexpr int pool_stride(int d) { return (nstats(d) + 1) & ~1; }
+// Heavy units (many candidates) are split over up to kMaxSplit warps by
+// 16-point slices: a unit whose previous iteration had C > kHeavyC candidates
+// is queued first, split into S = 2^j sub-units while C / S > split_c, where
+// split_c = kSplitC x (units per 4 warps, at least 1): a split only pays when
+// one unit is a large share of a warp's work (each sub-unit repeats the
+// unit's loads and candidate filter).
+constexpr int kMaxSplit = kSparseMaxSplit;
+constexpr int kHeavyC = 48;
+#ifndef GMMB_SPLIT_C
+#define GMMB_SPLIT_C 96
+#endif
+constexpr int kSplitC = GMMB_SPLIT_C;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -194,7 +212,10 @@ __global__ void __launch_bounds__(256)
     ctl[1] = 0;
     ctl[3] = 0;
     ctl[6 + ((st->iter + 1) & 1)] = 0;
-    ctl[8] += 1;
+    ctl[9 + ((st->iter + 1) & 1)] = 0;
+    // +2 at a run's first iteration: marks left by an abandoned run (pool
+    // overflow re-run) can never match
+    ctl[8] += st->iter == 0 ? 2 : 1;
   }
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int k_cur = st->k_cur;
@@ -345,7 +366,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
                         int* __restrict__ toff, unsigned* __restrict__ maskT,
                         unsigned short* __restrict__ preT, double* __restrict__ ll_tile,
                         int* __restrict__ heavy, unsigned* __restrict__ done,
-                        int exact_mode, float qcut, int U) {
+                        int exact_mode, float qcut, int U, int split_c) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int kNSP = pool_stride(D);
   if (st->done) return;
@@ -360,35 +381,57 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
   const ModelBuf& mb = st->cur ? b1 : b0;
   unsigned long long evaluated = 0;  // units evaluated (lane 0)
 
-  // Work order: first the items that were heavy in the previous iteration
-  // (more than 48 candidates; longest first is the classic fix for a tail),
-  // then every item in index order, skipping those already done this epoch.
-  // The order changes no result: an item's output depends only on the item.
+  // Work order: first the units that were heavy in the previous iteration
+  // (more than kHeavyC candidates; longest first is the classic fix for a
+  // tail): the split ones' sub-units (list front), then the rest (list back);
+  // then every unit in index order, skipping the heavy ones (marked with this
+  // epoch by the previous iteration, before this kernel started, so no unit
+  // is ever taken twice). The order changes no result: a (sub-)unit's output
+  // depends only on the unit, its slices and the split S, and S is a function
+  // of the previous iteration's candidate count.
   const int par = st->iter & 1;
-  const int nheavy = ctl[6 + par];
-  const int* hl_cur = heavy + static_cast<int64_t>(par) * nitems;
-  int* hl_next = heavy + static_cast<int64_t>(par ^ 1) * nitems;
+  const int hcap = kMaxSplit * nitems;
+  const int nA = ctl[6 + par], nheavy = nA + ctl[9 + par];
+  const int* hl_cur = heavy + static_cast<int64_t>(par) * hcap;
+  int* hl_next = heavy + static_cast<int64_t>(par ^ 1) * hcap;
   const unsigned epoch = static_cast<unsigned>(ctl[8]);
+  // marks by parity: this iteration reads its own, the pushes below write the
+  // next iteration's (a shared array would let a heavy unit re-marked early
+  // be taken again by the normal queue)
+  const unsigned* done_cur = done + static_cast<int64_t>(par) * nitems;
+  unsigned* done_next = done + static_cast<int64_t>(par ^ 1) * nitems;
+  int* toffS = toff + nitems;          // [nitems][kMaxSplit] sub-unit pool bases
+  double* llS = ll_tile + nitems;      // [nitems][kMaxSplit] sub-unit ll
   for (;;) {
-    // work item it = 32 consecutive points (quarter qi of layout tile t)
-    int it = 0;
+    // task = (unit << 6) | (sub << 3) | (S - 1)
+    int task = 0;
     if (lane == 0) {
       const int h = nheavy > 0 ? atomicAdd(&ctl[3], 1) : nheavy;
-      if (h < nheavy) {
-        it = hl_cur[h];
-        done[it] = epoch;
+      if (h < nA) {
+        task = hl_cur[h];
+      } else if (h < nheavy) {
+        task = hl_cur[hcap - 1 - (h - nA)];
       } else {
+        int u;
         do {
-          it = atomicAdd(&ctl[0], 1);
-        } while (it < nitems && done[it] == epoch);
+          u = atomicAdd(&ctl[0], 1);
+        } while (u < nitems && done_cur[u] == epoch);
+        task = u < nitems ? (u << 6) : -1;
       }
     }
-    it = __shfl_sync(0xffffffffu, it, 0);
-    if (it >= nitems) break;
-    // unit it: points [it U 32, (it + 1) U 32) of the sorted cloud, one tile
+    task = __shfl_sync(0xffffffffu, task, 0);
+    if (task < 0) break;
+#ifdef GMMB_SP_COUNT
+    if (lane == 0) atomicAdd(&ctl[12], 1);
+#endif
+    const int it = task >> 6;
+    const int sub = (task >> 3) & 7, nsub = (task & 7) + 1;
+    // unit it: points [it U 32, (it + 1) U 32) of the sorted cloud, one tile;
+    // this task: its 16-point slices [sl0, sl1)
     const int64_t p0 = static_cast<int64_t>(it) * U * kItem;
     const int t = static_cast<int>(p0 / kTile);
     const int nsl = 2 * U;  // 16-point slices
+    const int sl0 = sub * nsl / nsub, sl1 = (sub + 1) * nsl / nsub;
 #ifdef GMMB_SP_PROF
     unsigned long long prof_t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof_t0));
@@ -486,7 +529,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
       for (int q = 0; q < NS; ++q) facc[q][lane] = 0.0;
       double fll = 0.0;
       #pragma unroll 1
-        for (int s = 0; s < nsl; ++s) {
+        for (int s = sl0; s < sl1; ++s) {
         float e[kSlice], v[kSlice];
 #pragma unroll
         for (int pp = 0; pp < kSlice; pp += 2) {
@@ -543,7 +586,10 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
         // the slices' ll in point order: lanes 0, 2, .. hold points 0..15 of each slice
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) fll += __shfl_xor_sync(0xffffffffu, fll, off);
-        if (lane == 0) ll_tile[it] = fll;
+        if (lane == 0) {
+          if (nsub == 1) ll_tile[it] = fll;
+          else llS[it * kMaxSplit + sub] = fll;
+        }
       } else {
         for (int q = 0; q < U; ++q) ws.ssum[lane + 32 * q] = 0.f;
         __syncwarp();
@@ -556,7 +602,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
         Cand<D> cd;
         load_cand<D>(cd, g + lane < nc ? cand_at(g + lane) : -1, mb, ct);
         #pragma unroll 1
-        for (int s = 0; s < nsl; ++s) {
+        for (int s = sl0; s < sl1; ++s) {
           float v[kSlice];
 #pragma unroll
           for (int pp = 0; pp < kSlice; pp += 2) {
@@ -580,7 +626,8 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
     for (int q = 0; q < U; ++q) {
       const int p = lane + 32 * q;
       const float S = ws.ssum[p];
-      const bool bad = p < npts && (exact_mode != 0 || !(S >= 0x1p-64f && S <= 0x1p64f));
+      const bool own = p >= sl0 * kSlice && p < sl1 * kSlice;
+      const bool bad = own && p < npts && (exact_mode != 0 || !(S >= 0x1p-64f && S <= 0x1p64f));
       const unsigned m = __ballot_sync(0xffffffffu, bad);
       // lanes 0..15 -> slice 2q, 16..31 -> slice 2q + 1
       if (m & 0xffffu) xslices |= 1u << (2 * q);
@@ -670,7 +717,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
         Cand<D> cd;
         load_cand<D>(cd, g + lane < C ? cand_at(g + lane) : -1, mb, ct);
         #pragma unroll 1
-        for (int s = 0; s < nsl; ++s) {
+        for (int s = sl0; s < sl1; ++s) {
           float v[kSlice];
 #pragma unroll
           for (int pp = 0; pp < kSlice; pp += 2) {
@@ -691,30 +738,55 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
     double ll = 0.0;
     for (int q = 0; q < U; ++q) {
       const int p = lane + 32 * q;
+      const bool own = p >= sl0 * kSlice && p < sl1 * kSlice && p < npts;
       const float S = ws.ssum[p];
-      if (p < npts) ll += static_cast<double>(ws.sh[p] + lg2f(S));
-      ws.ssum[p] = p < npts ? rcpf(S) : 0.f;
+      if (own) ll += static_cast<double>(ws.sh[p] + lg2f(S));
+      ws.ssum[p] = own ? rcpf(S) : 0.f;
     }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) ll += __shfl_xor_sync(0xffffffffu, ll, off);
-    if (lane == 0) ll_tile[it] = ll;
+    if (lane == 0) {
+      if (nsub == 1) ll_tile[it] = ll;
+      else llS[it * kMaxSplit + sub] = ll;
+    }
     }  // !fused
 
     SP_PH(3);
-    // ---- output slots (CSR pool) + the tile's candidate bitmask
-    // fixed slots of ucap entries per unit; more candidates: the overflow
-    // region after them (cursor ctl[1])
+    // ---- output slots (CSR pool) + the unit's candidate bitmask
+    // fixed slots of ucap entries per whole unit; more candidates, and every
+    // sub-unit of a split unit: the overflow region after them (cursor ctl[1])
     int64_t base = static_cast<int64_t>(it) * ucap;
-    if (C > ucap) {
+    if (C > ucap || nsub > 1) {
       int o = 0;
       if (lane == 0) o = atomicAdd(&ctl[1], C);
       base = static_cast<int64_t>(nitems) * ucap + __shfl_sync(0xffffffffu, o, 0);
     }
     const bool fits = base + C <= pool_cap;
     if (lane == 0) {
-      toff[it] = fits ? static_cast<int>(base) : -1;
+      if (nsub == 1) {
+        toff[it] = fits ? static_cast<int>(base) : -1;
+      } else {
+        toff[it] = -nsub;  // split: the reduce adds the sub-units' entries
+        toffS[it * kMaxSplit + sub] = fits ? static_cast<int>(base) : -1;
+      }
       if (!fits) atomicExch(&ctl[2], 1);  // pool overflow: the host re-runs larger
     }
+    // the next iteration's heavy list (from the whole unit's count: every
+    // sub-unit has the same list; sub-unit 0 reports it)
+    if (lane == 0 && sub == 0 && C > kHeavyC) {
+      int ns = 1;
+      while (ns < nsl && ns < kMaxSplit && C > split_c * ns) ns *= 2;
+      if (ns > 1) {
+        const int h = atomicAdd(&ctl[6 + (par ^ 1)], ns);
+        for (int q = 0; q < ns; ++q) hl_next[h + q] = (it << 6) | (q << 3) | (ns - 1);
+      } else {
+        const int h = atomicAdd(&ctl[9 + (par ^ 1)], 1);
+        hl_next[hcap - 1 - h] = it << 6;
+      }
+      done_next[it] = epoch + 1;  // the next iteration's normal queue skips it
+    }
+    // the bitmask: identical for every sub-unit; sub-unit 0 writes it
+    const bool wmask = sub == 0;
     for (int w = lane; w < kw; w += 32) mw[w] = 0u;
     __syncwarp();
     // the candidates' bits, grouped per word in registers (no shared atomics:
@@ -740,15 +812,18 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
           const int o = __shfl_up_sync(0xffffffffu, incl, off);
           if (lane >= off) incl += o;
         }
-        if (w < kw) {
-          maskT[static_cast<int64_t>(w) * nitems + it] = fits ? word : 0u;
+        if (w < kw && wmask) {
+          // a sub-unit that did not fit leaves its base -1: the reduce skips it
+          maskT[static_cast<int64_t>(w) * nitems + it] = (fits || nsub > 1) ? word : 0u;
           preT[static_cast<int64_t>(w) * nitems + it] = static_cast<unsigned short>(run + incl - c);
         }
         run += __shfl_sync(0xffffffffu, incl, 31);
       }
     }
-    if (lane == 0 && npts > 0) evaluated += static_cast<unsigned long long>(npts) * C;
-    if (lane == 0 && C > 48) hl_next[atomicAdd(&ctl[6 + (par ^ 1)], 1)] = it;
+    if (lane == 0) {
+      const int own = min(npts, sl1 * kSlice) - sl0 * kSlice;
+      if (own > 0) evaluated += static_cast<unsigned long long>(own) * C;
+    }
 #ifdef GMMB_SP_PROF
     const int prof_c = C, prof_f = fused ? 1 : 0, prof_x = xslices ? 1 : 0;
 #endif
@@ -756,8 +831,10 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
 
     if (fused) {
       if (fits && lane < C) {
+        double2* dst = reinterpret_cast<double2*>(pool + (base + lane) * kNSP);
 #pragma unroll
-        for (int q = 0; q < NS; ++q) pool[(base + lane) * kNSP + q] = facc[q][lane];
+        for (int q = 0; q < kNSP / 2; ++q)
+          dst[q] = make_double2(facc[2 * q][lane], 2 * q + 1 < NS ? facc[2 * q + 1][lane] : 0.0);
       }
     } else
     // ---- pass 2: responsibilities + centred statistics
@@ -769,7 +846,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
 #pragma unroll
       for (int q = 0; q < NS; ++q) acc[q] = 0.0;
       #pragma unroll 1
-        for (int s = 0; s < nsl; ++s) {
+        for (int s = sl0; s < sl1; ++s) {
         const bool xs_s = (xslices >> s) & 1u;
         f2_t ACC[NS];
 #pragma unroll
@@ -806,8 +883,10 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
         for (int q = 0; q < NS; ++q) acc[q] += f32_to_f64(lo2(ACC[q]) + hi2(ACC[q]));
       }
       if (fits && ci < C) {
+        double2* dst = reinterpret_cast<double2*>(pool + (base + ci) * kNSP);
 #pragma unroll
-        for (int q = 0; q < NS; ++q) pool[(base + ci) * kNSP + q] = acc[q];
+        for (int q = 0; q < kNSP / 2; ++q)
+          dst[q] = make_double2(acc[2 * q], 2 * q + 1 < NS ? acc[2 * q + 1] : 0.0);
       }
     }
     __syncwarp();
@@ -861,12 +940,37 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
   for (int q = 0; q < NS; ++q) acc[q] = 0.0;
   const unsigned below = lanemask_lt();
+  const int* toffS = toff + ntiles;  // split units' sub-unit bases (ntiles = units)
   for (int tb = a0; tb < a1; tb += 32) {
     const int tt = tb + lane;
     const unsigned wv = tt < a1 ? maskT[static_cast<int64_t>(w) * ntiles + tt] : 0u;
     const int pv = tt < a1 ? preT[static_cast<int64_t>(w) * ntiles + tt] : 0;
     const int ov = tt < a1 ? toff[tt] : 0;
     unsigned any = __ballot_sync(0xffffffffu, wv != 0u);
+    // split units of this chunk first (rare), each sub-unit's entries in
+    // sub-unit order; then the plain units below
+    unsigned spl = __ballot_sync(0xffffffffu, wv != 0u && ov < -1);
+    any &= ~spl;
+    while (spl) {
+      const int j = __ffs(spl) - 1;
+      spl &= spl - 1;
+      const unsigned word = __shfl_sync(0xffffffffu, wv, j);
+      const int pre = __shfl_sync(0xffffffffu, pv, j);
+      const int ns = -__shfl_sync(0xffffffffu, ov, j);
+      const bool mine = (word >> lane) & 1u;
+      const int idx = pre + __popc(word & below);
+      for (int sb = 0; sb < ns; ++sb) {
+        const int b = toffS[static_cast<int64_t>(tb + j) * kMaxSplit + sb];
+        const double2* src = reinterpret_cast<const double2*>(pool + (static_cast<int64_t>(b) + idx) * kNSP);
+        const bool ld = mine && b >= 0;
+#pragma unroll
+        for (int q = 0; q < kNSP / 2; ++q) {
+          const double2 x = ld ? __ldcg(src + q) : make_double2(0.0, 0.0);
+          acc[2 * q] += x.x;
+          if (2 * q + 1 < NS) acc[2 * q + 1] += x.y;
+        }
+      }
+    }
     while (any) {
       // kRedStep units per step: their loads in flight before the (ordered) adds
       double v[kRedStep][NS];
@@ -898,7 +1002,15 @@ __global__ void __launch_bounds__(256)
   for (int q = 0; q < NS; ++q) red[warp][q][lane] = acc[q];
   double l = 0.0;
   if (w == 0) {
-    for (int tt = a0 + lane; tt < a1; tt += 32) l += ll_tile[tt];
+    const double* llS = ll_tile + ntiles;
+    for (int tt = a0 + lane; tt < a1; tt += 32) {
+      const int o = toff[tt];
+      if (o < -1) {
+        for (int sb = 0; sb < -o; ++sb) l += llS[static_cast<int64_t>(tt) * kMaxSplit + sb];
+      } else {
+        l += ll_tile[tt];
+      }
+    }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
     if (lane == 0) lred[warp] = l;
@@ -945,6 +1057,7 @@ int reduce_ranges(int kcap, int nunits, int sm_count) {
 bool sparse_supported(int k0, int ntiles) {
   const int nblk = (ntiles + kBlkTiles - 1) / kBlkTiles;
   return k0 <= 65535 && static_cast<int64_t>(nblk) * k0 <= (int64_t{1} << 26) &&
+         static_cast<int64_t>(ntiles) * kItemsPerTile < (int64_t{1} << 24) &&
          main_smem_bytes(k0) <= 200 * 1024;
 }
 
@@ -964,8 +1077,9 @@ int sparse_unit_items(int ntiles, int sm_count) {
   if (forced) return forced;
   const int warps = sm_count * kSpWarps * kSpMinBlocks;
   const int nitems = sparse_items(ntiles);
-  if (nitems >= 64 * warps) return 4;
-  if (nitems >= 32 * warps) return 2;
+  // (cfg4, 125k items on 148 SMs: U = 4 measured 25 % faster than U = 2)
+  if (nitems >= 32 * warps) return 4;
+  if (nitems >= 16 * warps) return 2;
   return 1;
 }
 
@@ -1014,6 +1128,16 @@ cudaError_t launch_estep_sparse(const PointsDev& pts, const ModelBuf* bufs, cons
     const char* e = getenv("GMMB_SPARSE_QCUT");
     return e ? static_cast<float>(atof(e)) : kQCut;
   }();
+  // GMMB_SP_EVENTS=1 (diagnostic; plain launches only, i.e. timing mode):
+  // events around each of the three kernels, read by gmmb_debug_sp_events
+  static const bool evs = getenv("GMMB_SP_EVENTS") != nullptr;
+  cudaEvent_t* ev = nullptr;
+  if (evs && g_sp_nev < kSpEvCalls) {
+    ev = g_sp_ev[g_sp_nev++];
+    for (int i = 0; i < 4; ++i)
+      if (!ev[i]) cudaEventCreate(&ev[i]);
+  }
+  if (ev) cudaEventRecord(ev[0], s);
   if (pts.d == 4)
     block_cand_kernel<4><<<nblk, 256, 0, s>>>(sp.bc, sp.bh, bufs[0], bufs[1], st, k0, sp.blist,
                                               sp.brec, sp.bcnt, sp.ctl, qcut);
@@ -1021,11 +1145,15 @@ cudaError_t launch_estep_sparse(const PointsDev& pts, const ModelBuf* bufs, cons
     block_cand_kernel<3><<<nblk, 256, 0, s>>>(sp.bc, sp.bh, bufs[0], bufs[1], st, k0, sp.blist,
                                               sp.brec, sp.bcnt, sp.ctl, qcut);
   const int ucap = sp.item_cap * U;
+  const int warps_all = sm_count * occ * kSpWarps;
+  const int split_c = kSplitC * std::max(1, nitems / (4 * warps_all));
+  if (ev) cudaEventRecord(ev[1], s);
   kern<<<grid, kSpWarps * 32, smem, s>>>(pts.xt, pts.tc, pts.n, nitems, bufs[0], bufs[1], st, k0,
                                          sp.blist, sp.brec, sp.bcnt, sp.bc, ucap, sp.ctl, sp.pool,
                                          sp.pool_cap, sp.toff,
                                          sp.maskT, sp.preT, sp.ll_tile, sp.heavy, sp.done,
-                                         exact_mode, qcut, U);
+                                         exact_mode, qcut, U, split_c);
+  if (ev) cudaEventRecord(ev[2], s);
   if (pts.d == 4)
     sparse_reduce_kernel<4><<<kw * R, 256, 0, s>>>(sp.maskT, sp.preT, sp.toff, sp.pool, sp.pool_cap,
                                                    sp.ll_tile, nitems, kw, R, k0, st, partials,
@@ -1034,10 +1162,23 @@ cudaError_t launch_estep_sparse(const PointsDev& pts, const ModelBuf* bufs, cons
     sparse_reduce_kernel<3><<<kw * R, 256, 0, s>>>(sp.maskT, sp.preT, sp.toff, sp.pool, sp.pool_cap,
                                                    sp.ll_tile, nitems, kw, R, k0, st, partials,
                                                    ll_part);
+  if (ev) cudaEventRecord(ev[3], s);
   return cudaGetLastError();
 }
 
 }  // namespace gmmb
+
+// per recorded E step: ms of block_cand, the main kernel, the reduce;
+// returns the number of steps and resets the recorder
+extern "C" int gmmb_debug_sp_events(float* out, int max_steps) {
+  using namespace gmmb;
+  const int n = g_sp_nev < max_steps ? g_sp_nev : max_steps;
+  cudaDeviceSynchronize();
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < 3; ++j) cudaEventElapsedTime(&out[3 * i + j], g_sp_ev[i][j], g_sp_ev[i][j + 1]);
+  g_sp_nev = 0;
+  return n;
+}
 
 #ifdef GMMB_SP_PROF
 extern "C" int gmmb_debug_sp_prof(unsigned long long* out, int count) {

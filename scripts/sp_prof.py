@@ -45,3 +45,6 @@ for lo, hi in [(0, 32), (32, 64), (64, 100000)]:
     m = (C > lo) & (C <= hi)
     if m.any():
         print(f"  C in ({lo},{hi}]: " + ", ".join(f"{n} {b[m, i].mean():.0f}" for i, n in enumerate(names)))
+order = np.argsort(-dur)[:8]
+print("longest units (us, C, start us, end us): " + "; ".join(
+    f"{dur[i]/1e3:.1f} C={C[i]} @{(t0[i]-base)/1e3:.1f}-{(t1[i]-base)/1e3:.1f}" for i in order))
