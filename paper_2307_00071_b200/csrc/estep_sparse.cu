@@ -438,6 +438,25 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
 #endif
     SP_PH(0);
     const int npts = static_cast<int>(min64(U * kItem, n - p0));  // may be <= 0 (padding)
+    // issued first, independent of the points: the block's candidate count,
+    // centre and first group of records (the filter below needs the box)
+    const int blk = t / kBlkTiles;
+    const int* bl = blist + static_cast<int64_t>(blk) * kcap;
+    const float4* br = brec + static_cast<int64_t>(blk) * kcap * 4;
+    const int cb_ld = bcnt[blk];
+    double bce[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bce[j] = bcen[blk * 4 + j];
+    int kn = -1;
+    float4 n0 = make_float4(0.f, 0.f, 0.f, 0.f), n1 = n0, n2 = n0, n3 = n0;
+    if (lane < kcap) {
+      kn = __ldcg(bl + lane);
+      const float4* rec = br + static_cast<int64_t>(lane) * 4;
+      n0 = __ldcg(rec);
+      n1 = __ldcg(rec + 1);
+      n2 = __ldcg(rec + 2);
+      n3 = __ldcg(rec + 3);
+    }
     double ct[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) ct[j] = tc[static_cast<int64_t>(t) * 4 + j];
@@ -476,25 +495,31 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
     }
     SP_PH(1);
     // ---- fine candidates (ascending): the block's list filtered by the tile box
-    const int blk = t / kBlkTiles;
-    const int cb = npts > 0 ? bcnt[blk] : 0;
-    const int* bl = blist + static_cast<int64_t>(blk) * kcap;
-    const float4* br = brec + static_cast<int64_t>(blk) * kcap * 4;
+    const int cb = npts > 0 ? cb_ld : 0;
     // box centre relative to the block centre (the records' frame); the
     // FP32 rounding of the two frames (~1e-7 of the block extent) is far
     // inside the 8-unit margin of the cut
     float bcb[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) bcb[j] = bcv[j] + static_cast<float>(ct[j] - bcen[blk * 4 + j]);
+    for (int j = 0; j < 4; ++j) bcb[j] = bcv[j] + static_cast<float>(ct[j] - bce[j]);
     int C = 0;
     for (int c0 = 0; c0 < cb; c0 += 32) {
       const int ci = c0 + lane;
       bool cand = false;
       int k = -1;
+      // this group's records (prefetched), then the next group's in flight
+      const float4 a0 = n0, a1 = n1, a2 = n2, mr = n3;
+      const int kc = kn;
+      if (c0 + 32 < cb && ci + 32 < cb) {
+        kn = __ldcg(bl + ci + 32);
+        const float4* rec = br + static_cast<int64_t>(ci + 32) * 4;
+        n0 = __ldcg(rec);
+        n1 = __ldcg(rec + 1);
+        n2 = __ldcg(rec + 2);
+        n3 = __ldcg(rec + 3);
+      }
       if (ci < cb) {
-        k = bl[ci];
-        const float4* rec = br + static_cast<int64_t>(ci) * 4;
-        const float4 a0 = rec[0], a1 = rec[1], a2 = rec[2], mr = rec[3];
+        k = kc;
         const float P[12] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
         const float mu_b[4] = {mr.x, mr.y, mr.z, mr.w};
         float v[4];
@@ -514,6 +539,19 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
     if (allk) C = k_cur;
     __syncwarp();
     auto cand_at = [&](int i) -> int { return allk ? i : list[i]; };
+    // the atomics whose results are needed only after the passes go out now
+    // (their latency hides behind the passes): the overflow-region slots and
+    // the next iteration's heavy-list slots (lane 0 holds the results)
+    const int C_pre = C;
+    int o_pre = 0, h_pre = 0, ns_pre = 0;
+    if (lane == 0) {
+      if (C > ucap || nsub > 1) o_pre = atomicAdd(&ctl[1], C);
+      if (sub == 0 && C > kHeavyC) {
+        ns_pre = 1;
+        while (ns_pre < nsl && ns_pre < kMaxSplit && C > split_c * ns_pre) ns_pre *= 2;
+        h_pre = atomicAdd(&ctl[(ns_pre > 1 ? 6 : 9) + (par ^ 1)], ns_pre > 1 ? ns_pre : 1);
+      }
+    }
     SP_PH(2);
 
     // ---- one group (C <= 32, most tiles): both passes per 16-point slice, the
@@ -757,8 +795,9 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
     // sub-unit of a split unit: the overflow region after them (cursor ctl[1])
     int64_t base = static_cast<int64_t>(it) * ucap;
     if (C > ucap || nsub > 1) {
-      int o = 0;
-      if (lane == 0) o = atomicAdd(&ctl[1], C);
+      int o = o_pre;
+      // (the exact path may have re-selected the candidates: new slots)
+      if (lane == 0 && (C != C_pre || !(C_pre > ucap || nsub > 1))) o = atomicAdd(&ctl[1], C);
       base = static_cast<int64_t>(nitems) * ucap + __shfl_sync(0xffffffffu, o, 0);
     }
     const bool fits = base + C <= pool_cap;
@@ -773,15 +812,12 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
     }
     // the next iteration's heavy list (from the whole unit's count: every
     // sub-unit has the same list; sub-unit 0 reports it)
-    if (lane == 0 && sub == 0 && C > kHeavyC) {
-      int ns = 1;
-      while (ns < nsl && ns < kMaxSplit && C > split_c * ns) ns *= 2;
-      if (ns > 1) {
-        const int h = atomicAdd(&ctl[6 + (par ^ 1)], ns);
-        for (int q = 0; q < ns; ++q) hl_next[h + q] = (it << 6) | (q << 3) | (ns - 1);
+    // (the candidate count before any exact-path re-selection decides)
+    if (lane == 0 && ns_pre > 0) {
+      if (ns_pre > 1) {
+        for (int q = 0; q < ns_pre; ++q) hl_next[h_pre + q] = (it << 6) | (q << 3) | (ns_pre - 1);
       } else {
-        const int h = atomicAdd(&ctl[9 + (par ^ 1)], 1);
-        hl_next[hcap - 1 - h] = it << 6;
+        hl_next[hcap - 1 - h_pre] = it << 6;
       }
       done_next[it] = epoch + 1;  // the next iteration's normal queue skips it
     }
@@ -795,9 +831,17 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
       const int i = i0 + lane;
       const int k = i < C ? cand_at(i) : -1;
       const int wk = k >= 0 ? (k >> 5) : -1;
-      const unsigned peers = __match_any_sync(0xffffffffu, wk);
-      const unsigned bits = __reduce_or_sync(peers, k >= 0 ? 1u << (k & 31) : 0u);
-      if (k >= 0 && (peers & lanemask_lt()) == 0) mw[wk] |= bits;  // one writer per word
+      // ascending: each word's candidates are a run of lanes; segmented
+      // inclusive OR-scan, the run's last lane writes
+      unsigned bits = k >= 0 ? 1u << (k & 31) : 0u;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const unsigned ob = __shfl_up_sync(0xffffffffu, bits, off);
+        const int ow = __shfl_up_sync(0xffffffffu, wk, off);
+        if (lane >= off && ow == wk) bits |= ob;
+      }
+      const int nw = __shfl_down_sync(0xffffffffu, wk, 1);
+      if (k >= 0 && (lane == 31 || nw != wk)) mw[wk] |= bits;
       __syncwarp();
     }
     {
