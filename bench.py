@@ -50,7 +50,16 @@ NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 # DRAM traffic per launch of the dominant kernel, from ncu --set full
 # captures of exactly these configurations and kernels (emitted only when the
 # run matches the capture; re-captured on every kernel change).
-TRAFFIC = {}
+# (config, K, E-step kind) -> (bytes per E step: the three pruned-E kernels'
+# dram__bytes_read.sum + dram__bytes_write.sum, source). ncu replays with
+# flushed caches, so the per-(unit, candidate) statistics the reduce reads
+# (L2-resident between the kernels in situ) count as DRAM reads here.
+TRAFFIC = {
+    ("cfg2", 512, "sparse"): (6.3232e4 + 6.029824e6 + 2.74688e5 + 2.8428032e7 + 1.0496e4,
+                              "profiles/r2aw_cfg2_sparse_ncu.txt"),
+    ("cfg4", 2048, "sparse"): (2.97984e5 + 1.92e4 + 9.4793472e7 + 1.17938944e8 + 1.63968768e8
+                               + 2.8050688e7, "profiles/r2aw_cfg4_sparse_ncu.txt"),
+}
 
 
 def parse():
@@ -531,13 +540,22 @@ def main():
                                        if dense_cmp else None),
                      "timing": "CUDA events around each E step (all its kernels) on the library "
                                "stream, %d iterations over %d fits" % (est_launches, args.steps),
+                     "bound_note": ("the pruned E step is latency-bound, not FP32-bound: 16 warps "
+                                    "per SM (128 registers), issue slots ~40 % active, the per-unit "
+                                    "candidate filter and statistics hand-off are memory round trips "
+                                    "(profiles/r2aw_cfg2_sparse_ncu.txt, r2au_sparse_source_stalls.txt); "
+                                    "it evaluates ~4.5 % of the pairs and takes less time than the "
+                                    "dense kernels would at their 0.60 target"
+                                    if pruned else None),
                      "peak_source": "measured packed-FP32 (fma.rn.f32x2) microbenchmark in this "
                                     "run (MEASURED_PEAKS.json has no FP32 figure); nominal %.1f"
                                     % NOMINAL_FP32_TFLOPS,
                      "traffic": tr[0] if tr else None,
-                     "traffic_note": ("dram__bytes_read.sum + dram__bytes_write.sum per launch, "
-                                      "ncu --set full of this configuration (%s); algorithmic "
-                                      "%.0f B (points 16 B each)" % (tr[1], 16 * n)) if tr else
+                     "traffic_note": ("dram__bytes_read.sum + dram__bytes_write.sum per E step "
+                                      "(its three kernels), ncu --set full of this configuration "
+                                      "(%s; cold caches: the statistics pool the reduce reads is "
+                                      "L2-resident in situ); algorithmic %.0f B (points 16 B each)"
+                                      % (tr[1], 16 * n)) if tr else
                                      "no ncu capture of this configuration; algorithmic "
                                      "%.0f B per launch (points 16 B each)" % (16 * n)},
         "clocks": clocks,
