@@ -19,6 +19,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/gmmb.h"
 #include "em_kernels.cuh"
 #include "kinit_kernels.cuh"
@@ -30,6 +32,15 @@
 #include "comm.cuh"
 
 using namespace gmmb;
+
+// NVTX ranges around the fit's stages (header-only nvtx3: free without a
+// profiler; visible in Nsight Systems / ncu --nvtx)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 namespace {
 
@@ -151,6 +162,7 @@ struct gmmb_ctx {
   int estep_mode = 0;             // 0: pruned when supported, 1: dense kernels
   bool sparse_on = false;         // the current EM run uses the pruned E step
   int pool_mult = 1;              // pool growth after an overflow
+  int sp_nosplit = 0;             // this EM run's retry without heavy-unit splits
   DevBuf<double> sp_bc, sp_pool, sp_ll;
   DevBuf<float4> sp_bh, sp_brec;
   DevBuf<int> sp_blist, sp_bcnt, sp_ctl, sp_toff, sp_heavy;
@@ -331,6 +343,7 @@ void validate(gmmb_ctx* c) {
 }
 
 void layout(gmmb_ctx* c) {
+  NvtxRange nv("gmmb.layout");
   const int64_t n = c->n;
   validate(c);
   const int ntiles = static_cast<int>((n + kTile - 1) / kTile);
@@ -402,6 +415,7 @@ KinitScratch kinit_scratch(gmmb_ctx* c, int k) {
 }
 
 void run_kinit(gmmb_ctx* c, int k, uint64_t seed) {
+  NvtxRange nv("gmmb.kinit");
   const int64_t n = c->n;
   KinitScratch ks = kinit_scratch(c, k);
   ck(cudaMemsetAsync(c->owned.p, 0, sizeof(int) * k, c->s), "memset");
@@ -690,7 +704,7 @@ EmGraphKey em_graph_key(gmmb_ctx* c, int k0) {
   k.d = c->d;
   k.n = c->n;
   k.world = c->world;
-  k.sparse = c->sparse_on ? 1 : 0;
+  k.sparse = c->sparse_on ? 1 + c->sp_nosplit : 0;
   const void* ps[20] = {c->xt.p, c->tc.p, c->partials.p, c->ll_part.p, c->red.p, c->ll_trace.p,
                         c->st.p, c->bufs[0].w, c->bufs[1].w, c->rec.count, c->bufs[0].cst,
                         c->bufs[1].cst, c->chunkf.p, c->chunki.p, c->sp_pool.p, c->sp_blist.p,
@@ -784,7 +798,7 @@ void ensure_em_buffers(gmmb_ctx* c, int k0, int max_iters) {
                               static_cast<int>(per_item), c->sp_bcnt.p, c->sp_ctl.p,
                               c->sp_heavy.p, c->sp_done.p,
                               c->sp_pool.p, static_cast<int64_t>(c->sp_pool.cap / NSP),
-                              c->sp_toff.p, c->sp_mask.p, c->sp_pre.p, c->sp_ll.p};
+                              c->sp_toff.p, c->sp_mask.p, c->sp_pre.p, c->sp_ll.p, c->sp_nosplit};
   }
   int ncl = 0;
   ck(launch_estep_stats(pts, c->bufs, c->st.p, k0, nullptr, nullptr, 0,
@@ -814,6 +828,8 @@ EmState run_em_once(gmmb_ctx* c, int k0, const gmmb_em_params* em);
 // reach most tiles), the EM run is repeated from its starting model with a
 // larger pool, so results never depend on the pool size.
 EmState run_em(gmmb_ctx* c, int k0, const gmmb_em_params* em) {
+  NvtxRange nv("gmmb.em");
+  c->sp_nosplit = 0;
   for (int attempt = 0;; ++attempt) {
     ensure_em_buffers(c, k0, em->max_iters);
     if (!c->sparse_on) {
@@ -845,7 +861,10 @@ EmState run_em(gmmb_ctx* c, int k0, const gmmb_em_params* em) {
     EmState h = run_em_once(c, k0, em);
     int ctl[16];
     copy_sync(c, ctl, c->sp_ctl.p, sizeof(ctl), cudaMemcpyDeviceToHost);
-    int overflow = ctl[2] != 0 ? 1 : 0;
+    // ctl[2] bit 0: pool overflow (retry with a larger pool); bit 1: a split
+    // heavy unit needed the exact path, whose re-selected candidates could
+    // differ between its sub-units (retry without splits)
+    int redo[2] = {ctl[2] & 1, (ctl[2] >> 1) & 1};
     if (getenv("GMMB_DEBUG"))
       fprintf(stderr,
               "gmmb: sparse run: iters %d pool cursor %d overflow %d heavy split tasks %d/%d "
@@ -853,11 +872,12 @@ EmState run_em(gmmb_ctx* c, int k0, const gmmb_em_params* em) {
               h.iter, ctl[1], ctl[2], ctl[6], ctl[7], ctl[9], ctl[10], ctl[8], ctl[12], ctl[13]);
     if (c->world > 1) {  // every rank repeats together
       c->kstatus.ensure(8);
-      copy_sync(c, c->kstatus.p + 6, &overflow, sizeof(int), cudaMemcpyHostToDevice);
-      coll(c, c->comm->allreduce(c->kstatus.p + 6, 1, DType::kI32, RedOp::kSum, c->s),
+      copy_sync(c, c->kstatus.p + 6, redo, sizeof(redo), cudaMemcpyHostToDevice);
+      coll(c, c->comm->allreduce(c->kstatus.p + 6, 2, DType::kI32, RedOp::kSum, c->s),
            "allreduce (pool overflow)");
-      copy_sync(c, &overflow, c->kstatus.p + 6, sizeof(int), cudaMemcpyDeviceToHost);
+      copy_sync(c, redo, c->kstatus.p + 6, sizeof(redo), cudaMemcpyDeviceToHost);
     }
+    const bool overflow = redo[0] != 0 || redo[1] != 0;
     unsigned long long ev = 0;
     std::memcpy(&ev, &ctl[4], sizeof(ev));
     c->units_eval = static_cast<double>(ev);
@@ -869,7 +889,10 @@ EmState run_em(gmmb_ctx* c, int k0, const gmmb_em_params* em) {
       d2d(c->mcov[b].p, c->bak_cov[b].p, sizeof(double) * kc * 10);
       d2d(c->mcst[b].p, c->bak_cst[b].p, sizeof(CompConst) * kc);
     }
-    c->pool_mult *= 2;
+    // (an attempt that overflowed ran on partial statistics: only its
+    // overflow counts, a split conflict there says nothing)
+    if (redo[0]) c->pool_mult *= 2;
+    else if (redo[1]) c->sp_nosplit = 1;
   }
 }
 
@@ -937,6 +960,7 @@ void fit_k_resident(gmmb_ctx* c, int K, const gmmb_em_params* em, double* w_out,
                     double* mu_out, double* cov_out, double* ll_trace,
                     gmmb_fit_stats* stats, int32_t* labels_out,
                     int64_t* centers_out) {
+  NvtxRange nv("gmmb.fit");
   if (!c->have_cloud) throw Err{2, "no point cloud uploaded"};
   check_em(em);
   if (K < 1) throw Err{2, "kinit: k must satisfy 1 <= k <= N"};

@@ -71,6 +71,7 @@ struct SparseScratch {
   unsigned* maskT;       // [K/32][nunits]
   unsigned short* preT;  // [K/32][nunits]
   double* ll_tile;       // [nunits] + [nunits][kSparseMaxSplit] (split units)
+  int no_split;          // 1: no heavy-unit splits (the retry after a split unit hit the exact path)
 };
 constexpr int kSparseMaxSplit = 8;  // sub-units per heavy unit (estep_sparse.cu)
 bool sparse_supported(int k0, int ntiles);

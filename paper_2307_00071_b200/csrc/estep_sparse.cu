@@ -672,6 +672,9 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
       if (m & 0xffff0000u) xslices |= 2u << (2 * q);
     }
     if (xslices) {
+      // a split unit's sub-units could re-select different candidate lists
+      // here: flag it, the EM run is repeated without splits
+      if (nsub > 1 && lane == 0) atomicOr(&ctl[2], 2);
       // Max shift on the flagged slices (the dense kernel's exact path). The
       // components that can matter: with UB_min the smallest upper bound of
       // Q over the tile box among ALL components, every point's minimum Q is
@@ -808,7 +811,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, kSpMinBlocks)
         toff[it] = -nsub;  // split: the reduce adds the sub-units' entries
         toffS[it * kMaxSplit + sub] = fits ? static_cast<int>(base) : -1;
       }
-      if (!fits) atomicExch(&ctl[2], 1);  // pool overflow: the host re-runs larger
+      if (!fits) atomicOr(&ctl[2], 1);  // pool overflow: the host re-runs larger
     }
     // the next iteration's heavy list (from the whole unit's count: every
     // sub-unit has the same list; sub-unit 0 reports it)
@@ -1081,6 +1084,7 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+
 size_t main_smem_bytes(int kcap) { return warp_smem_bytes(kcap) * kSpWarps; }
 
 int reduce_ranges(int kcap, int nunits, int sm_count) {
@@ -1190,7 +1194,13 @@ cudaError_t launch_estep_sparse(const PointsDev& pts, const ModelBuf* bufs, cons
                                               sp.brec, sp.bcnt, sp.ctl, qcut);
   const int ucap = sp.item_cap * U;
   const int warps_all = sm_count * occ * kSpWarps;
-  const int split_c = kSplitC * std::max(1, nitems / (4 * warps_all));
+  // GMMB_SPARSE_NOSPLIT=1 / GMMB_SPARSE_EXACT=1: validation knobs (no
+  // heavy-unit splits / the max-shift path on every slice)
+  static const bool env_nosplit = getenv("GMMB_SPARSE_NOSPLIT") != nullptr;
+  static const bool env_exact = getenv("GMMB_SPARSE_EXACT") != nullptr;
+  if (env_exact) exact_mode = 1;
+  const int split_c = (sp.no_split || env_nosplit) ? (1 << 30)
+                                                    : kSplitC * std::max(1, nitems / (4 * warps_all));
   if (ev) cudaEventRecord(ev[1], s);
   kern<<<grid, kSpWarps * 32, smem, s>>>(pts.xt, pts.tc, pts.n, nitems, bufs[0], bufs[1], st, k0,
                                          sp.blist, sp.brec, sp.bcnt, sp.bc, ucap, sp.ctl, sp.pool,

@@ -95,6 +95,24 @@ def test_pool_overflow_rerun_is_bit_identical():
     assert a == b
 
 
+def test_split_units_with_exact_path_rerun_unsplit():
+    """Heavy units are split over warps by 16-point slices. A split unit that
+    needs the max-shift (exact) path could re-select different candidates in
+    its sub-units, so the EM run is repeated without splits: with the exact
+    path forced everywhere (GMMB_SPARSE_EXACT), the result is bit-identical
+    to a run with splits disabled; and splitting moves results only at the
+    rounding level."""
+    forced = _child(_FIT, {"GMMB_SPARSE_EXACT": "1"})
+    forced_nosplit = _child(_FIT, {"GMMB_SPARSE_EXACT": "1", "GMMB_SPARSE_NOSPLIT": "1"})
+    assert forced == forced_nosplit
+    a = _child(_FIT, {})
+    b = _child(_FIT, {"GMMB_SPARSE_NOSPLIT": "1"})
+    assert a["it"] == b["it"]
+    for key in ("w", "mu", "cov"):
+        x, y = np.array(a[key]), np.array(b[key])
+        assert np.max(np.abs(x - y) / np.maximum(np.abs(y), 1e-3)) < 1e-6, key
+
+
 _KINIT = """
 import json, numpy as np, paper_2307_00071_b200 as gm
 rng = np.random.default_rng(7)
