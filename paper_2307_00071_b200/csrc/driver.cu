@@ -81,10 +81,10 @@ struct DevBuf {
 struct EmGraphKey {
   int k0, d, world, sparse;
   int64_t n;
-  const void* p[20];
+  const void* p[32];
   bool operator==(const EmGraphKey& o) const {
     if (k0 != o.k0 || d != o.d || n != o.n || world != o.world || sparse != o.sparse) return false;
-    for (int i = 0; i < 20; ++i)
+    for (int i = 0; i < 32; ++i)
       if (p[i] != o.p[i]) return false;
     return true;
   }
@@ -705,11 +705,15 @@ EmGraphKey em_graph_key(gmmb_ctx* c, int k0) {
   k.n = c->n;
   k.world = c->world;
   k.sparse = c->sparse_on ? 1 + c->sp_nosplit : 0;
-  const void* ps[20] = {c->xt.p, c->tc.p, c->partials.p, c->ll_part.p, c->red.p, c->ll_trace.p,
+  // every device buffer the captured kernels address (a grown buffer moves)
+  const void* ps[32] = {c->xt.p, c->tc.p, c->partials.p, c->ll_part.p, c->red.p, c->ll_trace.p,
                         c->st.p, c->bufs[0].w, c->bufs[1].w, c->rec.count, c->bufs[0].cst,
                         c->bufs[1].cst, c->chunkf.p, c->chunki.p, c->sp_pool.p, c->sp_blist.p,
-                        c->sp_mask.p, c->sp_ctl.p, c->sp_bc.p, c->sp_toff.p};
-  for (int i = 0; i < 20; ++i) k.p[i] = ps[i];
+                        c->sp_mask.p, c->sp_ctl.p, c->sp_bc.p, c->sp_toff.p, c->sp_bh.p,
+                        c->sp_brec.p, c->sp_bcnt.p, c->sp_heavy.p, c->sp_done.p, c->sp_pre.p,
+                        c->sp_ll.p, c->bufs[0].mu, c->bufs[1].mu, c->bufs[0].cov, c->bufs[1].cov,
+                        c->x64.p};
+  for (int i = 0; i < 32; ++i) k.p[i] = ps[i];
   return k;
 }
 

@@ -49,6 +49,39 @@ def case_ws_g():
     ctx.close()
 
 
+def case_sparse_split():
+    """the pruned E step with heavy units split over warps (the frame at
+    K = 512 has units with up to ~400 candidates), plain launches then graph."""
+    pts = gm.synthetic_frame_cloud()[::4].copy()
+    for timing in (True, False):
+        ctx = gm.Context(0)
+        ctx.set_timing(timing)
+        r = gm.fit_k(pts, 512, gm.EmParams(4, 0.0, 1e-6, 0), ctx=ctx)
+        print("sparse_split", timing, r.em_iterations, r.final_log_likelihood, r.units_evaluated)
+        ctx.close()
+
+
+def case_sparse_split_g():
+    """as sparse_split, the EM graph only (fresh process)."""
+    pts = gm.synthetic_frame_cloud()[::4].copy()
+    ctx = gm.Context(0)
+    r = gm.fit_k(pts, 512, gm.EmParams(4, 0.0, 1e-6, 0), ctx=ctx)
+    print("sparse_split_g", r.em_iterations, r.final_log_likelihood, r.units_evaluated)
+    ctx.close()
+
+
+def case_sparse_exact():
+    """as sparse_split with the exact path forced on every slice: the split
+    conflict is flagged and the EM run repeated without splits."""
+    os.environ["GMMB_SPARSE_EXACT"] = "1"
+    pts = gm.synthetic_frame_cloud()[::4].copy()
+    ctx = gm.Context(0)
+    ctx.set_timing(True)
+    r = gm.fit_k(pts, 512, gm.EmParams(3, 0.0, 1e-6, 0), ctx=ctx)
+    print("sparse_exact", r.em_iterations, r.final_log_likelihood)
+    ctx.close()
+
+
 def case_dense():
     """the dense E kernels (warp-specialised K <= 512, chunked K > 512)."""
     pts = blobs(4, 12, 300, 1)
@@ -115,7 +148,7 @@ def case_aux():
     print("aux ok")
 
 
-CASES = {"ws": case_ws, "ws_t": case_ws_t, "ws_g": case_ws_g, "dense": case_dense, "cluster": case_cluster, "kinit_mem": case_kinit_mem,
+CASES = {"ws": case_ws, "sparse_split": case_sparse_split, "sparse_split_g": case_sparse_split_g, "sparse_exact": case_sparse_exact, "ws_t": case_ws_t, "ws_g": case_ws_g, "dense": case_dense, "cluster": case_cluster, "kinit_mem": case_kinit_mem,
          "vshard": case_vshard, "batch": case_batch, "aux": case_aux}
 
 if __name__ == "__main__":
