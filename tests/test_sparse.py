@@ -129,12 +129,17 @@ print(json.dumps({"lab": int(np.sum(lab.astype(np.int64) * np.arange(len(lab)) %
 def test_tile_kinit_equals_resident_and_memory_kernels():
     """420k points (past the shared-memory kernel): the tile kernel and the
     memory-resident rounds; the cfg2 frame: the resident kernel and the tile
-    kernel forced (GMMB_KINIT=tile). Same centres and labels."""
+    kernel forced (GMMB_KINIT=tile); the tile kernel with one round per grid
+    exchange (GMMB_KPP_TILE=ws1) and with two (default). Same centres and
+    labels."""
     tile = _child(_KINIT, {})
     mem = _child(_KINIT, {"GMMB_KINIT": "mem"})
     forced = _child(_KINIT, {"GMMB_KINIT": "tile"})
+    one_round = _child(_KINIT, {"GMMB_KPP_TILE": "ws1", "GMMB_KINIT": "tile"})
     assert tile["cen"] == mem["cen"] and tile["lab"] == mem["lab"]
     assert tile["cen2"] == forced["cen2"] and tile["lab2"] == forced["lab2"]
+    # two rounds per exchange (default) = one round per exchange
+    assert one_round == forced
 
 
 def test_tile_kinit_matches_oracle(gm, orc):
