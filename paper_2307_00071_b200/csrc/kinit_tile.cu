@@ -1540,6 +1540,7 @@ __global__ void __launch_bounds__(kTileKppThreads, 1)
   }
 }
 
+
 }  // namespace
 
 bool kpp_tile_wanted(int64_t n, int sm_count) {

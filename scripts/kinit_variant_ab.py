@@ -22,7 +22,7 @@ h = int(np.sum(lab.astype(np.int64) * (np.arange(len(lab)) %% 1000003)) %% 21474
 print(json.dumps({"ms": ts, "cen": cen.tolist(), "lab": h}))
 """ % (ROOT, n, k, k)
 res = {}
-for v in ("ws1", "", "sync"):
+for v in [x for x in os.environ.get("VARIANTS", "ws1,,sync").split(",")]:
     env = dict(os.environ)
     if v:
         env["GMMB_KPP_TILE"] = v
