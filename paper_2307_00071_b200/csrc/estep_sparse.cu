@@ -1116,7 +1116,7 @@ int sparse_items(int ntiles) { return ntiles * kItemsPerTile; }
 // points per work unit: one item (32 points) while the cloud has few tiles per
 // warp (balance, tight boxes), whole tiles when there are plenty (4x fewer
 // per-unit statistics records to write and reduce)
-int sparse_unit_items(int ntiles, int sm_count) {
+int sparse_unit_items(int ntiles, int sm_count, int k0) {
   static const int forced = [] {  // GMMB_SPARSE_U=1|2|4 (experiments)
     const char* e = getenv("GMMB_SPARSE_U");
     const int u = e ? atoi(e) : 0;
@@ -1125,14 +1125,19 @@ int sparse_unit_items(int ntiles, int sm_count) {
   if (forced) return forced;
   const int warps = sm_count * kSpWarps * kSpMinBlocks;
   const int nitems = sparse_items(ntiles);
-  // (cfg4, 125k items on 148 SMs: U = 4 measured 25 % faster than U = 2)
+  // Measured EM ms per fit, U = 1 / 2 / 4 (scripts/ab_fits.py, fits to tol
+  // 1e-3; the heavy-unit split keeps larger units balanced):
+  //   frame (9,600 items) K = 64: 1.27 / 1.14 / 1.16, K = 256: 1.72 / 1.48 / 1.81,
+  //   K = 512: 1.90 / 1.61 / 1.79, K = 1024: 2.40 / 2.00 / 1.93,
+  //   K = 2048: 4.73 / 4.08 / 3.94, K = 4096: 9.20 / 7.73 / 7.60;
+  //   cfg4 (125k items, K = 2048): 10.65 / 6.74 / 4.94
   if (nitems >= 32 * warps) return 4;
-  if (nitems >= 16 * warps) return 2;
+  if (nitems >= 2 * warps) return k0 > 512 ? 4 : 2;
   return 1;
 }
 
 int sparse_ranges(int k0, int ntiles, int sm_count) {
-  return reduce_ranges(k0, sparse_items(ntiles) / sparse_unit_items(ntiles, sm_count), sm_count);
+  return reduce_ranges(k0, sparse_items(ntiles) / sparse_unit_items(ntiles, sm_count, k0), sm_count);
 }
 
 cudaError_t launch_sparse_layout(const PointsDev& pts, const SparseScratch& sp, cudaStream_t s) {
@@ -1146,7 +1151,7 @@ cudaError_t launch_estep_sparse(const PointsDev& pts, const ModelBuf* bufs, cons
                                 int sm_count, cudaStream_t s, int* ncl_out,
                                 const SparseScratch& sp) {
   const int ntiles = pts.ntiles;
-  const int U = sparse_unit_items(ntiles, sm_count);
+  const int U = sparse_unit_items(ntiles, sm_count, k0);
   const int nitems = sparse_items(ntiles) / U;  // work units
   const int R = reduce_ranges(k0, nitems, sm_count);
   *ncl_out = R;

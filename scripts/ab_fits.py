@@ -9,13 +9,13 @@ sys.path.insert(0, %r)
 import paper_2307_00071_b200 as gm
 ctx = gm.Context(0)
 out = []
-for name in ("cfg2", "k2048", "cfg4"):
+for name in os.environ.get("AB_CONFIGS", "cfg2,k2048,cfg4").split(","):
     if name == "cfg4":
         p = gm.structured_scene(4_000_000, 4, 0.005)[:, :3] * 25 + np.array([100.0, -40.0, 0.0])
         k = 2048
     else:
         p = gm.synthetic_frame_cloud()
-        k = 512 if name == "cfg2" else 2048
+        k = 512 if name == "cfg2" else int(name[1:])
     ctx.upload(p)
     em = gm.EmParams(100, 1e-3, 1e-6, 0)
     ctx.fit_k_resident(k, em)
