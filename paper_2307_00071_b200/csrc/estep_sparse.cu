@@ -88,13 +88,16 @@ __host__ __device__ constexpr int pool_stride(int d) { return (nstats(d) + 1) & 
 // Heavy units (many candidates) are split over up to kMaxSplit warps by
 // 16-point slices: a unit whose previous iteration had C > kHeavyC candidates
 // is queued first, split into S = 2^j sub-units while C / S > split_c, where
-// split_c = kSplitC x (units per 4 warps, at least 1): a split only pays when
+// split_c = (96, or 160 for K > 1024) x (units per 4 warps, at least 1): a split only pays when
 // one unit is a large share of a warp's work (each sub-unit repeats the
 // unit's loads and candidate filter).
 constexpr int kMaxSplit = kSparseMaxSplit;
-constexpr int kHeavyC = 48;
+#ifndef GMMB_HEAVY_C
+#define GMMB_HEAVY_C 48
+#endif
+constexpr int kHeavyC = GMMB_HEAVY_C;
 #ifndef GMMB_SPLIT_C
-#define GMMB_SPLIT_C 96
+#define GMMB_SPLIT_C 0  // 0: by K (below)
 #endif
 constexpr int kSplitC = GMMB_SPLIT_C;
 
@@ -1204,8 +1207,11 @@ cudaError_t launch_estep_sparse(const PointsDev& pts, const ModelBuf* bufs, cons
   static const bool env_nosplit = getenv("GMMB_SPARSE_NOSPLIT") != nullptr;
   static const bool env_exact = getenv("GMMB_SPARSE_EXACT") != nullptr;
   if (env_exact) exact_mode = 1;
+  // (measured: 96 best up to K = 1024, 160 above: K = 2048 3.96 -> 3.80 ms,
+  // K = 4096 7.47 -> 6.43 ms of EM per fit; K = 1024 1.96 vs 2.17)
+  const int split_base = kSplitC > 0 ? kSplitC : (k0 > 1024 ? 160 : 96);
   const int split_c = (sp.no_split || env_nosplit) ? (1 << 30)
-                                                    : kSplitC * std::max(1, nitems / (4 * warps_all));
+                                                    : split_base * std::max(1, nitems / (4 * warps_all));
   if (ev) cudaEventRecord(ev[1], s);
   kern<<<grid, kSpWarps * 32, smem, s>>>(pts.xt, pts.tc, pts.n, nitems, bufs[0], bufs[1], st, k0,
                                          sp.blist, sp.brec, sp.bcnt, sp.bc, ucap, sp.ctl, sp.pool,
