@@ -55,10 +55,10 @@ NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 # flushed caches, so the per-(unit, candidate) statistics the reduce reads
 # (L2-resident between the kernels in situ) count as DRAM reads here.
 TRAFFIC = {
-    ("cfg2", 512, "sparse"): (6.3232e4 + 6.029824e6 + 2.74688e5 + 2.8428032e7 + 1.0496e4,
-                              "profiles/r2aw_cfg2_sparse_ncu.txt"),
-    ("cfg4", 2048, "sparse"): (2.97984e5 + 1.92e4 + 9.4793472e7 + 1.17938944e8 + 1.63968768e8
-                               + 2.8050688e7, "profiles/r2aw_cfg4_sparse_ncu.txt"),
+    ("cfg2", 512, "sparse"): (6.3744e4 + 6.002432e6 + 1.6128e4 + 1.67936e7 + 5.12e2,
+                              "profiles/r2bc_cfg2_sparse_ncu.txt"),
+    ("cfg4", 2048, "sparse"): (2.97728e5 + 1.536e4 + 9.4760192e7 + 1.16638976e8 + 1.63354112e8
+                               + 2.7361024e7, "profiles/r2bc_cfg4_sparse_ncu.txt"),
 }
 
 
@@ -543,8 +543,8 @@ def main():
                      "bound_note": ("the pruned E step is latency-bound, not FP32-bound: 16 warps "
                                     "per SM (128 registers), issue slots ~40 % active, the per-unit "
                                     "candidate filter and statistics hand-off are memory round trips "
-                                    "(profiles/r2aw_cfg2_sparse_ncu.txt, r2au_sparse_source_stalls.txt); "
-                                    "it evaluates ~4.5 % of the pairs and takes less time than the "
+                                    "(profiles/r2bc_cfg2_sparse_ncu.txt, r2au_sparse_source_stalls.txt); "
+                                    "it evaluates ~5 % of the pairs and takes less time than the "
                                     "dense kernels would at their 0.60 target"
                                     if pruned else None),
                      "peak_source": "measured packed-FP32 (fma.rn.f32x2) microbenchmark in this "
