@@ -59,6 +59,7 @@ struct KppTileScratch {
   double* tsum;         // [ntiles]
 };
 bool kpp_tile_wanted(int64_t n, int sm_count);
+
 // keys must be computed; owned[] zeroed; labels (original order), owned and
 // centres are written (the fix-up follows).
 cudaError_t launch_kpp_tile(const double* x64, int64_t n, int ntiles, const int32_t* perm,

@@ -33,6 +33,7 @@
 // slots (arrival counter + fence), reduced by every CTA in the same order.
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -122,7 +123,7 @@ __device__ __forceinline__ void poll_slots(const uint2* base, unsigned tag, int 
       }
       if (ok) pending &= ~(1u << q);
     }
-    if (pending) __nanosleep(32);  // ease the pressure on the slot lines
+    // (no __nanosleep between attempts: it sleeps far longer than asked on B200)
   }
 #pragma unroll
   for (int q = 0; q < kPollSlots; ++q) {
@@ -985,9 +986,13 @@ __device__ __forceinline__ void poll_slots2(const uint2* base, unsigned tag, int
   for (int q = 0; q < kPollSlots; ++q)
     if (lane + 32 * q < nblk) pending |= 1u << q;
   while (pending) {
+    // the loads of every unseen slot go out back to back: which slots to read
+    // is fixed before the attempt (a predicate on the previous slot's tags
+    // would serialise one L2 round trip per slot)
+    const unsigned pend0 = pending;
 #pragma unroll
     for (int q = 0; q < kPollSlots; ++q) {
-      if (!((pending >> q) & 1u)) continue;
+      if (!((pend0 >> q) & 1u)) continue;
       const uint2* p = base + (lane + 32 * q) * kW2SlotWords;
       unsigned v[10];
       bool ok = true;
@@ -1021,7 +1026,8 @@ __device__ __forceinline__ void poll_slots2(const uint2* base, unsigned tag, int
         gd1 = d1;
       }
     }
-    if (pending) __nanosleep(32);
+    // (no __nanosleep between attempts: even 32 ns sleeps far longer on
+    // B200; with it the cfg4 seeding took 21.7 ms instead of 20.2)
   }
 }
 
@@ -1535,7 +1541,8 @@ __global__ void __launch_bounds__(kTileKppThreads, 1)
         break;
       }
       first = false;
-      tau = tau * 64.0 > 1e300 ? INFINITY : tau * 64.0;
+      // (no point with d2 > 0 left: straight to the fallback)
+      tau = !(isfinite(gsum) && gsum > 0.0) || tau * 64.0 > 1e300 ? INFINITY : tau * 64.0;
     }
   }
 }
