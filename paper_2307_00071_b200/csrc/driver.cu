@@ -871,9 +871,9 @@ EmState run_em(gmmb_ctx* c, int k0, const gmmb_em_params* em) {
     int redo[2] = {ctl[2] & 1, (ctl[2] >> 1) & 1};
     if (getenv("GMMB_DEBUG"))
       fprintf(stderr,
-              "gmmb: sparse run: iters %d pool cursor %d overflow %d heavy split tasks %d/%d "
-              "whole %d/%d epoch %d tasks %d combines %d\n",
-              h.iter, ctl[1], ctl[2], ctl[6], ctl[7], ctl[9], ctl[10], ctl[8], ctl[12], ctl[13]);
+              "gmmb: sparse run: iters %d pool cursor %d redo flags %d heavy split tasks %d/%d "
+              "whole %d/%d epoch %d tasks %d (GMMB_SP_COUNT builds)\n",
+              h.iter, ctl[1], ctl[2], ctl[6], ctl[7], ctl[9], ctl[10], ctl[8], ctl[12]);
     if (c->world > 1) {  // every rank repeats together
       c->kstatus.ensure(8);
       copy_sync(c, c->kstatus.p + 6, redo, sizeof(redo), cudaMemcpyHostToDevice);
