@@ -72,6 +72,9 @@ def parse():
     ap.add_argument("--frames", type=int, default=64, help="cfg3: frames per step")
     ap.add_argument("--k", type=int, default=0, help="override K (0: the config's)")
     ap.add_argument("--tol", type=float, default=1e-3)
+    ap.add_argument("--max-iters", type=int, default=100,
+                    help="EM iteration cap (cfg4 with --tol 0 --max-iters 20: the fixed-20-"
+                         "iteration throughput mode of SURVEY.md §8(d))")
     ap.add_argument("--vshard", type=int, default=0,
                     help="cfg4 on one GPU as G virtual ranks (sharded-path check)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -139,8 +142,9 @@ def config_dict(args, world):
                 "parallelism": "replicas%d" % world,
                 "l2": "flushed between steps (256 MiB write)"}
     par = "shard%d" % world if world > 1 else ("vshard%d" % args.vshard if args.vshard else "1")
-    return {"workload": "cfg4: 3D map N=4000000, K=%d, k-means++ + EM to tol %g "
-                        "(one fit per step, points sharded over the GPUs)" % (args.k, args.tol),
+    its = "" if args.max_iters == 100 else ", at most %d iterations" % args.max_iters
+    return {"workload": "cfg4: 3D map N=4000000, K=%d, k-means++ + EM to tol %g%s "
+                        "(one fit per step, points sharded over the GPUs)" % (args.k, args.tol, its),
             "global_batch": 1, "points_per_fit": 4_000_000, "k": args.k, "parallelism": par,
             "l2": "flushed between steps (256 MiB write); inputs 96 MB > L2"}
 
@@ -349,12 +353,12 @@ def main():
     sm, cc_major, cc_minor = ctx.device_info()
     if args.config == "cfg2":
         pts = cfg2_points(gm, rank)
-        em = gm.EmParams(100, args.tol, 1e-6, rank)
+        em = gm.EmParams(args.max_iters, args.tol, 1e-6, rank)
         full_n = len(pts)
     else:
         full = cfg4_points(gm)
         full_n = len(full)
-        em = gm.EmParams(100, args.tol, 1e-6, 0)
+        em = gm.EmParams(args.max_iters, args.tol, 1e-6, 0)
         if sharded:
             lo, hi = shard_bounds(full_n, world)[rank]
             pts = np.ascontiguousarray(full[lo:hi])
@@ -597,7 +601,7 @@ def run_cfg3(args, gm, torch, dist, rank, world, local):
         host.append(t)
     dev = [t.cuda() for t in host]
     host_views = [t.numpy().T for t in host]          # (N, 4) Fortran views, pinned
-    em = gm.EmParams(100, args.tol, 1e-6, 0)
+    em = gm.EmParams(args.max_iters, args.tol, 1e-6, 0)
     seeds = mine
     n = len(base)
 
@@ -660,7 +664,7 @@ def run_cfg3(args, gm, torch, dist, rank, world, local):
     # roofline: the fused E kernel per launch in timing mode on one frame
     ctx.upload(host_views[0])
     ctx.set_timing(True)
-    tf = [ctx.fit_k_resident(args.k, gm.EmParams(100, args.tol, 1e-6, seeds[0])) for _ in range(3)]
+    tf = [ctx.fit_k_resident(args.k, gm.EmParams(args.max_iters, args.tol, 1e-6, seeds[0])) for _ in range(3)]
     ctx.set_timing(False)
     est_ms = sum(r.ms_estep for r in tf)
     est_units = sum(r.units for r in tf)
