@@ -174,7 +174,10 @@ __global__ void keys_kernel(const double* __restrict__ x64, int64_t n,
 }
 
 constexpr int kSeedPPT = 8;
-constexpr int kSeedThreads = 384;
+#ifndef GMMB_SEED_THREADS
+#define GMMB_SEED_THREADS 384
+#endif
+constexpr int kSeedThreads = GMMB_SEED_THREADS;
 constexpr int kSeedWarps = kSeedThreads / 32;
 constexpr int kMaxSeedBlocks = 1024;
 
