@@ -74,7 +74,10 @@ constexpr int kRedStep = GMMB_RED_STEP;  // units whose statistics the reduce lo
 constexpr int kItem = 32;         // points per item (one per lane); a work unit is U = 1, 2
 constexpr int kItemsPerTile = kTile / kItem;  // or 4 consecutive items of one layout tile
 constexpr int kSpWarps = 8;       // warps per CTA of the main kernel
-constexpr int kSpMinBlocks = 2;   // two CTAs per SM (128 registers)
+#ifndef GMMB_SP_MINB
+#define GMMB_SP_MINB 2
+#endif
+constexpr int kSpMinBlocks = GMMB_SP_MINB;  // two CTAs per SM (128 registers)
 constexpr int kListCap = 1024;    // candidate list entries per warp (more: every component)
 constexpr int kSlice = 16;        // points per FP32 partial (widened to FP64 after)
 constexpr float kQCut = 134.f;    // candidates: LB < 134 (ex2.approx.ftz(-Q) = 0 for Q > 126)
