@@ -115,7 +115,7 @@ emit(cfg="cfg4", gpu_ms_per_fit=g_ms, gpu_units_per_s=r.units / (g_ms * 1e-3),
 del full
 
 # ---- cfg5 ------------------------------------------------------------------
-for k in (64, 256, 512, 1024, 2048, 4096):
+for k in (64, 128, 256, 512, 1024, 2048, 4096):
     g_ms, r = gpu_fits(frame, k, em, reps=2)
     lab, _ = oracle.kinit(frame, k, 0)
     w, mu, cov, _ = oracle.m_step_labels(frame, lab, k, 1e-6)
