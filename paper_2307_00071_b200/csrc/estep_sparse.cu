@@ -200,13 +200,17 @@ __global__ void __launch_bounds__(kTile)
 }
 
 // ---- coarse candidates per block (ascending component order) --------------
+#ifndef GMMB_BC_THREADS
+#define GMMB_BC_THREADS 256
+#endif
+constexpr int kBcThreads = GMMB_BC_THREADS;  // components per pass of block_cand
 template <int D>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kBcThreads)
     block_cand_kernel(const double* __restrict__ bc, const float4* __restrict__ bh, ModelBuf b0,
                       ModelBuf b1, const EmState* __restrict__ st, int kcap,
                       int* __restrict__ blist, float4* __restrict__ brec, int* __restrict__ bcnt,
                       int* __restrict__ ctl, float qcut) {
-  __shared__ int wcnt[8];
+  __shared__ int wcnt[kBcThreads / 32];
   __shared__ int s_base;
   if (st->done) return;
   // item queues and pool cursor restart every iteration (ctl[2] overflow and
@@ -233,7 +237,7 @@ __global__ void __launch_bounds__(256)
   const float h[4] = {hb.x, hb.y, hb.z, hb.w};
   if (tid == 0) s_base = 0;
   __syncthreads();
-  for (int k0 = 0; k0 < k_cur; k0 += 256) {
+  for (int k0 = 0; k0 < k_cur; k0 += kBcThreads) {
     const int k = k0 + tid;
     bool cand = false;
     float4 a0, a1, a2;
@@ -269,7 +273,7 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     if (tid == 0) {
       int tot = 0;
-      for (int q = 0; q < 8; ++q) tot += wcnt[q];
+      for (int q = 0; q < kBcThreads / 32; ++q) tot += wcnt[q];
       s_base += tot;
     }
     __syncthreads();
@@ -1198,10 +1202,10 @@ cudaError_t launch_estep_sparse(const PointsDev& pts, const ModelBuf* bufs, cons
   }
   if (ev) cudaEventRecord(ev[0], s);
   if (pts.d == 4)
-    block_cand_kernel<4><<<nblk, 256, 0, s>>>(sp.bc, sp.bh, bufs[0], bufs[1], st, k0, sp.blist,
+    block_cand_kernel<4><<<nblk, kBcThreads, 0, s>>>(sp.bc, sp.bh, bufs[0], bufs[1], st, k0, sp.blist,
                                               sp.brec, sp.bcnt, sp.ctl, qcut);
   else
-    block_cand_kernel<3><<<nblk, 256, 0, s>>>(sp.bc, sp.bh, bufs[0], bufs[1], st, k0, sp.blist,
+    block_cand_kernel<3><<<nblk, kBcThreads, 0, s>>>(sp.bc, sp.bh, bufs[0], bufs[1], st, k0, sp.blist,
                                               sp.brec, sp.bcnt, sp.ctl, qcut);
   const int ucap = sp.item_cap * U;
   const int warps_all = sm_count * occ * kSpWarps;
